@@ -1,0 +1,184 @@
+/*
+ * seqplan_isp.h — C ABI of the B200-native ISP (hybrid-sharded) transformer block.
+ *
+ * The reference (InternEvo "seqplan", /root/reference/proj) has no executor: its
+ * hot path exists only as prices and simulators —
+ *   per-layer comm/compute   proj/include/seqplan/cost.hpp:160-241
+ *   shard layout             proj/include/seqplan/strategy.hpp:52-62, placement.hpp:39-59
+ *   overlap schedule         proj/include/seqplan/overlap_sim.hpp:80-153
+ *   caching pool             proj/include/seqplan/mempool.hpp:168-387
+ * These entry points are the executor those functions model. Every
+ * struct below is a POD mirror of a seqplan:: value type so the C++ wrapper
+ * (include/seqplan/isp_block.hpp) converts losslessly:
+ *   seqplan_isp_shape     <- ModelConfig            (model.hpp:12-48)
+ *   seqplan_strategy      <- Strategy               (strategy.hpp:16-48)
+ *   seqplan_mempool_policy<- MempoolPolicy          (mempool.hpp:137-142)
+ *   seqplan_step_stats    <- StepStats              (mempool.hpp:144-149)
+ *   seqplan_timeline_event<- TimelineEvent          (overlap_sim.hpp:28-34)
+ *
+ * Error behaviour mirrors the reference's exception classes as status codes:
+ *   SEQPLAN_ISP_ERR_INVALID  <-> std::invalid_argument (model.hpp:40-47, strategy.hpp:58-59)
+ *   SEQPLAN_ISP_ERR_RUNTIME  <-> std::runtime_error (CUDA / peer-memory failure)
+ *   SEQPLAN_ISP_ERR_OOM      <-> device allocation failure (pool capacity, mempool.hpp:331)
+ *   SEQPLAN_ISP_ERR_UNSUPPORTED  shape the sm_100a kernels do not tile
+ * A per-context message is available from seqplan_isp_last_error().
+ *
+ * All tensors are bf16 row-major on the device unless stated. Activations
+ * x, y, dx, dy are caller-owned [S/p, H] slices (rank r owns tokens
+ * [r*S/p, (r+1)*S/p)); weights, gathered-weight buffers, gradients and
+ * collective scratch are owned by the context's device pool.
+ */
+#ifndef SEQPLAN_ISP_H_
+#define SEQPLAN_ISP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SEQPLAN_ISP_OK = 0,
+  SEQPLAN_ISP_ERR_INVALID = 1,
+  SEQPLAN_ISP_ERR_RUNTIME = 2,
+  SEQPLAN_ISP_ERR_OOM = 3,
+  SEQPLAN_ISP_ERR_UNSUPPORTED = 4,
+};
+
+/* Block weight tensors, in the order of SURVEY.md §8(d) tensor ids 2..8. */
+enum {
+  SEQPLAN_W_NORM1 = 0, /* [H]                 */
+  SEQPLAN_W_QKV = 1,   /* [3H, H]  rows q|k|v */
+  SEQPLAN_W_O = 2,     /* [H, H]              */
+  SEQPLAN_W_NORM2 = 3, /* [H]                 */
+  SEQPLAN_W_GATE = 4,  /* [I, H]              */
+  SEQPLAN_W_UP = 5,    /* [I, H]              */
+  SEQPLAN_W_DOWN = 6,  /* [H, I]              */
+  SEQPLAN_W_COUNT = 7
+};
+
+/* Context flags. */
+enum {
+  SEQPLAN_ISP_FLAG_NO_OVERLAP = 1u << 0,   /* serialise gathers with compute (ForwardPolicy::Naive) */
+  SEQPLAN_ISP_FLAG_FUSED_BWD = 1u << 1,    /* BackwardPolicy::Fused instead of Selective            */
+  SEQPLAN_ISP_FLAG_TIMELINE = 1u << 2,     /* record CUDA-event timeline                            */
+  SEQPLAN_ISP_FLAG_SKIP_COMM = 1u << 3,    /* measurement only: collectives become no-ops           */
+};
+
+typedef struct seqplan_isp_ctx seqplan_isp_ctx;
+
+typedef struct {
+  int64_t hidden_dim; /* H */
+  int64_t heads;      /* D */
+  int64_t seq_len;    /* S (whole sequence; each rank holds S/p tokens) */
+  int64_t ffn_dim;    /* I; 0 = mlp_intermediate_dim(H) (mempool.hpp:79-82) */
+  double rope_base;   /* 10000 */
+  double norm_eps;    /* 1e-5 */
+} seqplan_isp_shape;
+
+typedef struct {
+  int64_t micro_batch, micro_batch_num, recompute, pp, dp, tp, sp, ps, gs, oss;
+} seqplan_strategy;
+
+typedef struct {
+  int32_t pinned_comm_pool;
+  int64_t consolidate_every_k_mlp;
+  int32_t grad_premap;
+  int64_t capacity;
+} seqplan_mempool_policy;
+
+typedef struct {
+  int64_t reserved, allocated, free_cached, fragmented;
+  int64_t peak_reserved, peak_fragmented, peak_allocated;
+} seqplan_step_stats;
+
+typedef struct {
+  int32_t stream; /* 0 = compute, 1 = comm (StreamKind order) */
+  int32_t kind;   /* SEQPLAN_EV_* */
+  int64_t layer;
+  double start_s, end_s; /* seconds since the first event of the call */
+} seqplan_timeline_event;
+
+enum {
+  SEQPLAN_EV_FORWARD = 0,
+  SEQPLAN_EV_GRAD_INPUT = 1,
+  SEQPLAN_EV_GRAD_WEIGHT = 2,
+  SEQPLAN_EV_ALL_GATHER = 3,
+  SEQPLAN_EV_REDUCE_SCATTER = 4,
+  SEQPLAN_EV_ALL_TO_ALL = 5,
+};
+
+/* ---- lifecycle ---------------------------------------------------------- */
+
+/* Creates the context of rank `rank` of `world` on CUDA device `device`.
+ * The strategy must be the ISP plan [b=1,n=1,pp=1,dp=1,tp=1,sp=ps=world,gs=oss=1]
+ * and must pass seqplan::validate (strategy.hpp:72-99). policy may be NULL. */
+int seqplan_isp_ctx_create(int world, int rank, int device, const seqplan_isp_shape* shape,
+                           const seqplan_strategy* strategy, const seqplan_mempool_policy* policy,
+                           uint32_t flags, seqplan_isp_ctx** out);
+void seqplan_isp_ctx_destroy(seqplan_isp_ctx* ctx);
+const char* seqplan_isp_last_error(const seqplan_isp_ctx* ctx);
+
+/* Peer-memory bootstrap (world > 1): every rank exports the IPC handle of its
+ * symmetric heap, the caller exchanges the blobs (any transport), and every rank
+ * opens all of them. handles = world blobs of seqplan_isp_ipc_handle_size() bytes
+ * in rank order. */
+size_t seqplan_isp_ipc_handle_size(void);
+int seqplan_isp_ipc_handle(seqplan_isp_ctx* ctx, void* out);
+int seqplan_isp_open_peers(seqplan_isp_ctx* ctx, const void* handles);
+
+/* Single-process multi-rank mode: p contexts on one device whose "peers" are
+ * each other's heaps; collectives run as lock-step phases over all ranks. */
+int seqplan_isp_group_create(int world, int device, const seqplan_isp_shape* shape,
+                             const seqplan_mempool_policy* policy, uint32_t flags,
+                             seqplan_isp_ctx** out_ctxs);
+int seqplan_isp_group_fwd(seqplan_isp_ctx** ctxs, int world, const void* const* x,
+                          void* const* y, void* stream);
+int seqplan_isp_group_bwd(seqplan_isp_ctx** ctxs, int world, const void* const* dy,
+                          void* const* dx, void* stream);
+
+/* ---- weights and gradients ---------------------------------------------- */
+
+/* Index-keyed synthetic init (splitmix64 -> Box-Muller): linear
+ * weights N(0, 0.02), norm weights 1 + N(0, 0.02). Shard values are independent of p. */
+int seqplan_isp_init_weights(seqplan_isp_ctx* ctx, uint64_t seed);
+/* Number of elements of this rank's shard of tensor `tensor` (ShardingLayout E/F). */
+int64_t seqplan_isp_shard_numel(const seqplan_isp_ctx* ctx, int tensor);
+/* fp32 master shard in/out (host pointers). Setting refreshes the bf16 working shard. */
+int seqplan_isp_set_weight_shard(seqplan_isp_ctx* ctx, int tensor, const float* host, int64_t n);
+int seqplan_isp_get_weight_shard(seqplan_isp_ctx* ctx, int tensor, float* host, int64_t n);
+/* fp32 gradient shard written by the last block_bwd (host pointer). */
+int seqplan_isp_get_grad_shard(seqplan_isp_ctx* ctx, int tensor, float* host, int64_t n);
+/* Device pointer of the fp32 gradient shard (stream-ordered after block_bwd). */
+int seqplan_isp_grad_shard_ptr(seqplan_isp_ctx* ctx, int tensor, float** dev_ptr);
+
+/* Synthetic index-keyed bf16 activations for tokens [r*S/p, (r+1)*S/p) of tensor id. */
+int seqplan_isp_fill_activation(seqplan_isp_ctx* ctx, uint64_t seed, int tensor_id, void* dev_out,
+                                void* stream);
+
+/* ---- the hot path --------------------------------------------------------- */
+
+/* y = block(x) for this rank's S/p tokens; activations needed by backward are kept
+ * in the context's pool. x, y: device bf16 [S/p, H]. stream: cudaStream_t. */
+int seqplan_isp_block_fwd(seqplan_isp_ctx* ctx, const void* x, void* y, void* stream);
+/* dx = d block / dx . dy ; fp32 weight-gradient shards land in the pool
+ * (gradient reduce-scatter fused with the bf16->fp32 cast and scale). */
+int seqplan_isp_block_bwd(seqplan_isp_ctx* ctx, const void* dy, void* dx, void* stream);
+
+/* ---- observability ------------------------------------------------------ */
+int seqplan_isp_pool_stats(seqplan_isp_ctx* ctx, seqplan_step_stats* out);
+/* Copies up to *n events of the last fwd/bwd pair; *n receives the count. */
+int seqplan_isp_timeline(seqplan_isp_ctx* ctx, seqplan_timeline_event* events, int64_t* n);
+
+/* ---- kernel-level entry points (tests) ------------------------------------ */
+int seqplan_isp_debug_gemm(const void* a, int64_t lda, int a_mn, const void* b, int64_t ldb,
+                           int b_mn, void* out, int64_t ldo, int M, int N, int K, int epi,
+                           const void* resid, int64_t ldr, void* out2, int64_t ldo2, void* out_b,
+                           float scale, int accumulate, int interleave64, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SEQPLAN_ISP_H_ */

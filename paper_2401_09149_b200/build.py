@@ -1,0 +1,75 @@
+"""Builds libseqplan_isp.so in-tree with nvcc for sm_100a (no JIT cache).
+
+Every .cu/.cpp under csrc/ is compiled with
+  -gencode arch=compute_100a,code=sm_100a -lineinfo -O3
+and linked into paper_2401_09149_b200/libseqplan_isp.so, which travels to the
+GPU box with the repo snapshot. Incremental: objects are rebuilt only when the
+source or any header under csrc/ or include/ is newer.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+BUILD = PKG / "_build"
+LIB = PKG / "libseqplan_isp.so"
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(ROOT / "include"),
+          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+
+
+def _headers_mtime() -> float:
+    m = 0.0
+    for d in (CSRC, ROOT / "include"):
+        for p in d.rglob("*"):
+            if p.suffix in (".h", ".cuh", ".hpp"):
+                m = max(m, p.stat().st_mtime)
+    return m
+
+
+def _compile(src: Path, hdr_mtime: float, verbose: bool) -> Path:
+    obj = BUILD / (src.name + ".o")
+    if obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, hdr_mtime):
+        return obj
+    cmd = [NVCC, *ARCH, *COMMON, "-c", str(src), "-o", str(obj)]
+    if src.suffix == ".cpp":
+        cmd = [NVCC, *COMMON, "-x", "cu", *ARCH, "-c", str(src), "-o", str(obj)]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"nvcc failed for {src.name}")
+    if r.stderr.strip() and verbose:
+        sys.stderr.write(r.stderr)
+    return obj
+
+
+def build(verbose: bool = False) -> Path:
+    BUILD.mkdir(exist_ok=True)
+    srcs = sorted([*CSRC.glob("*.cu"), *CSRC.glob("*.cpp")])
+    hdr = _headers_mtime()
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        objs = list(ex.map(lambda s: _compile(s, hdr, verbose), srcs))
+    newest = max(o.stat().st_mtime for o in objs)
+    if not LIB.exists() or LIB.stat().st_mtime < newest:
+        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart_static",
+               "-lrt", "-lpthread", "-ldl"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("link failed")
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv))

@@ -1,0 +1,135 @@
+"""ctypes bindings of include/seqplan_isp.h (plumbing for tests and bench.py).
+
+This mirrors what a maintainer would bind from the reference side (see
+INTEGRATION.md): plain pointers, sizes and POD structs; torch is used only to
+own device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+_LIB_PATH = _PKG / "libseqplan_isp.so"
+_lib = None
+
+c_int, c_i64, c_u32, c_u64, c_vp, c_f, c_d = (ctypes.c_int, ctypes.c_int64, ctypes.c_uint32,
+                                             ctypes.c_uint64, ctypes.c_void_p, ctypes.c_float,
+                                             ctypes.c_double)
+
+
+class ShapeC(ctypes.Structure):
+    _fields_ = [("hidden_dim", c_i64), ("heads", c_i64), ("seq_len", c_i64), ("ffn_dim", c_i64),
+                ("rope_base", c_d), ("norm_eps", c_d)]
+
+
+class StrategyC(ctypes.Structure):
+    _fields_ = [(n, c_i64) for n in ("micro_batch", "micro_batch_num", "recompute", "pp", "dp",
+                                     "tp", "sp", "ps", "gs", "oss")]
+
+
+class PolicyC(ctypes.Structure):
+    _fields_ = [("pinned_comm_pool", ctypes.c_int32), ("consolidate_every_k_mlp", c_i64),
+                ("grad_premap", ctypes.c_int32), ("capacity", c_i64)]
+
+
+class StepStatsC(ctypes.Structure):
+    _fields_ = [(n, c_i64) for n in ("reserved", "allocated", "free_cached", "fragmented",
+                                     "peak_reserved", "peak_fragmented", "peak_allocated")]
+
+
+class EventC(ctypes.Structure):
+    _fields_ = [("stream", ctypes.c_int32), ("kind", ctypes.c_int32), ("layer", c_i64),
+                ("start_s", c_d), ("end_s", c_d)]
+
+
+STATUS = {0: "ok", 1: "invalid argument", 2: "runtime error", 3: "out of memory",
+          4: "unsupported"}
+
+W_NORM1, W_QKV, W_O, W_NORM2, W_GATE, W_UP, W_DOWN = range(7)
+W_NAMES = ["norm1", "qkv", "o", "norm2", "gate", "up", "down"]
+FLAG_NO_OVERLAP, FLAG_FUSED_BWD, FLAG_TIMELINE, FLAG_SKIP_COMM = 1, 2, 4, 8
+EV_NAMES = ["forward", "grad_input", "grad_weight", "all_gather", "reduce_scatter", "all_to_all"]
+
+
+def _sig(l, name, res, args):
+    f = getattr(l, name)
+    f.restype = res
+    f.argtypes = args
+
+
+def lib():
+    """Loads libseqplan_isp.so (building it if absent). Raises if it cannot be loaded."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not _LIB_PATH.exists() or os.environ.get("SEQPLAN_ISP_REBUILD"):
+        from .build import build
+        build()
+    l = ctypes.CDLL(str(_LIB_PATH), mode=ctypes.RTLD_GLOBAL)
+    P = ctypes.POINTER
+    _sig(l, "seqplan_isp_debug_gemm", c_int,
+         [c_vp, c_i64, c_int, c_vp, c_i64, c_int, c_vp, c_i64, c_int, c_int, c_int, c_int, c_vp,
+          c_i64, c_vp, c_i64, c_vp, c_f, c_int, c_int, c_vp])
+    for name, res, args in _EXTRA_SIGS:
+        if hasattr(l, name):
+            _sig(l, name, res, args)
+    _lib = l
+    return l
+
+
+P = ctypes.POINTER
+_EXTRA_SIGS = [
+    ("seqplan_isp_ctx_create", c_int, [c_int, c_int, c_int, P(ShapeC), P(StrategyC), P(PolicyC),
+                                       c_u32, P(c_vp)]),
+    ("seqplan_isp_ctx_destroy", None, [c_vp]),
+    ("seqplan_isp_last_error", ctypes.c_char_p, [c_vp]),
+    ("seqplan_isp_ipc_handle_size", ctypes.c_size_t, []),
+    ("seqplan_isp_ipc_handle", c_int, [c_vp, c_vp]),
+    ("seqplan_isp_open_peers", c_int, [c_vp, c_vp]),
+    ("seqplan_isp_group_create", c_int, [c_int, c_int, P(ShapeC), P(PolicyC), c_u32, P(c_vp)]),
+    ("seqplan_isp_group_fwd", c_int, [P(c_vp), c_int, P(c_vp), P(c_vp), c_vp]),
+    ("seqplan_isp_group_bwd", c_int, [P(c_vp), c_int, P(c_vp), P(c_vp), c_vp]),
+    ("seqplan_isp_init_weights", c_int, [c_vp, c_u64]),
+    ("seqplan_isp_shard_numel", c_i64, [c_vp, c_int]),
+    ("seqplan_isp_set_weight_shard", c_int, [c_vp, c_int, c_vp, c_i64]),
+    ("seqplan_isp_get_weight_shard", c_int, [c_vp, c_int, c_vp, c_i64]),
+    ("seqplan_isp_get_grad_shard", c_int, [c_vp, c_int, c_vp, c_i64]),
+    ("seqplan_isp_grad_shard_ptr", c_int, [c_vp, c_int, P(c_vp)]),
+    ("seqplan_isp_fill_activation", c_int, [c_vp, c_u64, c_int, c_vp, c_vp]),
+    ("seqplan_isp_block_fwd", c_int, [c_vp, c_vp, c_vp, c_vp]),
+    ("seqplan_isp_block_bwd", c_int, [c_vp, c_vp, c_vp, c_vp]),
+    ("seqplan_isp_pool_stats", c_int, [c_vp, P(StepStatsC)]),
+    ("seqplan_isp_timeline", c_int, [c_vp, P(EventC), P(c_i64)]),
+]
+
+
+def check(status, ctx=None, what=""):
+    if status != 0:
+        msg = ""
+        if ctx:
+            m = lib().seqplan_isp_last_error(ctx)
+            msg = m.decode() if m else ""
+        raise RuntimeError(f"{what}: {STATUS.get(status, status)}: {msg}")
+
+
+def debug_gemm(a, b, out, M, N, K, *, a_mn=False, b_mn=False, epi=0, resid=None, out2=None,
+               out_b=None, scale=1.0, accumulate=False, interleave64=False, stream=0):
+    """Kernel-level GEMM through the C ABI; tensors are torch CUDA tensors (plumbing)."""
+    st = lib().seqplan_isp_debug_gemm(
+        a.data_ptr(), a.stride(0), int(a_mn), b.data_ptr(), b.stride(0), int(b_mn),
+        out.data_ptr(), out.stride(0), M, N, K, epi,
+        resid.data_ptr() if resid is not None else None, resid.stride(0) if resid is not None else 0,
+        out2.data_ptr() if out2 is not None else None, out2.stride(0) if out2 is not None else 0,
+        out_b.data_ptr() if out_b is not None else None, float(scale), int(accumulate),
+        int(interleave64), stream)
+    check(st, what="debug_gemm")
+
+
+class IspBlock:  # filled in with the block-level API
+    pass
+
+
+class IspGroup:
+    pass

@@ -1,0 +1,409 @@
+// tcgen05 / TMEM / TMA GEMM for the ISP block (sm_100a).
+//
+// C[M,N] = A[M,K] * B[N,K]^T with bf16 operands and fp32 accumulation in TMEM.
+// Each operand may be K-major (row-major [rows, K]) or MN-major (stored as
+// [K, rows]), so one kernel family covers the three GEMM shapes of a linear
+// layer:
+//   forward  y  = x  * W^T   A=x  (K-major)      B=W  (K-major)
+//   dgrad    dx = dy * W     A=dy (K-major)      B=W  (MN-major)
+//   wgrad    dW = dy^T * x   A=dy (MN-major)     B=x  (MN-major)
+// The reference prices these as the "Linear" term of layer_forward_flops
+// (proj/include/seqplan/cost.hpp:212-219); it has no kernel of its own.
+//
+// Structure: persistent, warp-specialised. warp 0 = TMA producer, warp 1 =
+// tcgen05.mma issuer (one lane), warps 2..5 = epilogue (TMEM -> registers ->
+// global). A 4..6 stage smem ring feeds the tensor core; the accumulator is
+// double-buffered in TMEM so the epilogue of tile i overlaps the mainloop of
+// tile i+1. Fused epilogues: plain bf16 store, residual add, SwiGLU (gate/up
+// interleaved in 64-column blocks), fp32 store with scale/accumulate and
+// optional gate/up de-interleave (used for weight gradients).
+#include <cstdio>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "gemm.h"
+
+namespace isp {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kNumThreads = 192;  // 6 warps
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 512 /*barriers*/;
+};
+
+struct TileSched {
+  int num_m, num_n, num_tiles;
+  __device__ __forceinline__ void coords(int t, int& m_blk, int& n_blk) const {
+    // Group GROUP_M row-blocks together so the ~148 concurrently resident
+    // tiles share A rows and B columns in L2.
+    constexpr int kGroupM = 16;
+    const int per_group = kGroupM * num_n;
+    const int g = t / per_group;
+    const int first_m = g * kGroupM;
+    const int gm = min(num_m - first_m, kGroupM);
+    const int r = t - g * per_group;
+    m_blk = first_m + r % gm;
+    n_blk = r / gm;
+  }
+};
+
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+template <bool A_MN, bool B_MN, int BN, int EPI>
+__global__ void __launch_bounds__(kNumThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA,
+                   const __grid_constant__ CUtensorMap mapB, GemmArgs args) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint64_t* empty_bar = full_bar + S;
+  uint64_t* tfull_bar = empty_bar + S;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  TileSched sched{args.M / BM, args.N / BN, (args.M / BM) * (args.N / BN)};
+  const int num_kb = args.K / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapA);
+    tma_prefetch(&mapB);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull_bar[i], 1);
+      mbar_init(&tempty_bar[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < sched.num_tiles; t += gridDim.x) {
+        int mb, nb;
+        sched.coords(t, mb, nb);
+        const int m0 = mb * BM, n0 = nb * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          uint8_t* sa = smem + s * Cfg::kStageBytes;
+          uint8_t* sb = sa + Cfg::kABytes;
+          mbar_arrive_expect_tx(&full_bar[s], Cfg::kStageBytes);
+          if constexpr (!A_MN) {
+            tma_load_2d(sa, &mapA, &full_bar[s], kb * BK, m0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_2d(sa + j * 8192, &mapA, &full_bar[s], m0 + j * 64, kb * BK);
+          }
+          if constexpr (!B_MN) {
+            tma_load_2d(sb, &mapB, &full_bar[s], kb * BK, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(sb + j * 8192, &mapB, &full_bar[s], n0 + j * 64, kb * BK);
+          }
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc = make_idesc_bf16(BM, BN, A_MN, B_MN);
+    int s = 0;
+    uint32_t ph = 0;
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int t = blockIdx.x; t < sched.num_tiles; t += gridDim.x) {
+      mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full_bar[s], ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sa = smem_u32(smem + s * Cfg::kStageBytes);
+          const uint32_t sb = sa + Cfg::kABytes;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? make_sw128_desc(sa + k * 2048, 8192, 1024)
+                                     : make_sw128_desc(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_sw128_desc(sb + k * 2048, 8192, 1024)
+                                     : make_sw128_desc(sb + k * 32, 16, 1024);
+            tc_mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          tc_commit(&empty_bar[s]);
+        }
+        __syncwarp();
+        if (++s == S) { s = 0; ph ^= 1; }
+      }
+      if (lane == 0) tc_commit(&tfull_bar[acc]);
+      __syncwarp();
+      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..5) ----------------
+    const int lane_grp = warp & 3;  // TMEM lane quadrant this warp may access
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int t = blockIdx.x; t < sched.num_tiles; t += gridDim.x) {
+      int mb, nb;
+      sched.coords(t, mb, nb);
+      const int row = mb * BM + lane_grp * 32 + lane;
+      const int n0 = nb * BN;
+      mbar_wait(&tfull_bar[acc], acc_ph);
+      tc_fence_after();
+      const uint32_t t_base = tmem_base + (static_cast<uint32_t>(lane_grp * 32) << 16) + acc * BN;
+
+      if constexpr (EPI == EPI_SWIGLU) {
+        // 64-column blocks alternate gate / up; pair block 2j with 2j+1.
+#pragma unroll 1
+        for (int blk = 0; blk < BN / 128; ++blk) {
+#pragma unroll 1
+          for (int half = 0; half < 2; ++half) {
+            const int cg = blk * 128 + half * 32;  // gate column within tile
+            uint32_t g[32], u[32];
+            tmem_ld_32x32b_x32(t_base + cg, g);
+            tmem_ld_32x32b_x32(t_base + cg + 64, u);
+            tmem_ld_wait();
+            __nv_bfloat16* gu_row = reinterpret_cast<__nv_bfloat16*>(args.out) +
+                                    static_cast<int64_t>(row) * args.ldo + n0;
+            __nv_bfloat16* a_row = args.out2 + static_cast<int64_t>(row) * args.ldo2 +
+                                   (n0 / 2 + blk * 64 + half * 32);
+            uint4* gdst = reinterpret_cast<uint4*>(gu_row + cg);
+            uint4* udst = reinterpret_cast<uint4*>(gu_row + cg + 64);
+            uint4* adst = reinterpret_cast<uint4*>(a_row);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              uint32_t pg[4], pu[4], pa[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int i = v * 8 + e * 2;
+                const float g0 = __uint_as_float(g[i]), g1 = __uint_as_float(g[i + 1]);
+                const float u0 = __uint_as_float(u[i]), u1 = __uint_as_float(u[i + 1]);
+                pg[e] = pack_bf16(g0, g1);
+                pu[e] = pack_bf16(u0, u1);
+                // activation from the bf16-rounded values the backward will see
+                const float2 gr = unpack_bf16(pg[e]);
+                const float2 ur = unpack_bf16(pu[e]);
+                pa[e] = pack_bf16(silu(gr.x) * ur.x, silu(gr.y) * ur.y);
+              }
+              gdst[v] = make_uint4(pg[0], pg[1], pg[2], pg[3]);
+              udst[v] = make_uint4(pu[0], pu[1], pu[2], pu[3]);
+              adst[v] = make_uint4(pa[0], pa[1], pa[2], pa[3]);
+            }
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_base + c * 32, r);
+          tmem_ld_wait();
+          const int col = n0 + c * 32;
+          if constexpr (EPI == EPI_F32) {
+            float* dst;
+            int64_t orow = row;
+            if (args.interleave64) {
+              const int blk = row >> 6;
+              orow = static_cast<int64_t>(blk >> 1) * 64 + (row & 63);
+              dst = (blk & 1) ? args.out_b : reinterpret_cast<float*>(args.out);
+            } else {
+              dst = reinterpret_cast<float*>(args.out);
+            }
+            float4* p = reinterpret_cast<float4*>(dst + orow * args.ldo + col);
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              float4 o = make_float4(__uint_as_float(r[4 * v]) * args.scale,
+                                     __uint_as_float(r[4 * v + 1]) * args.scale,
+                                     __uint_as_float(r[4 * v + 2]) * args.scale,
+                                     __uint_as_float(r[4 * v + 3]) * args.scale);
+              if (args.accumulate) {
+                const float4 prev = p[v];
+                o.x += prev.x; o.y += prev.y; o.z += prev.z; o.w += prev.w;
+              }
+              p[v] = o;
+            }
+          } else {
+            __nv_bfloat16* dst_row = reinterpret_cast<__nv_bfloat16*>(args.out) +
+                                     static_cast<int64_t>(row) * args.ldo + col;
+            float add[32];
+            if constexpr (EPI == EPI_BF16_RESID) {
+              const uint4* rs = reinterpret_cast<const uint4*>(
+                  args.resid + static_cast<int64_t>(row) * args.ldr + col);
+#pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                const uint4 q = rs[v];
+                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 f = unpack_bf16(w[e]);
+                  add[v * 8 + e * 2] = f.x;
+                  add[v * 8 + e * 2 + 1] = f.y;
+                }
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) add[i] = 0.f;
+            }
+            uint4* d4 = reinterpret_cast<uint4*>(dst_row);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              uint32_t pk[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int i = v * 8 + e * 2;
+                pk[e] = pack_bf16(__uint_as_float(r[i]) * args.scale + add[i],
+                                  __uint_as_float(r[i + 1]) * args.scale + add[i + 1]);
+              }
+              d4[v] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 map over a row-major [rows, cols] matrix with leading dimension ld
+// (elements), 128-byte swizzle, box = {64 cols, box_rows}.
+bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
+              int box_rows) {
+  auto fn = get_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint32_t box[2] = {64u, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int g_num_sms = 0;
+
+template <bool A_MN, bool B_MN, int BN, int EPI>
+cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& args,
+                     cudaStream_t stream) {
+  using Cfg = GemmCfg<BN>;
+  auto kern = gemm_tc_kernel<A_MN, B_MN, BN, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int tiles = (args.M / BM) * (args.N / BN);
+  const int grid = tiles < g_num_sms ? tiles : g_num_sms;
+  kern<<<grid, kNumThreads, Cfg::kSmemBytes, stream>>>(ma, mb, args);
+  return cudaGetLastError();
+}
+
+template <bool A_MN, bool B_MN, int BN>
+cudaError_t dispatch_epi(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a,
+                         int epi, cudaStream_t st) {
+  switch (epi) {
+    case EPI_BF16: return launch_t<A_MN, B_MN, BN, EPI_BF16>(ma, mb, a, st);
+    case EPI_BF16_RESID: return launch_t<A_MN, B_MN, BN, EPI_BF16_RESID>(ma, mb, a, st);
+    case EPI_SWIGLU: return launch_t<A_MN, B_MN, BN, EPI_SWIGLU>(ma, mb, a, st);
+    case EPI_F32: return launch_t<A_MN, B_MN, BN, EPI_F32>(ma, mb, a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+int gemm_pick_bn(int N) { return (N % 256 == 0) ? 256 : ((N % 128 == 0) ? 128 : 0); }
+
+cudaError_t gemm_launch(const GemmOperand& A, const GemmOperand& B, GemmArgs args, int epi,
+                        cudaStream_t stream) {
+  if (args.M % BM || args.K % BK || args.M <= 0 || args.N <= 0 || args.K <= 0)
+    return cudaErrorInvalidValue;
+  int bn = gemm_pick_bn(args.N);
+  if (epi == EPI_SWIGLU) bn = (args.N % 256 == 0) ? 256 : (args.N % 128 == 0 ? 128 : 0);
+  if (bn == 0) return cudaErrorInvalidValue;
+  CUtensorMap ma, mb;
+  // A: logical [M, K]; K-major storage is [M, K], MN-major storage is [K, M].
+  bool ok = A.mn_major ? make_map(&ma, A.ptr, args.K, args.M, A.ld, 64)
+                       : make_map(&ma, A.ptr, args.M, args.K, A.ld, BM);
+  ok = ok && (B.mn_major ? make_map(&mb, B.ptr, args.K, args.N, B.ld, 64)
+                         : make_map(&mb, B.ptr, args.N, args.K, B.ld, bn));
+  if (!ok) return cudaErrorInvalidValue;
+  const int code = (A.mn_major ? 2 : 0) | (B.mn_major ? 1 : 0);
+  if (bn == 256) {
+    switch (code) {
+      case 0: return dispatch_epi<false, false, 256>(ma, mb, args, epi, stream);
+      case 1: return dispatch_epi<false, true, 256>(ma, mb, args, epi, stream);
+      case 2: return dispatch_epi<true, false, 256>(ma, mb, args, epi, stream);
+      case 3: return dispatch_epi<true, true, 256>(ma, mb, args, epi, stream);
+    }
+  } else {
+    switch (code) {
+      case 0: return dispatch_epi<false, false, 128>(ma, mb, args, epi, stream);
+      case 1: return dispatch_epi<false, true, 128>(ma, mb, args, epi, stream);
+      case 2: return dispatch_epi<true, false, 128>(ma, mb, args, epi, stream);
+      case 3: return dispatch_epi<true, true, 128>(ma, mb, args, epi, stream);
+    }
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace isp

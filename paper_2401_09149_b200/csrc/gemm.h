@@ -1,0 +1,44 @@
+// Host interface of the tcgen05 GEMM (see gemm.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace isp {
+
+enum GemmEpilogue : int {
+  EPI_BF16 = 0,        // out(bf16) = scale * acc
+  EPI_BF16_RESID = 1,  // out(bf16) = scale * acc + resid(bf16)
+  EPI_SWIGLU = 2,      // out(bf16) = acc (gate/up interleaved by 64 cols); out2 = silu(g) * u
+  EPI_F32 = 3,         // out(f32) (+)= scale * acc; optional 64-row gate/up de-interleave
+};
+
+// One GEMM operand. Logical shape is [rows, K] (A: rows = M, B: rows = N).
+// K-major: stored row-major as [rows, K] with leading dimension ld.
+// MN-major: stored row-major as [K, rows] with leading dimension ld.
+struct GemmOperand {
+  const void* ptr;
+  int64_t ld;
+  bool mn_major;
+};
+
+struct GemmArgs {
+  int M = 0, N = 0, K = 0;
+  void* out = nullptr;  // bf16 or f32
+  int64_t ldo = 0;
+  const __nv_bfloat16* resid = nullptr;
+  int64_t ldr = 0;
+  __nv_bfloat16* out2 = nullptr;  // SwiGLU activation [M, N/2]
+  int64_t ldo2 = 0;
+  float* out_b = nullptr;  // EPI_F32 + interleave64: destination of odd 64-row blocks
+  float scale = 1.0f;
+  int accumulate = 0;
+  int interleave64 = 0;
+};
+
+int gemm_pick_bn(int N);
+cudaError_t gemm_launch(const GemmOperand& A, const GemmOperand& B, GemmArgs args, int epi,
+                        cudaStream_t stream);
+
+}  // namespace isp

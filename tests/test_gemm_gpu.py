@@ -1,0 +1,89 @@
+"""tcgen05 GEMM parity vs a plain PyTorch fp32 reference of the same op.
+
+Covers the three linear-layer shapes (fwd NT, dgrad with MN-major B, wgrad with
+MN-major A and B) and every fused epilogue. bf16 inputs, fp32 accumulation:
+tolerance rel-L2 <= 2e-3 against fp32 math on the same bf16 inputs.
+"""
+import pytest
+import torch
+
+from paper_2401_09149_b200 import capi
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_l2(a, b):
+    a = a.float(); b = b.float()
+    return ((a - b).norm() / b.norm().clamp_min(1e-30)).item()
+
+
+def _rand(*shape, dev):
+    return torch.randn(*shape, device=dev).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False), (True, True)])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 128, 192), (512, 768, 512), (384, 1536, 320)])
+def test_gemm_layouts(cuda, a_mn, b_mn, M, N, K):
+    A = _rand(M, K, dev=cuda)
+    B = _rand(N, K, dev=cuda)
+    a_store = A.t().contiguous() if a_mn else A
+    b_store = B.t().contiguous() if b_mn else B
+    out = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    capi.debug_gemm(a_store, b_store, out, M, N, K, a_mn=a_mn, b_mn=b_mn, epi=0)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().t()
+    assert rel_l2(out, ref) < 4e-3
+
+
+def test_gemm_resid_and_scale(cuda):
+    M, N, K = 256, 512, 256
+    A, B, R = _rand(M, K, dev=cuda), _rand(N, K, dev=cuda), _rand(M, N, dev=cuda)
+    out = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    capi.debug_gemm(A, B, out, M, N, K, epi=1, resid=R, scale=0.5)
+    torch.cuda.synchronize()
+    ref = 0.5 * (A.float() @ B.float().t()) + R.float()
+    assert rel_l2(out, ref) < 4e-3
+
+
+def test_gemm_swiglu(cuda):
+    M, K, I = 256, 256, 384
+    A = _rand(M, K, dev=cuda)
+    Wg, Wu = _rand(I, K, dev=cuda), _rand(I, K, dev=cuda)
+    # interleave 64-row blocks: gate blk j, up blk j, ...
+    Wgu = torch.stack([Wg.view(I // 64, 64, K), Wu.view(I // 64, 64, K)], 1).reshape(2 * I, K)
+    gu = torch.empty(M, 2 * I, device=cuda, dtype=torch.bfloat16)
+    a = torch.empty(M, I, device=cuda, dtype=torch.bfloat16)
+    capi.debug_gemm(A, Wgu, gu, M, 2 * I, K, epi=2, out2=a)
+    torch.cuda.synchronize()
+    g = A.float() @ Wg.float().t()
+    u = A.float() @ Wu.float().t()
+    gu_v = gu.view(M, I // 64, 2, 64)
+    assert rel_l2(gu_v[:, :, 0].reshape(M, I), g) < 4e-3
+    assert rel_l2(gu_v[:, :, 1].reshape(M, I), u) < 4e-3
+    assert rel_l2(a, torch.nn.functional.silu(g) * u) < 1e-2
+
+
+def test_gemm_f32_interleaved_wgrad(cuda):
+    # dW_gu = dgu^T x  (A MN-major, B MN-major) de-interleaved into fp32 gate/up grads
+    T, I, H = 256, 192, 256
+    dgu = _rand(T, 2 * I, dev=cuda)
+    x = _rand(T, H, dev=cuda)
+    g_out = torch.full((I, H), 1.0, device=cuda)
+    u_out = torch.full((I, H), 1.0, device=cuda)
+    capi.debug_gemm(dgu, x, g_out, 2 * I, H, T, a_mn=True, b_mn=True, epi=3, out_b=u_out,
+                    scale=0.25, accumulate=True, interleave64=True)
+    torch.cuda.synchronize()
+    full = 0.25 * (dgu.float().t() @ x.float())  # [2I, H] interleaved
+    fv = full.view(I // 64, 2, 64, H)
+    assert rel_l2(g_out - 1.0, fv[:, 0].reshape(I, H)) < 2e-3
+    assert rel_l2(u_out - 1.0, fv[:, 1].reshape(I, H)) < 2e-3
+
+
+def test_gemm_large(cuda):
+    M, N, K = 4096, 12288, 4096
+    A, B = _rand(M, K, dev=cuda), _rand(N, K, dev=cuda)
+    out = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    capi.debug_gemm(A, B, out, M, N, K)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().t()
+    assert rel_l2(out, ref) < 4e-3
