@@ -160,7 +160,9 @@ int seqplan_isp_fill_activation(seqplan_isp_ctx* ctx, uint64_t seed, int tensor_
 /* ---- the hot path --------------------------------------------------------- */
 
 /* y = block(x) for this rank's S/p tokens; activations needed by backward are kept
- * in the context's pool. x, y: device bf16 [S/p, H]. stream: cudaStream_t. */
+ * in the context's pool. x, y: device bf16 [S/p, H]. stream: cudaStream_t.
+ * x must stay valid until the matching block_bwd (it is the RMSNorm-1 input, saved by
+ * reference rather than copied). */
 int seqplan_isp_block_fwd(seqplan_isp_ctx* ctx, const void* x, void* y, void* stream);
 /* dx = d block / dx . dy ; fp32 weight-gradient shards land in the pool
  * (gradient reduce-scatter fused with the bf16->fp32 cast and scale). */
@@ -176,6 +178,14 @@ int seqplan_isp_debug_gemm(const void* a, int64_t lda, int a_mn, const void* b, 
                            int b_mn, void* out, int64_t ldo, int M, int N, int K, int epi,
                            const void* resid, int64_t ldr, void* out2, int64_t ldo2, void* out_b,
                            float scale, int accumulate, int interleave64, void* stream);
+/* Causal attention over S tokens (dout == NULL: forward; else backward into dq/dk/dv). */
+int seqplan_isp_debug_attention(const void* q, const void* k, const void* v, int64_t ld_qkv, void* o,
+                                int64_t ld_o, float* lse, int S, int heads, int d, const void* dout,
+                                void* dq, void* dk, void* dv, int64_t ld_d, float* delta, float* dq_acc,
+                                void* stream);
+/* RMSNorm forward (dn == NULL) or backward: dx = dres + d(norm), dg += sum dn*xhat. */
+int seqplan_isp_debug_rmsnorm(const void* x, const void* g, void* y, float* rstd, const void* dn,
+                              const void* dres, void* dx, float* dg, int T, int H, float eps, void* stream);
 
 #ifdef __cplusplus
 }

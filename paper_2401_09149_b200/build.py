@@ -20,6 +20,7 @@ CSRC = PKG / "csrc"
 BUILD = PKG / "_build"
 LIB = PKG / "libseqplan_isp.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(ROOT / "include"),
           "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
@@ -39,8 +40,10 @@ def _compile(src: Path, hdr_mtime: float, verbose: bool) -> Path:
     if obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, hdr_mtime):
         return obj
     cmd = [NVCC, *ARCH, *COMMON, "-c", str(src), "-o", str(obj)]
-    if src.suffix == ".cpp":
-        cmd = [NVCC, *COMMON, "-x", "cu", *ARCH, "-c", str(src), "-o", str(obj)]
+    if src.suffix == ".cpp":  # host-only C++20 (executor, pool, C ABI)
+        cmd = [CXX, "-std=c++20", "-O2", "-g", "-fPIC", "-Wall", "-Wno-unused-function",
+               "-I", str(ROOT / "include"), "-I", "/usr/local/cuda/include", "-c", str(src),
+               "-o", str(obj)]
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -73,8 +73,7 @@ def lib():
          [c_vp, c_i64, c_int, c_vp, c_i64, c_int, c_vp, c_i64, c_int, c_int, c_int, c_int, c_vp,
           c_i64, c_vp, c_i64, c_vp, c_f, c_int, c_int, c_vp])
     for name, res, args in _EXTRA_SIGS:
-        if hasattr(l, name):
-            _sig(l, name, res, args)
+        _sig(l, name, res, args)
     _lib = l
     return l
 
@@ -102,6 +101,10 @@ _EXTRA_SIGS = [
     ("seqplan_isp_block_bwd", c_int, [c_vp, c_vp, c_vp, c_vp]),
     ("seqplan_isp_pool_stats", c_int, [c_vp, P(StepStatsC)]),
     ("seqplan_isp_timeline", c_int, [c_vp, P(EventC), P(c_i64)]),
+    ("seqplan_isp_debug_attention", c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_int, c_int, c_int,
+                                            c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    ("seqplan_isp_debug_rmsnorm", c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_f,
+                                          c_vp]),
 ]
 
 
@@ -127,9 +130,152 @@ def debug_gemm(a, b, out, M, N, K, *, a_mn=False, b_mn=False, epi=0, resid=None,
     check(st, what="debug_gemm")
 
 
-class IspBlock:  # filled in with the block-level API
-    pass
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream_handle(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+def make_shape(H, D, S, I=0, rope_base=10000.0, eps=1e-5):
+    return ShapeC(H, D, S, I, rope_base, eps)
+
+
+def make_policy(pinned=True, consolidate=0, premap=True, capacity=0):
+    return PolicyC(int(pinned), consolidate, int(premap), capacity)
+
+
+class IspBlock:
+    """One rank's ISP block context (multi-process mode: one process per GPU).
+
+    Thin ctypes wrapper; every call goes through the C ABI of include/seqplan_isp.h.
+    """
+
+    def __init__(self, H, D, S, world=1, rank=0, device=0, policy=None, flags=0, I=0):
+        l = lib()
+        self.world, self.rank = world, rank
+        self.shape = make_shape(H, D, S, I)
+        strat = StrategyC(1, 1, 0, 1, 1, 1, world, world, 1, 1)
+        pol = policy if policy is not None else make_policy()
+        h = c_vp()
+        st = l.seqplan_isp_ctx_create(world, rank, device, ctypes.byref(self.shape), ctypes.byref(strat),
+                                      ctypes.byref(pol), flags, ctypes.byref(h))
+        check(st, None, "seqplan_isp_ctx_create")
+        self.h = h
+
+    # -- peer bootstrap (world > 1) --
+    def ipc_handle(self) -> bytes:
+        n = lib().seqplan_isp_ipc_handle_size()
+        buf = ctypes.create_string_buffer(n)
+        check(lib().seqplan_isp_ipc_handle(self.h, buf), self.h, "ipc_handle")
+        return buf.raw
+
+    def open_peers(self, handles):
+        blob = b"".join(handles)
+        buf = ctypes.create_string_buffer(blob, len(blob))
+        check(lib().seqplan_isp_open_peers(self.h, buf), self.h, "open_peers")
+
+    def init_weights(self, seed):
+        check(lib().seqplan_isp_init_weights(self.h, seed), self.h, "init_weights")
+
+    def shard_numel(self, t):
+        return lib().seqplan_isp_shard_numel(self.h, t)
+
+    def set_weight_shard(self, t, arr):
+        import numpy as np
+        a = np.ascontiguousarray(arr, dtype=np.float32).reshape(-1)
+        check(lib().seqplan_isp_set_weight_shard(self.h, t, a.ctypes.data, a.size), self.h, "set_weight_shard")
+
+    def weight_shard(self, t):
+        import numpy as np
+        a = np.empty(self.shard_numel(t), np.float32)
+        check(lib().seqplan_isp_get_weight_shard(self.h, t, a.ctypes.data, a.size), self.h, "get_weight_shard")
+        return a
+
+    def grad_shard(self, t):
+        import numpy as np
+        a = np.empty(self.shard_numel(t), np.float32)
+        check(lib().seqplan_isp_get_grad_shard(self.h, t, a.ctypes.data, a.size), self.h, "get_grad_shard")
+        return a
+
+    def fill_activation(self, seed, tid, out, stream=None):
+        check(lib().seqplan_isp_fill_activation(self.h, seed, tid, out.data_ptr(), _stream_handle(stream)),
+              self.h, "fill_activation")
+
+    def fwd(self, x, y, stream=None):
+        check(lib().seqplan_isp_block_fwd(self.h, x.data_ptr(), y.data_ptr(), _stream_handle(stream)),
+              self.h, "block_fwd")
+
+    def bwd(self, dy, dx, stream=None):
+        check(lib().seqplan_isp_block_bwd(self.h, dy.data_ptr(), dx.data_ptr(), _stream_handle(stream)),
+              self.h, "block_bwd")
+
+    def pool_stats(self):
+        s = StepStatsC()
+        check(lib().seqplan_isp_pool_stats(self.h, ctypes.byref(s)), self.h, "pool_stats")
+        return {n: getattr(s, n) for n, _ in StepStatsC._fields_}
+
+    def timeline(self):
+        n = c_i64(0)
+        lib().seqplan_isp_timeline(self.h, None, ctypes.byref(n))
+        arr = (EventC * max(n.value, 1))()
+        lib().seqplan_isp_timeline(self.h, arr, ctypes.byref(n))
+        return [dict(stream=e.stream, kind=EV_NAMES[e.kind], layer=e.layer, start=e.start_s, end=e.end_s)
+                for e in arr[:n.value]]
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().seqplan_isp_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class IspGroup:
-    pass
+    """p ranks on one GPU in one process (lock-step phases; tests and single-GPU parity)."""
+
+    def __init__(self, H, D, S, world, device=0, policy=None, flags=0, I=0):
+        l = lib()
+        self.world = world
+        self.shape = make_shape(H, D, S, I)
+        pol = policy if policy is not None else make_policy()
+        arr = (c_vp * world)()
+        check(l.seqplan_isp_group_create(world, device, ctypes.byref(self.shape), ctypes.byref(pol), flags, arr),
+              None, "group_create")
+        self.hs = [c_vp(arr[i]) for i in range(world)]
+        self._arr = arr
+
+    def rank(self, r):
+        b = IspBlock.__new__(IspBlock)
+        b.h, b.world, b.rank, b.shape = self.hs[r], self.world, r, self.shape
+        return b
+
+    def fwd(self, xs, ys, stream=None):
+        X = (c_vp * self.world)(*[x.data_ptr() for x in xs])
+        Y = (c_vp * self.world)(*[y.data_ptr() for y in ys])
+        check(lib().seqplan_isp_group_fwd(self._arr, self.world, X, Y, _stream_handle(stream)), self.hs[0], "group_fwd")
+
+    def bwd(self, dys, dxs, stream=None):
+        X = (c_vp * self.world)(*[x.data_ptr() for x in dys])
+        Y = (c_vp * self.world)(*[y.data_ptr() for y in dxs])
+        check(lib().seqplan_isp_group_bwd(self._arr, self.world, X, Y, _stream_handle(stream)), self.hs[0], "group_bwd")
+
+    def close(self):
+        if getattr(self, "hs", None):
+            for h in self.hs:
+                lib().seqplan_isp_ctx_destroy(h)
+            self.hs = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -32,3 +32,50 @@ extern "C" int seqplan_isp_debug_gemm(const void* a, int64_t lda, int a_mn, cons
   cudaError_t e = isp::gemm_launch(A, B, args, epi, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SEQPLAN_ISP_OK : SEQPLAN_ISP_ERR_RUNTIME;
 }
+
+#include "kernels.h"
+
+extern "C" int seqplan_isp_debug_attention(const void* q, const void* k, const void* v, int64_t ld_qkv,
+                                           void* o, int64_t ld_o, float* lse, int S, int heads, int d,
+                                           const void* dout, void* dq, void* dk, void* dv, int64_t ld_d,
+                                           float* delta, float* dq_acc, void* stream) {
+  isp::AttnTensors t{};
+  t.q = static_cast<const __nv_bfloat16*>(q);
+  t.k = static_cast<const __nv_bfloat16*>(k);
+  t.v = static_cast<const __nv_bfloat16*>(v);
+  t.ld_qkv = ld_qkv;
+  t.o = static_cast<__nv_bfloat16*>(o);
+  t.ld_o = ld_o;
+  t.lse = lse;
+  t.S = S;
+  t.heads = heads;
+  t.d = d;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e;
+  if (!dout) {
+    e = isp::attention_fwd(t, st, sms);
+  } else {
+    e = isp::attention_bwd(t, static_cast<const __nv_bfloat16*>(dout), static_cast<__nv_bfloat16*>(dq),
+                           static_cast<__nv_bfloat16*>(dk), static_cast<__nv_bfloat16*>(dv), ld_d, delta,
+                           dq_acc, st, sms);
+  }
+  return e == cudaSuccess ? SEQPLAN_ISP_OK : SEQPLAN_ISP_ERR_RUNTIME;
+}
+
+extern "C" int seqplan_isp_debug_rmsnorm(const void* x, const void* g, void* y, float* rstd, const void* dn,
+                                         const void* dres, void* dx, float* dg, int T, int H, float eps,
+                                         void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (!dn)
+    e = isp::rmsnorm_fwd(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(g),
+                         static_cast<__nv_bfloat16*>(y), rstd, T, H, eps, st, 148);
+  else
+    e = isp::rmsnorm_bwd(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(g), rstd,
+                         static_cast<const __nv_bfloat16*>(dn), static_cast<const __nv_bfloat16*>(dres),
+                         static_cast<__nv_bfloat16*>(dx), dg, T, H, st, 148);
+  return e == cudaSuccess ? SEQPLAN_ISP_OK : SEQPLAN_ISP_ERR_RUNTIME;
+}

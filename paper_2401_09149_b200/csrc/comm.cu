@@ -1,0 +1,315 @@
+// Peer-memory collectives of the ISP block over NVLink / NVSwitch (sm_100a).
+//
+// Every rank owns a symmetric heap; peers' heaps are mapped into this process
+// (CUDA IPC in multi-process mode, plain device pointers in single-process
+// group mode), so collectives are ordinary kernels issuing 16-byte loads to
+// peer addresses — no NCCL on the data path. They are the executor-side
+// counterparts of the prices in proj/include/seqplan/cost.hpp:
+//   parameter all-gather (ps)            cost.hpp:184-188 (2n x AG of e*Psi/tp)
+//   gradient reduce-scatter (ps)         cost.hpp:187     (n x RS), fused with cast/scale
+//   Ulysses all-to-all (sp)              cost.hpp:179-183 (QKV and attention output)
+// All are "pull" kernels: rank r reads what it needs from every peer, so each
+// byte crosses NVLink exactly once and no remote writes need ordering. A small
+// system-scope flag barrier separates producer and consumer phases.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace isp {
+
+namespace {
+
+__device__ __forceinline__ uint4 ld_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// dst[q*shard + i] = src_q[i]; 16-byte vectors, 4 in flight per thread.
+__global__ void allgather_pull_kernel(PeerPtrs src, int world, int64_t shard_vec, uint4* dst) {
+  const int64_t total = shard_vec * world;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  for (; i + 3 * stride < total; i += 4 * stride) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t j = i + u * stride;
+      const int q = static_cast<int>(j / shard_vec);
+      v[u] = ld_v4(static_cast<const uint4*>(src.p[q]) + (j - q * shard_vec));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dst[i + u * stride] = v[u];
+  }
+  for (; i < total; i += stride) {
+    const int q = static_cast<int>(i / shard_vec);
+    dst[i] = ld_v4(static_cast<const uint4*>(src.p[q]) + (i - q * shard_vec));
+  }
+}
+
+// gate|up gathered into one [2*rows, cols] buffer interleaved in 64-row blocks.
+__global__ void allgather_interleave_kernel(PeerPtrs sg, PeerPtrs su, int world, int64_t rows,
+                                            int64_t cols, uint4* dst) {
+  const int64_t cvec = cols / 8;
+  const int64_t total = 2 * rows * cvec;
+  const int64_t rows_per_rank = rows / world;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t drow = i / cvec, c = i % cvec;
+    const int64_t blk = drow / 64, within = drow % 64;
+    const bool up = blk & 1;
+    const int64_t srow = (blk >> 1) * 64 + within;
+    const int q = static_cast<int>(srow / rows_per_rank);
+    const int64_t off = (srow - q * rows_per_rank) * cvec + c;
+    const uint4* s = static_cast<const uint4*>(up ? su.p[q] : sg.p[q]);
+    dst[i] = ld_v4(s + off);
+  }
+}
+
+__device__ __forceinline__ void add8(float (&acc)[8], const uint4& v) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 f = unpack_bf16(w[e]);
+    acc[2 * e] += f.x;
+    acc[2 * e + 1] += f.y;
+  }
+}
+
+// out[i] (+)= scale * sum_q part_q[base + i]; 8 elements per thread, fixed rank order.
+template <bool F32>
+__global__ void reduce_scatter_kernel(PeerPtrs part, int world, int64_t base, int64_t n8,
+                                      float scale, int accumulate, float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int q = 0; q < world; ++q) {
+      if constexpr (F32) {
+        const float* p = static_cast<const float*>(part.p[q]) + base + i * 8;
+        const uint4 a = ld_v4(p), b = ld_v4(p + 4);
+        acc[0] += __uint_as_float(a.x); acc[1] += __uint_as_float(a.y);
+        acc[2] += __uint_as_float(a.z); acc[3] += __uint_as_float(a.w);
+        acc[4] += __uint_as_float(b.x); acc[5] += __uint_as_float(b.y);
+        acc[6] += __uint_as_float(b.z); acc[7] += __uint_as_float(b.w);
+      } else {
+        add8(acc, ld_v4(static_cast<const __nv_bfloat16*>(part.p[q]) + base + i * 8));
+      }
+    }
+    float4* o = reinterpret_cast<float4*>(out + i * 8);
+    float4 r0 = make_float4(acc[0] * scale, acc[1] * scale, acc[2] * scale, acc[3] * scale);
+    float4 r1 = make_float4(acc[4] * scale, acc[5] * scale, acc[6] * scale, acc[7] * scale);
+    if (accumulate) {
+      const float4 p0 = o[0], p1 = o[1];
+      r0.x += p0.x; r0.y += p0.y; r0.z += p0.z; r0.w += p0.w;
+      r1.x += p1.x; r1.y += p1.y; r1.z += p1.z; r1.w += p1.w;
+    }
+    o[0] = r0;
+    o[1] = r1;
+  }
+}
+
+// gate/up shards of rank `rank` from interleaved bf16 partials [2*rows, cols].
+__global__ void reduce_scatter_interleave_kernel(PeerPtrs part, int world, int rank, int64_t rows,
+                                                 int64_t cols, float scale, int accumulate,
+                                                 float* __restrict__ og, float* __restrict__ ou) {
+  const int64_t rpr = rows / world;
+  const int64_t c8 = cols / 8;
+  const int64_t total = 2 * rpr * c8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const bool up = i >= rpr * c8;
+    const int64_t li = up ? i - rpr * c8 : i;
+    const int64_t lrow = li / c8, c = li % c8;
+    const int64_t srow = rank * rpr + lrow;
+    const int64_t irow = (srow / 64) * 128 + (up ? 64 : 0) + srow % 64;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int q = 0; q < world; ++q)
+      add8(acc, ld_v4(static_cast<const __nv_bfloat16*>(part.p[q]) + irow * cols + c * 8));
+    float* dst = (up ? ou : og) + lrow * cols + c * 8;
+    float4* o = reinterpret_cast<float4*>(dst);
+    float4 r0 = make_float4(acc[0] * scale, acc[1] * scale, acc[2] * scale, acc[3] * scale);
+    float4 r1 = make_float4(acc[4] * scale, acc[5] * scale, acc[6] * scale, acc[7] * scale);
+    if (accumulate) {
+      const float4 p0 = o[0], p1 = o[1];
+      r0.x += p0.x; r0.y += p0.y; r0.z += p0.z; r0.w += p0.w;
+      r1.x += p1.x; r1.y += p1.y; r1.z += p1.z; r1.w += p1.w;
+    }
+    o[0] = r0;
+    o[1] = r1;
+  }
+}
+
+__device__ __forceinline__ void rotate8(uint4& lo, uint4& hi, const float* c, const float* s,
+                                        float sign) {
+  uint32_t* a = reinterpret_cast<uint32_t*>(&lo);
+  uint32_t* b = reinterpret_cast<uint32_t*>(&hi);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 x = unpack_bf16(a[e]), y = unpack_bf16(b[e]);
+    const float c0 = c[2 * e], c1 = c[2 * e + 1];
+    const float s0 = sign * s[2 * e], s1 = sign * s[2 * e + 1];
+    a[e] = pack_bf16(x.x * c0 - y.x * s0, x.y * c1 - y.y * s1);
+    b[e] = pack_bf16(y.x * c0 + x.x * s0, y.y * c1 + x.y * s1);
+  }
+}
+
+// Token-sharded [T, parts*H] on every rank -> head-sharded [S, parts*Hl] on this rank.
+// Work unit: (global token s, part, local head, 8-element group j of the low half);
+// optional RoPE on parts < rope_parts at global position s.
+__global__ void a2a_to_heads_kernel(PeerPtrs src, int world, int rank, int T, int H, int parts,
+                                    int d, __nv_bfloat16* __restrict__ dst,
+                                    const float* __restrict__ cos_t,
+                                    const float* __restrict__ sin_t, int rope_parts) {
+  const int Hl = H / world, heads_l = Hl / d, half = d / 2, g8 = half / 8;
+  const int64_t S = static_cast<int64_t>(T) * world;
+  const int64_t per_row = static_cast<int64_t>(parts) * heads_l * g8;
+  const int64_t total = S * per_row;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = i / per_row;
+    int rem = static_cast<int>(i % per_row);
+    const int part = rem / (heads_l * g8);
+    rem %= heads_l * g8;
+    const int hl = rem / g8, j = (rem % g8) * 8;
+    const int q = static_cast<int>(s / T);
+    const int64_t t = s % T;
+    const __nv_bfloat16* sp = static_cast<const __nv_bfloat16*>(src.p[q]) + t * parts * H +
+                              part * H + rank * Hl + hl * d + j;
+    __nv_bfloat16* dp = dst + s * parts * Hl + part * Hl + hl * d + j;
+    uint4 lo = ld_v4(sp), hi = ld_v4(sp + half);
+    if (part < rope_parts) rotate8(lo, hi, cos_t + s * half + j, sin_t + s * half + j, 1.f);
+    *reinterpret_cast<uint4*>(dp) = lo;
+    *reinterpret_cast<uint4*>(dp + half) = hi;
+  }
+}
+
+// Head-sharded [S, parts*Hl] on every rank -> token-sharded [T, parts*H] on this rank.
+__global__ void a2a_to_tokens_kernel(PeerPtrs src, int world, int rank, int T, int H, int parts,
+                                     int d, __nv_bfloat16* __restrict__ dst,
+                                     const float* __restrict__ cos_t,
+                                     const float* __restrict__ sin_t, int rope_parts) {
+  const int Hl = H / world, heads = H / d, half = d / 2, g8 = half / 8;
+  const int64_t per_row = static_cast<int64_t>(parts) * heads * g8;
+  const int64_t total = static_cast<int64_t>(T) * per_row;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = i / per_row;
+    int rem = static_cast<int>(i % per_row);
+    const int part = rem / (heads * g8);
+    rem %= heads * g8;
+    const int hg = rem / g8, j = (rem % g8) * 8;  // hg = global head
+    const int q = (hg * d) / Hl;                  // owner rank of that head
+    const int hl = hg - q * (Hl / d);
+    const int64_t s = static_cast<int64_t>(rank) * T + t;  // global position
+    const __nv_bfloat16* sp = static_cast<const __nv_bfloat16*>(src.p[q]) + s * parts * Hl +
+                              part * Hl + hl * d + j;
+    __nv_bfloat16* dp = dst + t * parts * H + part * H + hg * d + j;
+    uint4 lo = ld_v4(sp), hi = ld_v4(sp + half);
+    if (part < rope_parts) rotate8(lo, hi, cos_t + s * half + j, sin_t + s * half + j, -1.f);
+    *reinterpret_cast<uint4*>(dp) = lo;
+    *reinterpret_cast<uint4*>(dp + half) = hi;
+  }
+}
+
+__global__ void peer_barrier_kernel(PeerPtrs flags, int world, int rank, uint32_t epoch,
+                                    uint32_t* error_flag) {
+  const int q = threadIdx.x;
+  if (q >= world) return;
+  __threadfence_system();
+  // publish: flags_q[rank] = epoch on every peer (including self)
+  st_release_sys(static_cast<uint32_t*>(flags.p[q]) + rank, epoch);
+  // wait: own flags[q] >= epoch
+  const uint32_t* mine = static_cast<const uint32_t*>(flags.p[rank]) + q;
+  const long long start = clock64();
+  const long long limit = 40000000000LL;  // ~20 s at 2 GHz
+  while (static_cast<int32_t>(ld_acquire_sys(mine) - epoch) < 0) {
+    if (clock64() - start > limit) {
+      atomicExch(error_flag, 1u);
+      break;
+    }
+    __nanosleep(64);
+  }
+  __threadfence_system();
+}
+
+int ctas(int64_t work, int threads, int cap) {
+  const int64_t b = (work + threads - 1) / threads;
+  return static_cast<int>(b < cap ? (b > 0 ? b : 1) : cap);
+}
+
+}  // namespace
+
+cudaError_t allgather_pull(const PeerPtrs& src, int world, int64_t shard_elems, __nv_bfloat16* dst,
+                           cudaStream_t st, int num_sms, int num_ctas) {
+  (void)num_sms;
+  if (shard_elems % 8) return cudaErrorInvalidValue;
+  const int64_t sv = shard_elems / 8;
+  allgather_pull_kernel<<<ctas(sv * world, 256, num_ctas), 256, 0, st>>>(src, world, sv,
+                                                                        reinterpret_cast<uint4*>(dst));
+  return cudaGetLastError();
+}
+
+cudaError_t allgather_pull_interleave(const PeerPtrs& sg, const PeerPtrs& su, int world,
+                                      int64_t rows, int64_t cols, __nv_bfloat16* dst,
+                                      cudaStream_t st, int num_ctas) {
+  if (cols % 8 || rows % 64 || rows % world) return cudaErrorInvalidValue;
+  allgather_interleave_kernel<<<ctas(2 * rows * cols / 8, 256, num_ctas), 256, 0, st>>>(
+      sg, su, world, rows, cols, reinterpret_cast<uint4*>(dst));
+  return cudaGetLastError();
+}
+
+cudaError_t reduce_scatter_pull(const PeerPtrs& part, int world, int rank, int64_t shard_elems,
+                                bool part_is_f32, float scale, int accumulate, float* out,
+                                cudaStream_t st, int num_ctas) {
+  if (shard_elems % 8) return cudaErrorInvalidValue;
+  const int64_t n8 = shard_elems / 8;
+  const int64_t base = static_cast<int64_t>(rank) * shard_elems;
+  if (part_is_f32)
+    reduce_scatter_kernel<true><<<ctas(n8, 256, num_ctas), 256, 0, st>>>(part, world, base, n8, scale,
+                                                                       accumulate, out);
+  else
+    reduce_scatter_kernel<false><<<ctas(n8, 256, num_ctas), 256, 0, st>>>(part, world, base, n8, scale,
+                                                                        accumulate, out);
+  return cudaGetLastError();
+}
+
+cudaError_t reduce_scatter_pull_interleave(const PeerPtrs& part, int world, int rank, int64_t rows,
+                                           int64_t cols, float scale, int accumulate,
+                                           float* out_gate, float* out_up, cudaStream_t st,
+                                           int num_ctas) {
+  if (cols % 8 || rows % world || rows % 64) return cudaErrorInvalidValue;
+  reduce_scatter_interleave_kernel<<<ctas(2 * rows / world * cols / 8, 256, num_ctas), 256, 0, st>>>(
+      part, world, rank, rows, cols, scale, accumulate, out_gate, out_up);
+  return cudaGetLastError();
+}
+
+cudaError_t a2a_tokens_to_heads(const PeerPtrs& src, int world, int rank, int T, int H, int parts,
+                                __nv_bfloat16* dst, const float* cos_t, const float* sin_t, int d,
+                                int rope_parts, cudaStream_t st, int num_ctas) {
+  if ((H / world) % d || d % 16) return cudaErrorInvalidValue;
+  const int64_t work = static_cast<int64_t>(T) * world * parts * (H / world / d) * (d / 16);
+  a2a_to_heads_kernel<<<ctas(work, 256, num_ctas), 256, 0, st>>>(src, world, rank, T, H, parts, d,
+                                                                  dst, cos_t, sin_t, rope_parts);
+  return cudaGetLastError();
+}
+
+cudaError_t a2a_heads_to_tokens(const PeerPtrs& src, int world, int rank, int T, int H, int parts,
+                                __nv_bfloat16* dst, const float* cos_t, const float* sin_t, int d,
+                                int rope_parts, cudaStream_t st, int num_ctas) {
+  if ((H / world) % d || d % 16) return cudaErrorInvalidValue;
+  const int64_t work = static_cast<int64_t>(T) * parts * (H / d) * (d / 16);
+  a2a_to_tokens_kernel<<<ctas(work, 256, num_ctas), 256, 0, st>>>(src, world, rank, T, H, parts, d,
+                                                                   dst, cos_t, sin_t, rope_parts);
+  return cudaGetLastError();
+}
+
+cudaError_t peer_barrier(const PeerPtrs& flags, int world, int rank, uint32_t epoch,
+                         uint32_t* error_flag, cudaStream_t st) {
+  peer_barrier_kernel<<<1, 32, 0, st>>>(flags, world, rank, epoch, error_flag);
+  return cudaGetLastError();
+}
+
+}  // namespace isp

@@ -1,0 +1,1030 @@
+// The ISP block executor behind the C ABI (include/seqplan_isp.h).
+//
+// One context per rank. The block's forward and backward are written as a short
+// list of phases separated by the exchange points of the ISP plan:
+//
+//   fwd  F1  norm1 -> QKV GEMM (-> RoPE at p = 1)               | AG(W) on the comm stream
+//        --- barrier ---  A2A qkv tokens->heads (+RoPE)
+//        F2  causal attention on D/p heads
+//        --- barrier ---  A2A o heads->tokens
+//        F3  O GEMM(+x) -> norm2 -> gate|up GEMM(+SwiGLU) -> down GEMM(+h)
+//   bwd  B1  down dgrad/wgrad -> SwiGLU bwd -> gate|up dgrad/wgrad -> norm2 bwd
+//            -> O dgrad/wgrad                                  | re-AG(W), RS(dW) on comm
+//        --- barrier ---  A2A dO tokens->heads
+//        B2  attention backward
+//        --- barrier ---  A2A dq|dk|dv heads->tokens (+inverse RoPE)
+//        B3  QKV dgrad/wgrad -> norm1 bwd
+//        --- barrier ---  RS of every weight gradient (fused bf16->fp32 cast/scale)
+//
+// Multi-process mode (one process per GPU): phases run on the caller's stream,
+// gathers and reduce-scatters on an internal comm stream fenced by events; the
+// forward prefetches every weight of the block up front (inter-layer prefetch,
+// overlap_sim.hpp:95-102) and the backward runs G-W before G-X so each RS overlaps
+// the remaining compute (selective overlap, overlap_sim.hpp:141-150).
+// Group mode (p contexts on one GPU, tests): the same phases run in lock-step on
+// one stream with the collectives inline, which needs no cross-rank spinning.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "../../include/seqplan_isp.h"
+#include "device_pool.h"
+#include "gemm.h"
+#include "kernels.h"
+#include "seqplan/mempool.hpp"
+#include "seqplan/strategy.hpp"
+
+using bf16 = __nv_bfloat16;
+
+namespace isp {
+namespace {
+
+constexpr int kCommCtas = 32;     // SMs lent to a gather / reduce-scatter
+constexpr int kA2ACtas = 148 * 4;  // the all-to-all is on the critical path: use the chip
+constexpr size_t kFlagBytes = 4096;
+
+struct Status {
+  int code = SEQPLAN_ISP_OK;
+  std::string msg;
+};
+
+#define ISP_CUDA(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess) {                                                             \
+      throw IspError(SEQPLAN_ISP_ERR_RUNTIME,                                            \
+                     std::string(#expr) + ": " + cudaGetErrorString(_e));                \
+    }                                                                                    \
+  } while (0)
+
+struct IspError {
+  int code;
+  std::string msg;
+  IspError(int c, std::string m) : code(c), msg(std::move(m)) {}
+};
+
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+}  // namespace isp
+
+using namespace isp;
+
+struct seqplan_isp_ctx {
+  // ---- configuration ----
+  int world = 1, rank = 0, device = 0, num_sms = 148;
+  bool group_mode = false;
+  uint32_t flags = 0;
+  int64_t H = 0, D = 0, S = 0, I = 0, d = 0, T = 0, Hl = 0, Dl = 0;
+  float eps = 1e-5f;
+  double rope_base = 10000.0;
+  std::string last_error;
+
+  // ---- symmetric heap (exchange buffers; identical offsets on every rank) ----
+  char* heap = nullptr;
+  size_t heap_bytes = 0;
+  void* peer_heap[kMaxRanks] = {};
+  bool peer_opened[kMaxRanks] = {};
+  size_t off_flags = 0, off_wshard[SEQPLAN_W_COUNT] = {}, off_qkv_tok = 0, off_o_heads = 0,
+         off_do_tok = 0, off_dqkv_heads = 0, off_part[SEQPLAN_W_COUNT] = {};
+  uint32_t epoch_compute = 0, epoch_comm = 0;
+  uint32_t* error_flag = nullptr;  // device, in the heap flags page
+
+  // ---- device pool (subsystem 5) and persistent buffers ----
+  DevicePool pool;
+  float* master[SEQPLAN_W_COUNT] = {};
+  float* grad[SEQPLAN_W_COUNT] = {};
+  bf16* wgu_local = nullptr;  // p = 1: interleaved gate|up working copy
+  float* cos_t = nullptr;
+  float* sin_t = nullptr;
+  // saved activations
+  bf16 *n1 = nullptr, *qkv_heads = nullptr, *o_tok = nullptr, *h = nullptr, *n2 = nullptr;
+  float *rstd1 = nullptr, *rstd2 = nullptr, *lse = nullptr;
+  bf16 *gu = nullptr, *a = nullptr;  // transient: fwd -> bwd
+  // backward scratch
+  bf16 *dh = nullptr, *dn = nullptr, *dO_heads = nullptr, *dqkv_tok = nullptr;
+  float *delta = nullptr, *dq_acc = nullptr;
+  bf16* local_part[SEQPLAN_W_COUNT] = {};  // p = 1 not used
+
+  // ---- streams / events ----
+  cudaStream_t comm = nullptr;
+  cudaEvent_t ev_gathered[SEQPLAN_W_COUNT] = {};
+  cudaEvent_t ev_wgrad[SEQPLAN_W_COUNT] = {};
+  cudaEvent_t ev_comm_done = nullptr, ev_start = nullptr;
+  bool weights_dirty = true;
+  bool fwd_done = false;
+  const void* last_x = nullptr;
+
+  // gathered weights of the current pass (pool CommBuffer allocations)
+  bf16* gathered[SEQPLAN_W_COUNT] = {};
+
+  // timeline
+  struct TEv {
+    int stream, kind;
+    int64_t layer;
+    cudaEvent_t b, e;
+  };
+  std::vector<TEv> tl_pending;
+  std::vector<seqplan_timeline_event> timeline;
+
+  // ---- helpers ----
+  template <typename T>
+  T* hp(size_t off) { return reinterpret_cast<T*>(heap + off); }
+  template <typename T>
+  T* peer(int q, size_t off) { return reinterpret_cast<T*>(static_cast<char*>(peer_heap[q]) + off); }
+  PeerPtrs peers_at(size_t off) {
+    PeerPtrs p{};
+    for (int q = 0; q < world; ++q) p.p[q] = static_cast<char*>(peer_heap[q]) + off;
+    return p;
+  }
+  int64_t numel(int t) const {
+    switch (t) {
+      case SEQPLAN_W_NORM1: case SEQPLAN_W_NORM2: return H;
+      case SEQPLAN_W_QKV: return 3 * H * H;
+      case SEQPLAN_W_O: return H * H;
+      default: return I * H;
+    }
+  }
+  int64_t shard(int t) const { return numel(t) / world; }
+  bf16* wshard(int t) { return hp<bf16>(off_wshard[t]); }
+};
+
+namespace {
+
+using Ctx = seqplan_isp_ctx;
+
+void* pool_alloc(Ctx* c, int64_t bytes, seqplan::AllocTag tag, cudaStream_t st) {
+  void* p = c->pool.alloc(bytes, tag, st);
+  if (!p) throw IspError(SEQPLAN_ISP_ERR_OOM, "device pool: " + c->pool.error());
+  return p;
+}
+
+void gemm(const GemmOperand& A, const GemmOperand& B, const GemmArgs& args, int epi, cudaStream_t st) {
+  cudaError_t e = gemm_launch(A, B, args, epi, st);
+  if (e == cudaErrorInvalidValue)
+    throw IspError(SEQPLAN_ISP_ERR_UNSUPPORTED, "GEMM shape not tiled by the sm_100a kernel (M%128, N%128, K%64)");
+  ISP_CUDA(e);
+}
+
+// ---- timeline -------------------------------------------------------------------
+struct Span {
+  Ctx* c;
+  cudaStream_t st;
+  int stream_kind, kind;
+  int64_t layer;
+  cudaEvent_t b = nullptr;
+  Span(Ctx* cc, cudaStream_t s, int sk, int k, int64_t l) : c(cc), st(s), stream_kind(sk), kind(k), layer(l) {
+    if (c->flags & SEQPLAN_ISP_FLAG_TIMELINE) {
+      cudaEventCreate(&b);
+      cudaEventRecord(b, st);
+    }
+  }
+  ~Span() {
+    if (!b) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    c->tl_pending.push_back({stream_kind, kind, layer, b, e});
+  }
+};
+
+// ---- collectives (dispatch on mode) -----------------------------------------------
+void barrier(Ctx* c, cudaStream_t st, bool comm_lane) {
+  if (c->world == 1 || c->group_mode) return;
+  uint32_t& ep = comm_lane ? c->epoch_comm : c->epoch_compute;
+  ++ep;
+  const size_t off = c->off_flags + (comm_lane ? 64 * sizeof(uint32_t) : 0);
+  ISP_CUDA(peer_barrier(c->peers_at(off), c->world, c->rank, ep, c->error_flag, st));
+}
+
+// Gather tensor t into a pool CommBuffer (or return the local working copy at p = 1).
+void gather_weight(Ctx* c, int t, cudaStream_t st) {
+  if (c->world == 1) {
+    c->gathered[t] = (t == SEQPLAN_W_GATE) ? c->wgu_local : c->wshard(t);
+    return;
+  }
+  Span sp(c, st, 1, SEQPLAN_EV_ALL_GATHER, t);
+  if (t == SEQPLAN_W_GATE) {  // gate|up gathered together, interleaved
+    const int64_t bytes = 2 * c->I * c->H * 2;
+    bf16* dst = static_cast<bf16*>(pool_alloc(c, bytes, seqplan::AllocTag::CommBuffer, st));
+    ISP_CUDA(allgather_pull_interleave(c->peers_at(c->off_wshard[SEQPLAN_W_GATE]),
+                                       c->peers_at(c->off_wshard[SEQPLAN_W_UP]), c->world, c->I, c->H,
+                                       dst, st, kCommCtas));
+    c->gathered[t] = dst;
+  } else {
+    const int64_t bytes = c->numel(t) * 2;
+    bf16* dst = static_cast<bf16*>(pool_alloc(c, bytes, seqplan::AllocTag::CommBuffer, st));
+    ISP_CUDA(allgather_pull(c->peers_at(c->off_wshard[t]), c->world, c->shard(t), dst, st, c->num_sms,
+                            kCommCtas));
+    c->gathered[t] = dst;
+  }
+}
+
+void release_weight(Ctx* c, int t, cudaStream_t st) {
+  if (c->world > 1 && c->gathered[t]) c->pool.free(c->gathered[t], st);
+  c->gathered[t] = nullptr;
+}
+
+// Reduce-scatter the weight gradient partial of tensor t into the fp32 grad shard.
+void reduce_scatter_grad(Ctx* c, int t, cudaStream_t st) {
+  Span sp(c, st, 1, SEQPLAN_EV_REDUCE_SCATTER, t);
+  if (t == SEQPLAN_W_GATE) {
+    ISP_CUDA(reduce_scatter_pull_interleave(c->peers_at(c->off_part[SEQPLAN_W_GATE]), c->world, c->rank,
+                                            c->I, c->H, 1.0f, 0, c->grad[SEQPLAN_W_GATE],
+                                            c->grad[SEQPLAN_W_UP], st, kCommCtas));
+  } else {
+    const bool f32 = (t == SEQPLAN_W_NORM1 || t == SEQPLAN_W_NORM2);
+    ISP_CUDA(reduce_scatter_pull(c->peers_at(c->off_part[t]), c->world, c->rank, c->shard(t), f32, 1.0f,
+                                 0, c->grad[t], st, kCommCtas));
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// forward phases
+// ---------------------------------------------------------------------------------
+bf16* qkv_tok_buf(Ctx* c) { return c->hp<bf16>(c->off_qkv_tok); }
+
+void fwd_issue_gathers(Ctx* c, cudaStream_t st) {
+  if (c->world == 1) {
+    for (int t : {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN})
+      gather_weight(c, t, st);
+    return;
+  }
+  cudaStream_t cs = c->group_mode ? st : c->comm;
+  if (!c->group_mode) {  // comm stream starts after the caller's prior work
+    ISP_CUDA(cudaEventRecord(c->ev_start, st));
+    ISP_CUDA(cudaStreamWaitEvent(cs, c->ev_start, 0));
+  }
+  for (int t : {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN}) {
+    gather_weight(c, t, cs);
+    if (!c->group_mode) ISP_CUDA(cudaEventRecord(c->ev_gathered[t], cs));
+  }
+}
+
+void wait_gathered(Ctx* c, int t, cudaStream_t st) {
+  if (c->world > 1 && !c->group_mode) ISP_CUDA(cudaStreamWaitEvent(st, c->ev_gathered[t], 0));
+}
+
+void fwd_phase1(Ctx* c, const bf16* x, cudaStream_t st) {
+  Span sp(c, st, 0, SEQPLAN_EV_FORWARD, 0);
+  const int T = static_cast<int>(c->T), H = static_cast<int>(c->H);
+  wait_gathered(c, SEQPLAN_W_NORM1, st);
+  ISP_CUDA(rmsnorm_fwd(x, c->gathered[SEQPLAN_W_NORM1], c->n1, c->rstd1, T, H, c->eps, st, c->num_sms));
+  wait_gathered(c, SEQPLAN_W_QKV, st);
+  GemmArgs g;
+  g.M = T; g.N = 3 * H; g.K = H;
+  g.out = c->world == 1 ? static_cast<void*>(c->qkv_heads) : static_cast<void*>(qkv_tok_buf(c));
+  g.ldo = 3 * H;
+  gemm({c->n1, H, false}, {c->gathered[SEQPLAN_W_QKV], H, false}, g, EPI_BF16, st);
+  if (c->world == 1)
+    ISP_CUDA(rope_inplace(c->qkv_heads, 3 * H, T, 0, static_cast<int>(c->D), static_cast<int>(c->d), c->cos_t,
+                          c->sin_t, H, +1, st, c->num_sms));
+}
+
+AttnTensors attn_tensors(Ctx* c) {
+  AttnTensors t{};
+  const int64_t ldq = 3 * c->Hl;
+  t.q = c->qkv_heads;
+  t.k = c->qkv_heads + c->Hl;
+  t.v = c->qkv_heads + 2 * c->Hl;
+  t.ld_qkv = ldq;
+  t.o = c->world == 1 ? c->o_tok : c->hp<bf16>(c->off_o_heads);
+  t.ld_o = c->Hl;
+  t.lse = c->lse;
+  t.S = static_cast<int>(c->S);
+  t.heads = static_cast<int>(c->Dl);
+  t.d = static_cast<int>(c->d);
+  return t;
+}
+
+void fwd_phase2(Ctx* c, cudaStream_t st) {
+  if (c->world > 1) {
+    Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 0);
+    ISP_CUDA(a2a_tokens_to_heads(c->peers_at(c->off_qkv_tok), c->world, c->rank, static_cast<int>(c->T),
+                                 static_cast<int>(c->H), 3, c->qkv_heads, c->cos_t, c->sin_t,
+                                 static_cast<int>(c->d), 2, st, kA2ACtas));
+  }
+  Span sp(c, st, 0, SEQPLAN_EV_FORWARD, 1);
+  ISP_CUDA(attention_fwd(attn_tensors(c), st, c->num_sms));
+}
+
+void fwd_phase3(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
+  const int T = static_cast<int>(c->T), H = static_cast<int>(c->H), I = static_cast<int>(c->I);
+  if (c->world > 1) {
+    Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 1);
+    ISP_CUDA(a2a_heads_to_tokens(c->peers_at(c->off_o_heads), c->world, c->rank, T, H, 1, c->o_tok, c->cos_t,
+                                 c->sin_t, static_cast<int>(c->d), 0, st, kA2ACtas));
+  }
+  Span sp(c, st, 0, SEQPLAN_EV_FORWARD, 2);
+  wait_gathered(c, SEQPLAN_W_O, st);
+  {
+    GemmArgs g;
+    g.M = T; g.N = H; g.K = H;
+    g.out = c->h; g.ldo = H;
+    g.resid = x; g.ldr = H;
+    gemm({c->o_tok, H, false}, {c->gathered[SEQPLAN_W_O], H, false}, g, EPI_BF16_RESID, st);
+  }
+  release_weight(c, SEQPLAN_W_O, st);
+  wait_gathered(c, SEQPLAN_W_NORM2, st);
+  ISP_CUDA(rmsnorm_fwd(c->h, c->gathered[SEQPLAN_W_NORM2], c->n2, c->rstd2, T, H, c->eps, st, c->num_sms));
+  c->gu = static_cast<bf16*>(pool_alloc(c, int64_t(T) * 2 * I * 2, seqplan::AllocTag::MlpIntermediate, st));
+  c->a = static_cast<bf16*>(pool_alloc(c, int64_t(T) * I * 2, seqplan::AllocTag::MlpIntermediate, st));
+  wait_gathered(c, SEQPLAN_W_GATE, st);
+  {
+    GemmArgs g;
+    g.M = T; g.N = 2 * I; g.K = H;
+    g.out = c->gu; g.ldo = 2 * I;
+    g.out2 = c->a; g.ldo2 = I;
+    gemm({c->n2, H, false}, {c->gathered[SEQPLAN_W_GATE], H, false}, g, EPI_SWIGLU, st);
+  }
+  release_weight(c, SEQPLAN_W_GATE, st);
+  wait_gathered(c, SEQPLAN_W_DOWN, st);
+  {
+    GemmArgs g;
+    g.M = T; g.N = H; g.K = I;
+    g.out = y; g.ldo = H;
+    g.resid = c->h; g.ldr = H;
+    gemm({c->a, I, false}, {c->gathered[SEQPLAN_W_DOWN], I, false}, g, EPI_BF16_RESID, st);
+  }
+  release_weight(c, SEQPLAN_W_DOWN, st);
+  release_weight(c, SEQPLAN_W_QKV, st);
+  release_weight(c, SEQPLAN_W_NORM1, st);
+  release_weight(c, SEQPLAN_W_NORM2, st);
+}
+
+// ---------------------------------------------------------------------------------
+// backward phases
+// ---------------------------------------------------------------------------------
+void bwd_issue_gathers(Ctx* c, cudaStream_t st) {
+  const int order[] = {SEQPLAN_W_DOWN, SEQPLAN_W_GATE, SEQPLAN_W_NORM2, SEQPLAN_W_O, SEQPLAN_W_QKV, SEQPLAN_W_NORM1};
+  if (c->world == 1) {
+    for (int t : order) gather_weight(c, t, st);
+    return;
+  }
+  cudaStream_t cs = c->group_mode ? st : c->comm;
+  if (!c->group_mode) {
+    ISP_CUDA(cudaEventRecord(c->ev_start, st));
+    ISP_CUDA(cudaStreamWaitEvent(cs, c->ev_start, 0));
+  }
+  for (int t : order) {
+    gather_weight(c, t, cs);
+    if (!c->group_mode) ISP_CUDA(cudaEventRecord(c->ev_gathered[t], cs));
+  }
+}
+
+// Weight-gradient destination: fp32 grad shard directly at p = 1, bf16 partial in the heap otherwise.
+void wgrad(Ctx* c, int t, const GemmOperand& A, const GemmOperand& B, int M, int N, int K, cudaStream_t st) {
+  GemmArgs g;
+  g.M = M; g.N = N; g.K = K;
+  if (c->world == 1) {
+    g.out = c->grad[t];
+    g.ldo = N;
+    if (t == SEQPLAN_W_GATE) {
+      g.interleave64 = 1;
+      g.out_b = c->grad[SEQPLAN_W_UP];
+    }
+    gemm(A, B, g, EPI_F32, st);
+  } else {
+    g.out = c->hp<bf16>(c->off_part[t]);
+    g.ldo = N;
+    gemm(A, B, g, EPI_BF16, st);
+  }
+}
+
+// After the G-W of tensor t: hand its partial to the comm stream for the reduce-scatter.
+void schedule_rs(Ctx* c, int t, cudaStream_t st) {
+  if (c->world == 1 || c->group_mode) return;
+  ISP_CUDA(cudaEventRecord(c->ev_wgrad[t], st));
+  ISP_CUDA(cudaStreamWaitEvent(c->comm, c->ev_wgrad[t], 0));
+  barrier(c, c->comm, true);
+  reduce_scatter_grad(c, t, c->comm);
+}
+
+void bwd_phase1(Ctx* c, const bf16* dy, cudaStream_t st) {
+  const int T = static_cast<int>(c->T), H = static_cast<int>(c->H), I = static_cast<int>(c->I);
+  const bool selective = !(c->flags & SEQPLAN_ISP_FLAG_FUSED_BWD);
+  // ---- down projection: G-W first (its RS overlaps the rest), then G-X ----
+  wait_gathered(c, SEQPLAN_W_DOWN, st);
+  bf16* da = static_cast<bf16*>(pool_alloc(c, int64_t(T) * I * 2, seqplan::AllocTag::MlpIntermediate, st));
+  {
+    Span sp(c, st, 0, SEQPLAN_EV_GRAD_WEIGHT, 3);
+    wgrad(c, SEQPLAN_W_DOWN, {dy, H, true}, {c->a, I, true}, H, I, T, st);
+  }
+  if (selective) schedule_rs(c, SEQPLAN_W_DOWN, st);
+  {
+    Span sp(c, st, 0, SEQPLAN_EV_GRAD_INPUT, 3);
+    GemmArgs g;
+    g.M = T; g.N = I; g.K = H;
+    g.out = da; g.ldo = I;
+    gemm({dy, H, false}, {c->gathered[SEQPLAN_W_DOWN], I, true}, g, EPI_BF16, st);
+  }
+  release_weight(c, SEQPLAN_W_DOWN, st);
+  c->pool.free(c->a, st);
+  c->a = nullptr;
+  // ---- SwiGLU backward ----
+  bf16* dgu = static_cast<bf16*>(pool_alloc(c, int64_t(T) * 2 * I * 2, seqplan::AllocTag::MlpIntermediate, st));
+  ISP_CUDA(swiglu_bwd(da, c->gu, dgu, T, I, st, c->num_sms));
+  c->pool.free(da, st);
+  c->pool.free(c->gu, st);
+  c->gu = nullptr;
+  // ---- gate|up ----
+  wait_gathered(c, SEQPLAN_W_GATE, st);
+  {
+    Span sp(c, st, 0, SEQPLAN_EV_GRAD_WEIGHT, 2);
+    wgrad(c, SEQPLAN_W_GATE, {dgu, 2 * I, true}, {c->n2, H, true}, 2 * I, H, T, st);
+  }
+  if (selective) schedule_rs(c, SEQPLAN_W_GATE, st);
+  {
+    Span sp(c, st, 0, SEQPLAN_EV_GRAD_INPUT, 2);
+    GemmArgs g;
+    g.M = T; g.N = H; g.K = 2 * I;
+    g.out = c->dn; g.ldo = H;
+    gemm({dgu, 2 * I, false}, {c->gathered[SEQPLAN_W_GATE], H, true}, g, EPI_BF16, st);
+  }
+  release_weight(c, SEQPLAN_W_GATE, st);
+  c->pool.free(dgu, st);
+  // ---- norm2 backward: dh = dy + d(norm2) ----
+  wait_gathered(c, SEQPLAN_W_NORM2, st);
+  float* dg2 = c->world == 1 ? c->grad[SEQPLAN_W_NORM2] : c->hp<float>(c->off_part[SEQPLAN_W_NORM2]);
+  ISP_CUDA(cudaMemsetAsync(dg2, 0, sizeof(float) * H, st));
+  ISP_CUDA(rmsnorm_bwd(c->h, c->gathered[SEQPLAN_W_NORM2], c->rstd2, c->dn, dy, c->dh, dg2, T, H, st, c->num_sms));
+  release_weight(c, SEQPLAN_W_NORM2, st);
+  if (selective) schedule_rs(c, SEQPLAN_W_NORM2, st);
+  // ---- output projection ----
+  wait_gathered(c, SEQPLAN_W_O, st);
+  {
+    Span sp(c, st, 0, SEQPLAN_EV_GRAD_WEIGHT, 1);
+    wgrad(c, SEQPLAN_W_O, {c->dh, H, true}, {c->o_tok, H, true}, H, H, T, st);
+  }
+  if (selective) schedule_rs(c, SEQPLAN_W_O, st);
+  {
+    Span sp(c, st, 0, SEQPLAN_EV_GRAD_INPUT, 1);
+    GemmArgs g;
+    g.M = T; g.N = H; g.K = H;
+    g.out = c->world == 1 ? c->dO_heads : c->hp<bf16>(c->off_do_tok);
+    g.ldo = H;
+    gemm({c->dh, H, false}, {c->gathered[SEQPLAN_W_O], H, true}, g, EPI_BF16, st);
+  }
+  release_weight(c, SEQPLAN_W_O, st);
+}
+
+void bwd_phase2(Ctx* c, cudaStream_t st) {
+  const int T = static_cast<int>(c->T), H = static_cast<int>(c->H);
+  if (c->world > 1) {
+    Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 2);
+    ISP_CUDA(a2a_tokens_to_heads(c->peers_at(c->off_do_tok), c->world, c->rank, T, H, 1, c->dO_heads, c->cos_t,
+                                 c->sin_t, static_cast<int>(c->d), 0, st, kA2ACtas));
+  }
+  Span sp(c, st, 0, SEQPLAN_EV_GRAD_INPUT, 0);
+  AttnTensors t = attn_tensors(c);
+  bf16* dqkv = c->world == 1 ? c->dqkv_tok : c->hp<bf16>(c->off_dqkv_heads);
+  const int64_t ld = 3 * c->Hl;
+  ISP_CUDA(attention_bwd(t, c->dO_heads, dqkv, dqkv + c->Hl, dqkv + 2 * c->Hl, ld, c->delta, c->dq_acc, st,
+                         c->num_sms));
+  if (c->world == 1)
+    ISP_CUDA(rope_inplace(c->dqkv_tok, 3 * H, T, 0, static_cast<int>(c->D), static_cast<int>(c->d), c->cos_t,
+                          c->sin_t, H, -1, st, c->num_sms));
+}
+
+void bwd_phase3(Ctx* c, const bf16* x, bf16* dx, cudaStream_t st) {
+  const int T = static_cast<int>(c->T), H = static_cast<int>(c->H);
+  const bool selective = !(c->flags & SEQPLAN_ISP_FLAG_FUSED_BWD);
+  if (c->world > 1) {
+    Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 3);
+    ISP_CUDA(a2a_heads_to_tokens(c->peers_at(c->off_dqkv_heads), c->world, c->rank, T, H, 3, c->dqkv_tok,
+                                 c->cos_t, c->sin_t, static_cast<int>(c->d), 2, st, kA2ACtas));
+  }
+  wait_gathered(c, SEQPLAN_W_QKV, st);
+  {
+    Span sp(c, st, 0, SEQPLAN_EV_GRAD_WEIGHT, 0);
+    wgrad(c, SEQPLAN_W_QKV, {c->dqkv_tok, 3 * H, true}, {c->n1, H, true}, 3 * H, H, T, st);
+  }
+  if (selective) schedule_rs(c, SEQPLAN_W_QKV, st);
+  {
+    Span sp(c, st, 0, SEQPLAN_EV_GRAD_INPUT, 0);
+    GemmArgs g;
+    g.M = T; g.N = H; g.K = 3 * H;
+    g.out = c->dn; g.ldo = H;
+    gemm({c->dqkv_tok, 3 * H, false}, {c->gathered[SEQPLAN_W_QKV], H, true}, g, EPI_BF16, st);
+  }
+  release_weight(c, SEQPLAN_W_QKV, st);
+  wait_gathered(c, SEQPLAN_W_NORM1, st);
+  float* dg1 = c->world == 1 ? c->grad[SEQPLAN_W_NORM1] : c->hp<float>(c->off_part[SEQPLAN_W_NORM1]);
+  ISP_CUDA(cudaMemsetAsync(dg1, 0, sizeof(float) * H, st));
+  ISP_CUDA(rmsnorm_bwd(x, c->gathered[SEQPLAN_W_NORM1], c->rstd1, c->dn, c->dh, dx, dg1, T, H, st, c->num_sms));
+  release_weight(c, SEQPLAN_W_NORM1, st);
+  if (selective) schedule_rs(c, SEQPLAN_W_NORM1, st);
+}
+
+// Fused backward (or group mode): every reduce-scatter after the last G-X.
+void bwd_reduce_all(Ctx* c, cudaStream_t st) {
+  if (c->world == 1) return;
+  for (int t : {SEQPLAN_W_DOWN, SEQPLAN_W_GATE, SEQPLAN_W_NORM2, SEQPLAN_W_O, SEQPLAN_W_QKV, SEQPLAN_W_NORM1})
+    reduce_scatter_grad(c, t, st);
+}
+
+// ---------------------------------------------------------------------------------
+// context setup
+// ---------------------------------------------------------------------------------
+void layout_heap(Ctx* c) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + bytes, 4096);
+    return o;
+  };
+  c->off_flags = take(kFlagBytes);
+  for (int t = 0; t < SEQPLAN_W_COUNT; ++t) c->off_wshard[t] = take(size_t(c->shard(t)) * 2);
+  if (c->world > 1) {
+    c->off_qkv_tok = take(size_t(c->T) * 3 * c->H * 2);
+    c->off_o_heads = take(size_t(c->S) * c->Hl * 2);
+    c->off_do_tok = take(size_t(c->T) * c->H * 2);
+    c->off_dqkv_heads = take(size_t(c->S) * 3 * c->Hl * 2);
+    for (int t : {SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_DOWN}) c->off_part[t] = take(size_t(c->numel(t)) * 2);
+    c->off_part[SEQPLAN_W_GATE] = take(size_t(2 * c->I * c->H) * 2);
+    c->off_part[SEQPLAN_W_NORM1] = take(size_t(c->H) * 4);
+    c->off_part[SEQPLAN_W_NORM2] = take(size_t(c->H) * 4);
+  }
+  c->heap_bytes = off;
+}
+
+void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy* policy) {
+  c->H = shape->hidden_dim;
+  c->D = shape->heads;
+  c->S = shape->seq_len;
+  c->I = shape->ffn_dim > 0 ? shape->ffn_dim : seqplan::mlp_intermediate_dim(c->H);
+  c->rope_base = shape->rope_base > 0 ? shape->rope_base : 10000.0;
+  c->eps = shape->norm_eps > 0 ? static_cast<float>(shape->norm_eps) : 1e-5f;
+  if (c->H <= 0 || c->D <= 0 || c->S <= 0 || c->H % c->D)
+    throw IspError(SEQPLAN_ISP_ERR_INVALID, "invalid model config: hidden_dim must be divisible by heads");
+  c->d = c->H / c->D;
+  if (c->world < 1 || c->world > kMaxRanks || c->D % c->world || c->S % c->world)
+    throw IspError(SEQPLAN_ISP_ERR_INVALID, "head count and sequence must be divisible by the ISP degree");
+  c->T = c->S / c->world;
+  c->Hl = c->H / c->world;
+  c->Dl = c->D / c->world;
+  if ((c->d != 64 && c->d != 128) || c->T % 128 || c->H % 256 || c->I % 256 || (c->I / c->world) % 64 ||
+      c->S % 128)
+    throw IspError(SEQPLAN_ISP_ERR_UNSUPPORTED,
+                   "shape not tiled by the sm_100a kernels (head dim 64/128, S/p % 128, H % 256, I % 256)");
+  ISP_CUDA(cudaSetDevice(c->device));
+  ISP_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+  seqplan::MempoolPolicy pol;
+  if (policy) {
+    pol.pinned_comm_pool = policy->pinned_comm_pool != 0;
+    pol.consolidate_every_k_mlp = policy->consolidate_every_k_mlp;
+    pol.grad_premap = policy->grad_premap != 0;
+    pol.capacity = policy->capacity;
+  } else {
+    pol.pinned_comm_pool = true;
+    pol.grad_premap = true;
+  }
+  c->pool.set_policy(pol);
+
+  layout_heap(c);
+  ISP_CUDA(cudaMalloc(&c->heap, c->heap_bytes));
+  ISP_CUDA(cudaMemset(c->heap, 0, kFlagBytes));
+  c->peer_heap[c->rank] = c->heap;
+  c->peer_opened[c->rank] = false;
+  c->error_flag = reinterpret_cast<uint32_t*>(c->heap + 1024);
+
+  // persistent buffers through the pool
+  const cudaStream_t s0 = nullptr;
+  int64_t grad_bytes = 0;
+  for (int t = 0; t < SEQPLAN_W_COUNT; ++t) grad_bytes += (c->shard(t) * 4 + 511) / 512 * 512;
+  if (!c->pool.premap_grads(grad_bytes)) throw IspError(SEQPLAN_ISP_ERR_OOM, "grad arena");
+  for (int t = 0; t < SEQPLAN_W_COUNT; ++t) {
+    c->master[t] = static_cast<float*>(pool_alloc(c, c->shard(t) * 4, seqplan::AllocTag::Other, s0));
+    c->grad[t] = static_cast<float*>(pool_alloc(c, c->shard(t) * 4, seqplan::AllocTag::Grad, s0));
+  }
+  if (c->world == 1)
+    c->wgu_local = static_cast<bf16*>(pool_alloc(c, 2 * c->I * c->H * 2, seqplan::AllocTag::Other, s0));
+  const int64_t T = c->T, H = c->H, S = c->S, Hl = c->Hl;
+  auto A = [&](int64_t bytes, seqplan::AllocTag tag = seqplan::AllocTag::Other) {
+    return pool_alloc(c, bytes, tag, s0);
+  };
+  c->cos_t = static_cast<float*>(A(S * (c->d / 2) * 4));
+  c->sin_t = static_cast<float*>(A(S * (c->d / 2) * 4));
+  c->n1 = static_cast<bf16*>(A(T * H * 2));
+  c->rstd1 = static_cast<float*>(A(T * 4));
+  c->qkv_heads = static_cast<bf16*>(A(S * 3 * Hl * 2));
+  c->o_tok = static_cast<bf16*>(A(T * H * 2));
+  c->h = static_cast<bf16*>(A(T * H * 2, seqplan::AllocTag::MlpOutput));
+  c->n2 = static_cast<bf16*>(A(T * H * 2));
+  c->rstd2 = static_cast<float*>(A(T * 4));
+  c->lse = static_cast<float*>(A(c->Dl * S * 4));
+  c->dh = static_cast<bf16*>(A(T * H * 2));
+  c->dn = static_cast<bf16*>(A(T * H * 2));
+  c->dO_heads = static_cast<bf16*>(A(S * Hl * 2));
+  c->dqkv_tok = static_cast<bf16*>(A(T * 3 * H * 2));
+  c->delta = static_cast<float*>(A(c->Dl * S * 4));
+  c->dq_acc = static_cast<float*>(A(c->Dl * S * c->d * 4));
+
+  ISP_CUDA(cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking));
+  for (int t = 0; t < SEQPLAN_W_COUNT; ++t) {
+    ISP_CUDA(cudaEventCreateWithFlags(&c->ev_gathered[t], cudaEventDisableTiming));
+    ISP_CUDA(cudaEventCreateWithFlags(&c->ev_wgrad[t], cudaEventDisableTiming));
+  }
+  ISP_CUDA(cudaEventCreateWithFlags(&c->ev_comm_done, cudaEventDisableTiming));
+  ISP_CUDA(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
+
+  // RoPE table, computed like oracle/block_oracle.c:ob_rope_table (double -> fp32)
+  {
+    const int64_t half = c->d / 2;
+    std::vector<float> cs(size_t(S * half)), sn(size_t(S * half));
+    for (int64_t i = 0; i < half; ++i) {
+      const double inv = std::pow(c->rope_base, -2.0 * double(i) / double(c->d));
+      for (int64_t t = 0; t < S; ++t) {
+        const double ang = double(t) * inv;
+        cs[size_t(t * half + i)] = static_cast<float>(std::cos(ang));
+        sn[size_t(t * half + i)] = static_cast<float>(std::sin(ang));
+      }
+    }
+    ISP_CUDA(cudaMemcpy(c->cos_t, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice));
+    ISP_CUDA(cudaMemcpy(c->sin_t, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice));
+  }
+  c->pool.step_boundary();
+}
+
+// Refresh the bf16 working shard(s) from the fp32 master of tensor t.
+void refresh_working(Ctx* c, int t, cudaStream_t st) {
+  ISP_CUDA(cast_f32_bf16(c->master[t], c->wshard(t), c->shard(t), st, c->num_sms));
+  if (c->world == 1 && (t == SEQPLAN_W_GATE || t == SEQPLAN_W_UP)) {
+    // p = 1: keep the gate|up working copy interleaved in 64-row blocks for the fused GEMM
+    const int64_t rows = c->I, cols = c->H;
+    for (int64_t blk = 0; blk < rows / 64; ++blk) {
+      const int64_t drow = blk * 128 + (t == SEQPLAN_W_UP ? 64 : 0);
+      ISP_CUDA(cudaMemcpyAsync(c->wgu_local + drow * cols, c->wshard(t) + blk * 64 * cols, 64 * cols * 2,
+                               cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  c->weights_dirty = true;
+}
+
+int fail(Ctx* c, const IspError& e) {
+  if (c) c->last_error = e.msg;
+  return e.code;
+}
+
+void collect_timeline(Ctx* c) {
+  if (c->tl_pending.empty()) return;
+  cudaEvent_t t0 = c->tl_pending.front().b;
+  for (auto& ev : c->tl_pending) {
+    cudaEventSynchronize(ev.e);
+    float s = 0, e = 0;
+    cudaEventElapsedTime(&s, t0, ev.b);
+    cudaEventElapsedTime(&e, t0, ev.e);
+    c->timeline.push_back({ev.stream, ev.kind, ev.layer, s * 1e-3, e * 1e-3});
+  }
+  for (auto& ev : c->tl_pending) {
+    if (ev.b != t0) cudaEventDestroy(ev.b);
+    cudaEventDestroy(ev.e);
+  }
+  cudaEventDestroy(t0);
+  c->tl_pending.clear();
+}
+
+void check_device_error(Ctx* c) {
+  if (c->world == 1 || c->group_mode) return;
+  uint32_t flag = 0;
+  cudaMemcpy(&flag, c->error_flag, 4, cudaMemcpyDeviceToHost);
+  if (flag) throw IspError(SEQPLAN_ISP_ERR_RUNTIME, "peer barrier timed out (a rank stopped responding)");
+}
+
+}  // namespace
+
+// =====================================================================================
+// C ABI
+// =====================================================================================
+extern "C" {
+
+int seqplan_isp_ctx_create(int world, int rank, int device, const seqplan_isp_shape* shape,
+                           const seqplan_strategy* strategy, const seqplan_mempool_policy* policy,
+                           uint32_t flags, seqplan_isp_ctx** out) {
+  if (!out || !shape) return SEQPLAN_ISP_ERR_INVALID;
+  *out = nullptr;
+  if (rank < 0 || rank >= world) return SEQPLAN_ISP_ERR_INVALID;
+  if (strategy) {
+    // The executor runs exactly the ISP plan: validate it with the reference's rules.
+    seqplan::Strategy s;
+    s.micro_batch = strategy->micro_batch; s.micro_batch_num = strategy->micro_batch_num;
+    s.recompute = strategy->recompute; s.pp = strategy->pp; s.dp = strategy->dp; s.tp = strategy->tp;
+    s.sp = strategy->sp; s.ps = strategy->ps; s.gs = strategy->gs; s.oss = strategy->oss;
+    seqplan::ModelConfig m;
+    m.hidden_dim = shape->hidden_dim; m.layers = 1; m.heads = shape->heads; m.vocab = 1;
+    m.seq_len = shape->seq_len; m.global_batch_tokens = shape->seq_len * s.micro_batch * s.micro_batch_num * s.dp;
+    seqplan::ClusterConfig cl{world, world, 0};
+    if (!seqplan::validate(s, m, cl).ok() || s.sp != world || s.ps != world || s.tp != 1 || s.pp != 1 ||
+        s.dp != 1 || s.recompute != 0)
+      return SEQPLAN_ISP_ERR_INVALID;
+  }
+  Ctx* c = new Ctx();
+  c->world = world;
+  c->rank = rank;
+  c->device = device;
+  c->flags = flags;
+  try {
+    setup(c, shape, policy);
+  } catch (const IspError& e) {
+    const int code = e.code;
+    std::fprintf(stderr, "seqplan_isp_ctx_create: %s\n", e.msg.c_str());
+    seqplan_isp_ctx_destroy(c);
+    return code;
+  }
+  *out = c;
+  return SEQPLAN_ISP_OK;
+}
+
+void seqplan_isp_ctx_destroy(seqplan_isp_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (int q = 0; q < c->world; ++q)
+    if (c->peer_opened[q]) cudaIpcCloseMemHandle(c->peer_heap[q]);
+  c->pool.release_all();
+  if (c->heap) cudaFree(c->heap);
+  if (c->comm) cudaStreamDestroy(c->comm);
+  for (int t = 0; t < SEQPLAN_W_COUNT; ++t) {
+    if (c->ev_gathered[t]) cudaEventDestroy(c->ev_gathered[t]);
+    if (c->ev_wgrad[t]) cudaEventDestroy(c->ev_wgrad[t]);
+  }
+  if (c->ev_comm_done) cudaEventDestroy(c->ev_comm_done);
+  if (c->ev_start) cudaEventDestroy(c->ev_start);
+  delete c;
+}
+
+const char* seqplan_isp_last_error(const seqplan_isp_ctx* c) { return c ? c->last_error.c_str() : ""; }
+
+size_t seqplan_isp_ipc_handle_size(void) { return sizeof(cudaIpcMemHandle_t); }
+
+int seqplan_isp_ipc_handle(seqplan_isp_ctx* c, void* out) {
+  if (!c || !out) return SEQPLAN_ISP_ERR_INVALID;
+  try {
+    ISP_CUDA(cudaSetDevice(c->device));
+    cudaIpcMemHandle_t h;
+    ISP_CUDA(cudaIpcGetMemHandle(&h, c->heap));
+    std::memcpy(out, &h, sizeof(h));
+  } catch (const IspError& e) {
+    return fail(c, e);
+  }
+  return SEQPLAN_ISP_OK;
+}
+
+int seqplan_isp_open_peers(seqplan_isp_ctx* c, const void* handles) {
+  if (!c || !handles) return SEQPLAN_ISP_ERR_INVALID;
+  try {
+    ISP_CUDA(cudaSetDevice(c->device));
+    const auto* hs = static_cast<const cudaIpcMemHandle_t*>(handles);
+    for (int q = 0; q < c->world; ++q) {
+      if (q == c->rank) continue;
+      void* p = nullptr;
+      ISP_CUDA(cudaIpcOpenMemHandle(&p, hs[q], cudaIpcMemLazyEnablePeerAccess));
+      c->peer_heap[q] = p;
+      c->peer_opened[q] = true;
+    }
+  } catch (const IspError& e) {
+    return fail(c, e);
+  }
+  return SEQPLAN_ISP_OK;
+}
+
+int seqplan_isp_group_create(int world, int device, const seqplan_isp_shape* shape,
+                             const seqplan_mempool_policy* policy, uint32_t flags, seqplan_isp_ctx** out_ctxs) {
+  if (!out_ctxs || world < 1 || world > kMaxRanks) return SEQPLAN_ISP_ERR_INVALID;
+  for (int r = 0; r < world; ++r) out_ctxs[r] = nullptr;
+  for (int r = 0; r < world; ++r) {
+    int st = seqplan_isp_ctx_create(world, r, device, shape, nullptr, policy, flags, &out_ctxs[r]);
+    if (st != SEQPLAN_ISP_OK) {
+      for (int q = 0; q < r; ++q) seqplan_isp_ctx_destroy(out_ctxs[q]);
+      return st;
+    }
+    out_ctxs[r]->group_mode = true;
+  }
+  for (int r = 0; r < world; ++r)
+    for (int q = 0; q < world; ++q) out_ctxs[r]->peer_heap[q] = out_ctxs[q]->heap;
+  return SEQPLAN_ISP_OK;
+}
+
+int seqplan_isp_init_weights(seqplan_isp_ctx* c, uint64_t seed) {
+  if (!c) return SEQPLAN_ISP_ERR_INVALID;
+  try {
+    ISP_CUDA(cudaSetDevice(c->device));
+    // tensor ids 2..8: norms 1 + N(0, .02), linear N(0, .02)
+    for (int t = 0; t < SEQPLAN_W_COUNT; ++t) {
+      const bool norm = (t == SEQPLAN_W_NORM1 || t == SEQPLAN_W_NORM2);
+      ISP_CUDA(keyed_fill(seed, t + 2, c->rank * c->shard(t), c->shard(t), norm ? 1.0 : 0.0, 0.02, c->master[t],
+                          nullptr, nullptr, c->num_sms));
+      refresh_working(c, t, nullptr);
+    }
+    ISP_CUDA(cudaDeviceSynchronize());
+  } catch (const IspError& e) {
+    return fail(c, e);
+  }
+  return SEQPLAN_ISP_OK;
+}
+
+int64_t seqplan_isp_shard_numel(const seqplan_isp_ctx* c, int t) {
+  if (!c || t < 0 || t >= SEQPLAN_W_COUNT) return -1;
+  return c->shard(t);
+}
+
+int seqplan_isp_set_weight_shard(seqplan_isp_ctx* c, int t, const float* host, int64_t n) {
+  if (!c || !host || t < 0 || t >= SEQPLAN_W_COUNT || n != c->shard(t)) return SEQPLAN_ISP_ERR_INVALID;
+  try {
+    ISP_CUDA(cudaSetDevice(c->device));
+    ISP_CUDA(cudaMemcpy(c->master[t], host, size_t(n) * 4, cudaMemcpyHostToDevice));
+    refresh_working(c, t, nullptr);
+    ISP_CUDA(cudaDeviceSynchronize());
+  } catch (const IspError& e) {
+    return fail(c, e);
+  }
+  return SEQPLAN_ISP_OK;
+}
+
+int seqplan_isp_get_weight_shard(seqplan_isp_ctx* c, int t, float* host, int64_t n) {
+  if (!c || !host || t < 0 || t >= SEQPLAN_W_COUNT || n != c->shard(t)) return SEQPLAN_ISP_ERR_INVALID;
+  try {
+    ISP_CUDA(cudaSetDevice(c->device));
+    ISP_CUDA(cudaMemcpy(host, c->master[t], size_t(n) * 4, cudaMemcpyDeviceToHost));
+  } catch (const IspError& e) {
+    return fail(c, e);
+  }
+  return SEQPLAN_ISP_OK;
+}
+
+int seqplan_isp_get_grad_shard(seqplan_isp_ctx* c, int t, float* host, int64_t n) {
+  if (!c || !host || t < 0 || t >= SEQPLAN_W_COUNT || n != c->shard(t)) return SEQPLAN_ISP_ERR_INVALID;
+  try {
+    ISP_CUDA(cudaSetDevice(c->device));
+    ISP_CUDA(cudaDeviceSynchronize());
+    ISP_CUDA(cudaMemcpy(host, c->grad[t], size_t(n) * 4, cudaMemcpyDeviceToHost));
+  } catch (const IspError& e) {
+    return fail(c, e);
+  }
+  return SEQPLAN_ISP_OK;
+}
+
+int seqplan_isp_grad_shard_ptr(seqplan_isp_ctx* c, int t, float** dev_ptr) {
+  if (!c || !dev_ptr || t < 0 || t >= SEQPLAN_W_COUNT) return SEQPLAN_ISP_ERR_INVALID;
+  *dev_ptr = c->grad[t];
+  return SEQPLAN_ISP_OK;
+}
+
+int seqplan_isp_fill_activation(seqplan_isp_ctx* c, uint64_t seed, int tensor_id, void* dev_out, void* stream) {
+  if (!c || !dev_out) return SEQPLAN_ISP_ERR_INVALID;
+  try {
+    ISP_CUDA(cudaSetDevice(c->device));
+    ISP_CUDA(keyed_fill(seed, tensor_id, c->rank * c->T * c->H, c->T * c->H, 0.0, 1.0, nullptr,
+                        static_cast<bf16*>(dev_out), static_cast<cudaStream_t>(stream), c->num_sms));
+  } catch (const IspError& e) {
+    return fail(c, e);
+  }
+  return SEQPLAN_ISP_OK;
+}
+
+static void run_fwd(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
+  if (c->weights_dirty) {  // peers must see refreshed working shards before gathering
+    barrier(c, st, false);
+    c->weights_dirty = false;
+  }
+  c->timeline.clear();
+  fwd_issue_gathers(c, st);
+  fwd_phase1(c, x, st);
+  barrier(c, st, false);
+  fwd_phase2(c, st);
+  barrier(c, st, false);
+  fwd_phase3(c, x, y, st);
+  c->fwd_done = true;
+}
+
+static void run_bwd(Ctx* c, const bf16* x, const bf16* dy, bf16* dx, cudaStream_t st) {
+  bwd_issue_gathers(c, st);
+  bwd_phase1(c, dy, st);
+  barrier(c, st, false);
+  bwd_phase2(c, st);
+  barrier(c, st, false);
+  bwd_phase3(c, x, dx, st);
+  if (c->flags & SEQPLAN_ISP_FLAG_FUSED_BWD) {
+    barrier(c, st, false);
+    bwd_reduce_all(c, st);
+  } else if (c->world > 1) {
+    // join the comm stream (its reduce-scatters) back into the caller's stream
+    ISP_CUDA(cudaEventRecord(c->ev_comm_done, c->comm));
+    ISP_CUDA(cudaStreamWaitEvent(st, c->ev_comm_done, 0));
+  }
+  c->pool.step_boundary();
+}
+
+int seqplan_isp_block_fwd(seqplan_isp_ctx* c, const void* x, void* y, void* stream) {
+  if (!c || !x || !y || c->group_mode) return SEQPLAN_ISP_ERR_INVALID;
+  try {
+    ISP_CUDA(cudaSetDevice(c->device));
+    run_fwd(c, static_cast<const bf16*>(x), static_cast<bf16*>(y), static_cast<cudaStream_t>(stream));
+    c->last_x = x;  // RMSNorm-1 input, needed again by block_bwd (caller keeps it alive)
+  } catch (const IspError& e) {
+    return fail(c, e);
+  }
+  return SEQPLAN_ISP_OK;
+}
+
+int seqplan_isp_block_bwd(seqplan_isp_ctx* c, const void* dy, void* dx, void* stream) {
+  if (!c || !dy || !dx || c->group_mode) return SEQPLAN_ISP_ERR_INVALID;
+  if (!c->fwd_done || !c->last_x) {
+    c->last_error = "block_bwd without a preceding block_fwd";
+    return SEQPLAN_ISP_ERR_INVALID;
+  }
+  try {
+    ISP_CUDA(cudaSetDevice(c->device));
+    run_bwd(c, static_cast<const bf16*>(c->last_x), static_cast<const bf16*>(dy), static_cast<bf16*>(dx),
+            static_cast<cudaStream_t>(stream));
+    c->fwd_done = false;
+    if (c->flags & SEQPLAN_ISP_FLAG_TIMELINE) {
+      ISP_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+      check_device_error(c);
+      collect_timeline(c);
+    }
+  } catch (const IspError& e) {
+    return fail(c, e);
+  }
+  return SEQPLAN_ISP_OK;
+}
+
+int seqplan_isp_group_fwd(seqplan_isp_ctx** cs, int world, const void* const* x, void* const* y, void* stream) {
+  if (!cs || !x || !y || world < 1) return SEQPLAN_ISP_ERR_INVALID;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  try {
+    ISP_CUDA(cudaSetDevice(cs[0]->device));
+    for (int r = 0; r < world; ++r) {
+      cs[r]->timeline.clear();
+      cs[r]->weights_dirty = false;
+      fwd_issue_gathers(cs[r], st);
+    }
+    for (int r = 0; r < world; ++r) fwd_phase1(cs[r], static_cast<const bf16*>(x[r]), st);
+    for (int r = 0; r < world; ++r) fwd_phase2(cs[r], st);
+    for (int r = 0; r < world; ++r) {
+      fwd_phase3(cs[r], static_cast<const bf16*>(x[r]), static_cast<bf16*>(y[r]), st);
+      cs[r]->fwd_done = true;
+      cs[r]->last_x = x[r];
+    }
+  } catch (const IspError& e) {
+    return fail(cs[0], e);
+  }
+  return SEQPLAN_ISP_OK;
+}
+
+int seqplan_isp_group_bwd(seqplan_isp_ctx** cs, int world, const void* const* dy, void* const* dx, void* stream) {
+  if (!cs || !dy || !dx || world < 1) return SEQPLAN_ISP_ERR_INVALID;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  try {
+    ISP_CUDA(cudaSetDevice(cs[0]->device));
+    for (int r = 0; r < world; ++r)
+      if (!cs[r]->fwd_done) throw IspError(SEQPLAN_ISP_ERR_INVALID, "group_bwd without group_fwd");
+    for (int r = 0; r < world; ++r) bwd_issue_gathers(cs[r], st);
+    for (int r = 0; r < world; ++r) bwd_phase1(cs[r], static_cast<const bf16*>(dy[r]), st);
+    for (int r = 0; r < world; ++r) bwd_phase2(cs[r], st);
+    for (int r = 0; r < world; ++r)
+      bwd_phase3(cs[r], static_cast<const bf16*>(cs[r]->last_x), static_cast<bf16*>(dx[r]), st);
+    for (int r = 0; r < world; ++r) {
+      bwd_reduce_all(cs[r], st);
+      cs[r]->pool.step_boundary();
+      cs[r]->fwd_done = false;
+    }
+  } catch (const IspError& e) {
+    return fail(cs[0], e);
+  }
+  return SEQPLAN_ISP_OK;
+}
+
+int seqplan_isp_pool_stats(seqplan_isp_ctx* c, seqplan_step_stats* out) {
+  if (!c || !out) return SEQPLAN_ISP_ERR_INVALID;
+  const auto s = c->pool.stats();
+  out->reserved = s.reserved;
+  out->allocated = s.allocated;
+  out->free_cached = s.free_cached;
+  out->fragmented = s.fragmented;
+  out->peak_reserved = s.peak_reserved;
+  out->peak_fragmented = s.peak_fragmented;
+  out->peak_allocated = s.peak_allocated;
+  return SEQPLAN_ISP_OK;
+}
+
+int seqplan_isp_timeline(seqplan_isp_ctx* c, seqplan_timeline_event* events, int64_t* n) {
+  if (!c || !n) return SEQPLAN_ISP_ERR_INVALID;
+  const int64_t have = static_cast<int64_t>(c->timeline.size());
+  if (events) {
+    const int64_t k = std::min(*n, have);
+    for (int64_t i = 0; i < k; ++i) events[i] = c->timeline[size_t(i)];
+  }
+  *n = have;
+  return SEQPLAN_ISP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+// Host launchers of the non-GEMM sm_100a kernels of the ISP block.
+#pragma once
+
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace isp {
+
+// ---- elementwise.cu -------------------------------------------------------
+uint64_t keyed_stream_base(uint64_t seed, int tensor_id);
+cudaError_t keyed_fill(uint64_t seed, int tensor_id, int64_t offset, int64_t n, double mean,
+                       double stdv, float* out_f32, __nv_bfloat16* out_bf16, cudaStream_t st,
+                       int num_sms);
+cudaError_t cast_f32_bf16(const float* in, __nv_bfloat16* out, int64_t n, cudaStream_t st,
+                          int num_sms);
+cudaError_t rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* y,
+                        float* rstd, int T, int H, float eps, cudaStream_t st, int num_sms);
+cudaError_t rmsnorm_bwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const float* rstd,
+                        const __nv_bfloat16* dn, const __nv_bfloat16* dres, __nv_bfloat16* dx,
+                        float* dg, int T, int H, cudaStream_t st, int num_sms);
+cudaError_t rope_inplace(__nv_bfloat16* qkv, int64_t ld, int T, int t0, int heads, int d,
+                         const float* cos_t, const float* sin_t, int k_offset, int dir,
+                         cudaStream_t st, int num_sms);
+cudaError_t swiglu_bwd(const __nv_bfloat16* da, const __nv_bfloat16* gu, __nv_bfloat16* dgu, int T,
+                       int I, cudaStream_t st, int num_sms);
+
+// ---- attention.cu ---------------------------------------------------------
+// Causal attention over S tokens for `heads` heads of width d (64 or 128).
+// Q/K/V/O rows are `ld*` elements apart per token; head h starts at column h*d.
+// lse: fp32 [heads, S] (natural log).
+struct AttnTensors {
+  const __nv_bfloat16* q;
+  const __nv_bfloat16* k;
+  const __nv_bfloat16* v;
+  int64_t ld_qkv;
+  __nv_bfloat16* o;
+  int64_t ld_o;
+  float* lse;
+  int S, heads, d;
+};
+cudaError_t attention_fwd(const AttnTensors& t, cudaStream_t st, int num_sms);
+// dq/dk/dv written (bf16) with row stride ld_dqkv; scratch: fp32 [heads*S] (delta) and
+// fp32 [heads*S*d] (dq accumulator).
+cudaError_t attention_bwd(const AttnTensors& t, const __nv_bfloat16* dout, __nv_bfloat16* dq,
+                          __nv_bfloat16* dk, __nv_bfloat16* dv, int64_t ld_dqkv, float* delta,
+                          float* dq_acc, cudaStream_t st, int num_sms);
+
+// ---- comm.cu --------------------------------------------------------------
+constexpr int kMaxRanks = 8;
+struct PeerPtrs {
+  void* p[kMaxRanks];
+};
+// Weight all-gather (pull): dst[q*shard + i] = src_q[i] for every rank q; src_q is rank
+// q's bf16 working shard at the same symmetric offset. row_map != 0 applies the 64-row
+// gate|up interleave (two tensors of `rows` x `cols` gathered into one [2*rows, cols]).
+cudaError_t allgather_pull(const PeerPtrs& src, int world, int64_t shard_elems, __nv_bfloat16* dst,
+                           cudaStream_t st, int num_sms, int num_ctas);
+cudaError_t allgather_pull_interleave(const PeerPtrs& src_gate, const PeerPtrs& src_up, int world,
+                                      int64_t rows, int64_t cols, __nv_bfloat16* dst,
+                                      cudaStream_t st, int num_ctas);
+// Gradient reduce-scatter fused with the cast/scale: out[i] (+)= scale * sum_q part_q[off + i]
+// (bf16 or fp32 partials, fp32 accumulate, fixed rank order).
+cudaError_t reduce_scatter_pull(const PeerPtrs& part, int world, int rank, int64_t shard_elems,
+                                bool part_is_f32, float scale, int accumulate, float* out,
+                                cudaStream_t st, int num_ctas);
+// Same for the interleaved gate|up partial [2*rows, cols]: produces this rank's gate and up
+// shards (each rows*cols/world elements).
+cudaError_t reduce_scatter_pull_interleave(const PeerPtrs& part, int world, int rank, int64_t rows,
+                                           int64_t cols, float scale, int accumulate,
+                                           float* out_gate, float* out_up, cudaStream_t st,
+                                           int num_ctas);
+// Ulysses all-to-all (pull). Token-sharded [T, parts*H] on every rank -> head-sharded
+// [S, parts*Hl] on this rank (Hl = H/world). Optional RoPE on parts 0,1 (dir=+1).
+cudaError_t a2a_tokens_to_heads(const PeerPtrs& src, int world, int rank, int T, int H, int parts,
+                                __nv_bfloat16* dst, const float* cos_t, const float* sin_t, int d,
+                                int rope_parts, cudaStream_t st, int num_ctas);
+// Head-sharded [S, parts*Hl] on every rank -> token-sharded [T, parts*H] on this rank;
+// optional inverse RoPE on parts 0,1 (the dq/dk path).
+cudaError_t a2a_heads_to_tokens(const PeerPtrs& src, int world, int rank, int T, int H, int parts,
+                                __nv_bfloat16* dst, const float* cos_t, const float* sin_t, int d,
+                                int rope_parts, cudaStream_t st, int num_ctas);
+// Cross-GPU barrier over system-scope flags in every rank's heap. epoch increases by one per
+// call; a rank spins (bounded, ~20 s) until all peers have published `epoch`.
+cudaError_t peer_barrier(const PeerPtrs& flags, int world, int rank, uint32_t epoch,
+                         uint32_t* error_flag, cudaStream_t st);
+
+}  // namespace isp
