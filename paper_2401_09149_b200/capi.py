@@ -228,9 +228,9 @@ class IspBlock:
                 for e in arr[:n.value]]
 
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and getattr(self, "_owner", True):
             lib().seqplan_isp_ctx_destroy(self.h)
-            self.h = None
+        self.h = None
 
     def __del__(self):
         try:
@@ -256,6 +256,7 @@ class IspGroup:
     def rank(self, r):
         b = IspBlock.__new__(IspBlock)
         b.h, b.world, b.rank, b.shape = self.hs[r], self.world, r, self.shape
+        b._owner = False  # a view: the group owns and destroys the context
         return b
 
     def fwd(self, xs, ys, stream=None):
