@@ -64,7 +64,25 @@ enum {
   SEQPLAN_ISP_FLAG_FUSED_BWD = 1u << 1,    /* BackwardPolicy::Fused instead of Selective            */
   SEQPLAN_ISP_FLAG_TIMELINE = 1u << 2,     /* record CUDA-event timeline                            */
   SEQPLAN_ISP_FLAG_SKIP_COMM = 1u << 3,    /* measurement only: collectives become no-ops           */
+  SEQPLAN_ISP_FLAG_PROFILE = 1u << 4,      /* per-kernel CUDA events (seqplan_isp_kernel_profile)    */
 };
+
+/* Kernel classes of the per-kernel profile. */
+enum {
+  SEQPLAN_K_GEMM = 0,
+  SEQPLAN_K_ATTN_FWD = 1,
+  SEQPLAN_K_ATTN_BWD = 2,
+  SEQPLAN_K_ALL_GATHER = 3,
+  SEQPLAN_K_REDUCE_SCATTER = 4,
+  SEQPLAN_K_ALL_TO_ALL = 5,
+};
+
+typedef struct {
+  int32_t kind;   /* SEQPLAN_K_* */
+  double flops;   /* algorithmic FLOPs of the launch */
+  double bytes;   /* algorithmic bytes (NVLink bytes for collectives) */
+  double seconds; /* CUDA-event duration on the launching stream */
+} seqplan_kernel_record;
 
 typedef struct seqplan_isp_ctx seqplan_isp_ctx;
 
@@ -172,6 +190,12 @@ int seqplan_isp_block_bwd(seqplan_isp_ctx* ctx, const void* dy, void* dx, void* 
 int seqplan_isp_pool_stats(seqplan_isp_ctx* ctx, seqplan_step_stats* out);
 /* Copies up to *n events of the last fwd/bwd pair; *n receives the count. */
 int seqplan_isp_timeline(seqplan_isp_ctx* ctx, seqplan_timeline_event* events, int64_t* n);
+
+/* Per-kernel records of the calls made with SEQPLAN_ISP_FLAG_PROFILE (collected at the end
+ * of each block_bwd). clear != 0 empties the buffer after copying. */
+int seqplan_isp_kernel_profile(seqplan_isp_ctx* ctx, seqplan_kernel_record* out, int64_t* n, int clear);
+/* Number of kernels this context has launched on the hot path (fwd/bwd). */
+int64_t seqplan_isp_launch_count(const seqplan_isp_ctx* ctx);
 
 /* ---- kernel-level entry points (tests) ------------------------------------ */
 int seqplan_isp_debug_gemm(const void* a, int64_t lda, int a_mn, const void* b, int64_t ldb,

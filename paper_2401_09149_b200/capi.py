@@ -44,12 +44,18 @@ class EventC(ctypes.Structure):
                 ("start_s", c_d), ("end_s", c_d)]
 
 
+class KernelRecC(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("flops", c_d), ("bytes", c_d), ("seconds", c_d)]
+
+
+K_NAMES = ["gemm", "attn_fwd", "attn_bwd", "all_gather", "reduce_scatter", "all_to_all"]
+
 STATUS = {0: "ok", 1: "invalid argument", 2: "runtime error", 3: "out of memory",
           4: "unsupported"}
 
 W_NORM1, W_QKV, W_O, W_NORM2, W_GATE, W_UP, W_DOWN = range(7)
 W_NAMES = ["norm1", "qkv", "o", "norm2", "gate", "up", "down"]
-FLAG_NO_OVERLAP, FLAG_FUSED_BWD, FLAG_TIMELINE, FLAG_SKIP_COMM = 1, 2, 4, 8
+FLAG_NO_OVERLAP, FLAG_FUSED_BWD, FLAG_TIMELINE, FLAG_SKIP_COMM, FLAG_PROFILE = 1, 2, 4, 8, 16
 EV_NAMES = ["forward", "grad_input", "grad_weight", "all_gather", "reduce_scatter", "all_to_all"]
 
 
@@ -101,6 +107,8 @@ _EXTRA_SIGS = [
     ("seqplan_isp_block_bwd", c_int, [c_vp, c_vp, c_vp, c_vp]),
     ("seqplan_isp_pool_stats", c_int, [c_vp, P(StepStatsC)]),
     ("seqplan_isp_timeline", c_int, [c_vp, P(EventC), P(c_i64)]),
+    ("seqplan_isp_kernel_profile", c_int, [c_vp, P(KernelRecC), P(c_i64), c_int]),
+    ("seqplan_isp_launch_count", c_i64, [c_vp]),
     ("seqplan_isp_debug_attention", c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_int, c_int, c_int,
                                             c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     ("seqplan_isp_debug_rmsnorm", c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_f,
@@ -226,6 +234,16 @@ class IspBlock:
         lib().seqplan_isp_timeline(self.h, arr, ctypes.byref(n))
         return [dict(stream=e.stream, kind=EV_NAMES[e.kind], layer=e.layer, start=e.start_s, end=e.end_s)
                 for e in arr[:n.value]]
+
+    def kernel_profile(self, clear=True):
+        n = c_i64(0)
+        lib().seqplan_isp_kernel_profile(self.h, None, ctypes.byref(n), 0)
+        arr = (KernelRecC * max(n.value, 1))()
+        lib().seqplan_isp_kernel_profile(self.h, arr, ctypes.byref(n), int(clear))
+        return [dict(kind=K_NAMES[r.kind], flops=r.flops, bytes=r.bytes, seconds=r.seconds) for r in arr[:n.value]]
+
+    def launch_count(self):
+        return lib().seqplan_isp_launch_count(self.h)
 
     def close(self):
         if getattr(self, "h", None) and getattr(self, "_owner", True):

@@ -125,6 +125,9 @@ struct seqplan_isp_ctx {
 
   // gathered weights of the current pass (pool CommBuffer allocations)
   bf16* gathered[SEQPLAN_W_COUNT] = {};
+  // SEQPLAN_ISP_FLAG_SKIP_COMM: weights gathered once and kept (measurement of exposed comm)
+  bf16* pregathered[SEQPLAN_W_COUNT] = {};
+  bool skip_comm() const { return (flags & SEQPLAN_ISP_FLAG_SKIP_COMM) && world > 1; }
 
   // timeline
   struct TEv {
@@ -134,6 +137,15 @@ struct seqplan_isp_ctx {
   };
   std::vector<TEv> tl_pending;
   std::vector<seqplan_timeline_event> timeline;
+  // per-kernel profile (SEQPLAN_ISP_FLAG_PROFILE) and launch counter
+  struct KEv {
+    int kind;
+    double flops, bytes;
+    cudaEvent_t b, e;
+  };
+  std::vector<KEv> kprof_pending;
+  std::vector<seqplan_kernel_record> kprof;
+  int64_t launches = 0;
 
   // ---- helpers ----
   template <typename T>
@@ -167,13 +179,6 @@ void* pool_alloc(Ctx* c, int64_t bytes, seqplan::AllocTag tag, cudaStream_t st) 
   return p;
 }
 
-void gemm(const GemmOperand& A, const GemmOperand& B, const GemmArgs& args, int epi, cudaStream_t st) {
-  cudaError_t e = gemm_launch(A, B, args, epi, st);
-  if (e == cudaErrorInvalidValue)
-    throw IspError(SEQPLAN_ISP_ERR_UNSUPPORTED, "GEMM shape not tiled by the sm_100a kernel (M%128, N%128, K%64)");
-  ISP_CUDA(e);
-}
-
 // ---- timeline -------------------------------------------------------------------
 struct Span {
   Ctx* c;
@@ -196,13 +201,52 @@ struct Span {
   }
 };
 
+// Per-kernel CUDA events (SEQPLAN_ISP_FLAG_PROFILE): algorithmic flops/bytes per launch.
+struct KTimer {
+  Ctx* c;
+  cudaStream_t st;
+  int kind;
+  double flops, bytes;
+  cudaEvent_t b = nullptr;
+  KTimer(Ctx* cc, cudaStream_t s, int k, double f, double by) : c(cc), st(s), kind(k), flops(f), bytes(by) {
+    if (c->flags & SEQPLAN_ISP_FLAG_PROFILE) {
+      cudaEventCreate(&b);
+      cudaEventRecord(b, st);
+    }
+  }
+  ~KTimer() {
+    if (!b) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    c->kprof_pending.push_back({kind, flops, bytes, b, e});
+  }
+};
+
+#define ISP_LAUNCH(n, expr) \
+  do {                      \
+    ISP_CUDA(expr);         \
+    c->launches += (n);     \
+  } while (0)
+
+void gemm(Ctx* c, const GemmOperand& A, const GemmOperand& B, const GemmArgs& args, int epi, cudaStream_t st) {
+  const double M = args.M, N = args.N, K = args.K;
+  const double out_bytes = (epi == EPI_F32 ? 4.0 : 2.0) * M * N * (epi == EPI_SWIGLU ? 1.5 : 1.0);
+  KTimer kt(c, st, SEQPLAN_K_GEMM, 2.0 * M * N * K, 2.0 * (M * K + N * K) + out_bytes);
+  c->launches += 1;
+  cudaError_t e = gemm_launch(A, B, args, epi, st);
+  if (e == cudaErrorInvalidValue)
+    throw IspError(SEQPLAN_ISP_ERR_UNSUPPORTED, "GEMM shape not tiled by the sm_100a kernel (M%128, N%128, K%64)");
+  ISP_CUDA(e);
+}
+
 // ---- collectives (dispatch on mode) -----------------------------------------------
 void barrier(Ctx* c, cudaStream_t st, bool comm_lane) {
-  if (c->world == 1 || c->group_mode) return;
+  if (c->world == 1 || c->group_mode || c->skip_comm()) return;
   uint32_t& ep = comm_lane ? c->epoch_comm : c->epoch_compute;
   ++ep;
   const size_t off = c->off_flags + (comm_lane ? 64 * sizeof(uint32_t) : 0);
-  ISP_CUDA(peer_barrier(c->peers_at(off), c->world, c->rank, ep, c->error_flag, st));
+  ISP_LAUNCH(1, peer_barrier(c->peers_at(off), c->world, c->rank, ep, c->error_flag, st));
 }
 
 // Gather tensor t into a pool CommBuffer (or return the local working copy at p = 1).
@@ -211,38 +255,55 @@ void gather_weight(Ctx* c, int t, cudaStream_t st) {
     c->gathered[t] = (t == SEQPLAN_W_GATE) ? c->wgu_local : c->wshard(t);
     return;
   }
+  if (c->skip_comm() && c->pregathered[t]) {
+    c->gathered[t] = c->pregathered[t];
+    return;
+  }
   Span sp(c, st, 1, SEQPLAN_EV_ALL_GATHER, t);
+  const double frac = double(c->world - 1) / double(c->world);
   if (t == SEQPLAN_W_GATE) {  // gate|up gathered together, interleaved
     const int64_t bytes = 2 * c->I * c->H * 2;
+    KTimer kt(c, st, SEQPLAN_K_ALL_GATHER, 0, frac * double(bytes));
     bf16* dst = static_cast<bf16*>(pool_alloc(c, bytes, seqplan::AllocTag::CommBuffer, st));
-    ISP_CUDA(allgather_pull_interleave(c->peers_at(c->off_wshard[SEQPLAN_W_GATE]),
+    ISP_LAUNCH(1, allgather_pull_interleave(c->peers_at(c->off_wshard[SEQPLAN_W_GATE]),
                                        c->peers_at(c->off_wshard[SEQPLAN_W_UP]), c->world, c->I, c->H,
                                        dst, st, kCommCtas));
     c->gathered[t] = dst;
   } else {
     const int64_t bytes = c->numel(t) * 2;
+    KTimer kt(c, st, SEQPLAN_K_ALL_GATHER, 0, frac * double(bytes));
     bf16* dst = static_cast<bf16*>(pool_alloc(c, bytes, seqplan::AllocTag::CommBuffer, st));
-    ISP_CUDA(allgather_pull(c->peers_at(c->off_wshard[t]), c->world, c->shard(t), dst, st, c->num_sms,
+    ISP_LAUNCH(1, allgather_pull(c->peers_at(c->off_wshard[t]), c->world, c->shard(t), dst, st, c->num_sms,
                             kCommCtas));
     c->gathered[t] = dst;
   }
 }
 
 void release_weight(Ctx* c, int t, cudaStream_t st) {
+  if (c->skip_comm()) {
+    c->pregathered[t] = c->gathered[t];
+    c->gathered[t] = nullptr;
+    return;
+  }
   if (c->world > 1 && c->gathered[t]) c->pool.free(c->gathered[t], st);
   c->gathered[t] = nullptr;
 }
 
 // Reduce-scatter the weight gradient partial of tensor t into the fp32 grad shard.
 void reduce_scatter_grad(Ctx* c, int t, cudaStream_t st) {
+  if (c->skip_comm()) return;
   Span sp(c, st, 1, SEQPLAN_EV_REDUCE_SCATTER, t);
+  const double frac = double(c->world - 1) / double(c->world);
+  const bool norm = (t == SEQPLAN_W_NORM1 || t == SEQPLAN_W_NORM2);
+  const double part_bytes = t == SEQPLAN_W_GATE ? 2.0 * c->I * c->H * 2 : double(c->numel(t)) * (norm ? 4 : 2);
+  KTimer kt(c, st, SEQPLAN_K_REDUCE_SCATTER, 0, frac * part_bytes);
   if (t == SEQPLAN_W_GATE) {
-    ISP_CUDA(reduce_scatter_pull_interleave(c->peers_at(c->off_part[SEQPLAN_W_GATE]), c->world, c->rank,
+    ISP_LAUNCH(1, reduce_scatter_pull_interleave(c->peers_at(c->off_part[SEQPLAN_W_GATE]), c->world, c->rank,
                                             c->I, c->H, 1.0f, 0, c->grad[SEQPLAN_W_GATE],
                                             c->grad[SEQPLAN_W_UP], st, kCommCtas));
   } else {
     const bool f32 = (t == SEQPLAN_W_NORM1 || t == SEQPLAN_W_NORM2);
-    ISP_CUDA(reduce_scatter_pull(c->peers_at(c->off_part[t]), c->world, c->rank, c->shard(t), f32, 1.0f,
+    ISP_LAUNCH(1, reduce_scatter_pull(c->peers_at(c->off_part[t]), c->world, c->rank, c->shard(t), f32, 1.0f,
                                  0, c->grad[t], st, kCommCtas));
   }
 }
@@ -277,15 +338,15 @@ void fwd_phase1(Ctx* c, const bf16* x, cudaStream_t st) {
   Span sp(c, st, 0, SEQPLAN_EV_FORWARD, 0);
   const int T = static_cast<int>(c->T), H = static_cast<int>(c->H);
   wait_gathered(c, SEQPLAN_W_NORM1, st);
-  ISP_CUDA(rmsnorm_fwd(x, c->gathered[SEQPLAN_W_NORM1], c->n1, c->rstd1, T, H, c->eps, st, c->num_sms));
+  ISP_LAUNCH(1, rmsnorm_fwd(x, c->gathered[SEQPLAN_W_NORM1], c->n1, c->rstd1, T, H, c->eps, st, c->num_sms));
   wait_gathered(c, SEQPLAN_W_QKV, st);
   GemmArgs g;
   g.M = T; g.N = 3 * H; g.K = H;
   g.out = c->world == 1 ? static_cast<void*>(c->qkv_heads) : static_cast<void*>(qkv_tok_buf(c));
   g.ldo = 3 * H;
-  gemm({c->n1, H, false}, {c->gathered[SEQPLAN_W_QKV], H, false}, g, EPI_BF16, st);
+  gemm(c, {c->n1, H, false}, {c->gathered[SEQPLAN_W_QKV], H, false}, g, EPI_BF16, st);
   if (c->world == 1)
-    ISP_CUDA(rope_inplace(c->qkv_heads, 3 * H, T, 0, static_cast<int>(c->D), static_cast<int>(c->d), c->cos_t,
+    ISP_LAUNCH(1, rope_inplace(c->qkv_heads, 3 * H, T, 0, static_cast<int>(c->D), static_cast<int>(c->d), c->cos_t,
                           c->sin_t, H, +1, st, c->num_sms));
 }
 
@@ -306,21 +367,24 @@ AttnTensors attn_tensors(Ctx* c) {
 }
 
 void fwd_phase2(Ctx* c, cudaStream_t st) {
-  if (c->world > 1) {
+  if (c->world > 1 && !c->skip_comm()) {
     Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 0);
-    ISP_CUDA(a2a_tokens_to_heads(c->peers_at(c->off_qkv_tok), c->world, c->rank, static_cast<int>(c->T),
+    KTimer kt(c, st, SEQPLAN_K_ALL_TO_ALL, 0, double(c->world - 1) / double(c->world) * double(c->T) * 3 * double(c->H) * 2);
+    ISP_LAUNCH(1, a2a_tokens_to_heads(c->peers_at(c->off_qkv_tok), c->world, c->rank, static_cast<int>(c->T),
                                  static_cast<int>(c->H), 3, c->qkv_heads, c->cos_t, c->sin_t,
                                  static_cast<int>(c->d), 2, st, kA2ACtas));
   }
   Span sp(c, st, 0, SEQPLAN_EV_FORWARD, 1);
-  ISP_CUDA(attention_fwd(attn_tensors(c), st, c->num_sms));
+  KTimer kt(c, st, SEQPLAN_K_ATTN_FWD, 2.0 * double(c->S) * double(c->S) * double(c->Hl), 0);
+  ISP_LAUNCH(1, attention_fwd(attn_tensors(c), st, c->num_sms));
 }
 
 void fwd_phase3(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
   const int T = static_cast<int>(c->T), H = static_cast<int>(c->H), I = static_cast<int>(c->I);
-  if (c->world > 1) {
+  if (c->world > 1 && !c->skip_comm()) {
     Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 1);
-    ISP_CUDA(a2a_heads_to_tokens(c->peers_at(c->off_o_heads), c->world, c->rank, T, H, 1, c->o_tok, c->cos_t,
+    KTimer kt(c, st, SEQPLAN_K_ALL_TO_ALL, 0, double(c->world - 1) / double(c->world) * double(c->T) * 1 * double(c->H) * 2);
+    ISP_LAUNCH(1, a2a_heads_to_tokens(c->peers_at(c->off_o_heads), c->world, c->rank, T, H, 1, c->o_tok, c->cos_t,
                                  c->sin_t, static_cast<int>(c->d), 0, st, kA2ACtas));
   }
   Span sp(c, st, 0, SEQPLAN_EV_FORWARD, 2);
@@ -330,11 +394,11 @@ void fwd_phase3(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
     g.M = T; g.N = H; g.K = H;
     g.out = c->h; g.ldo = H;
     g.resid = x; g.ldr = H;
-    gemm({c->o_tok, H, false}, {c->gathered[SEQPLAN_W_O], H, false}, g, EPI_BF16_RESID, st);
+    gemm(c, {c->o_tok, H, false}, {c->gathered[SEQPLAN_W_O], H, false}, g, EPI_BF16_RESID, st);
   }
   release_weight(c, SEQPLAN_W_O, st);
   wait_gathered(c, SEQPLAN_W_NORM2, st);
-  ISP_CUDA(rmsnorm_fwd(c->h, c->gathered[SEQPLAN_W_NORM2], c->n2, c->rstd2, T, H, c->eps, st, c->num_sms));
+  ISP_LAUNCH(1, rmsnorm_fwd(c->h, c->gathered[SEQPLAN_W_NORM2], c->n2, c->rstd2, T, H, c->eps, st, c->num_sms));
   c->gu = static_cast<bf16*>(pool_alloc(c, int64_t(T) * 2 * I * 2, seqplan::AllocTag::MlpIntermediate, st));
   c->a = static_cast<bf16*>(pool_alloc(c, int64_t(T) * I * 2, seqplan::AllocTag::MlpIntermediate, st));
   wait_gathered(c, SEQPLAN_W_GATE, st);
@@ -343,7 +407,7 @@ void fwd_phase3(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
     g.M = T; g.N = 2 * I; g.K = H;
     g.out = c->gu; g.ldo = 2 * I;
     g.out2 = c->a; g.ldo2 = I;
-    gemm({c->n2, H, false}, {c->gathered[SEQPLAN_W_GATE], H, false}, g, EPI_SWIGLU, st);
+    gemm(c, {c->n2, H, false}, {c->gathered[SEQPLAN_W_GATE], H, false}, g, EPI_SWIGLU, st);
   }
   release_weight(c, SEQPLAN_W_GATE, st);
   wait_gathered(c, SEQPLAN_W_DOWN, st);
@@ -352,7 +416,7 @@ void fwd_phase3(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
     g.M = T; g.N = H; g.K = I;
     g.out = y; g.ldo = H;
     g.resid = c->h; g.ldr = H;
-    gemm({c->a, I, false}, {c->gathered[SEQPLAN_W_DOWN], I, false}, g, EPI_BF16_RESID, st);
+    gemm(c, {c->a, I, false}, {c->gathered[SEQPLAN_W_DOWN], I, false}, g, EPI_BF16_RESID, st);
   }
   release_weight(c, SEQPLAN_W_DOWN, st);
   release_weight(c, SEQPLAN_W_QKV, st);
@@ -391,11 +455,11 @@ void wgrad(Ctx* c, int t, const GemmOperand& A, const GemmOperand& B, int M, int
       g.interleave64 = 1;
       g.out_b = c->grad[SEQPLAN_W_UP];
     }
-    gemm(A, B, g, EPI_F32, st);
+    gemm(c, A, B, g, EPI_F32, st);
   } else {
     g.out = c->hp<bf16>(c->off_part[t]);
     g.ldo = N;
-    gemm(A, B, g, EPI_BF16, st);
+    gemm(c, A, B, g, EPI_BF16, st);
   }
 }
 
@@ -424,14 +488,14 @@ void bwd_phase1(Ctx* c, const bf16* dy, cudaStream_t st) {
     GemmArgs g;
     g.M = T; g.N = I; g.K = H;
     g.out = da; g.ldo = I;
-    gemm({dy, H, false}, {c->gathered[SEQPLAN_W_DOWN], I, true}, g, EPI_BF16, st);
+    gemm(c, {dy, H, false}, {c->gathered[SEQPLAN_W_DOWN], I, true}, g, EPI_BF16, st);
   }
   release_weight(c, SEQPLAN_W_DOWN, st);
   c->pool.free(c->a, st);
   c->a = nullptr;
   // ---- SwiGLU backward ----
   bf16* dgu = static_cast<bf16*>(pool_alloc(c, int64_t(T) * 2 * I * 2, seqplan::AllocTag::MlpIntermediate, st));
-  ISP_CUDA(swiglu_bwd(da, c->gu, dgu, T, I, st, c->num_sms));
+  ISP_LAUNCH(1, swiglu_bwd(da, c->gu, dgu, T, I, st, c->num_sms));
   c->pool.free(da, st);
   c->pool.free(c->gu, st);
   c->gu = nullptr;
@@ -447,7 +511,7 @@ void bwd_phase1(Ctx* c, const bf16* dy, cudaStream_t st) {
     GemmArgs g;
     g.M = T; g.N = H; g.K = 2 * I;
     g.out = c->dn; g.ldo = H;
-    gemm({dgu, 2 * I, false}, {c->gathered[SEQPLAN_W_GATE], H, true}, g, EPI_BF16, st);
+    gemm(c, {dgu, 2 * I, false}, {c->gathered[SEQPLAN_W_GATE], H, true}, g, EPI_BF16, st);
   }
   release_weight(c, SEQPLAN_W_GATE, st);
   c->pool.free(dgu, st);
@@ -455,7 +519,7 @@ void bwd_phase1(Ctx* c, const bf16* dy, cudaStream_t st) {
   wait_gathered(c, SEQPLAN_W_NORM2, st);
   float* dg2 = c->world == 1 ? c->grad[SEQPLAN_W_NORM2] : c->hp<float>(c->off_part[SEQPLAN_W_NORM2]);
   ISP_CUDA(cudaMemsetAsync(dg2, 0, sizeof(float) * H, st));
-  ISP_CUDA(rmsnorm_bwd(c->h, c->gathered[SEQPLAN_W_NORM2], c->rstd2, c->dn, dy, c->dh, dg2, T, H, st, c->num_sms));
+  ISP_LAUNCH(1, rmsnorm_bwd(c->h, c->gathered[SEQPLAN_W_NORM2], c->rstd2, c->dn, dy, c->dh, dg2, T, H, st, c->num_sms));
   release_weight(c, SEQPLAN_W_NORM2, st);
   if (selective) schedule_rs(c, SEQPLAN_W_NORM2, st);
   // ---- output projection ----
@@ -471,35 +535,38 @@ void bwd_phase1(Ctx* c, const bf16* dy, cudaStream_t st) {
     g.M = T; g.N = H; g.K = H;
     g.out = c->world == 1 ? c->dO_heads : c->hp<bf16>(c->off_do_tok);
     g.ldo = H;
-    gemm({c->dh, H, false}, {c->gathered[SEQPLAN_W_O], H, true}, g, EPI_BF16, st);
+    gemm(c, {c->dh, H, false}, {c->gathered[SEQPLAN_W_O], H, true}, g, EPI_BF16, st);
   }
   release_weight(c, SEQPLAN_W_O, st);
 }
 
 void bwd_phase2(Ctx* c, cudaStream_t st) {
   const int T = static_cast<int>(c->T), H = static_cast<int>(c->H);
-  if (c->world > 1) {
+  if (c->world > 1 && !c->skip_comm()) {
     Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 2);
-    ISP_CUDA(a2a_tokens_to_heads(c->peers_at(c->off_do_tok), c->world, c->rank, T, H, 1, c->dO_heads, c->cos_t,
+    KTimer kt(c, st, SEQPLAN_K_ALL_TO_ALL, 0, double(c->world - 1) / double(c->world) * double(c->T) * 1 * double(c->H) * 2);
+    ISP_LAUNCH(1, a2a_tokens_to_heads(c->peers_at(c->off_do_tok), c->world, c->rank, T, H, 1, c->dO_heads, c->cos_t,
                                  c->sin_t, static_cast<int>(c->d), 0, st, kA2ACtas));
   }
   Span sp(c, st, 0, SEQPLAN_EV_GRAD_INPUT, 0);
   AttnTensors t = attn_tensors(c);
   bf16* dqkv = c->world == 1 ? c->dqkv_tok : c->hp<bf16>(c->off_dqkv_heads);
   const int64_t ld = 3 * c->Hl;
-  ISP_CUDA(attention_bwd(t, c->dO_heads, dqkv, dqkv + c->Hl, dqkv + 2 * c->Hl, ld, c->delta, c->dq_acc, st,
+  KTimer kt(c, st, SEQPLAN_K_ATTN_BWD, 4.0 * double(c->S) * double(c->S) * double(c->Hl), 0);
+  ISP_LAUNCH(3, attention_bwd(t, c->dO_heads, dqkv, dqkv + c->Hl, dqkv + 2 * c->Hl, ld, c->delta, c->dq_acc, st,
                          c->num_sms));
   if (c->world == 1)
-    ISP_CUDA(rope_inplace(c->dqkv_tok, 3 * H, T, 0, static_cast<int>(c->D), static_cast<int>(c->d), c->cos_t,
+    ISP_LAUNCH(1, rope_inplace(c->dqkv_tok, 3 * H, T, 0, static_cast<int>(c->D), static_cast<int>(c->d), c->cos_t,
                           c->sin_t, H, -1, st, c->num_sms));
 }
 
 void bwd_phase3(Ctx* c, const bf16* x, bf16* dx, cudaStream_t st) {
   const int T = static_cast<int>(c->T), H = static_cast<int>(c->H);
   const bool selective = !(c->flags & SEQPLAN_ISP_FLAG_FUSED_BWD);
-  if (c->world > 1) {
+  if (c->world > 1 && !c->skip_comm()) {
     Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 3);
-    ISP_CUDA(a2a_heads_to_tokens(c->peers_at(c->off_dqkv_heads), c->world, c->rank, T, H, 3, c->dqkv_tok,
+    KTimer kt(c, st, SEQPLAN_K_ALL_TO_ALL, 0, double(c->world - 1) / double(c->world) * double(c->T) * 3 * double(c->H) * 2);
+    ISP_LAUNCH(1, a2a_heads_to_tokens(c->peers_at(c->off_dqkv_heads), c->world, c->rank, T, H, 3, c->dqkv_tok,
                                  c->cos_t, c->sin_t, static_cast<int>(c->d), 2, st, kA2ACtas));
   }
   wait_gathered(c, SEQPLAN_W_QKV, st);
@@ -513,13 +580,13 @@ void bwd_phase3(Ctx* c, const bf16* x, bf16* dx, cudaStream_t st) {
     GemmArgs g;
     g.M = T; g.N = H; g.K = 3 * H;
     g.out = c->dn; g.ldo = H;
-    gemm({c->dqkv_tok, 3 * H, false}, {c->gathered[SEQPLAN_W_QKV], H, true}, g, EPI_BF16, st);
+    gemm(c, {c->dqkv_tok, 3 * H, false}, {c->gathered[SEQPLAN_W_QKV], H, true}, g, EPI_BF16, st);
   }
   release_weight(c, SEQPLAN_W_QKV, st);
   wait_gathered(c, SEQPLAN_W_NORM1, st);
   float* dg1 = c->world == 1 ? c->grad[SEQPLAN_W_NORM1] : c->hp<float>(c->off_part[SEQPLAN_W_NORM1]);
   ISP_CUDA(cudaMemsetAsync(dg1, 0, sizeof(float) * H, st));
-  ISP_CUDA(rmsnorm_bwd(x, c->gathered[SEQPLAN_W_NORM1], c->rstd1, c->dn, c->dh, dx, dg1, T, H, st, c->num_sms));
+  ISP_LAUNCH(1, rmsnorm_bwd(x, c->gathered[SEQPLAN_W_NORM1], c->rstd1, c->dn, c->dh, dx, dg1, T, H, st, c->num_sms));
   release_weight(c, SEQPLAN_W_NORM1, st);
   if (selective) schedule_rs(c, SEQPLAN_W_NORM1, st);
 }
@@ -690,6 +757,18 @@ void collect_timeline(Ctx* c) {
   }
   cudaEventDestroy(t0);
   c->tl_pending.clear();
+}
+
+void collect_kprof(Ctx* c) {
+  for (auto& k : c->kprof_pending) {
+    cudaEventSynchronize(k.e);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, k.b, k.e);
+    c->kprof.push_back({k.kind, k.flops, k.bytes, static_cast<double>(ms) * 1e-3});
+    cudaEventDestroy(k.b);
+    cudaEventDestroy(k.e);
+  }
+  c->kprof_pending.clear();
 }
 
 void check_device_error(Ctx* c) {
@@ -946,10 +1025,11 @@ int seqplan_isp_block_bwd(seqplan_isp_ctx* c, const void* dy, void* dx, void* st
     run_bwd(c, static_cast<const bf16*>(c->last_x), static_cast<const bf16*>(dy), static_cast<bf16*>(dx),
             static_cast<cudaStream_t>(stream));
     c->fwd_done = false;
-    if (c->flags & SEQPLAN_ISP_FLAG_TIMELINE) {
+    if (c->flags & (SEQPLAN_ISP_FLAG_TIMELINE | SEQPLAN_ISP_FLAG_PROFILE)) {
       ISP_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
       check_device_error(c);
       collect_timeline(c);
+      collect_kprof(c);
     }
   } catch (const IspError& e) {
     return fail(c, e);
@@ -997,11 +1077,32 @@ int seqplan_isp_group_bwd(seqplan_isp_ctx** cs, int world, const void* const* dy
       cs[r]->pool.step_boundary();
       cs[r]->fwd_done = false;
     }
+    if (cs[0]->flags & (SEQPLAN_ISP_FLAG_TIMELINE | SEQPLAN_ISP_FLAG_PROFILE)) {
+      ISP_CUDA(cudaStreamSynchronize(st));
+      for (int r = 0; r < world; ++r) {
+        collect_timeline(cs[r]);
+        collect_kprof(cs[r]);
+      }
+    }
   } catch (const IspError& e) {
     return fail(cs[0], e);
   }
   return SEQPLAN_ISP_OK;
 }
+
+int seqplan_isp_kernel_profile(seqplan_isp_ctx* c, seqplan_kernel_record* out, int64_t* n, int clear) {
+  if (!c || !n) return SEQPLAN_ISP_ERR_INVALID;
+  const int64_t have = static_cast<int64_t>(c->kprof.size());
+  if (out) {
+    const int64_t k = std::min(*n, have);
+    for (int64_t i = 0; i < k; ++i) out[i] = c->kprof[size_t(i)];
+  }
+  *n = have;
+  if (clear) c->kprof.clear();
+  return SEQPLAN_ISP_OK;
+}
+
+int64_t seqplan_isp_launch_count(const seqplan_isp_ctx* c) { return c ? c->launches : -1; }
 
 int seqplan_isp_pool_stats(seqplan_isp_ctx* c, seqplan_step_stats* out) {
   if (!c || !out) return SEQPLAN_ISP_ERR_INVALID;
