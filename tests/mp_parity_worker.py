@@ -1,0 +1,73 @@
+"""torchrun worker: multi-process ISP block (real CUDA IPC peers) vs the CPU oracle.
+Launched by tests/test_multiprocess_gpu.py; prints one JSON line per rank."""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from oracle import block as ob  # noqa: E402
+from paper_2401_09149_b200 import capi  # noqa: E402
+from paper_2401_09149_b200.dist import bootstrap_peers  # noqa: E402
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64); b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def main():
+    H, D, S = (int(v) for v in sys.argv[1:4])
+    fused = len(sys.argv) > 4 and sys.argv[4] == "fused"
+    world, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    sh = ob.Shape(H=H, D=D, S=S)
+    w = ob.make_weights(sh)
+    x = torch.from_numpy(ob.make_activation(sh, ob.TID_X)).bfloat16()
+    dy = torch.from_numpy(ob.make_activation(sh, ob.TID_DY)).bfloat16()
+    T = S // world
+    flags = capi.FLAG_TIMELINE | (capi.FLAG_FUSED_BWD if fused else 0)
+    blk = capi.IspBlock(H, D, S, world=world, rank=rank, device=local, flags=flags)
+    bootstrap_peers(blk, world)
+    for t in range(7):
+        flat = w[t].reshape(-1)
+        per = flat.size // world
+        blk.set_weight_shard(t, flat[rank * per:(rank + 1) * per])
+    dist.barrier()
+    xd = x[rank * T:(rank + 1) * T].to(dev)
+    dyd = dy[rank * T:(rank + 1) * T].to(dev)
+    y, dx = torch.empty_like(xd), torch.empty_like(xd)
+    for _ in range(2):  # second step checks recycling / epochs
+        blk.fwd(xd, y)
+        blk.bwd(dyd, dx)
+        torch.cuda.synchronize()
+    res = {"rank": rank}
+    if rank == 0:
+        y_ref, dx_ref, g_ref = ob.block(sh, w, x.float().numpy(), dy.float().numpy(), p=1)
+        ref = (y_ref, dx_ref, g_ref)
+    else:
+        ref = None
+    obj = [ref]
+    dist.broadcast_object_list(obj, src=0)
+    y_ref, dx_ref, g_ref = obj[0]
+    res["y"] = rel(y.float().cpu(), y_ref[rank * T:(rank + 1) * T])
+    res["dx"] = rel(dx.float().cpu(), dx_ref[rank * T:(rank + 1) * T])
+    for t in range(7):
+        flat = g_ref[t].reshape(-1)
+        per = flat.size // world
+        res[capi.W_NAMES[t]] = rel(blk.grad_shard(t), flat[rank * per:(rank + 1) * per])
+    res["timeline_events"] = len(blk.timeline())
+    print(json.dumps(res), flush=True)
+    blk.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
