@@ -1,0 +1,55 @@
+"""CPU tests of host-side logic: device-pool placement vs the reference pool model, and the
+multi-process peer bootstrap over a world-size-2 gloo group."""
+import os
+import subprocess
+from pathlib import Path
+
+import pytest
+import torch.multiprocessing as mp
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_device_pool_matches_run_mempool(tmp_path):
+    exe = tmp_path / "test_device_pool"
+    subprocess.run(["g++", "-std=c++20", "-O1", f"-I{ROOT/'include'}", "-I/usr/local/cuda/include",
+                    str(ROOT / "tests" / "cpp" / "test_device_pool.cpp"), "-o", str(exe),
+                    "-L/usr/local/cuda/lib64", "-lcudart"], check=True, capture_output=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True,
+                       env={**os.environ, "LD_LIBRARY_PATH": "/usr/local/cuda/lib64"})
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+class _FakeBlock:
+    def __init__(self, rank):
+        self.rank = rank
+        self.opened = None
+
+    def ipc_handle(self):
+        return bytes([self.rank]) * 64
+
+    def open_peers(self, handles):
+        self.opened = handles
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    from paper_2401_09149_b200.dist import bootstrap_peers
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    blk = _FakeBlock(rank)
+    bootstrap_peers(blk, world)
+    q.put((rank, [h[0] for h in blk.opened], [len(h) for h in blk.opened]))
+    dist.destroy_process_group()
+
+
+def test_peer_bootstrap_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, 29611, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == [(0, [0, 1], [64, 64]), (1, [0, 1], [64, 64])]
