@@ -14,6 +14,7 @@
 #include <cuda_bf16.h>
 
 #include "common.cuh"
+#include "gemm.h"
 #include "kernels.h"
 
 namespace isp {
@@ -50,7 +51,7 @@ __global__ void allgather_pull_kernel(PeerPtrs src, int world, int64_t shard_vec
   }
 }
 
-// gate|up gathered into one [2*rows, cols] buffer interleaved in 64-row blocks.
+// gate|up gathered into one [2*rows, cols] buffer interleaved in kGuBlock-row blocks.
 __global__ void allgather_interleave_kernel(PeerPtrs sg, PeerPtrs su, int world, int64_t rows,
                                             int64_t cols, uint4* dst) {
   const int64_t cvec = cols / 8;
@@ -59,9 +60,9 @@ __global__ void allgather_interleave_kernel(PeerPtrs sg, PeerPtrs su, int world,
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t drow = i / cvec, c = i % cvec;
-    const int64_t blk = drow / 64, within = drow % 64;
+    const int64_t blk = drow / kGuBlock, within = drow % kGuBlock;
     const bool up = blk & 1;
-    const int64_t srow = (blk >> 1) * 64 + within;
+    const int64_t srow = (blk >> 1) * kGuBlock + within;
     const int q = static_cast<int>(srow / rows_per_rank);
     const int64_t off = (srow - q * rows_per_rank) * cvec + c;
     const uint4* s = static_cast<const uint4*>(up ? su.p[q] : sg.p[q]);
@@ -124,7 +125,7 @@ __global__ void reduce_scatter_interleave_kernel(PeerPtrs part, int world, int r
     const int64_t li = up ? i - rpr * c8 : i;
     const int64_t lrow = li / c8, c = li % c8;
     const int64_t srow = rank * rpr + lrow;
-    const int64_t irow = (srow / 64) * 128 + (up ? 64 : 0) + srow % 64;
+    const int64_t irow = (srow / kGuBlock) * 2 * kGuBlock + (up ? kGuBlock : 0) + srow % kGuBlock;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int q = 0; q < world; ++q)
       add8(acc, ld_v4(static_cast<const __nv_bfloat16*>(part.p[q]) + irow * cols + c * 8));
@@ -255,7 +256,7 @@ cudaError_t allgather_pull(const PeerPtrs& src, int world, int64_t shard_elems, 
 cudaError_t allgather_pull_interleave(const PeerPtrs& sg, const PeerPtrs& su, int world,
                                       int64_t rows, int64_t cols, __nv_bfloat16* dst,
                                       cudaStream_t st, int num_ctas) {
-  if (cols % 8 || rows % 64 || rows % world) return cudaErrorInvalidValue;
+  if (cols % 8 || rows % kGuBlock || rows % world) return cudaErrorInvalidValue;
   allgather_interleave_kernel<<<ctas(2 * rows * cols / 8, 256, num_ctas), 256, 0, st>>>(
       sg, su, world, rows, cols, reinterpret_cast<uint4*>(dst));
   return cudaGetLastError();
@@ -280,7 +281,7 @@ cudaError_t reduce_scatter_pull_interleave(const PeerPtrs& part, int world, int 
                                            int64_t cols, float scale, int accumulate,
                                            float* out_gate, float* out_up, cudaStream_t st,
                                            int num_ctas) {
-  if (cols % 8 || rows % world || rows % 64) return cudaErrorInvalidValue;
+  if (cols % 8 || rows % world || rows % kGuBlock) return cudaErrorInvalidValue;
   reduce_scatter_interleave_kernel<<<ctas(2 * rows / world * cols / 8, 256, num_ctas), 256, 0, st>>>(
       part, world, rank, rows, cols, scale, accumulate, out_gate, out_up);
   return cudaGetLastError();

@@ -8,6 +8,7 @@
 #include <cuda_bf16.h>
 
 #include "common.cuh"
+#include "gemm.h"
 #include "kernels.h"
 
 namespace isp {
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_bwd_kernel(
     const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
     const float* __restrict__ rstd, const __nv_bfloat16* __restrict__ dn,
     const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx,
-    float* __restrict__ dg, int T, int H) {
+    float* __restrict__ dg, float* __restrict__ dg_part, int T, int H) {
   __shared__ float red[4];
   const int nvec = H / 8;
   float dgacc[kNormMaxVec][8];
@@ -165,41 +166,65 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_bwd_kernel(
 #pragma unroll
   for (int c = 0; c < kNormMaxVec; ++c) {
     const int vi = threadIdx.x + c * kNormThreads;
-    if (vi < nvec)
+    if (vi < nvec) {
+      if (dg_part) {  // stage 1 of a deterministic two-stage column reduction
+        float4* o = reinterpret_cast<float4*>(dg_part + static_cast<int64_t>(blockIdx.x) * H + vi * 8);
+        o[0] = make_float4(dgacc[c][0], dgacc[c][1], dgacc[c][2], dgacc[c][3]);
+        o[1] = make_float4(dgacc[c][4], dgacc[c][5], dgacc[c][6], dgacc[c][7]);
+      } else {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) atomicAdd(dg + vi * 8 + e, dgacc[c][e]);
+        for (int e = 0; e < 8; ++e) atomicAdd(dg + vi * 8 + e, dgacc[c][e]);
+      }
+    }
   }
+}
+
+// dg[j] += sum_b part[b, j]
+__global__ void column_sum_kernel(const float* __restrict__ part, int rows, int H, float* __restrict__ dg) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= H) return;
+  float s = 0.f;
+  for (int b = 0; b < rows; ++b) s += part[static_cast<int64_t>(b) * H + j];
+  dg[j] += s;
 }
 
 // In-place rotate-half RoPE on the q and k parts of token rows (ld elements apart).
-// dir = +1 forward rotation, -1 its transpose (backward).
+// dir = +1 forward rotation, -1 its transpose (backward). One thread = 8 pairs (16-B vectors).
 __global__ void rope_kernel(__nv_bfloat16* __restrict__ qkv, int64_t ld, int T, int t0,
                             int heads, int d, const float* __restrict__ cos_t,
                             const float* __restrict__ sin_t, int k_offset, int dir) {
-  const int half = d / 2;
-  const int pairs_per_row = 2 * heads * half;  // q and k
-  const int64_t total = static_cast<int64_t>(T) * pairs_per_row / 2;  // 2 pairs per thread
+  const int half = d / 2, g8 = half / 8;
+  const int per_row = 2 * heads * g8;  // q and k
+  const int64_t total = static_cast<int64_t>(T) * per_row;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t pidx = i * 2;
-    const int t = static_cast<int>(pidx / pairs_per_row);
-    int rem = static_cast<int>(pidx % pairs_per_row);
-    const int part = rem / (heads * half);
-    rem %= heads * half;
-    const int h = rem / half, j = rem % half;  // j even
+    const int t = static_cast<int>(i / per_row);
+    int rem = static_cast<int>(i % per_row);
+    const int part = rem / (heads * g8);
+    rem %= heads * g8;
+    const int h = rem / g8, j = (rem % g8) * 8;
     __nv_bfloat16* base = qkv + static_cast<int64_t>(t) * ld + (part ? k_offset : 0) + h * d;
-    const float2 c = *reinterpret_cast<const float2*>(cos_t + static_cast<int64_t>(t0 + t) * half + j);
-    float2 s = *reinterpret_cast<const float2*>(sin_t + static_cast<int64_t>(t0 + t) * half + j);
-    if (dir < 0) { s.x = -s.x; s.y = -s.y; }
-    const float2 a = unpack_bf16(*reinterpret_cast<uint32_t*>(base + j));
-    const float2 b = unpack_bf16(*reinterpret_cast<uint32_t*>(base + j + half));
-    *reinterpret_cast<uint32_t*>(base + j) = pack_bf16(a.x * c.x - b.x * s.x, a.y * c.y - b.y * s.y);
-    *reinterpret_cast<uint32_t*>(base + j + half) =
-        pack_bf16(b.x * c.x + a.x * s.x, b.y * c.y + a.y * s.y);
+    const float* cp = cos_t + static_cast<int64_t>(t0 + t) * half + j;
+    const float* sp = sin_t + static_cast<int64_t>(t0 + t) * half + j;
+    const float4 c0 = *reinterpret_cast<const float4*>(cp), c1 = *reinterpret_cast<const float4*>(cp + 4);
+    const float4 s0 = *reinterpret_cast<const float4*>(sp), s1 = *reinterpret_cast<const float4*>(sp + 4);
+    const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    const float sg = dir < 0 ? -1.f : 1.f;
+    const float sn[8] = {sg * s0.x, sg * s0.y, sg * s0.z, sg * s0.w, sg * s1.x, sg * s1.y, sg * s1.z, sg * s1.w};
+    float a[8], b[8], oa[8], ob[8];
+    load8(base + j, a);
+    load8(base + j + half, b);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      oa[e] = a[e] * cs[e] - b[e] * sn[e];
+      ob[e] = b[e] * cs[e] + a[e] * sn[e];
+    }
+    store8(base + j, oa);
+    store8(base + j + half, ob);
   }
 }
 
-// dgu (64-col interleaved gate|up) from da and saved gu.
+// dgu (kGuBlock-col interleaved gate|up) from da and saved gu.
 __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ da,
                                   const __nv_bfloat16* __restrict__ gu,
                                   __nv_bfloat16* __restrict__ dgu, int T, int I) {
@@ -208,8 +233,8 @@ __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ da,
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t col8 = (i % (I / 8)) * 8;
     const int64_t t = i / (I / 8);
-    const int64_t blk = col8 / 64, within = col8 % 64;
-    const int64_t gcol = blk * 128 + within, ucol = gcol + 64;
+    const int64_t blk = col8 / kGuBlock, within = col8 % kGuBlock;
+    const int64_t gcol = blk * 2 * kGuBlock + within, ucol = gcol + kGuBlock;
     float dav[8], gv[8], uv[8], dg[8], du[8];
     load8(da + t * I + col8, dav);
     load8(gu + t * 2 * I + gcol, gv);
@@ -232,6 +257,8 @@ int grid_for(int64_t work, int threads, int num_sms) {
 }
 
 }  // namespace
+
+int rmsnorm_bwd_scratch_rows(int num_sms) { return num_sms; }
 
 uint64_t keyed_stream_base(uint64_t seed, int tensor_id) {
   uint64_t z = seed * 0x9E3779B97F4A7C15ULL + static_cast<uint64_t>(tensor_id);
@@ -274,23 +301,26 @@ cudaError_t rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfl
 
 cudaError_t rmsnorm_bwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const float* rstd,
                         const __nv_bfloat16* dn, const __nv_bfloat16* dres, __nv_bfloat16* dx,
-                        float* dg, int T, int H, cudaStream_t st, int num_sms) {
+                        float* dg, int T, int H, cudaStream_t st, int num_sms, float* dg_scratch) {
   if (H % 8 || H > kNormThreads * kNormVecCap * 8) return cudaErrorInvalidValue;
-  const int grid = T < num_sms * 4 ? T : num_sms * 4;
+  const int cap = dg_scratch ? rmsnorm_bwd_scratch_rows(num_sms) : num_sms * 4;
+  const int grid = T < cap ? T : cap;
   const int nv = (H / 8 + kNormThreads - 1) / kNormThreads;
   switch (nv) {
-#define ISP_NORM_CASE(N) case N: rmsnorm_bwd_kernel<N><<<grid, kNormThreads, 0, st>>>(x, g, rstd, dn, dres, dx, dg, T, H); break;
+#define ISP_NORM_CASE(N) case N: rmsnorm_bwd_kernel<N><<<grid, kNormThreads, 0, st>>>(x, g, rstd, dn, dres, dx, dg, dg_scratch, T, H); break;
     ISP_NORM_CASE(1) ISP_NORM_CASE(2) ISP_NORM_CASE(3) ISP_NORM_CASE(4)
     ISP_NORM_CASE(5) ISP_NORM_CASE(6) ISP_NORM_CASE(7) ISP_NORM_CASE(8)
 #undef ISP_NORM_CASE
   }
+  if (dg_scratch) column_sum_kernel<<<(H + 255) / 256, 256, 0, st>>>(dg_scratch, grid, H, dg);
   return cudaGetLastError();
 }
 
 cudaError_t rope_inplace(__nv_bfloat16* qkv, int64_t ld, int T, int t0, int heads, int d,
                          const float* cos_t, const float* sin_t, int k_offset, int dir,
                          cudaStream_t st, int num_sms) {
-  const int64_t work = static_cast<int64_t>(T) * heads * (d / 2);
+  if (d % 16) return cudaErrorInvalidValue;
+  const int64_t work = static_cast<int64_t>(T) * 2 * heads * (d / 16);
   rope_kernel<<<grid_for(work, 256, num_sms), 256, 0, st>>>(qkv, ld, T, t0, heads, d, cos_t, sin_t,
                                                             k_offset, dir);
   return cudaGetLastError();
@@ -298,7 +328,7 @@ cudaError_t rope_inplace(__nv_bfloat16* qkv, int64_t ld, int T, int t0, int head
 
 cudaError_t swiglu_bwd(const __nv_bfloat16* da, const __nv_bfloat16* gu, __nv_bfloat16* dgu, int T,
                        int I, cudaStream_t st, int num_sms) {
-  if (I % 64) return cudaErrorInvalidValue;
+  if (I % kGuBlock) return cudaErrorInvalidValue;
   const int64_t work = static_cast<int64_t>(T) * I / 8;
   swiglu_bwd_kernel<<<grid_for(work, 256, num_sms), 256, 0, st>>>(da, gu, dgu, T, I);
   return cudaGetLastError();

@@ -15,7 +15,7 @@
 // global). A 4..6 stage smem ring feeds the tensor core; the accumulator is
 // double-buffered in TMEM so the epilogue of tile i overlaps the mainloop of
 // tile i+1. Fused epilogues: plain bf16 store, residual add, SwiGLU (gate/up
-// interleaved in 64-column blocks), fp32 store with scale/accumulate and
+// interleaved in 32-column blocks), fp32 store with scale/accumulate and
 // optional gate/up de-interleave (used for weight gradients).
 #include <cstdio>
 #include <cudaTypedefs.h>
@@ -180,42 +180,38 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const uint32_t t_base = tmem_base + (static_cast<uint32_t>(lane_grp * 32) << 16) + acc * BN;
 
       if constexpr (EPI == EPI_SWIGLU) {
-        // 64-column blocks alternate gate / up; pair block 2j with 2j+1.
+        // kGuBlock(=32)-column blocks alternate gate / up: pair chunk 2j (gate) with 2j+1 (up).
 #pragma unroll 1
-        for (int blk = 0; blk < BN / 128; ++blk) {
-#pragma unroll 1
-          for (int half = 0; half < 2; ++half) {
-            const int cg = blk * 128 + half * 32;  // gate column within tile
-            uint32_t g[32], u[32];
-            tmem_ld_32x32b_x32(t_base + cg, g);
-            tmem_ld_32x32b_x32(t_base + cg + 64, u);
-            tmem_ld_wait();
-            __nv_bfloat16* gu_row = reinterpret_cast<__nv_bfloat16*>(args.out) +
-                                    static_cast<int64_t>(row) * args.ldo + n0;
-            __nv_bfloat16* a_row = args.out2 + static_cast<int64_t>(row) * args.ldo2 +
-                                   (n0 / 2 + blk * 64 + half * 32);
-            uint4* gdst = reinterpret_cast<uint4*>(gu_row + cg);
-            uint4* udst = reinterpret_cast<uint4*>(gu_row + cg + 64);
-            uint4* adst = reinterpret_cast<uint4*>(a_row);
+        for (int pr = 0; pr < BN / 64; ++pr) {
+          const int cg = pr * 64;  // gate column within tile
+          uint32_t g[32], u[32];
+          tmem_ld_32x32b_x32(t_base + cg, g);
+          tmem_ld_32x32b_x32(t_base + cg + kGuBlock, u);
+          tmem_ld_wait();
+          __nv_bfloat16* gu_row = reinterpret_cast<__nv_bfloat16*>(args.out) +
+                                  static_cast<int64_t>(row) * args.ldo + n0;
+          __nv_bfloat16* a_row = args.out2 + static_cast<int64_t>(row) * args.ldo2 + (n0 / 2 + pr * 32);
+          uint4* gdst = reinterpret_cast<uint4*>(gu_row + cg);
+          uint4* udst = reinterpret_cast<uint4*>(gu_row + cg + kGuBlock);
+          uint4* adst = reinterpret_cast<uint4*>(a_row);
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              uint32_t pg[4], pu[4], pa[4];
+          for (int v = 0; v < 4; ++v) {
+            uint32_t pg[4], pu[4], pa[4];
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int i = v * 8 + e * 2;
-                const float g0 = __uint_as_float(g[i]), g1 = __uint_as_float(g[i + 1]);
-                const float u0 = __uint_as_float(u[i]), u1 = __uint_as_float(u[i + 1]);
-                pg[e] = pack_bf16(g0, g1);
-                pu[e] = pack_bf16(u0, u1);
-                // activation from the bf16-rounded values the backward will see
-                const float2 gr = unpack_bf16(pg[e]);
-                const float2 ur = unpack_bf16(pu[e]);
-                pa[e] = pack_bf16(silu(gr.x) * ur.x, silu(gr.y) * ur.y);
-              }
-              gdst[v] = make_uint4(pg[0], pg[1], pg[2], pg[3]);
-              udst[v] = make_uint4(pu[0], pu[1], pu[2], pu[3]);
-              adst[v] = make_uint4(pa[0], pa[1], pa[2], pa[3]);
+            for (int e = 0; e < 4; ++e) {
+              const int i = v * 8 + e * 2;
+              const float g0 = __uint_as_float(g[i]), g1 = __uint_as_float(g[i + 1]);
+              const float u0 = __uint_as_float(u[i]), u1 = __uint_as_float(u[i + 1]);
+              pg[e] = pack_bf16(g0, g1);
+              pu[e] = pack_bf16(u0, u1);
+              // activation from the bf16-rounded values the backward will see
+              const float2 gr = unpack_bf16(pg[e]);
+              const float2 ur = unpack_bf16(pu[e]);
+              pa[e] = pack_bf16(silu(gr.x) * ur.x, silu(gr.y) * ur.y);
             }
+            gdst[v] = make_uint4(pg[0], pg[1], pg[2], pg[3]);
+            udst[v] = make_uint4(pu[0], pu[1], pu[2], pu[3]);
+            adst[v] = make_uint4(pa[0], pa[1], pa[2], pa[3]);
           }
         }
       } else {
@@ -228,9 +224,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           if constexpr (EPI == EPI_F32) {
             float* dst;
             int64_t orow = row;
-            if (args.interleave64) {
-              const int blk = row >> 6;
-              orow = static_cast<int64_t>(blk >> 1) * 64 + (row & 63);
+            if (args.interleave64) {  // gate|up rows interleaved in kGuBlock-row blocks
+              const int blk = row / kGuBlock;
+              orow = static_cast<int64_t>(blk >> 1) * kGuBlock + (row % kGuBlock);
               dst = (blk & 1) ? args.out_b : reinterpret_cast<float*>(args.out);
             } else {
               dst = reinterpret_cast<float*>(args.out);

@@ -7,11 +7,16 @@
 
 namespace isp {
 
+// gate|up are interleaved in blocks of kGuBlock rows (weights) / columns (activations) so one
+// GEMM produces both and its epilogue applies SwiGLU. 32 keeps every rank's I/p-row shard
+// (I % 256 == 0, p <= 8) block-aligned, so gathers are strided copy-engine copies.
+constexpr int kGuBlock = 32;
+
 enum GemmEpilogue : int {
   EPI_BF16 = 0,        // out(bf16) = scale * acc
   EPI_BF16_RESID = 1,  // out(bf16) = scale * acc + resid(bf16)
-  EPI_SWIGLU = 2,      // out(bf16) = acc (gate/up interleaved by 64 cols); out2 = silu(g) * u
-  EPI_F32 = 3,         // out(f32) (+)= scale * acc; optional 64-row gate/up de-interleave
+  EPI_SWIGLU = 2,      // out(bf16) = acc (gate/up interleaved by kGuBlock cols); out2 = silu(g) * u
+  EPI_F32 = 3,         // out(f32) (+)= scale * acc; optional kGuBlock-row gate/up de-interleave
 };
 
 // One GEMM operand. Logical shape is [rows, K] (A: rows = M, B: rows = N).

@@ -23,6 +23,7 @@
 // the remaining compute (selective overlap, overlap_sim.hpp:141-150).
 // Group mode (p contexts on one GPU, tests): the same phases run in lock-step on
 // one stream with the collectives inline, which needs no cross-rank spinning.
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -30,6 +31,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <string>
@@ -73,6 +75,32 @@ struct IspError {
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// Stream memory operations (executed by the GPU front end, no SM needed): used for the
+// cross-GPU barrier so a comm-stream barrier never waits for SMs held by a persistent GEMM.
+using PfnWriteValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using PfnWaitValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+struct MemOps {
+  PfnWriteValue32 write = nullptr;
+  PfnWaitValue32 wait = nullptr;
+  bool ok() const { return write && wait; }
+};
+const MemOps& memops() {
+  static MemOps m = [] {
+    MemOps r;
+    if (std::getenv("SEQPLAN_ISP_KERNEL_BARRIER")) return r;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      r.write = reinterpret_cast<PfnWriteValue32>(p);
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      r.wait = reinterpret_cast<PfnWaitValue32>(p);
+    return r;
+  }();
+  return m;
+}
+
 }  // namespace
 }  // namespace isp
 
@@ -111,7 +139,7 @@ struct seqplan_isp_ctx {
   bf16 *gu = nullptr, *a = nullptr;  // transient: fwd -> bwd
   // backward scratch
   bf16 *dh = nullptr, *dn = nullptr, *dO_heads = nullptr, *dqkv_tok = nullptr;
-  float *delta = nullptr, *dq_acc = nullptr;
+  float *delta = nullptr, *dq_acc = nullptr, *dg_scratch = nullptr;
   bf16* local_part[SEQPLAN_W_COUNT] = {};  // p = 1 not used
 
   // ---- streams / events ----
@@ -119,6 +147,8 @@ struct seqplan_isp_ctx {
   cudaEvent_t ev_gathered[SEQPLAN_W_COUNT] = {};
   cudaEvent_t ev_wgrad[SEQPLAN_W_COUNT] = {};
   cudaEvent_t ev_comm_done = nullptr, ev_start = nullptr;
+  cudaEvent_t ev_staged[SEQPLAN_W_COUNT] = {};
+  void* stage[SEQPLAN_W_COUNT] = {};  // RS staging: this rank's slice of every rank's partial
   bool weights_dirty = true;
   bool fwd_done = false;
   const void* last_x = nullptr;
@@ -246,6 +276,20 @@ void barrier(Ctx* c, cudaStream_t st, bool comm_lane) {
   uint32_t& ep = comm_lane ? c->epoch_comm : c->epoch_compute;
   ++ep;
   const size_t off = c->off_flags + (comm_lane ? 64 * sizeof(uint32_t) : 0);
+  const MemOps& mo = memops();
+  if (mo.ok()) {  // publish epoch into every peer's slot for this rank, then wait for all peers
+    for (int q = 0; q < c->world; ++q) {
+      auto dst = reinterpret_cast<CUdeviceptr>(c->peer<uint32_t>(q, off) + c->rank);
+      if (mo.write(reinterpret_cast<CUstream>(st), dst, ep, 0) != CUDA_SUCCESS)
+        throw IspError(SEQPLAN_ISP_ERR_RUNTIME, "cuStreamWriteValue32 to a peer failed");
+    }
+    for (int q = 0; q < c->world; ++q) {
+      auto mine = reinterpret_cast<CUdeviceptr>(c->hp<uint32_t>(off) + q);
+      if (mo.wait(reinterpret_cast<CUstream>(st), mine, ep, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+        throw IspError(SEQPLAN_ISP_ERR_RUNTIME, "cuStreamWaitValue32 failed");
+    }
+    return;
+  }
   ISP_LAUNCH(1, peer_barrier(c->peers_at(off), c->world, c->rank, ep, c->error_flag, st));
 }
 
@@ -261,20 +305,39 @@ void gather_weight(Ctx* c, int t, cudaStream_t st) {
   }
   Span sp(c, st, 1, SEQPLAN_EV_ALL_GATHER, t);
   const double frac = double(c->world - 1) / double(c->world);
-  if (t == SEQPLAN_W_GATE) {  // gate|up gathered together, interleaved
+  const bool ce = !c->group_mode;  // copy engines: no SM is taken from the compute stream
+  if (t == SEQPLAN_W_GATE) {  // gate|up gathered together, interleaved in kGuBlock-row blocks
     const int64_t bytes = 2 * c->I * c->H * 2;
     KTimer kt(c, st, SEQPLAN_K_ALL_GATHER, 0, frac * double(bytes));
     bf16* dst = static_cast<bf16*>(pool_alloc(c, bytes, seqplan::AllocTag::CommBuffer, st));
-    ISP_LAUNCH(1, allgather_pull_interleave(c->peers_at(c->off_wshard[SEQPLAN_W_GATE]),
-                                       c->peers_at(c->off_wshard[SEQPLAN_W_UP]), c->world, c->I, c->H,
-                                       dst, st, kCommCtas));
+    if (ce) {
+      const int64_t B = kGuBlock, H = c->H, rpr = c->I / c->world;
+      for (int q = 0; q < c->world; ++q)
+        for (int which = 0; which < 2; ++which) {
+          const bf16* src = c->peer<bf16>(q, c->off_wshard[which ? SEQPLAN_W_UP : SEQPLAN_W_GATE]);
+          bf16* d0 = dst + ((q * rpr / B) * 2 * B + which * B) * H;
+          ISP_CUDA(cudaMemcpy2DAsync(d0, size_t(2 * B * H * 2), src, size_t(B * H * 2), size_t(B * H * 2),
+                                     size_t(rpr / B), cudaMemcpyDefault, st));
+        }
+    } else {
+      ISP_LAUNCH(1, allgather_pull_interleave(c->peers_at(c->off_wshard[SEQPLAN_W_GATE]),
+                                              c->peers_at(c->off_wshard[SEQPLAN_W_UP]), c->world, c->I, c->H,
+                                              dst, st, kCommCtas));
+    }
     c->gathered[t] = dst;
   } else {
     const int64_t bytes = c->numel(t) * 2;
     KTimer kt(c, st, SEQPLAN_K_ALL_GATHER, 0, frac * double(bytes));
     bf16* dst = static_cast<bf16*>(pool_alloc(c, bytes, seqplan::AllocTag::CommBuffer, st));
-    ISP_LAUNCH(1, allgather_pull(c->peers_at(c->off_wshard[t]), c->world, c->shard(t), dst, st, c->num_sms,
-                            kCommCtas));
+    if (ce) {
+      const int64_t sh = c->shard(t);
+      for (int q = 0; q < c->world; ++q)
+        ISP_CUDA(cudaMemcpyAsync(dst + q * sh, c->peer<bf16>(q, c->off_wshard[t]), size_t(sh * 2),
+                                 cudaMemcpyDefault, st));
+    } else {
+      ISP_LAUNCH(1, allgather_pull(c->peers_at(c->off_wshard[t]), c->world, c->shard(t), dst, st, c->num_sms,
+                                   kCommCtas));
+    }
     c->gathered[t] = dst;
   }
 }
@@ -464,12 +527,64 @@ void wgrad(Ctx* c, int t, const GemmOperand& A, const GemmOperand& B, int M, int
 }
 
 // After the G-W of tensor t: hand its partial to the comm stream for the reduce-scatter.
+// Copy-engine staging of this rank's slice of every rank's partial (rank order) on the comm
+// stream; the fp32 reduction + cast/scale runs later on the compute stream (reduce_staged).
+void stage_rs(Ctx* c, int t, cudaStream_t cs) {
+  const bool norm = (t == SEQPLAN_W_NORM1 || t == SEQPLAN_W_NORM2);
+  const int64_t esz = norm ? 4 : 2;
+  const int64_t H = c->H, p = c->world;
+  Span sp(c, cs, 1, SEQPLAN_EV_REDUCE_SCATTER, t);
+  if (t == SEQPLAN_W_GATE) {
+    const int64_t rpr = c->I / p, B = kGuBlock, slot = 2 * rpr * H;  // [gate rpr x H | up rpr x H]
+    KTimer kt(c, cs, SEQPLAN_K_REDUCE_SCATTER, 0, double(p - 1) * double(slot) * 2);
+    bf16* stg = static_cast<bf16*>(pool_alloc(c, p * slot * 2, seqplan::AllocTag::CommBuffer, cs));
+    for (int q = 0; q < p; ++q)
+      for (int which = 0; which < 2; ++which) {
+        const bf16* src = c->peer<bf16>(q, c->off_part[SEQPLAN_W_GATE]) + ((c->rank * rpr / B) * 2 * B + which * B) * H;
+        ISP_CUDA(cudaMemcpy2DAsync(stg + q * slot + which * rpr * H, size_t(B * H * 2), src, size_t(2 * B * H * 2),
+                                   size_t(B * H * 2), size_t(rpr / B), cudaMemcpyDefault, cs));
+      }
+    c->stage[t] = stg;
+  } else {
+    const int64_t sh = c->shard(t);
+    KTimer kt(c, cs, SEQPLAN_K_REDUCE_SCATTER, 0, double(p - 1) * double(sh) * double(esz));
+    char* stg = static_cast<char*>(pool_alloc(c, p * sh * esz, seqplan::AllocTag::CommBuffer, cs));
+    for (int q = 0; q < p; ++q)
+      ISP_CUDA(cudaMemcpyAsync(stg + q * sh * esz, c->peer<char>(q, c->off_part[t]) + c->rank * sh * esz,
+                               size_t(sh * esz), cudaMemcpyDefault, cs));
+    c->stage[t] = stg;
+  }
+  ISP_CUDA(cudaEventRecord(c->ev_staged[t], cs));
+}
+
+void reduce_staged(Ctx* c, int t, cudaStream_t st) {
+  if (!c->stage[t]) return;
+  ISP_CUDA(cudaStreamWaitEvent(st, c->ev_staged[t], 0));
+  const bool norm = (t == SEQPLAN_W_NORM1 || t == SEQPLAN_W_NORM2);
+  PeerPtrs src{};
+  if (t == SEQPLAN_W_GATE) {
+    const int64_t slot = 2 * (c->I / c->world) * c->H, half = slot / 2;
+    bf16* stg = static_cast<bf16*>(c->stage[t]);
+    for (int q = 0; q < c->world; ++q) src.p[q] = stg + q * slot;
+    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, half, false, 1.0f, 0, c->grad[SEQPLAN_W_GATE], st, c->num_sms * 4));
+    for (int q = 0; q < c->world; ++q) src.p[q] = stg + q * slot + half;
+    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, half, false, 1.0f, 0, c->grad[SEQPLAN_W_UP], st, c->num_sms * 4));
+  } else {
+    const int64_t sh = c->shard(t), esz = norm ? 4 : 2;
+    char* stg = static_cast<char*>(c->stage[t]);
+    for (int q = 0; q < c->world; ++q) src.p[q] = stg + q * sh * esz;
+    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, sh, norm, 1.0f, 0, c->grad[t], st, c->num_sms * 4));
+  }
+  c->pool.free(c->stage[t], st);
+  c->stage[t] = nullptr;
+}
+
 void schedule_rs(Ctx* c, int t, cudaStream_t st) {
-  if (c->world == 1 || c->group_mode) return;
+  if (c->world == 1 || c->group_mode || c->skip_comm()) return;
   ISP_CUDA(cudaEventRecord(c->ev_wgrad[t], st));
   ISP_CUDA(cudaStreamWaitEvent(c->comm, c->ev_wgrad[t], 0));
   barrier(c, c->comm, true);
-  reduce_scatter_grad(c, t, c->comm);
+  stage_rs(c, t, c->comm);
 }
 
 void bwd_phase1(Ctx* c, const bf16* dy, cudaStream_t st) {
@@ -519,7 +634,7 @@ void bwd_phase1(Ctx* c, const bf16* dy, cudaStream_t st) {
   wait_gathered(c, SEQPLAN_W_NORM2, st);
   float* dg2 = c->world == 1 ? c->grad[SEQPLAN_W_NORM2] : c->hp<float>(c->off_part[SEQPLAN_W_NORM2]);
   ISP_CUDA(cudaMemsetAsync(dg2, 0, sizeof(float) * H, st));
-  ISP_LAUNCH(1, rmsnorm_bwd(c->h, c->gathered[SEQPLAN_W_NORM2], c->rstd2, c->dn, dy, c->dh, dg2, T, H, st, c->num_sms));
+  ISP_LAUNCH(2, rmsnorm_bwd(c->h, c->gathered[SEQPLAN_W_NORM2], c->rstd2, c->dn, dy, c->dh, dg2, T, H, st, c->num_sms, c->dg_scratch));
   release_weight(c, SEQPLAN_W_NORM2, st);
   if (selective) schedule_rs(c, SEQPLAN_W_NORM2, st);
   // ---- output projection ----
@@ -586,7 +701,7 @@ void bwd_phase3(Ctx* c, const bf16* x, bf16* dx, cudaStream_t st) {
   wait_gathered(c, SEQPLAN_W_NORM1, st);
   float* dg1 = c->world == 1 ? c->grad[SEQPLAN_W_NORM1] : c->hp<float>(c->off_part[SEQPLAN_W_NORM1]);
   ISP_CUDA(cudaMemsetAsync(dg1, 0, sizeof(float) * H, st));
-  ISP_LAUNCH(1, rmsnorm_bwd(x, c->gathered[SEQPLAN_W_NORM1], c->rstd1, c->dn, c->dh, dx, dg1, T, H, st, c->num_sms));
+  ISP_LAUNCH(2, rmsnorm_bwd(x, c->gathered[SEQPLAN_W_NORM1], c->rstd1, c->dn, c->dh, dx, dg1, T, H, st, c->num_sms, c->dg_scratch));
   release_weight(c, SEQPLAN_W_NORM1, st);
   if (selective) schedule_rs(c, SEQPLAN_W_NORM1, st);
 }
@@ -694,11 +809,13 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   c->dqkv_tok = static_cast<bf16*>(A(T * 3 * H * 2));
   c->delta = static_cast<float*>(A(c->Dl * S * 4));
   c->dq_acc = static_cast<float*>(A(c->Dl * S * c->d * 4));
+  c->dg_scratch = static_cast<float*>(A(int64_t(rmsnorm_bwd_scratch_rows(c->num_sms)) * H * 4));
 
   ISP_CUDA(cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking));
   for (int t = 0; t < SEQPLAN_W_COUNT; ++t) {
     ISP_CUDA(cudaEventCreateWithFlags(&c->ev_gathered[t], cudaEventDisableTiming));
     ISP_CUDA(cudaEventCreateWithFlags(&c->ev_wgrad[t], cudaEventDisableTiming));
+    ISP_CUDA(cudaEventCreateWithFlags(&c->ev_staged[t], cudaEventDisableTiming));
   }
   ISP_CUDA(cudaEventCreateWithFlags(&c->ev_comm_done, cudaEventDisableTiming));
   ISP_CUDA(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
@@ -725,13 +842,11 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
 void refresh_working(Ctx* c, int t, cudaStream_t st) {
   ISP_CUDA(cast_f32_bf16(c->master[t], c->wshard(t), c->shard(t), st, c->num_sms));
   if (c->world == 1 && (t == SEQPLAN_W_GATE || t == SEQPLAN_W_UP)) {
-    // p = 1: keep the gate|up working copy interleaved in 64-row blocks for the fused GEMM
-    const int64_t rows = c->I, cols = c->H;
-    for (int64_t blk = 0; blk < rows / 64; ++blk) {
-      const int64_t drow = blk * 128 + (t == SEQPLAN_W_UP ? 64 : 0);
-      ISP_CUDA(cudaMemcpyAsync(c->wgu_local + drow * cols, c->wshard(t) + blk * 64 * cols, 64 * cols * 2,
+    // p = 1: keep the gate|up working copy interleaved in kGuBlock-row blocks for the fused GEMM
+    const int64_t rows = c->I, cols = c->H, B = kGuBlock;
+    ISP_CUDA(cudaMemcpy2DAsync(c->wgu_local + (t == SEQPLAN_W_UP ? B : 0) * cols, size_t(2 * B * cols * 2),
+                               c->wshard(t), size_t(B * cols * 2), size_t(B * cols * 2), size_t(rows / B),
                                cudaMemcpyDeviceToDevice, st));
-    }
   }
   c->weights_dirty = true;
 }
@@ -834,6 +949,7 @@ void seqplan_isp_ctx_destroy(seqplan_isp_ctx* c) {
   for (int t = 0; t < SEQPLAN_W_COUNT; ++t) {
     if (c->ev_gathered[t]) cudaEventDestroy(c->ev_gathered[t]);
     if (c->ev_wgrad[t]) cudaEventDestroy(c->ev_wgrad[t]);
+    if (c->ev_staged[t]) cudaEventDestroy(c->ev_staged[t]);
   }
   if (c->ev_comm_done) cudaEventDestroy(c->ev_comm_done);
   if (c->ev_start) cudaEventDestroy(c->ev_start);
@@ -995,7 +1111,9 @@ static void run_bwd(Ctx* c, const bf16* x, const bf16* dy, bf16* dx, cudaStream_
     barrier(c, st, false);
     bwd_reduce_all(c, st);
   } else if (c->world > 1) {
-    // join the comm stream (its reduce-scatters) back into the caller's stream
+    // reduce the staged slices (fp32 accumulate, cast/scale) and join the comm stream
+    for (int t : {SEQPLAN_W_DOWN, SEQPLAN_W_GATE, SEQPLAN_W_NORM2, SEQPLAN_W_O, SEQPLAN_W_QKV, SEQPLAN_W_NORM1})
+      reduce_staged(c, t, st);
     ISP_CUDA(cudaEventRecord(c->ev_comm_done, c->comm));
     ISP_CUDA(cudaStreamWaitEvent(st, c->ev_comm_done, 0));
   }

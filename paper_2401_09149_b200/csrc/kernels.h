@@ -16,9 +16,13 @@ cudaError_t cast_f32_bf16(const float* in, __nv_bfloat16* out, int64_t n, cudaSt
                           int num_sms);
 cudaError_t rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* y,
                         float* rstd, int T, int H, float eps, cudaStream_t st, int num_sms);
+// dg += column sums; with dg_scratch (>= rmsnorm_bwd_scratch_rows(num_sms) x H fp32) the
+// reduction is two-stage and deterministic, otherwise fp32 atomics.
 cudaError_t rmsnorm_bwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const float* rstd,
                         const __nv_bfloat16* dn, const __nv_bfloat16* dres, __nv_bfloat16* dx,
-                        float* dg, int T, int H, cudaStream_t st, int num_sms);
+                        float* dg, int T, int H, cudaStream_t st, int num_sms,
+                        float* dg_scratch = nullptr);
+int rmsnorm_bwd_scratch_rows(int num_sms);
 cudaError_t rope_inplace(__nv_bfloat16* qkv, int64_t ld, int T, int t0, int heads, int d,
                          const float* cos_t, const float* sin_t, int k_offset, int dir,
                          cudaStream_t st, int num_sms);

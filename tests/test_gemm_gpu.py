@@ -49,15 +49,15 @@ def test_gemm_swiglu(cuda):
     M, K, I = 256, 256, 384
     A = _rand(M, K, dev=cuda)
     Wg, Wu = _rand(I, K, dev=cuda), _rand(I, K, dev=cuda)
-    # interleave 64-row blocks: gate blk j, up blk j, ...
-    Wgu = torch.stack([Wg.view(I // 64, 64, K), Wu.view(I // 64, 64, K)], 1).reshape(2 * I, K)
+    # interleave 32-row blocks (kGuBlock): gate blk j, up blk j, ...
+    Wgu = torch.stack([Wg.view(I // 32, 32, K), Wu.view(I // 32, 32, K)], 1).reshape(2 * I, K)
     gu = torch.empty(M, 2 * I, device=cuda, dtype=torch.bfloat16)
     a = torch.empty(M, I, device=cuda, dtype=torch.bfloat16)
     capi.debug_gemm(A, Wgu, gu, M, 2 * I, K, epi=2, out2=a)
     torch.cuda.synchronize()
     g = A.float() @ Wg.float().t()
     u = A.float() @ Wu.float().t()
-    gu_v = gu.view(M, I // 64, 2, 64)
+    gu_v = gu.view(M, I // 32, 2, 32)
     assert rel_l2(gu_v[:, :, 0].reshape(M, I), g) < 4e-3
     assert rel_l2(gu_v[:, :, 1].reshape(M, I), u) < 4e-3
     assert rel_l2(a, torch.nn.functional.silu(g) * u) < 1e-2
@@ -74,7 +74,7 @@ def test_gemm_f32_interleaved_wgrad(cuda):
                     scale=0.25, accumulate=True, interleave64=True)
     torch.cuda.synchronize()
     full = 0.25 * (dgu.float().t() @ x.float())  # [2I, H] interleaved
-    fv = full.view(I // 64, 2, 64, H)
+    fv = full.view(I // 32, 2, 32, H)
     assert rel_l2(g_out - 1.0, fv[:, 0].reshape(I, H)) < 2e-3
     assert rel_l2(u_out - 1.0, fv[:, 1].reshape(I, H)) < 2e-3
 
