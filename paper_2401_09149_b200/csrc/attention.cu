@@ -14,6 +14,8 @@
 //             dK/dV in registers, dQ accumulated in fp32 with vector atomics.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -461,6 +463,13 @@ cudaError_t bwd_impl(const AttnTensors& t, const __nv_bfloat16* dout, __nv_bfloa
   cudaError_t e = cudaMemsetAsync(dq_acc, 0, sizeof(float) * static_cast<size_t>(t.heads) * t.S * D, st);
   if (e != cudaSuccess) return e;
   attn_delta_kernel<D><<<num_sms * 8, 256, 0, st>>>(t.o, t.ld_o, dout, delta, t.S, t.heads);
+  if (D == 128 && !std::getenv("SEQPLAN_ISP_ATTN_MMA_SYNC")) {
+    // tcgen05/TMEM backward (attention_tc.cu); it applies the softmax scale to dq_acc itself
+    e = attention_bwd_tc(t, dout, t.ld_o, dk, dv, ld_d, delta, dq_acc, st);
+    if (e != cudaSuccess) return e;
+    attn_dq_convert_kernel<D><<<num_sms * 8, 256, 0, st>>>(dq_acc, dq, ld_d, t.S, t.heads, 1.0f);
+    return cudaGetLastError();
+  }
   attn_bwd_kernel<D><<<dim3(t.S / BN, t.heads), 256, smem, st>>>(t, dout, dk, dv, ld_d, delta, dq_acc, scale);
   attn_dq_convert_kernel<D><<<num_sms * 8, 256, 0, st>>>(dq_acc, dq, ld_d, t.S, t.heads, scale);
   return cudaGetLastError();
@@ -471,6 +480,7 @@ cudaError_t bwd_impl(const AttnTensors& t, const __nv_bfloat16* dout, __nv_bfloa
 cudaError_t attention_fwd(const AttnTensors& t, cudaStream_t st, int num_sms) {
   (void)num_sms;
   if (t.S % 128) return cudaErrorInvalidValue;
+  if (!std::getenv("SEQPLAN_ISP_ATTN_MMA_SYNC")) return attention_fwd_tc(t, st);
   if (t.d == 128) return fwd_impl<128>(t, st);
   if (t.d == 64) return fwd_impl<64>(t, st);
   return cudaErrorInvalidValue;

@@ -1,0 +1,630 @@
+// Causal flash-attention forward on tcgen05 / TMEM / TMA (sm_100a).
+//
+// Per rank this is the attention of D/p heads over the full sequence after the Ulysses
+// all-to-all (priced at cost.hpp:217). CTA = 128 queries x 1 head.
+//   warp 0      TMA producer: Q once, then K/V tiles of 64 keys into a 2-stage ring
+//   warp 1      MMA issuer (one lane): S_j = Q K_j^T into a double-buffered TMEM S, then
+//               O += P_{j-1} V_{j-1} with O resident in TMEM (software-pipelined by one tile)
+//   warps 2..5  softmax, one thread per query row (= TMEM lane): S row from TMEM, online
+//               softmax in exp2 with a stale-max rule (O rescaled in TMEM only when the row
+//               max grows by > 2^8, warp-uniformly), P (bf16) into a double-buffered
+//               SW128 smem tile that is the A operand of the PV MMA; epilogue O / l -> bf16.
+// Shared memory (d = 128): Q 32 KB + K/V 2 x 32 KB + P 2 x 16 KB = 128 KB; TMEM 256 columns.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace isp {
+
+namespace {
+
+constexpr int kBM = 128;      // queries per CTA
+constexpr int kBN = 64;       // keys per tile
+constexpr int kThreads = 192;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+__device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+      "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]),
+      "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int D>
+struct FwdSmem {
+  static constexpr int kQ = kBM * D * 2;       // D/64 chunks of [128 x 64]
+  static constexpr int kKV = kBN * D * 2;      // K (or V) tile: D/64 chunks of [64 x 64]
+  static constexpr int kP = kBM * kBN * 2;     // [128 x 64]
+  static constexpr int kOffQ = 0;
+  static constexpr int kOffK = kOffQ + kQ;     // 2 stages
+  static constexpr int kOffV = kOffK + 2 * kKV;
+  static constexpr int kOffP = kOffV + 2 * kKV;  // 2 buffers
+  static constexpr int kOffBar = kOffP + 2 * kP;
+  static constexpr int kBytes = kOffBar + 256 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
+                       const __grid_constant__ CUtensorMap mV, __nv_bfloat16* __restrict__ out,
+                       int64_t ld_o, float* __restrict__ lse, int S, float scale_log2) {
+  using L = FwdSmem<D>;
+  constexpr int NCH = D / 64;  // 64-wide chunks of the head dim
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
+  uint64_t* q_full = bar + 0;
+  uint64_t* kv_full = bar + 1;   // [2]
+  uint64_t* kv_empty = bar + 3;  // [2]
+  uint64_t* s_full = bar + 5;    // [2]
+  uint64_t* s_free = bar + 7;    // [2]
+  uint64_t* p_full = bar + 9;    // [2]
+  uint64_t* p_free = bar + 11;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int qt = gridDim.x - 1 - blockIdx.x;  // heavy (late) tiles first
+  const int h = blockIdx.y;
+  const int q0 = qt * kBM;
+  const int n_kv = (q0 + kBM) / kBN;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mQ);
+    tma_prefetch(&mK);
+    tma_prefetch(&mV);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 128);
+      mbar_init(&p_full[i], 128);
+      mbar_init(&p_free[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem;          // S buffers at columns 0 and 64
+  const uint32_t tO = tmem + 128;    // O at columns 128 .. 128 + D
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      mbar_arrive_expect_tx(q_full, L::kQ);
+      for (int c = 0; c < NCH; ++c)
+        tma_load_2d(smem + L::kOffQ + c * kBM * 128, &mQ, q_full, h * D + c * 64, q0);
+      for (int j = 0; j < n_kv; ++j) {
+        const int s = j & 1;
+        if (j >= 2) mbar_wait(&kv_empty[s], ((j >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(&kv_full[s], 2 * L::kKV);
+        for (int c = 0; c < NCH; ++c) {
+          tma_load_2d(smem + L::kOffK + s * L::kKV + c * kBN * 128, &mK, &kv_full[s], h * D + c * 64, j * kBN);
+          tma_load_2d(smem + L::kOffV + s * L::kKV + c * kBN * 128, &mV, &kv_full[s], h * D + c * 64, j * kBN);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      constexpr uint32_t idesc_s = make_idesc_bf16(kBM, kBN, false, false);
+      constexpr uint32_t idesc_o = make_idesc_bf16(kBM, D, false, true);
+      const uint32_t sQ = smem_u32(smem + L::kOffQ);
+      mbar_wait(q_full, 0);
+      auto issue_pv = [&](int j) {
+        const int b = j & 1;
+        mbar_wait(&p_full[b], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sP = smem_u32(smem + L::kOffP + b * L::kP);
+        const uint32_t sV = smem_u32(smem + L::kOffV + b * L::kKV);
+#pragma unroll
+        for (int k = 0; k < kBN / 16; ++k) {
+          const uint64_t ad = make_sw128_desc(sP + k * 32, 16, 1024);
+          const uint64_t bd = make_sw128_desc(sV + k * 2048, kBN * 128, 1024);
+          tc_mma_bf16(tO, ad, bd, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
+        }
+        tc_commit(&kv_empty[b]);
+        tc_commit(&p_free[b]);
+      };
+      for (int j = 0; j < n_kv; ++j) {
+        const int b = j & 1;
+        mbar_wait(&kv_full[b], (j >> 1) & 1);
+        if (j >= 2) mbar_wait(&s_free[b], ((j >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t sK = smem_u32(smem + L::kOffK + b * L::kKV);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const int c = k / 4, kk = k % 4;
+          const uint64_t ad = make_sw128_desc(sQ + c * kBM * 128 + kk * 32, 16, 1024);
+          const uint64_t bd = make_sw128_desc(sK + c * kBN * 128 + kk * 32, 16, 1024);
+          tc_mma_bf16(tS + b * kBN, ad, bd, idesc_s, k > 0 ? 1u : 0u);
+        }
+        tc_commit(&s_full[b]);
+        if (j >= 1) issue_pv(j - 1);
+      }
+      issue_pv(n_kv - 1);
+    }
+  } else {
+    // ---------------- softmax + epilogue (warps 2..5) ----------------
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;  // query row within the tile == TMEM lane
+    const int q = q0 + r;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    float m = -INFINITY, l = 0.f;
+    int pfree_seen[2] = {0, 0};
+    auto ensure_pfree = [&](int b, int count) {
+      while (pfree_seen[b] < count) {
+        mbar_wait(&p_free[b], pfree_seen[b] & 1);
+        ++pfree_seen[b];
+      }
+    };
+    for (int j = 0; j < n_kv; ++j) {
+      const int b = j & 1;
+      mbar_wait(&s_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t sr[64];
+      tmem_ld_32x32b_x32(tS + lane_off + b * kBN, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+      tmem_ld_32x32b_x32(tS + lane_off + b * kBN + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&s_free[b]);
+      float sv[64];
+      const bool diag = (j + 1) * kBN > q0;  // tile may contain keys > some query of the CTA
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        float v = __uint_as_float(sr[i]) * scale_log2;
+        if (diag && j * kBN + i > q) v = -INFINITY;
+        sv[i] = v;
+        mx = fmaxf(mx, v);
+      }
+      // stale-max online softmax: correct O only when the max grows by > 2^8 (warp-uniform)
+      const float m_new = fmaxf(m, mx);
+      if (j == 0) {
+        m = m_new;
+      } else if (__any_sync(0xffffffffu, m_new > m + kRescaleThreshold)) {
+        ensure_pfree((j - 1) & 1, ((j - 1) >> 1) + 1);  // PV_{j-1} has landed in O
+        tc_fence_after();
+        const float alpha = exp2f(m - m_new);
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t o[32];
+          tmem_ld_32x32b_x32(tO + lane_off + c * 32, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st_32x32b_x32(tO + lane_off + c * 32, o);
+        }
+        tmem_st_wait();
+        l *= alpha;
+        m = m_new;
+      }
+      // P = exp2(s - m) into the swizzled bf16 A tile
+      ensure_pfree(b, j >> 1);  // PV_{j-2} has finished reading this P buffer
+      uint8_t* prow = smem + L::kOffP + b * L::kP + r * 128;
+      float psum = 0.f;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint32_t pk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float p0 = exp2f(sv[c * 8 + 2 * e] - m), p1 = exp2f(sv[c * 8 + 2 * e + 1] - m);
+          psum += p0 + p1;
+          pk[e] = pack_bf16(p0, p1);
+        }
+        *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      }
+      l += psum;
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(&p_full[b]);
+    }
+    // epilogue: wait for the last PV, O / l -> bf16
+    ensure_pfree((n_kv - 1) & 1, ((n_kv - 1) >> 1) + 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    __nv_bfloat16* orow = out + static_cast<int64_t>(q) * ld_o + h * D;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t o[32];
+      tmem_ld_32x32b_x32(tO + lane_off + c * 32, o);
+      tmem_ld_wait();
+      uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint32_t pk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          pk[e] = pack_bf16(__uint_as_float(o[v * 8 + 2 * e]) * inv, __uint_as_float(o[v * 8 + 2 * e + 1]) * inv);
+        dst[v] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      }
+    }
+    lse[static_cast<int64_t>(h) * S + q] = (m + log2f(l)) * 0.6931471805599453f;
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// [rows, cols] bf16 with row stride ld elements; box {64 cols, box_rows}, 128-B swizzle.
+bool map2d(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint32_t box[2] = {64u, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t es[2] = {1u, 1u};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int D>
+cudaError_t launch_fwd(const AttnTensors& t, cudaStream_t st) {
+  using L = FwdSmem<D>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  CUtensorMap mq, mk, mv;
+  const int64_t cols = static_cast<int64_t>(t.heads) * D;
+  if (!map2d(&mq, t.q, t.S, cols, t.ld_qkv, kBM) || !map2d(&mk, t.k, t.S, cols, t.ld_qkv, kBN) ||
+      !map2d(&mv, t.v, t.S, cols, t.ld_qkv, kBN))
+    return cudaErrorInvalidValue;
+  const float scale_log2 = (1.0f / sqrtf(static_cast<float>(D))) * kLog2e;
+  attn_fwd_tc_kernel<D><<<dim3(t.S / kBM, t.heads), kThreads, L::kBytes, st>>>(mq, mk, mv, t.o, t.ld_o, t.lse, t.S,
+                                                                               scale_log2);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t attention_fwd_tc(const AttnTensors& t, cudaStream_t st) {
+  if (t.S % kBM) return cudaErrorInvalidValue;
+  if (t.d == 128) return launch_fwd<128>(t, st);
+  if (t.d == 64) return launch_fwd<64>(t, st);
+  return cudaErrorInvalidValue;
+}
+
+
+// =====================================================================================
+// Causal flash-attention backward on tcgen05 / TMEM / TMA (d = 128).
+//
+// CTA = 128 keys x 1 head; iterates over 64-query tiles i >= k0 (causal). Per tile:
+//   S^T  = K Q_i^T,  dP^T = V dO_i^T                (M=128 keys, N=64, K=d)   -> TMEM
+//   P^T  = exp2(S^T*scale*log2e - lse_i*log2e),  dS^T = P^T (dP^T - delta_i)  (8 warps:
+//          a warp pair per TMEM lane quadrant splits the 64 query columns; the math is
+//          elementwise given lse/delta per column, so no cross-warp reduction)
+//   dV  += P^T dO_i,  dK += dS^T Q_i               (M=128 keys, N=d, K=64)   TMEM-resident
+//   dQ_i^T = K^T dS^T                              (M=d, N=64, K=128 keys)   -> TMEM
+//          -> smem [64 q][d] fp32 -> one cp.reduce.async.bulk add.f32 into dq_acc (32 KB)
+// The MMA warp software-pipelines S/dP of tile i with the gradient MMAs of tile i-1.
+// Shared memory: K, V 64 KB + Q/dO 2-stage 64 KB + P^T, dS^T 32 KB + dQ staging 32 KB.
+// TMEM 512 columns: S^T 0, dP^T 64, dK 128, dV 256, dQ^T 384.
+// =====================================================================================
+namespace {
+
+constexpr int kBwdKeys = 128;
+constexpr int kBwdQ = 64;
+constexpr int kBwdThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 compute
+
+struct BwdSmem {
+  static constexpr int kKV = kBwdKeys * 128 * 2;      // [2 chunks][128 keys][64 d]
+  static constexpr int kQ = kBwdQ * 128 * 2;          // [2 chunks][64 q][64 d]
+  static constexpr int kP = kBwdKeys * kBwdQ * 2;     // [128 keys][64 q]
+  static constexpr int kStg = kBwdQ * 128 * 4;        // [64 q][128 d] fp32
+  static constexpr int kOffK = 0;
+  static constexpr int kOffV = kOffK + kKV;
+  static constexpr int kOffQ = kOffV + kKV;           // 2 stages
+  static constexpr int kOffDO = kOffQ + 2 * kQ;       // 2 stages
+  static constexpr int kOffP = kOffDO + 2 * kQ;
+  static constexpr int kOffDS = kOffP + kP;
+  static constexpr int kOffStg = kOffDS + kP;
+  static constexpr int kOffL = kOffStg + kStg;        // [2][64] lse
+  static constexpr int kOffD = kOffL + 2 * kBwdQ * 4; // [2][64] delta
+  static constexpr int kOffBar = kOffD + 2 * kBwdQ * 4;
+  static constexpr int kBytes = kOffBar + 256 + 1024;
+};
+
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_reduce_add_f32(float* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
+                       const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mDO,
+                       const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ dq_acc,
+                       __nv_bfloat16* __restrict__ dk_out, __nv_bfloat16* __restrict__ dv_out, int64_t ld_d,
+                       int S, float scale) {
+  using L = BwdSmem;
+  constexpr int D = 128;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* q_full = bar + 1;   // [2]
+  uint64_t* q_empty = bar + 3;  // [2]
+  uint64_t* s_full = bar + 5;
+  uint64_t* s_free = bar + 6;
+  uint64_t* p_full = bar + 7;
+  uint64_t* p_free = bar + 8;
+  uint64_t* dq_full = bar + 9;
+  uint64_t* dq_free = bar + 10;
+  uint64_t* dkv_full = bar + 11;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int kt = blockIdx.x, h = blockIdx.y;
+  const int k0 = kt * kBwdKeys;
+  const int qi0 = k0 / kBwdQ, nq = S / kBwdQ - qi0;
+  const float scale_log2 = scale * kLog2e;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mQ); tma_prefetch(&mK); tma_prefetch(&mV); tma_prefetch(&mDO);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&q_full[i], 1); mbar_init(&q_empty[i], 1); }
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 256);
+    mbar_init(p_full, 256);
+    mbar_init(p_free, 1);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_free, 256);
+    mbar_init(dkv_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tP = tmem + 64, tDK = tmem + 128, tDV = tmem + 256, tDQ = tmem + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      mbar_arrive_expect_tx(kv_full, 2 * L::kKV);
+      for (int c = 0; c < 2; ++c) {
+        tma_load_2d(smem + L::kOffK + c * kBwdKeys * 128, &mK, kv_full, h * D + c * 64, k0);
+        tma_load_2d(smem + L::kOffV + c * kBwdKeys * 128, &mV, kv_full, h * D + c * 64, k0);
+      }
+      const float* lse_h = lse + static_cast<int64_t>(h) * S;
+      const float* del_h = delta + static_cast<int64_t>(h) * S;
+      for (int i = 0; i < nq; ++i) {
+        const int s = i & 1, q0 = (qi0 + i) * kBwdQ;
+        if (i >= 2) mbar_wait(&q_empty[s], ((i >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(&q_full[s], 2 * L::kQ + 2 * kBwdQ * 4);
+        for (int c = 0; c < 2; ++c) {
+          tma_load_2d(smem + L::kOffQ + s * L::kQ + c * kBwdQ * 128, &mQ, &q_full[s], h * D + c * 64, q0);
+          tma_load_2d(smem + L::kOffDO + s * L::kQ + c * kBwdQ * 128, &mDO, &q_full[s], h * D + c * 64, q0);
+        }
+        bulk_load(smem + L::kOffL + s * kBwdQ * 4, lse_h + q0, kBwdQ * 4, &q_full[s]);
+        bulk_load(smem + L::kOffD + s * kBwdQ * 4, del_h + q0, kBwdQ * 4, &q_full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      constexpr uint32_t id_s = make_idesc_bf16(kBwdKeys, kBwdQ, false, false);  // S^T, dP^T
+      constexpr uint32_t id_g = make_idesc_bf16(kBwdKeys, D, false, true);       // dV, dK
+      constexpr uint32_t id_q = make_idesc_bf16(D, kBwdQ, true, true);           // dQ^T
+      const uint32_t sK = smem_u32(smem + L::kOffK), sV = smem_u32(smem + L::kOffV);
+      const uint32_t sP = smem_u32(smem + L::kOffP), sDS = smem_u32(smem + L::kOffDS);
+      mbar_wait(kv_full, 0);
+      auto grads = [&](int j) {
+        const int s = j & 1;
+        mbar_wait(p_full, j & 1);
+        if (j >= 1) mbar_wait(dq_free, (j - 1) & 1);
+        tc_fence_after();
+        const uint32_t sQ = smem_u32(smem + L::kOffQ + s * L::kQ), sDO = smem_u32(smem + L::kOffDO + s * L::kQ);
+#pragma unroll
+        for (int k = 0; k < kBwdQ / 16; ++k) {
+          tc_mma_bf16(tDV, make_sw128_desc(sP + k * 32, 16, 1024), make_sw128_desc(sDO + k * 2048, kBwdQ * 128, 1024),
+                      id_g, (j > 0 || k > 0) ? 1u : 0u);
+          tc_mma_bf16(tDK, make_sw128_desc(sDS + k * 32, 16, 1024), make_sw128_desc(sQ + k * 2048, kBwdQ * 128, 1024),
+                      id_g, (j > 0 || k > 0) ? 1u : 0u);
+        }
+#pragma unroll
+        for (int k = 0; k < kBwdKeys / 16; ++k)
+          tc_mma_bf16(tDQ, make_sw128_desc(sK + k * 2048, kBwdKeys * 128, 1024),
+                      make_sw128_desc(sDS + k * 2048, kBwdQ * 128, 1024), id_q, k > 0 ? 1u : 0u);
+        tc_commit(&q_empty[s]);
+        tc_commit(p_free);
+        tc_commit(dq_full);
+      };
+      for (int i = 0; i < nq; ++i) {
+        const int s = i & 1;
+        mbar_wait(&q_full[s], (i >> 1) & 1);
+        if (i >= 1) mbar_wait(s_free, (i - 1) & 1);
+        tc_fence_after();
+        const uint32_t sQ = smem_u32(smem + L::kOffQ + s * L::kQ), sDO = smem_u32(smem + L::kOffDO + s * L::kQ);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const int c = k / 4, kk = k % 4;
+          tc_mma_bf16(tS, make_sw128_desc(sK + c * kBwdKeys * 128 + kk * 32, 16, 1024),
+                      make_sw128_desc(sQ + c * kBwdQ * 128 + kk * 32, 16, 1024), id_s, k > 0 ? 1u : 0u);
+          tc_mma_bf16(tP, make_sw128_desc(sV + c * kBwdKeys * 128 + kk * 32, 16, 1024),
+                      make_sw128_desc(sDO + c * kBwdQ * 128 + kk * 32, 16, 1024), id_s, k > 0 ? 1u : 0u);
+        }
+        tc_commit(s_full);
+        if (i >= 1) grads(i - 1);
+      }
+      grads(nq - 1);
+      tc_commit(dkv_full);
+    }
+  } else {
+    // ---------------- compute warps 2..9 ----------------
+    const int quad = warp & 3, half = (warp - 2) >> 2;
+    const int r = quad * 32 + lane;            // key row (S/dP/dK/dV) or head-dim row (dQ^T)
+    const uint32_t lo = static_cast<uint32_t>(quad * 32) << 16;
+    const int key = k0 + r;
+    float* stg = reinterpret_cast<float*>(smem + L::kOffStg);
+    const bool leader = (warp == 2 && lane == 0);
+    auto dq_epilogue = [&](int j) {  // dQ^T of tile j -> staging -> bulk reduce-add
+      mbar_wait(dq_full, j & 1);
+      tc_fence_after();
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tDQ + lo + half * 32, v);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(dq_free);
+      if (leader) bulk_wait_read();  // previous reduce finished reading the staging tile
+      named_bar(1, 256);
+#pragma unroll
+      for (int c = 0; c < 32; ++c) stg[(half * 32 + c) * D + r] = __uint_as_float(v[c]) * scale;
+      fence_proxy_async();
+      named_bar(1, 256);
+      if (leader) {
+        const int q0 = (qi0 + j) * kBwdQ;
+        bulk_reduce_add_f32(dq_acc + (static_cast<int64_t>(h) * S + q0) * D, stg, L::kStg);
+      }
+    };
+    for (int i = 0; i < nq; ++i) {
+      const int s = i & 1, q0 = (qi0 + i) * kBwdQ;
+      mbar_wait(&q_full[s], (i >> 1) & 1);  // lse / delta of this tile
+      mbar_wait(s_full, i & 1);
+      tc_fence_after();
+      uint32_t sv[32], pv[32];
+      tmem_ld_32x32b_x32(tS + lo + half * 32, sv);
+      tmem_ld_32x32b_x32(tP + lo + half * 32, pv);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(s_free);
+      const float* sL = reinterpret_cast<const float*>(smem + L::kOffL + s * kBwdQ * 4) + half * 32;
+      const float* sD = reinterpret_cast<const float*>(smem + L::kOffD + s * kBwdQ * 4) + half * 32;
+      const bool diag = q0 < k0 + kBwdKeys;
+      uint32_t pk[16], dk[16];
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) {
+        float p2[2], d2[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int qc = half * 32 + c + e;
+          float p = exp2f(__uint_as_float(sv[c + e]) * scale_log2 - sL[c + e] * kLog2e);
+          if (diag && key > q0 + qc) p = 0.f;
+          p2[e] = p;
+          d2[e] = p * (__uint_as_float(pv[c + e]) - sD[c + e]);
+        }
+        pk[c / 2] = pack_bf16(p2[0], p2[1]);
+        dk[c / 2] = pack_bf16(d2[0], d2[1]);
+      }
+      if (i >= 1) mbar_wait(p_free, (i - 1) & 1);  // gradient MMAs of tile i-1 released P^T / dS^T
+      uint8_t* prow = smem + L::kOffP + r * 128;
+      uint8_t* drow = smem + L::kOffDS + r * 128;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const int chunk = (half * 4 + cc) ^ (r & 7);
+        *reinterpret_cast<uint4*>(prow + chunk * 16) = make_uint4(pk[4 * cc], pk[4 * cc + 1], pk[4 * cc + 2], pk[4 * cc + 3]);
+        *reinterpret_cast<uint4*>(drow + chunk * 16) = make_uint4(dk[4 * cc], dk[4 * cc + 1], dk[4 * cc + 2], dk[4 * cc + 3]);
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(p_full);
+      if (i >= 1) dq_epilogue(i - 1);
+    }
+    dq_epilogue(nq - 1);
+    if (leader) bulk_wait_all();
+    // dK (scaled), dV -> bf16
+    mbar_wait(dkv_full, 0);
+    tc_fence_after();
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      const int col = half * 64 + c * 32;
+      uint32_t a[32], b[32];
+      tmem_ld_32x32b_x32(tDK + lo + col, a);
+      tmem_ld_32x32b_x32(tDV + lo + col, b);
+      tmem_ld_wait();
+      uint4* pk_out = reinterpret_cast<uint4*>(dk_out + static_cast<int64_t>(key) * ld_d + h * D + col);
+      uint4* pv_out = reinterpret_cast<uint4*>(dv_out + static_cast<int64_t>(key) * ld_d + h * D + col);
+#pragma unroll
+      for (int v4 = 0; v4 < 4; ++v4) {
+        uint32_t x[4], y[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          x[e] = pack_bf16(__uint_as_float(a[v4 * 8 + 2 * e]) * scale, __uint_as_float(a[v4 * 8 + 2 * e + 1]) * scale);
+          y[e] = pack_bf16(__uint_as_float(b[v4 * 8 + 2 * e]), __uint_as_float(b[v4 * 8 + 2 * e + 1]));
+        }
+        pk_out[v4] = make_uint4(x[0], x[1], x[2], x[3]);
+        pv_out[v4] = make_uint4(y[0], y[1], y[2], y[3]);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace
+
+// dq_acc must be zeroed and delta = rowsum(dO * O) computed before this launch.
+cudaError_t attention_bwd_tc(const AttnTensors& t, const __nv_bfloat16* dout, int64_t ld_dout, __nv_bfloat16* dk,
+                             __nv_bfloat16* dv, int64_t ld_d, const float* delta, float* dq_acc, cudaStream_t st) {
+  if (t.d != 128 || t.S % kBwdKeys) return cudaErrorInvalidValue;
+  using L = BwdSmem;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  CUtensorMap mq, mk, mv, mdo;
+  const int64_t cols = static_cast<int64_t>(t.heads) * 128;
+  if (!map2d(&mq, t.q, t.S, cols, t.ld_qkv, kBwdQ) || !map2d(&mk, t.k, t.S, cols, t.ld_qkv, kBwdKeys) ||
+      !map2d(&mv, t.v, t.S, cols, t.ld_qkv, kBwdKeys) || !map2d(&mdo, dout, t.S, cols, ld_dout, kBwdQ))
+    return cudaErrorInvalidValue;
+  const float scale = 1.0f / sqrtf(128.0f);
+  attn_bwd_tc_kernel<<<dim3(t.S / kBwdKeys, t.heads), kBwdThreads, L::kBytes, st>>>(
+      mq, mk, mv, mdo, t.lse, delta, dq_acc, dk, dv, ld_d, t.S, scale);
+  return cudaGetLastError();
+}
+
+}  // namespace isp

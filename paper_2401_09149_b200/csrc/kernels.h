@@ -44,6 +44,11 @@ struct AttnTensors {
   int S, heads, d;
 };
 cudaError_t attention_fwd(const AttnTensors& t, cudaStream_t st, int num_sms);
+// tcgen05/TMEM/TMA forward (attention_tc.cu); attention_fwd dispatches here.
+cudaError_t attention_fwd_tc(const AttnTensors& t, cudaStream_t st);
+// tcgen05/TMEM backward for d = 128 (dK, dV written; dq_acc += scale * dS K, fp32).
+cudaError_t attention_bwd_tc(const AttnTensors& t, const __nv_bfloat16* dout, int64_t ld_dout, __nv_bfloat16* dk,
+                             __nv_bfloat16* dv, int64_t ld_d, const float* delta, float* dq_acc, cudaStream_t st);
 // dq/dk/dv written (bf16) with row stride ld_dqkv; scratch: fp32 [heads*S] (delta) and
 // fp32 [heads*S*d] (dq accumulator).
 cudaError_t attention_bwd(const AttnTensors& t, const __nv_bfloat16* dout, __nv_bfloat16* dq,

@@ -1,5 +1,6 @@
 """Quick GEMM timing (CUDA events) for development; not part of the bench contract."""
-import sys, time
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2401_09149_b200 import capi
 
