@@ -23,7 +23,7 @@ namespace {
 
 constexpr int kBM = 128;      // queries per CTA
 constexpr int kBN = 64;       // keys per tile
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 softmax
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
@@ -42,6 +42,14 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+__device__ __forceinline__ float fast_exp2(float x) {  // MUFU.EX2, flush-to-zero
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void named_barrier(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 
 template <int D>
 struct FwdSmem {
@@ -49,11 +57,13 @@ struct FwdSmem {
   static constexpr int kKV = kBN * D * 2;      // K (or V) tile: D/64 chunks of [64 x 64]
   static constexpr int kP = kBM * kBN * 2;     // [128 x 64]
   static constexpr int kOffQ = 0;
-  static constexpr int kOffK = kOffQ + kQ;     // 2 stages
-  static constexpr int kOffV = kOffK + 2 * kKV;
-  static constexpr int kOffP = kOffV + 2 * kKV;  // 2 buffers
+  static constexpr int kStages = D == 128 ? 4 : 6;  // K/V ring depth (hides TMA latency)
+  static constexpr int kOffK = kOffQ + kQ;
+  static constexpr int kOffV = kOffK + kStages * kKV;
+  static constexpr int kOffP = kOffV + kStages * kKV;  // 2 buffers
   static constexpr int kOffBar = kOffP + 2 * kP;
-  static constexpr int kBytes = kOffBar + 256 + 1024;
+  static constexpr int kBarBytes = 256;
+  static constexpr int kBytes = kOffBar + kBarBytes + 6 * kBM * 4 + 1024;  // barriers + max/sum exchange
 };
 
 template <int D>
@@ -66,14 +76,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
+  constexpr int NS = L::kStages;
   uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;   // [2]
-  uint64_t* kv_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;    // [2]
-  uint64_t* s_free = bar + 7;    // [2]
-  uint64_t* p_full = bar + 9;    // [2]
-  uint64_t* p_free = bar + 11;   // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
+  uint64_t* s_full = bar + 1;    // [2]
+  uint64_t* s_free = bar + 3;    // [2]
+  uint64_t* p_full = bar + 5;    // [2]
+  uint64_t* p_free = bar + 7;    // [2]
+  uint64_t* kv_full = bar + 9;   // [NS]
+  uint64_t* kv_empty = bar + 9 + NS;  // [NS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9 + 2 * NS);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int qt = gridDim.x - 1 - blockIdx.x;  // heavy (late) tiles first
@@ -86,12 +97,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&mK);
     tma_prefetch(&mV);
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NS; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 128);
-      mbar_init(&p_full[i], 128);
+      mbar_init(&s_free[i], 256);
+      mbar_init(&p_full[i], 256);
       mbar_init(&p_free[i], 1);
     }
     fence_barrier_init();
@@ -111,8 +124,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = 0; c < NCH; ++c)
         tma_load_2d(smem + L::kOffQ + c * kBM * 128, &mQ, q_full, h * D + c * 64, q0);
       for (int j = 0; j < n_kv; ++j) {
-        const int s = j & 1;
-        if (j >= 2) mbar_wait(&kv_empty[s], ((j >> 1) - 1) & 1);
+        const int s = j % NS;
+        if (j >= NS) mbar_wait(&kv_empty[s], ((j / NS) - 1) & 1);
         mbar_arrive_expect_tx(&kv_full[s], 2 * L::kKV);
         for (int c = 0; c < NCH; ++c) {
           tma_load_2d(smem + L::kOffK + s * L::kKV + c * kBN * 128, &mK, &kv_full[s], h * D + c * 64, j * kBN);
@@ -132,22 +145,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&p_full[b], (j >> 1) & 1);
         tc_fence_after();
         const uint32_t sP = smem_u32(smem + L::kOffP + b * L::kP);
-        const uint32_t sV = smem_u32(smem + L::kOffV + b * L::kKV);
+        const uint32_t sV = smem_u32(smem + L::kOffV + (j % NS) * L::kKV);
 #pragma unroll
         for (int k = 0; k < kBN / 16; ++k) {
           const uint64_t ad = make_sw128_desc(sP + k * 32, 16, 1024);
           const uint64_t bd = make_sw128_desc(sV + k * 2048, kBN * 128, 1024);
           tc_mma_bf16(tO, ad, bd, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
         }
-        tc_commit(&kv_empty[b]);
+        tc_commit(&kv_empty[j % NS]);
         tc_commit(&p_free[b]);
       };
       for (int j = 0; j < n_kv; ++j) {
         const int b = j & 1;
-        mbar_wait(&kv_full[b], (j >> 1) & 1);
+        mbar_wait(&kv_full[j % NS], (j / NS) & 1);
         if (j >= 2) mbar_wait(&s_free[b], ((j >> 1) - 1) & 1);
         tc_fence_after();
-        const uint32_t sK = smem_u32(smem + L::kOffK + b * L::kKV);
+        const uint32_t sK = smem_u32(smem + L::kOffK + (j % NS) * L::kKV);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const int c = k / 4, kk = k % 4;
@@ -161,11 +174,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       issue_pv(n_kv - 1);
     }
   } else {
-    // ---------------- softmax + epilogue (warps 2..5) ----------------
-    const int quad = warp & 3;
+    // ---------------- softmax + epilogue (warps 2..9) ----------------
+    // A warp pair per TMEM lane quadrant shares 32 query rows and splits the 64 key columns
+    // of S (and the D columns of O); the row max is exchanged through smem each tile.
+    const int quad = warp & 3, half = (warp - 2) >> 2;
     const int r = quad * 32 + lane;  // query row within the tile == TMEM lane
     const int q = q0 + r;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    float* xmax = reinterpret_cast<float*>(smem + L::kOffBar + L::kBarBytes);  // [2 slots][2 halves][128 rows]
     float m = -INFINITY, l = 0.f;
     int pfree_seen[2] = {0, 0};
     auto ensure_pfree = [&](int b, int count) {
@@ -178,72 +194,80 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int b = j & 1;
       mbar_wait(&s_full[b], (j >> 1) & 1);
       tc_fence_after();
-      uint32_t sr[64];
-      tmem_ld_32x32b_x32(tS + lane_off + b * kBN, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-      tmem_ld_32x32b_x32(tS + lane_off + b * kBN + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+      uint32_t sr[32];
+      tmem_ld_32x32b_x32(tS + lane_off + b * kBN + half * 32, sr);
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&s_free[b]);
-      float sv[64];
       const bool diag = (j + 1) * kBN > q0;  // tile may contain keys > some query of the CTA
       float mx = -INFINITY;
+      if (diag) {
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        float v = __uint_as_float(sr[i]) * scale_log2;
-        if (diag && j * kBN + i > q) v = -INFINITY;
-        sv[i] = v;
-        mx = fmaxf(mx, v);
+        for (int i = 0; i < 32; ++i)
+          if (j * kBN + half * 32 + i > q) sr[i] = __float_as_uint(-INFINITY);
       }
-      // stale-max online softmax: correct O only when the max grows by > 2^8 (warp-uniform)
+#pragma unroll
+      for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(sr[i]));
+      xmax[(b * 2 + half) * kBM + r] = mx;
+      named_barrier(2 + quad, 64);
+      mx = fmaxf(mx, xmax[(b * 2 + (half ^ 1)) * kBM + r]) * scale_log2;
+      // stale-max online softmax: correct O only when the max grows by > 2^8 (uniform across
+      // the pair: both warps hold the same rows and the same m)
       const float m_new = fmaxf(m, mx);
       if (j == 0) {
         m = m_new;
       } else if (__any_sync(0xffffffffu, m_new > m + kRescaleThreshold)) {
         ensure_pfree((j - 1) & 1, ((j - 1) >> 1) + 1);  // PV_{j-1} has landed in O
         tc_fence_after();
-        const float alpha = exp2f(m - m_new);
+        const float alpha = fast_exp2(m - m_new);
 #pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
+        for (int c = 0; c < D / 64; ++c) {
           uint32_t o[32];
-          tmem_ld_32x32b_x32(tO + lane_off + c * 32, o);
+          const uint32_t ta = tO + lane_off + half * (D / 2) + c * 32;
+          tmem_ld_32x32b_x32(ta, o);
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-          tmem_st_32x32b_x32(tO + lane_off + c * 32, o);
+          tmem_st_32x32b_x32(ta, o);
         }
         tmem_st_wait();
         l *= alpha;
         m = m_new;
       }
-      // P = exp2(s - m) into the swizzled bf16 A tile
-      ensure_pfree(b, j >> 1);  // PV_{j-2} has finished reading this P buffer
-      uint8_t* prow = smem + L::kOffP + b * L::kP + r * 128;
+      // P = exp2(s * scale - m) into this warp's half of the swizzled bf16 A tile
+      uint32_t pk[16];
       float psum = 0.f;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        uint32_t pk[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float p0 = exp2f(sv[c * 8 + 2 * e] - m), p1 = exp2f(sv[c * 8 + 2 * e + 1] - m);
-          psum += p0 + p1;
-          pk[e] = pack_bf16(p0, p1);
-        }
-        *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      for (int i = 0; i < 32; i += 2) {
+        const float p0 = fast_exp2(fmaf(__uint_as_float(sr[i]), scale_log2, -m));
+        const float p1 = fast_exp2(fmaf(__uint_as_float(sr[i + 1]), scale_log2, -m));
+        psum += p0 + p1;
+        pk[i / 2] = pack_bf16(p0, p1);
       }
       l += psum;
+      ensure_pfree(b, j >> 1);  // PV_{j-2} has finished reading this P buffer
+      uint8_t* prow = smem + L::kOffP + b * L::kP + r * 128;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc)
+        *reinterpret_cast<uint4*>(prow + (((half * 4 + cc) ^ (r & 7)) * 16)) =
+            make_uint4(pk[4 * cc], pk[4 * cc + 1], pk[4 * cc + 2], pk[4 * cc + 3]);
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(&p_full[b]);
     }
-    // epilogue: wait for the last PV, O / l -> bf16
+    // epilogue: combine the pair's partial row sums, wait for the last PV, O / l -> bf16
+    float* xsum = xmax + 4 * kBM;
+    xsum[half * kBM + r] = l;
+    named_barrier(2 + quad, 64);
+    const float l_tot = l + xsum[(half ^ 1) * kBM + r];
     ensure_pfree((n_kv - 1) & 1, ((n_kv - 1) >> 1) + 1);
     tc_fence_after();
-    const float inv = 1.f / l;
-    __nv_bfloat16* orow = out + static_cast<int64_t>(q) * ld_o + h * D;
+    const float inv = 1.f / l_tot;
+    __nv_bfloat16* orow = out + static_cast<int64_t>(q) * ld_o + h * D + half * (D / 2);
 #pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = 0; c < D / 64; ++c) {
       uint32_t o[32];
-      tmem_ld_32x32b_x32(tO + lane_off + c * 32, o);
+      tmem_ld_32x32b_x32(tO + lane_off + half * (D / 2) + c * 32, o);
       tmem_ld_wait();
       uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
@@ -255,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         dst[v] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
     }
-    lse[static_cast<int64_t>(h) * S + q] = (m + log2f(l)) * 0.6931471805599453f;
+    if (half == 0) lse[static_cast<int64_t>(h) * S + q] = (m + log2f(l_tot)) * 0.6931471805599453f;
   }
 
   tc_fence_before();
@@ -343,21 +367,23 @@ constexpr int kBwdQ = 64;
 constexpr int kBwdThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 compute
 
 struct BwdSmem {
+  static constexpr int kStages = 3;                   // Q/dO ring depth
   static constexpr int kKV = kBwdKeys * 128 * 2;      // [2 chunks][128 keys][64 d]
   static constexpr int kQ = kBwdQ * 128 * 2;          // [2 chunks][64 q][64 d]
+  static constexpr int kStage = 2 * kQ;               // Q_i | dO_i
   static constexpr int kP = kBwdKeys * kBwdQ * 2;     // [128 keys][64 q]
-  static constexpr int kStg = kBwdQ * 128 * 4;        // [64 q][128 d] fp32
+  static constexpr int kStg = kBwdQ * 128 * 4;        // [64 q][128 d] fp32 dQ staging
   static constexpr int kOffK = 0;
   static constexpr int kOffV = kOffK + kKV;
-  static constexpr int kOffQ = kOffV + kKV;           // 2 stages
-  static constexpr int kOffDO = kOffQ + 2 * kQ;       // 2 stages
-  static constexpr int kOffP = kOffDO + 2 * kQ;
+  static constexpr int kOffQ = kOffV + kKV;           // stage s: Q at kOffQ + s*kStage, dO at +kQ
+  static constexpr int kOffP = kOffQ + kStages * kStage;
   static constexpr int kOffDS = kOffP + kP;
   static constexpr int kOffStg = kOffDS + kP;
-  static constexpr int kOffL = kOffStg + kStg;        // [2][64] lse
-  static constexpr int kOffD = kOffL + 2 * kBwdQ * 4; // [2][64] delta
-  static constexpr int kOffBar = kOffD + 2 * kBwdQ * 4;
+  static constexpr int kOffL = kOffStg + kStg;        // [stages][64] lse
+  static constexpr int kOffD = kOffL + kStages * kBwdQ * 4;  // [stages][64] delta
+  static constexpr int kOffBar = kOffD + kStages * kBwdQ * 4;
   static constexpr int kBytes = kOffBar + 256 + 1024;
+  static_assert(kBytes <= 232448, "exceeds the 227 KB per-CTA shared memory");
 };
 
 __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
@@ -387,17 +413,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
+  constexpr int NS = L::kStages;
   uint64_t* kv_full = bar + 0;
-  uint64_t* q_full = bar + 1;   // [2]
-  uint64_t* q_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;
-  uint64_t* s_free = bar + 6;
-  uint64_t* p_full = bar + 7;
-  uint64_t* p_free = bar + 8;
-  uint64_t* dq_full = bar + 9;
-  uint64_t* dq_free = bar + 10;
-  uint64_t* dkv_full = bar + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t* s_full = bar + 1;
+  uint64_t* s_free = bar + 2;
+  uint64_t* p_full = bar + 3;
+  uint64_t* p_free = bar + 4;
+  uint64_t* dq_full = bar + 5;
+  uint64_t* dq_free = bar + 6;
+  uint64_t* dkv_full = bar + 7;
+  uint64_t* q_full = bar + 8;        // [NS]
+  uint64_t* q_empty = bar + 8 + NS;  // [NS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8 + 2 * NS);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int kt = blockIdx.x, h = blockIdx.y;
@@ -408,7 +435,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mQ); tma_prefetch(&mK); tma_prefetch(&mV); tma_prefetch(&mDO);
     mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) { mbar_init(&q_full[i], 1); mbar_init(&q_empty[i], 1); }
+    for (int i = 0; i < NS; ++i) { mbar_init(&q_full[i], 1); mbar_init(&q_empty[i], 1); }
     mbar_init(s_full, 1);
     mbar_init(s_free, 256);
     mbar_init(p_full, 256);
@@ -436,12 +463,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const float* lse_h = lse + static_cast<int64_t>(h) * S;
       const float* del_h = delta + static_cast<int64_t>(h) * S;
       for (int i = 0; i < nq; ++i) {
-        const int s = i & 1, q0 = (qi0 + i) * kBwdQ;
-        if (i >= 2) mbar_wait(&q_empty[s], ((i >> 1) - 1) & 1);
+        const int s = i % NS, q0 = (qi0 + i) * kBwdQ;
+        if (i >= NS) mbar_wait(&q_empty[s], ((i / NS) - 1) & 1);
         mbar_arrive_expect_tx(&q_full[s], 2 * L::kQ + 2 * kBwdQ * 4);
         for (int c = 0; c < 2; ++c) {
-          tma_load_2d(smem + L::kOffQ + s * L::kQ + c * kBwdQ * 128, &mQ, &q_full[s], h * D + c * 64, q0);
-          tma_load_2d(smem + L::kOffDO + s * L::kQ + c * kBwdQ * 128, &mDO, &q_full[s], h * D + c * 64, q0);
+          tma_load_2d(smem + L::kOffQ + s * L::kStage + c * kBwdQ * 128, &mQ, &q_full[s], h * D + c * 64, q0);
+          tma_load_2d(smem + L::kOffQ + s * L::kStage + L::kQ + c * kBwdQ * 128, &mDO, &q_full[s], h * D + c * 64, q0);
         }
         bulk_load(smem + L::kOffL + s * kBwdQ * 4, lse_h + q0, kBwdQ * 4, &q_full[s]);
         bulk_load(smem + L::kOffD + s * kBwdQ * 4, del_h + q0, kBwdQ * 4, &q_full[s]);
@@ -457,11 +484,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint32_t sP = smem_u32(smem + L::kOffP), sDS = smem_u32(smem + L::kOffDS);
       mbar_wait(kv_full, 0);
       auto grads = [&](int j) {
-        const int s = j & 1;
+        const int s = j % NS;
         mbar_wait(p_full, j & 1);
         if (j >= 1) mbar_wait(dq_free, (j - 1) & 1);
         tc_fence_after();
-        const uint32_t sQ = smem_u32(smem + L::kOffQ + s * L::kQ), sDO = smem_u32(smem + L::kOffDO + s * L::kQ);
+        const uint32_t sQ = smem_u32(smem + L::kOffQ + s * L::kStage), sDO = sQ + L::kQ;
 #pragma unroll
         for (int k = 0; k < kBwdQ / 16; ++k) {
           tc_mma_bf16(tDV, make_sw128_desc(sP + k * 32, 16, 1024), make_sw128_desc(sDO + k * 2048, kBwdQ * 128, 1024),
@@ -478,11 +505,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_commit(dq_full);
       };
       for (int i = 0; i < nq; ++i) {
-        const int s = i & 1;
-        mbar_wait(&q_full[s], (i >> 1) & 1);
+        const int s = i % NS;
+        mbar_wait(&q_full[s], (i / NS) & 1);
         if (i >= 1) mbar_wait(s_free, (i - 1) & 1);
         tc_fence_after();
-        const uint32_t sQ = smem_u32(smem + L::kOffQ + s * L::kQ), sDO = smem_u32(smem + L::kOffDO + s * L::kQ);
+        const uint32_t sQ = smem_u32(smem + L::kOffQ + s * L::kStage), sDO = sQ + L::kQ;
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const int c = k / 4, kk = k % 4;
@@ -503,9 +530,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int r = quad * 32 + lane;            // key row (S/dP/dK/dV) or head-dim row (dQ^T)
     const uint32_t lo = static_cast<uint32_t>(quad * 32) << 16;
     const int key = k0 + r;
-    float* stg = reinterpret_cast<float*>(smem + L::kOffStg);
     const bool leader = (warp == 2 && lane == 0);
-    auto dq_epilogue = [&](int j) {  // dQ^T of tile j -> staging -> bulk reduce-add
+    float* stg = reinterpret_cast<float*>(smem + L::kOffStg);
+    auto dq_epilogue = [&](int j) {  // dQ^T of tile j -> smem staging -> bulk reduce-add
       mbar_wait(dq_full, j & 1);
       tc_fence_after();
       uint32_t v[32];
@@ -513,10 +540,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(dq_free);
-      if (leader) bulk_wait_read();  // previous reduce finished reading the staging tile
+      if (leader) bulk_wait_read();  // the reduce of tile j-1 has finished reading the staging
       named_bar(1, 256);
+      const uint32_t stg_a = smem_u32(stg) + static_cast<uint32_t>((half * 32 * D + r) * 4);
 #pragma unroll
-      for (int c = 0; c < 32; ++c) stg[(half * 32 + c) * D + r] = __uint_as_float(v[c]) * scale;
+      for (int c = 0; c < 32; ++c)
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(stg_a + c * D * 4), "f"(__uint_as_float(v[c]) * scale) : "memory");
       fence_proxy_async();
       named_bar(1, 256);
       if (leader) {
@@ -525,8 +554,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
     };
     for (int i = 0; i < nq; ++i) {
-      const int s = i & 1, q0 = (qi0 + i) * kBwdQ;
-      mbar_wait(&q_full[s], (i >> 1) & 1);  // lse / delta of this tile
+      const int s = i % NS, q0 = (qi0 + i) * kBwdQ;
+      mbar_wait(&q_full[s], (i / NS) & 1);  // lse / delta of this tile
       mbar_wait(s_full, i & 1);
       tc_fence_after();
       uint32_t sv[32], pv[32];
@@ -545,7 +574,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int qc = half * 32 + c + e;
-          float p = exp2f(__uint_as_float(sv[c + e]) * scale_log2 - sL[c + e] * kLog2e);
+          float p = fast_exp2(fmaf(__uint_as_float(sv[c + e]), scale_log2, -sL[c + e] * kLog2e));
           if (diag && key > q0 + qc) p = 0.f;
           p2[e] = p;
           d2[e] = p * (__uint_as_float(pv[c + e]) - sD[c + e]);
