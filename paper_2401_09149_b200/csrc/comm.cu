@@ -158,58 +158,62 @@ __device__ __forceinline__ void rotate8(uint4& lo, uint4& hi, const float* c, co
 }
 
 // Token-sharded [T, parts*H] on every rank -> head-sharded [S, parts*Hl] on this rank.
-// Work unit: (global token s, part, local head, 8-element group j of the low half);
-// optional RoPE on parts < rope_parts at global position s.
-__global__ void a2a_to_heads_kernel(PeerPtrs src, int world, int rank, int T, int H, int parts,
-                                    int d, __nv_bfloat16* __restrict__ dst,
-                                    const float* __restrict__ cos_t,
-                                    const float* __restrict__ sin_t, int rope_parts) {
+// Work unit: (global token s, part, local head, 8-element group j of the low half); optional
+// RoPE on parts < rope_parts at global position s. 32-bit index math (units < 2^31).
+__global__ void __launch_bounds__(256) a2a_to_heads_kernel(PeerPtrs src, int world, int rank, int T, int H,
+                                                           int parts, int d, __nv_bfloat16* __restrict__ dst,
+                                                           const float* __restrict__ cos_t,
+                                                           const float* __restrict__ sin_t, int rope_parts) {
   const int Hl = H / world, heads_l = Hl / d, half = d / 2, g8 = half / 8;
-  const int64_t S = static_cast<int64_t>(T) * world;
-  const int64_t per_row = static_cast<int64_t>(parts) * heads_l * g8;
-  const int64_t total = S * per_row;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t s = i / per_row;
-    int rem = static_cast<int>(i % per_row);
-    const int part = rem / (heads_l * g8);
-    rem %= heads_l * g8;
-    const int hl = rem / g8, j = (rem % g8) * 8;
-    const int q = static_cast<int>(s / T);
-    const int64_t t = s % T;
-    const __nv_bfloat16* sp = static_cast<const __nv_bfloat16*>(src.p[q]) + t * parts * H +
-                              part * H + rank * Hl + hl * d + j;
-    __nv_bfloat16* dp = dst + s * parts * Hl + part * Hl + hl * d + j;
+  const int per_part = heads_l * g8;
+  const int per_row = parts * per_part;
+  const int total = T * world * per_row;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int s = i / per_row;
+    int rem = i - s * per_row;
+    const int part = rem / per_part;
+    rem -= part * per_part;
+    const int hl = rem / g8, j = (rem - hl * g8) * 8;
+    const int q = s / T, t = s - q * T;
+    const __nv_bfloat16* sp = static_cast<const __nv_bfloat16*>(src.p[q]) +
+                              (static_cast<int64_t>(t) * parts + part) * H + rank * Hl + hl * d + j;
+    __nv_bfloat16* dp = dst + (static_cast<int64_t>(s) * parts + part) * Hl + hl * d + j;
     uint4 lo = ld_v4(sp), hi = ld_v4(sp + half);
-    if (part < rope_parts) rotate8(lo, hi, cos_t + s * half + j, sin_t + s * half + j, 1.f);
+    if (part < rope_parts) {
+      const int64_t cs = static_cast<int64_t>(s) * half + j;
+      rotate8(lo, hi, cos_t + cs, sin_t + cs, 1.f);
+    }
     *reinterpret_cast<uint4*>(dp) = lo;
     *reinterpret_cast<uint4*>(dp + half) = hi;
   }
 }
 
 // Head-sharded [S, parts*Hl] on every rank -> token-sharded [T, parts*H] on this rank.
-__global__ void a2a_to_tokens_kernel(PeerPtrs src, int world, int rank, int T, int H, int parts,
-                                     int d, __nv_bfloat16* __restrict__ dst,
-                                     const float* __restrict__ cos_t,
-                                     const float* __restrict__ sin_t, int rope_parts) {
-  const int Hl = H / world, heads = H / d, half = d / 2, g8 = half / 8;
-  const int64_t per_row = static_cast<int64_t>(parts) * heads * g8;
-  const int64_t total = static_cast<int64_t>(T) * per_row;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t t = i / per_row;
-    int rem = static_cast<int>(i % per_row);
-    const int part = rem / (heads * g8);
-    rem %= heads * g8;
-    const int hg = rem / g8, j = (rem % g8) * 8;  // hg = global head
-    const int q = (hg * d) / Hl;                  // owner rank of that head
-    const int hl = hg - q * (Hl / d);
-    const int64_t s = static_cast<int64_t>(rank) * T + t;  // global position
-    const __nv_bfloat16* sp = static_cast<const __nv_bfloat16*>(src.p[q]) + s * parts * Hl +
-                              part * Hl + hl * d + j;
-    __nv_bfloat16* dp = dst + t * parts * H + part * H + hg * d + j;
+__global__ void __launch_bounds__(256) a2a_to_tokens_kernel(PeerPtrs src, int world, int rank, int T, int H,
+                                                            int parts, int d, __nv_bfloat16* __restrict__ dst,
+                                                            const float* __restrict__ cos_t,
+                                                            const float* __restrict__ sin_t, int rope_parts) {
+  const int Hl = H / world, heads = H / d, heads_l = Hl / d, half = d / 2, g8 = half / 8;
+  const int per_part = heads * g8;
+  const int per_row = parts * per_part;
+  const int total = T * per_row;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int t = i / per_row;
+    int rem = i - t * per_row;
+    const int part = rem / per_part;
+    rem -= part * per_part;
+    const int hg = rem / g8, j = (rem - hg * g8) * 8;  // hg = global head
+    const int q = hg / heads_l;                        // owner rank of that head
+    const int hl = hg - q * heads_l;
+    const int s = rank * T + t;                        // global position
+    const __nv_bfloat16* sp = static_cast<const __nv_bfloat16*>(src.p[q]) +
+                              (static_cast<int64_t>(s) * parts + part) * Hl + hl * d + j;
+    __nv_bfloat16* dp = dst + (static_cast<int64_t>(t) * parts + part) * H + hg * d + j;
     uint4 lo = ld_v4(sp), hi = ld_v4(sp + half);
-    if (part < rope_parts) rotate8(lo, hi, cos_t + s * half + j, sin_t + s * half + j, -1.f);
+    if (part < rope_parts) {
+      const int64_t cs = static_cast<int64_t>(s) * half + j;
+      rotate8(lo, hi, cos_t + cs, sin_t + cs, -1.f);
+    }
     *reinterpret_cast<uint4*>(dp) = lo;
     *reinterpret_cast<uint4*>(dp + half) = hi;
   }

@@ -144,6 +144,9 @@ struct seqplan_isp_ctx {
 
   // ---- streams / events ----
   cudaStream_t comm = nullptr;
+  // one stream per peer: copy-engine transfers from different peers run concurrently
+  cudaStream_t peer_st[kMaxRanks] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[kMaxRanks] = {};
   cudaEvent_t ev_gathered[SEQPLAN_W_COUNT] = {};
   cudaEvent_t ev_wgrad[SEQPLAN_W_COUNT] = {};
   cudaEvent_t ev_comm_done = nullptr, ev_start = nullptr;
@@ -293,6 +296,22 @@ void barrier(Ctx* c, cudaStream_t st, bool comm_lane) {
   ISP_LAUNCH(1, peer_barrier(c->peers_at(off), c->world, c->rank, ep, c->error_flag, st));
 }
 
+// Runs fn(q, stream) for every rank q: the local rank on `cs`, each peer on its own stream so
+// copy-engine transfers from different peers proceed in parallel; joined back into `cs`.
+template <typename F>
+void fan_out(Ctx* c, cudaStream_t cs, F&& fn) {
+  ISP_CUDA(cudaEventRecord(c->ev_fork, cs));
+  for (int q = 0; q < c->world; ++q) {
+    if (q == c->rank) continue;
+    ISP_CUDA(cudaStreamWaitEvent(c->peer_st[q], c->ev_fork, 0));
+    fn(q, c->peer_st[q]);
+    ISP_CUDA(cudaEventRecord(c->ev_join[q], c->peer_st[q]));
+  }
+  fn(c->rank, cs);
+  for (int q = 0; q < c->world; ++q)
+    if (q != c->rank) ISP_CUDA(cudaStreamWaitEvent(cs, c->ev_join[q], 0));
+}
+
 // Gather tensor t into a pool CommBuffer (or return the local working copy at p = 1).
 void gather_weight(Ctx* c, int t, cudaStream_t st) {
   if (c->world == 1) {
@@ -312,13 +331,14 @@ void gather_weight(Ctx* c, int t, cudaStream_t st) {
     bf16* dst = static_cast<bf16*>(pool_alloc(c, bytes, seqplan::AllocTag::CommBuffer, st));
     if (ce) {
       const int64_t B = kGuBlock, H = c->H, rpr = c->I / c->world;
-      for (int q = 0; q < c->world; ++q)
+      fan_out(c, st, [&](int q, cudaStream_t qs) {
         for (int which = 0; which < 2; ++which) {
           const bf16* src = c->peer<bf16>(q, c->off_wshard[which ? SEQPLAN_W_UP : SEQPLAN_W_GATE]);
           bf16* d0 = dst + ((q * rpr / B) * 2 * B + which * B) * H;
           ISP_CUDA(cudaMemcpy2DAsync(d0, size_t(2 * B * H * 2), src, size_t(B * H * 2), size_t(B * H * 2),
-                                     size_t(rpr / B), cudaMemcpyDefault, st));
+                                     size_t(rpr / B), cudaMemcpyDefault, qs));
         }
+      });
     } else {
       ISP_LAUNCH(1, allgather_pull_interleave(c->peers_at(c->off_wshard[SEQPLAN_W_GATE]),
                                               c->peers_at(c->off_wshard[SEQPLAN_W_UP]), c->world, c->I, c->H,
@@ -331,9 +351,10 @@ void gather_weight(Ctx* c, int t, cudaStream_t st) {
     bf16* dst = static_cast<bf16*>(pool_alloc(c, bytes, seqplan::AllocTag::CommBuffer, st));
     if (ce) {
       const int64_t sh = c->shard(t);
-      for (int q = 0; q < c->world; ++q)
+      fan_out(c, st, [&](int q, cudaStream_t qs) {
         ISP_CUDA(cudaMemcpyAsync(dst + q * sh, c->peer<bf16>(q, c->off_wshard[t]), size_t(sh * 2),
-                                 cudaMemcpyDefault, st));
+                                 cudaMemcpyDefault, qs));
+      });
     } else {
       ISP_LAUNCH(1, allgather_pull(c->peers_at(c->off_wshard[t]), c->world, c->shard(t), dst, st, c->num_sms,
                                    kCommCtas));
@@ -538,20 +559,22 @@ void stage_rs(Ctx* c, int t, cudaStream_t cs) {
     const int64_t rpr = c->I / p, B = kGuBlock, slot = 2 * rpr * H;  // [gate rpr x H | up rpr x H]
     KTimer kt(c, cs, SEQPLAN_K_REDUCE_SCATTER, 0, double(p - 1) * double(slot) * 2);
     bf16* stg = static_cast<bf16*>(pool_alloc(c, p * slot * 2, seqplan::AllocTag::CommBuffer, cs));
-    for (int q = 0; q < p; ++q)
+    fan_out(c, cs, [&](int q, cudaStream_t qs) {
       for (int which = 0; which < 2; ++which) {
         const bf16* src = c->peer<bf16>(q, c->off_part[SEQPLAN_W_GATE]) + ((c->rank * rpr / B) * 2 * B + which * B) * H;
         ISP_CUDA(cudaMemcpy2DAsync(stg + q * slot + which * rpr * H, size_t(B * H * 2), src, size_t(2 * B * H * 2),
-                                   size_t(B * H * 2), size_t(rpr / B), cudaMemcpyDefault, cs));
+                                   size_t(B * H * 2), size_t(rpr / B), cudaMemcpyDefault, qs));
       }
+    });
     c->stage[t] = stg;
   } else {
     const int64_t sh = c->shard(t);
     KTimer kt(c, cs, SEQPLAN_K_REDUCE_SCATTER, 0, double(p - 1) * double(sh) * double(esz));
     char* stg = static_cast<char*>(pool_alloc(c, p * sh * esz, seqplan::AllocTag::CommBuffer, cs));
-    for (int q = 0; q < p; ++q)
+    fan_out(c, cs, [&](int q, cudaStream_t qs) {
       ISP_CUDA(cudaMemcpyAsync(stg + q * sh * esz, c->peer<char>(q, c->off_part[t]) + c->rank * sh * esz,
-                               size_t(sh * esz), cudaMemcpyDefault, cs));
+                               size_t(sh * esz), cudaMemcpyDefault, qs));
+    });
     c->stage[t] = stg;
   }
   ISP_CUDA(cudaEventRecord(c->ev_staged[t], cs));
@@ -812,6 +835,11 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   c->dg_scratch = static_cast<float*>(A(int64_t(rmsnorm_bwd_scratch_rows(c->num_sms)) * H * 4));
 
   ISP_CUDA(cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking));
+  ISP_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  for (int q = 0; q < c->world; ++q) {
+    ISP_CUDA(cudaStreamCreateWithFlags(&c->peer_st[q], cudaStreamNonBlocking));
+    ISP_CUDA(cudaEventCreateWithFlags(&c->ev_join[q], cudaEventDisableTiming));
+  }
   for (int t = 0; t < SEQPLAN_W_COUNT; ++t) {
     ISP_CUDA(cudaEventCreateWithFlags(&c->ev_gathered[t], cudaEventDisableTiming));
     ISP_CUDA(cudaEventCreateWithFlags(&c->ev_wgrad[t], cudaEventDisableTiming));
@@ -946,6 +974,11 @@ void seqplan_isp_ctx_destroy(seqplan_isp_ctx* c) {
   c->pool.release_all();
   if (c->heap) cudaFree(c->heap);
   if (c->comm) cudaStreamDestroy(c->comm);
+  for (int q = 0; q < kMaxRanks; ++q) {
+    if (c->peer_st[q]) cudaStreamDestroy(c->peer_st[q]);
+    if (c->ev_join[q]) cudaEventDestroy(c->ev_join[q]);
+  }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   for (int t = 0; t < SEQPLAN_W_COUNT; ++t) {
     if (c->ev_gathered[t]) cudaEventDestroy(c->ev_gathered[t]);
     if (c->ev_wgrad[t]) cudaEventDestroy(c->ev_wgrad[t]);
