@@ -18,6 +18,7 @@
 // interleaved in 32-column blocks), fp32 store with scale/accumulate and
 // optional gate/up de-interleave (used for weight gradients).
 #include <cstdio>
+#include <cstdlib>
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -58,6 +59,113 @@ struct TileSched {
 };
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+// TMEM accumulator tile (this thread's row, BN columns) -> global, fused epilogue.
+template <int BN, int EPI>
+__device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_base, int row, int n0) {
+  if constexpr (EPI == EPI_SWIGLU) {
+    // kGuBlock(=32)-column blocks alternate gate / up: pair chunk 2j (gate) with 2j+1 (up).
+#pragma unroll 1
+    for (int pr = 0; pr < BN / 64; ++pr) {
+      const int cg = pr * 64;  // gate column within tile
+      uint32_t g[32], u[32];
+      tmem_ld_32x32b_x32(t_base + cg, g);
+      tmem_ld_32x32b_x32(t_base + cg + kGuBlock, u);
+      tmem_ld_wait();
+      __nv_bfloat16* gu_row = reinterpret_cast<__nv_bfloat16*>(args.out) +
+                              static_cast<int64_t>(row) * args.ldo + n0;
+      __nv_bfloat16* a_row = args.out2 + static_cast<int64_t>(row) * args.ldo2 + (n0 / 2 + pr * 32);
+      uint4* gdst = reinterpret_cast<uint4*>(gu_row + cg);
+      uint4* udst = reinterpret_cast<uint4*>(gu_row + cg + kGuBlock);
+      uint4* adst = reinterpret_cast<uint4*>(a_row);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint32_t pg[4], pu[4], pa[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int i = v * 8 + e * 2;
+          const float g0 = __uint_as_float(g[i]), g1 = __uint_as_float(g[i + 1]);
+          const float u0 = __uint_as_float(u[i]), u1 = __uint_as_float(u[i + 1]);
+          pg[e] = pack_bf16(g0, g1);
+          pu[e] = pack_bf16(u0, u1);
+          // activation from the bf16-rounded values the backward will see
+          const float2 gr = unpack_bf16(pg[e]);
+          const float2 ur = unpack_bf16(pu[e]);
+          pa[e] = pack_bf16(silu(gr.x) * ur.x, silu(gr.y) * ur.y);
+        }
+        gdst[v] = make_uint4(pg[0], pg[1], pg[2], pg[3]);
+        udst[v] = make_uint4(pu[0], pu[1], pu[2], pu[3]);
+        adst[v] = make_uint4(pa[0], pa[1], pa[2], pa[3]);
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(t_base + c * 32, r);
+      tmem_ld_wait();
+      const int col = n0 + c * 32;
+      if constexpr (EPI == EPI_F32) {
+        float* dst;
+        int64_t orow = row;
+        if (args.interleave64) {  // gate|up rows interleaved in kGuBlock-row blocks
+          const int blk = row / kGuBlock;
+          orow = static_cast<int64_t>(blk >> 1) * kGuBlock + (row % kGuBlock);
+          dst = (blk & 1) ? args.out_b : reinterpret_cast<float*>(args.out);
+        } else {
+          dst = reinterpret_cast<float*>(args.out);
+        }
+        float4* p = reinterpret_cast<float4*>(dst + orow * args.ldo + col);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          float4 o = make_float4(__uint_as_float(r[4 * v]) * args.scale,
+                                 __uint_as_float(r[4 * v + 1]) * args.scale,
+                                 __uint_as_float(r[4 * v + 2]) * args.scale,
+                                 __uint_as_float(r[4 * v + 3]) * args.scale);
+          if (args.accumulate) {
+            const float4 prev = p[v];
+            o.x += prev.x; o.y += prev.y; o.z += prev.z; o.w += prev.w;
+          }
+          p[v] = o;
+        }
+      } else {
+        __nv_bfloat16* dst_row = reinterpret_cast<__nv_bfloat16*>(args.out) +
+                                 static_cast<int64_t>(row) * args.ldo + col;
+        float add[32];
+        if constexpr (EPI == EPI_BF16_RESID) {
+          const uint4* rs = reinterpret_cast<const uint4*>(
+              args.resid + static_cast<int64_t>(row) * args.ldr + col);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const uint4 q = rs[v];
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = unpack_bf16(w[e]);
+              add[v * 8 + e * 2] = f.x;
+              add[v * 8 + e * 2 + 1] = f.y;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) add[i] = 0.f;
+        }
+        uint4* d4 = reinterpret_cast<uint4*>(dst_row);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          uint32_t pk[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int i = v * 8 + e * 2;
+            pk[e] = pack_bf16(__uint_as_float(r[i]) * args.scale + add[i],
+                              __uint_as_float(r[i + 1]) * args.scale + add[i + 1]);
+          }
+          d4[v] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+      }
+    }
+  }
+}
 
 template <bool A_MN, bool B_MN, int BN, int EPI>
 __global__ void __launch_bounds__(kNumThreads, 1)
@@ -179,108 +287,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       tc_fence_after();
       const uint32_t t_base = tmem_base + (static_cast<uint32_t>(lane_grp * 32) << 16) + acc * BN;
 
-      if constexpr (EPI == EPI_SWIGLU) {
-        // kGuBlock(=32)-column blocks alternate gate / up: pair chunk 2j (gate) with 2j+1 (up).
-#pragma unroll 1
-        for (int pr = 0; pr < BN / 64; ++pr) {
-          const int cg = pr * 64;  // gate column within tile
-          uint32_t g[32], u[32];
-          tmem_ld_32x32b_x32(t_base + cg, g);
-          tmem_ld_32x32b_x32(t_base + cg + kGuBlock, u);
-          tmem_ld_wait();
-          __nv_bfloat16* gu_row = reinterpret_cast<__nv_bfloat16*>(args.out) +
-                                  static_cast<int64_t>(row) * args.ldo + n0;
-          __nv_bfloat16* a_row = args.out2 + static_cast<int64_t>(row) * args.ldo2 + (n0 / 2 + pr * 32);
-          uint4* gdst = reinterpret_cast<uint4*>(gu_row + cg);
-          uint4* udst = reinterpret_cast<uint4*>(gu_row + cg + kGuBlock);
-          uint4* adst = reinterpret_cast<uint4*>(a_row);
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            uint32_t pg[4], pu[4], pa[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int i = v * 8 + e * 2;
-              const float g0 = __uint_as_float(g[i]), g1 = __uint_as_float(g[i + 1]);
-              const float u0 = __uint_as_float(u[i]), u1 = __uint_as_float(u[i + 1]);
-              pg[e] = pack_bf16(g0, g1);
-              pu[e] = pack_bf16(u0, u1);
-              // activation from the bf16-rounded values the backward will see
-              const float2 gr = unpack_bf16(pg[e]);
-              const float2 ur = unpack_bf16(pu[e]);
-              pa[e] = pack_bf16(silu(gr.x) * ur.x, silu(gr.y) * ur.y);
-            }
-            gdst[v] = make_uint4(pg[0], pg[1], pg[2], pg[3]);
-            udst[v] = make_uint4(pu[0], pu[1], pu[2], pu[3]);
-            adst[v] = make_uint4(pa[0], pa[1], pa[2], pa[3]);
-          }
-        }
-      } else {
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(t_base + c * 32, r);
-          tmem_ld_wait();
-          const int col = n0 + c * 32;
-          if constexpr (EPI == EPI_F32) {
-            float* dst;
-            int64_t orow = row;
-            if (args.interleave64) {  // gate|up rows interleaved in kGuBlock-row blocks
-              const int blk = row / kGuBlock;
-              orow = static_cast<int64_t>(blk >> 1) * kGuBlock + (row % kGuBlock);
-              dst = (blk & 1) ? args.out_b : reinterpret_cast<float*>(args.out);
-            } else {
-              dst = reinterpret_cast<float*>(args.out);
-            }
-            float4* p = reinterpret_cast<float4*>(dst + orow * args.ldo + col);
-#pragma unroll
-            for (int v = 0; v < 8; ++v) {
-              float4 o = make_float4(__uint_as_float(r[4 * v]) * args.scale,
-                                     __uint_as_float(r[4 * v + 1]) * args.scale,
-                                     __uint_as_float(r[4 * v + 2]) * args.scale,
-                                     __uint_as_float(r[4 * v + 3]) * args.scale);
-              if (args.accumulate) {
-                const float4 prev = p[v];
-                o.x += prev.x; o.y += prev.y; o.z += prev.z; o.w += prev.w;
-              }
-              p[v] = o;
-            }
-          } else {
-            __nv_bfloat16* dst_row = reinterpret_cast<__nv_bfloat16*>(args.out) +
-                                     static_cast<int64_t>(row) * args.ldo + col;
-            float add[32];
-            if constexpr (EPI == EPI_BF16_RESID) {
-              const uint4* rs = reinterpret_cast<const uint4*>(
-                  args.resid + static_cast<int64_t>(row) * args.ldr + col);
-#pragma unroll
-              for (int v = 0; v < 4; ++v) {
-                const uint4 q = rs[v];
-                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const float2 f = unpack_bf16(w[e]);
-                  add[v * 8 + e * 2] = f.x;
-                  add[v * 8 + e * 2 + 1] = f.y;
-                }
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) add[i] = 0.f;
-            }
-            uint4* d4 = reinterpret_cast<uint4*>(dst_row);
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              uint32_t pk[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int i = v * 8 + e * 2;
-                pk[e] = pack_bf16(__uint_as_float(r[i]) * args.scale + add[i],
-                                  __uint_as_float(r[i + 1]) * args.scale + add[i + 1]);
-              }
-              d4[v] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            }
-          }
-        }
-      }
+      epilogue_tile<BN, EPI>(args, t_base, row, n0);
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
@@ -292,6 +299,183 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant (tcgen05.mma.cta_group::2): a cluster of 2 CTAs computes a 256 x BN tile.
+// CTA r loads A rows [m0 + 128 r, +128) and B rows [n0 + BN/2 r, +BN/2) into its own smem
+// (TMA completes on the leader's barrier); the leader issues M=256 MMAs that read both CTAs'
+// smem and accumulate into each CTA's own TMEM (128 lanes x BN). Per-SM smem traffic per MMA
+// halves vs the single-CTA kernel, which is what lets the tensor pipe run near peak.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                                 int32_t c1) {
+  const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;  // the leader CTA's barrier
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_bf16_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on bar in both CTAs
+  const uint16_t mask = 0x3;
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {  // arrive on the leader CTA's barrier
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
+template <bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(kNumThreads, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                    GemmArgs args) {
+  constexpr int BN = 256, BNH = BN / 2, S = 6;
+  constexpr int kABytes = BM * BK * 2, kBBytes = BNH * BK * 2, kStageBytes = kABytes + kBBytes;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * kStageBytes);
+  uint64_t* empty_bar = full_bar + S;
+  uint64_t* tfull_bar = empty_bar + S;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t crank = cluster_rank();
+  const bool leader = crank == 0;
+  const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+  TileSched sched{args.M / (2 * BM), args.N / BN, (args.M / (2 * BM)) * (args.N / BN)};
+  const int num_kb = args.K / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapA);
+    tma_prefetch(&mapB);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull_bar[i], 1);
+      mbar_init(&tempty_bar[i], 2 * 128);  // both CTAs' epilogue threads (leader's copy is used)
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = cid; t < sched.num_tiles; t += ncl) {
+        int mb, nb;
+        sched.coords(t, mb, nb);
+        const int m0 = mb * 2 * BM + static_cast<int>(crank) * BM, n0 = nb * BN + static_cast<int>(crank) * BNH;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          uint8_t* sa = smem + s * kStageBytes;
+          uint8_t* sb = sa + kABytes;
+          if (leader) mbar_arrive_expect_tx(&full_bar[s], 2 * kStageBytes);
+          if constexpr (!A_MN) {
+            tma_load_2d_pair(sa, &mapA, &full_bar[s], kb * BK, m0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(sa + j * 8192, &mapA, &full_bar[s], m0 + j * 64, kb * BK);
+          }
+          if constexpr (!B_MN) {
+            tma_load_2d_pair(sb, &mapB, &full_bar[s], kb * BK, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BNH / 64; ++j) tma_load_2d_pair(sb + j * 8192, &mapB, &full_bar[s], n0 + j * 64, kb * BK);
+          }
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(2 * BM, BN, A_MN, B_MN);
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t acc_ph = 0;
+      for (int t = cid; t < sched.num_tiles; t += ncl) {
+        mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * kStageBytes);
+          const uint32_t sb = sa + kABytes;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? make_sw128_desc(sa + k * 2048, 8192, 1024) : make_sw128_desc(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_sw128_desc(sb + k * 2048, 8192, 1024) : make_sw128_desc(sb + k * 32, 16, 1024);
+            tc_mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          tc_commit_pair(&empty_bar[s]);
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+        tc_commit_pair(&tfull_bar[acc]);
+        if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+      }
+    }
+  } else {
+    const int lane_grp = warp & 3;
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int t = cid; t < sched.num_tiles; t += ncl) {
+      int mb, nb;
+      sched.coords(t, mb, nb);
+      const int row = mb * 2 * BM + static_cast<int>(crank) * BM + lane_grp * 32 + lane;
+      const int n0 = nb * BN;
+      mbar_wait(&tfull_bar[acc], acc_ph);
+      tc_fence_after();
+      const uint32_t t_base = tmem_base + (static_cast<uint32_t>(lane_grp * 32) << 16) + acc * BN;
+      epilogue_tile<BN, EPI>(args, t_base, row, n0);
+      tc_fence_before();
+      if (leader) mbar_arrive(&tempty_bar[acc]);
+      else mbar_arrive_leader(&tempty_bar[acc]);
+      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
   }
 }
 
@@ -353,6 +537,49 @@ cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArg
   return cudaGetLastError();
 }
 
+template <bool A_MN, bool B_MN, int EPI>
+cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& args, cudaStream_t stream) {
+  constexpr int kSmem = 6 * (BM * BK * 2 + 128 * BK * 2) + 1024 + 512;
+  auto kern = gemm_tc2_kernel<A_MN, B_MN, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int tiles = (args.M / 256) * (args.N / 256);
+  const int clusters = tiles < g_num_sms / 2 ? tiles : g_num_sms / 2;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * clusters);
+  cfg.blockDim = dim3(kNumThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, ma, mb, args);
+}
+
+template <bool A_MN, bool B_MN>
+cudaError_t dispatch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, int epi, cudaStream_t st) {
+  switch (epi) {
+    case EPI_BF16: return launch_pair<A_MN, B_MN, EPI_BF16>(ma, mb, a, st);
+    case EPI_BF16_RESID: return launch_pair<A_MN, B_MN, EPI_BF16_RESID>(ma, mb, a, st);
+    case EPI_SWIGLU: return launch_pair<A_MN, B_MN, EPI_SWIGLU>(ma, mb, a, st);
+    case EPI_F32: return launch_pair<A_MN, B_MN, EPI_F32>(ma, mb, a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
 template <bool A_MN, bool B_MN, int BN>
 cudaError_t dispatch_epi(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a,
                          int epi, cudaStream_t st) {
@@ -374,16 +601,29 @@ cudaError_t gemm_launch(const GemmOperand& A, const GemmOperand& B, GemmArgs arg
   if (args.M % BM || args.K % BK || args.M <= 0 || args.N <= 0 || args.K <= 0)
     return cudaErrorInvalidValue;
   int bn = gemm_pick_bn(args.N);
+  if (const char* f = std::getenv("SEQPLAN_GEMM_BN")) {  // development override
+    const int want = std::atoi(f);
+    if ((want == 128 || want == 256) && args.N % want == 0) bn = want;
+  }
   if (epi == EPI_SWIGLU) bn = (args.N % 256 == 0) ? 256 : (args.N % 128 == 0 ? 128 : 0);
   if (bn == 0) return cudaErrorInvalidValue;
+  const bool pair = bn == 256 && args.M % 256 == 0 && !std::getenv("SEQPLAN_GEMM_NO_PAIR");
   CUtensorMap ma, mb;
   // A: logical [M, K]; K-major storage is [M, K], MN-major storage is [K, M].
   bool ok = A.mn_major ? make_map(&ma, A.ptr, args.K, args.M, A.ld, 64)
                        : make_map(&ma, A.ptr, args.M, args.K, A.ld, BM);
   ok = ok && (B.mn_major ? make_map(&mb, B.ptr, args.K, args.N, B.ld, 64)
-                         : make_map(&mb, B.ptr, args.N, args.K, B.ld, bn));
+                         : make_map(&mb, B.ptr, args.N, args.K, B.ld, pair ? bn / 2 : bn));
   if (!ok) return cudaErrorInvalidValue;
   const int code = (A.mn_major ? 2 : 0) | (B.mn_major ? 1 : 0);
+  if (pair) {
+    switch (code) {
+      case 0: return dispatch_pair<false, false>(ma, mb, args, epi, stream);
+      case 1: return dispatch_pair<false, true>(ma, mb, args, epi, stream);
+      case 2: return dispatch_pair<true, false>(ma, mb, args, epi, stream);
+      case 3: return dispatch_pair<true, true>(ma, mb, args, epi, stream);
+    }
+  }
   if (bn == 256) {
     switch (code) {
       case 0: return dispatch_epi<false, false, 256>(ma, mb, args, epi, stream);
