@@ -277,10 +277,19 @@ def main():
         hx.copy_(x.cpu())
         hdy.copy_(dy.cpu())
 
+        copy_stream = torch.cuda.Stream(device=dev)
+        dy_ready = torch.cuda.Event()
+
         def e2e_step():
+            # this step's inputs come from pinned host memory: x before the forward, dy on a
+            # side stream overlapping the forward; the result dx is read back every step
             x.copy_(hx, non_blocking=True)
-            dy.copy_(hdy, non_blocking=True)
+            copy_stream.wait_stream(stream)
+            with torch.cuda.stream(copy_stream):
+                dy.copy_(hdy, non_blocking=True)
+                dy_ready.record(copy_stream)
             blk.fwd(x, y, stream)
+            stream.wait_event(dy_ready)
             blk.bwd(dy, dx, stream)
             hdx.copy_(dx, non_blocking=True)
 
