@@ -14,6 +14,8 @@
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -183,11 +185,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     float* xmax = reinterpret_cast<float*>(smem + L::kOffBar + L::kBarBytes);  // [2 slots][2 halves][128 rows]
     float m = -INFINITY, l = 0.f;
-    int pfree_seen[2] = {0, 0};
+    int pf_seen0 = 0, pf_seen1 = 0;  // completed p_free phases consumed per buffer (registers)
     auto ensure_pfree = [&](int b, int count) {
-      while (pfree_seen[b] < count) {
-        mbar_wait(&p_free[b], pfree_seen[b] & 1);
-        ++pfree_seen[b];
+      int& seen = b ? pf_seen1 : pf_seen0;
+      while (seen < count) {
+        mbar_wait(&p_free[b], seen & 1);
+        ++seen;
       }
     };
     for (int j = 0; j < n_kv; ++j) {
@@ -364,24 +367,20 @@ namespace {
 
 constexpr int kBwdKeys = 128;
 constexpr int kBwdQ = 64;
-constexpr int kBwdThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 compute
+constexpr int kBwdThreads = 448;  // warp 0 TMA, warp 1 MMA, warps 2..9 P/dS, warps 10..13 dQ
 
 struct BwdSmem {
-  static constexpr int kStages = 3;                   // Q/dO ring depth
+  static constexpr int kStages = 4;                   // Q/dO ring depth (TMA latency lookahead)
   static constexpr int kKV = kBwdKeys * 128 * 2;      // [2 chunks][128 keys][64 d]
   static constexpr int kQ = kBwdQ * 128 * 2;          // [2 chunks][64 q][64 d]
   static constexpr int kStage = 2 * kQ;               // Q_i | dO_i
   static constexpr int kP = kBwdKeys * kBwdQ * 2;     // [128 keys][64 q]
-  static constexpr int kStg = kBwdQ * 128 * 4;        // [64 q][128 d] fp32 dQ staging
   static constexpr int kOffK = 0;
   static constexpr int kOffV = kOffK + kKV;
   static constexpr int kOffQ = kOffV + kKV;           // stage s: Q at kOffQ + s*kStage, dO at +kQ
   static constexpr int kOffP = kOffQ + kStages * kStage;
   static constexpr int kOffDS = kOffP + kP;
-  static constexpr int kOffStg = kOffDS + kP;
-  static constexpr int kOffL = kOffStg + kStg;        // [stages][64] lse
-  static constexpr int kOffD = kOffL + kStages * kBwdQ * 4;  // [stages][64] delta
-  static constexpr int kOffBar = kOffD + kStages * kBwdQ * 4;
+  static constexpr int kOffBar = kOffDS + kP;
   static constexpr int kBytes = kOffBar + 256 + 1024;
   static_assert(kBytes <= 232448, "exceeds the 227 KB per-CTA shared memory");
 };
@@ -407,7 +406,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                        const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mDO,
                        const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ dq_acc,
                        __nv_bfloat16* __restrict__ dk_out, __nv_bfloat16* __restrict__ dv_out, int64_t ld_d,
-                       int S, float scale) {
+                       int S, float scale, int dbg, long long* trace) {
   using L = BwdSmem;
   constexpr int D = 128;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -441,7 +440,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(p_full, 256);
     mbar_init(p_free, 1);
     mbar_init(dq_full, 1);
-    mbar_init(dq_free, 256);
+    mbar_init(dq_free, 128);
     mbar_init(dkv_full, 1);
     fence_barrier_init();
   }
@@ -460,18 +459,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tma_load_2d(smem + L::kOffK + c * kBwdKeys * 128, &mK, kv_full, h * D + c * 64, k0);
         tma_load_2d(smem + L::kOffV + c * kBwdKeys * 128, &mV, kv_full, h * D + c * 64, k0);
       }
-      const float* lse_h = lse + static_cast<int64_t>(h) * S;
-      const float* del_h = delta + static_cast<int64_t>(h) * S;
       for (int i = 0; i < nq; ++i) {
         const int s = i % NS, q0 = (qi0 + i) * kBwdQ;
         if (i >= NS) mbar_wait(&q_empty[s], ((i / NS) - 1) & 1);
-        mbar_arrive_expect_tx(&q_full[s], 2 * L::kQ + 2 * kBwdQ * 4);
+        mbar_arrive_expect_tx(&q_full[s], 2 * L::kQ);
         for (int c = 0; c < 2; ++c) {
           tma_load_2d(smem + L::kOffQ + s * L::kStage + c * kBwdQ * 128, &mQ, &q_full[s], h * D + c * 64, q0);
           tma_load_2d(smem + L::kOffQ + s * L::kStage + L::kQ + c * kBwdQ * 128, &mDO, &q_full[s], h * D + c * 64, q0);
         }
-        bulk_load(smem + L::kOffL + s * kBwdQ * 4, lse_h + q0, kBwdQ * 4, &q_full[s]);
-        bulk_load(smem + L::kOffD + s * kBwdQ * 4, del_h + q0, kBwdQ * 4, &q_full[s]);
       }
     }
   } else if (warp == 1) {
@@ -519,70 +514,100 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                       make_sw128_desc(sDO + c * kBwdQ * 128 + kk * 32, 16, 1024), id_s, k > 0 ? 1u : 0u);
         }
         tc_commit(s_full);
+        if (trace && blockIdx.x == 0 && blockIdx.y == 0 && i < 64) trace[i * 8 + 0] = clock64();
         if (i >= 1) grads(i - 1);
+        if (trace && blockIdx.x == 0 && blockIdx.y == 0 && i < 64) trace[i * 8 + 1] = clock64();
       }
       grads(nq - 1);
       tc_commit(dkv_full);
     }
-  } else {
-    // ---------------- compute warps 2..9 ----------------
-    const int quad = warp & 3, half = (warp - 2) >> 2;
-    const int r = quad * 32 + lane;            // key row (S/dP/dK/dV) or head-dim row (dQ^T)
+  } else if (warp >= 10) {
+    // ---------------- dQ warps 10..13: dQ^T (lane = head dim) -> fp32 reductions ----------------
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
     const uint32_t lo = static_cast<uint32_t>(quad * 32) << 16;
-    const int key = k0 + r;
-    const bool leader = (warp == 2 && lane == 0);
-    float* stg = reinterpret_cast<float*>(smem + L::kOffStg);
-    auto dq_epilogue = [&](int j) {  // dQ^T of tile j -> smem staging -> bulk reduce-add
+    for (int j = 0; j < nq; ++j) {
       mbar_wait(dq_full, j & 1);
       tc_fence_after();
-      uint32_t v[32];
-      tmem_ld_32x32b_x32(tDQ + lo + half * 32, v);
+      uint32_t v0[32], v1[32];
+      tmem_ld_32x32b_x32(tDQ + lo, v0);
+      tmem_ld_32x32b_x32(tDQ + lo + 32, v1);
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(dq_free);
-      if (leader) bulk_wait_read();  // the reduce of tile j-1 has finished reading the staging
-      named_bar(1, 256);
-      const uint32_t stg_a = smem_u32(stg) + static_cast<uint32_t>((half * 32 * D + r) * 4);
+      // a warp instruction covers 32 consecutive floats (one query row, 32 head dims)
+      float* dst = dq_acc + (static_cast<int64_t>(h) * S + (qi0 + j) * kBwdQ) * D + r;
 #pragma unroll
       for (int c = 0; c < 32; ++c)
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(stg_a + c * D * 4), "f"(__uint_as_float(v[c]) * scale) : "memory");
-      fence_proxy_async();
-      named_bar(1, 256);
-      if (leader) {
-        const int q0 = (qi0 + j) * kBwdQ;
-        bulk_reduce_add_f32(dq_acc + (static_cast<int64_t>(h) * S + q0) * D, stg, L::kStg);
-      }
-    };
+        asm volatile("red.global.add.f32 [%0], %1;" ::"l"(dst + c * D), "f"(__uint_as_float(v0[c]) * scale) : "memory");
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        asm volatile("red.global.add.f32 [%0], %1;" ::"l"(dst + (32 + c) * D), "f"(__uint_as_float(v1[c]) * scale)
+                     : "memory");
+    }
+  } else {
+    // ---------------- P^T / dS^T warps 2..9 ----------------
+    // A warp pair per TMEM lane quadrant (key rows); each warp owns 32 of the 64 query
+    // columns, processed in two 16-column chunks to bound register pressure.
+    const int quad = warp & 3, half = (warp - 2) >> 2;
+    const int r = quad * 32 + lane;  // key row
+    const uint32_t lo = static_cast<uint32_t>(quad * 32) << 16;
+    const int key = k0 + r;
+    const float* lse_h = lse + static_cast<int64_t>(h) * S + half * 32;
+    const float* del_h = delta + static_cast<int64_t>(h) * S + half * 32;
     for (int i = 0; i < nq; ++i) {
-      const int s = i % NS, q0 = (qi0 + i) * kBwdQ;
-      mbar_wait(&q_full[s], (i / NS) & 1);  // lse / delta of this tile
+      const int q0 = (qi0 + i) * kBwdQ;
+      const bool tr = trace && blockIdx.x == 0 && blockIdx.y == 0 && i < 64 && warp == 2 && lane == 0;
+      if (tr) trace[i * 8 + 2] = clock64();
       mbar_wait(s_full, i & 1);
+      if (tr) trace[i * 8 + 3] = clock64();
       tc_fence_after();
-      uint32_t sv[32], pv[32];
-      tmem_ld_32x32b_x32(tS + lo + half * 32, sv);
-      tmem_ld_32x32b_x32(tP + lo + half * 32, pv);
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(s_free);
-      const float* sL = reinterpret_cast<const float*>(smem + L::kOffL + s * kBwdQ * 4) + half * 32;
-      const float* sD = reinterpret_cast<const float*>(smem + L::kOffD + s * kBwdQ * 4) + half * 32;
       const bool diag = q0 < k0 + kBwdKeys;
       uint32_t pk[16], dk[16];
 #pragma unroll
-      for (int c = 0; c < 32; c += 2) {
-        float p2[2], d2[2];
+      for (int hc = 0; hc < 2; ++hc) {
+        uint32_t sv[16], pv[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(sv[0]), "=r"(sv[1]), "=r"(sv[2]), "=r"(sv[3]), "=r"(sv[4]), "=r"(sv[5]), "=r"(sv[6]),
+              "=r"(sv[7]), "=r"(sv[8]), "=r"(sv[9]), "=r"(sv[10]), "=r"(sv[11]), "=r"(sv[12]), "=r"(sv[13]),
+              "=r"(sv[14]), "=r"(sv[15])
+            : "r"(tS + lo + half * 32 + hc * 16));
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(pv[0]), "=r"(pv[1]), "=r"(pv[2]), "=r"(pv[3]), "=r"(pv[4]), "=r"(pv[5]), "=r"(pv[6]),
+              "=r"(pv[7]), "=r"(pv[8]), "=r"(pv[9]), "=r"(pv[10]), "=r"(pv[11]), "=r"(pv[12]), "=r"(pv[13]),
+              "=r"(pv[14]), "=r"(pv[15])
+            : "r"(tP + lo + half * 32 + hc * 16));
+        float4 l4[4], d4[4];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int qc = half * 32 + c + e;
-          float p = fast_exp2(fmaf(__uint_as_float(sv[c + e]), scale_log2, -sL[c + e] * kLog2e));
-          if (diag && key > q0 + qc) p = 0.f;
-          p2[e] = p;
-          d2[e] = p * (__uint_as_float(pv[c + e]) - sD[c + e]);
+        for (int k = 0; k < 4; ++k) {
+          l4[k] = __ldg(reinterpret_cast<const float4*>(lse_h + q0 + hc * 16) + k);
+          d4[k] = __ldg(reinterpret_cast<const float4*>(del_h + q0 + hc * 16) + k);
         }
-        pk[c / 2] = pack_bf16(p2[0], p2[1]);
-        dk[c / 2] = pack_bf16(d2[0], d2[1]);
+        tmem_ld_wait();
+        const float* lr = reinterpret_cast<const float*>(l4);
+        const float* dr = reinterpret_cast<const float*>(d4);
+#pragma unroll
+        for (int c = 0; c < 16; c += 2) {
+          float p2[2], d2[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int qc = half * 32 + hc * 16 + c + e;
+            float p = fast_exp2(fmaf(__uint_as_float(sv[c + e]), scale_log2, -lr[c + e] * kLog2e));
+            if (diag && key > q0 + qc) p = 0.f;
+            p2[e] = p;
+            d2[e] = p * (__uint_as_float(pv[c + e]) - dr[c + e]);
+          }
+          pk[hc * 8 + c / 2] = pack_bf16(p2[0], p2[1]);
+          dk[hc * 8 + c / 2] = pack_bf16(d2[0], d2[1]);
+        }
       }
+      tc_fence_before();
+      mbar_arrive(s_free);
+      if (tr) trace[i * 8 + 4] = clock64();
       if (i >= 1) mbar_wait(p_free, (i - 1) & 1);  // gradient MMAs of tile i-1 released P^T / dS^T
+      if (tr) trace[i * 8 + 5] = clock64();
       uint8_t* prow = smem + L::kOffP + r * 128;
       uint8_t* drow = smem + L::kOffDS + r * 128;
 #pragma unroll
@@ -594,10 +619,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(p_full);
-      if (i >= 1) dq_epilogue(i - 1);
+      if (tr) trace[i * 8 + 6] = clock64();
     }
-    dq_epilogue(nq - 1);
-    if (leader) bulk_wait_all();
     // dK (scaled), dV -> bf16
     mbar_wait(dkv_full, 0);
     tc_fence_after();
@@ -634,6 +657,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
 }  // namespace
 
+long long* g_attn_trace = nullptr;  // development: clock64 trace of CTA (0,0)
+extern "C" void seqplan_isp_debug_set_trace(long long* dev_buf) { g_attn_trace = dev_buf; }
+
 // dq_acc must be zeroed and delta = rowsum(dO * O) computed before this launch.
 cudaError_t attention_bwd_tc(const AttnTensors& t, const __nv_bfloat16* dout, int64_t ld_dout, __nv_bfloat16* dk,
                              __nv_bfloat16* dv, int64_t ld_d, const float* delta, float* dq_acc, cudaStream_t st) {
@@ -652,7 +678,8 @@ cudaError_t attention_bwd_tc(const AttnTensors& t, const __nv_bfloat16* dout, in
     return cudaErrorInvalidValue;
   const float scale = 1.0f / sqrtf(128.0f);
   attn_bwd_tc_kernel<<<dim3(t.S / kBwdKeys, t.heads), kBwdThreads, L::kBytes, st>>>(
-      mq, mk, mv, mdo, t.lse, delta, dq_acc, dk, dv, ld_d, t.S, scale);
+      mq, mk, mv, mdo, t.lse, delta, dq_acc, dk, dv, ld_d, t.S, scale,
+      std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0, g_attn_trace);
   return cudaGetLastError();
 }
 
