@@ -183,9 +183,16 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_bwd_kernel(
 __global__ void column_sum_kernel(const float* __restrict__ part, int rows, int H, float* __restrict__ dg) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= H) return;
-  float s = 0.f;
-  for (int b = 0; b < rows; ++b) s += part[static_cast<int64_t>(b) * H + j];
-  dg[j] += s;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  int b = 0;
+  for (; b + 4 <= rows; b += 4) {
+    s0 += part[static_cast<int64_t>(b) * H + j];
+    s1 += part[static_cast<int64_t>(b + 1) * H + j];
+    s2 += part[static_cast<int64_t>(b + 2) * H + j];
+    s3 += part[static_cast<int64_t>(b + 3) * H + j];
+  }
+  for (; b < rows; ++b) s0 += part[static_cast<int64_t>(b) * H + j];
+  dg[j] += (s0 + s1) + (s2 + s3);
 }
 
 // In-place rotate-half RoPE on the q and k parts of token rows (ld elements apart).
@@ -258,7 +265,7 @@ int grid_for(int64_t work, int threads, int num_sms) {
 
 }  // namespace
 
-int rmsnorm_bwd_scratch_rows(int num_sms) { return num_sms; }
+int rmsnorm_bwd_scratch_rows(int num_sms) { return 8 * num_sms; }  // 8 CTAs (32 warps) per SM
 
 uint64_t keyed_stream_base(uint64_t seed, int tensor_id) {
   uint64_t z = seed * 0x9E3779B97F4A7C15ULL + static_cast<uint64_t>(tensor_id);
@@ -312,7 +319,7 @@ cudaError_t rmsnorm_bwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const fl
     ISP_NORM_CASE(5) ISP_NORM_CASE(6) ISP_NORM_CASE(7) ISP_NORM_CASE(8)
 #undef ISP_NORM_CASE
   }
-  if (dg_scratch) column_sum_kernel<<<(H + 255) / 256, 256, 0, st>>>(dg_scratch, grid, H, dg);
+  if (dg_scratch) column_sum_kernel<<<(H + 127) / 128, 128, 0, st>>>(dg_scratch, grid, H, dg);
   return cudaGetLastError();
 }
 
