@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_kernel(AttnTensors t,
 // dq (bf16, row stride ld) = scale * dq_acc[h, t, :]
 template <int D>
 __global__ void attn_dq_convert_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dq,
-                                       int64_t ld, int S, int heads, float scale) {
+                                       int64_t ld, int S, int heads, float scale, const AttnPush push) {
   const int64_t n = static_cast<int64_t>(heads) * S * (D / 4);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -428,7 +428,13 @@ __global__ void attn_dq_convert_kernel(const float* __restrict__ dq_acc, __nv_bf
     uint2 o;
     o.x = pack_bf16(v.x * scale, v.y * scale);
     o.y = pack_bf16(v.z * scale, v.w * scale);
-    *reinterpret_cast<uint2*>(dq + static_cast<int64_t>(tok) * ld + h * D + c4 * 4) = o;
+    if (push.p[0]) {  // fused all-to-all: dq of token tok goes to its owner rank
+      const int owner = tok / push.T;
+      *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(push.p[owner]) +
+                                static_cast<int64_t>(tok - owner * push.T) * push.ld + push.col_q + h * D + c4 * 4) = o;
+    } else {
+      *reinterpret_cast<uint2*>(dq + static_cast<int64_t>(tok) * ld + h * D + c4 * 4) = o;
+    }
   }
 }
 
@@ -467,11 +473,12 @@ cudaError_t bwd_impl(const AttnTensors& t, const __nv_bfloat16* dout, __nv_bfloa
     // tcgen05/TMEM backward (attention_tc.cu); it applies the softmax scale to dq_acc itself
     e = attention_bwd_tc(t, dout, t.ld_o, dk, dv, ld_d, delta, dq_acc, st);
     if (e != cudaSuccess) return e;
-    attn_dq_convert_kernel<D><<<num_sms * 8, 256, 0, st>>>(dq_acc, dq, ld_d, t.S, t.heads, 1.0f);
+    attn_dq_convert_kernel<D><<<num_sms * 8, 256, 0, st>>>(dq_acc, dq, ld_d, t.S, t.heads, 1.0f, t.push);
     return cudaGetLastError();
   }
   attn_bwd_kernel<D><<<dim3(t.S / BN, t.heads), 256, smem, st>>>(t, dout, dk, dv, ld_d, delta, dq_acc, scale);
-  attn_dq_convert_kernel<D><<<num_sms * 8, 256, 0, st>>>(dq_acc, dq, ld_d, t.S, t.heads, scale);
+  if (t.push.p[0]) return cudaErrorInvalidValue;  // fused all-to-all needs the tcgen05 kernels
+  attn_dq_convert_kernel<D><<<num_sms * 8, 256, 0, st>>>(dq_acc, dq, ld_d, t.S, t.heads, scale, t.push);
   return cudaGetLastError();
 }
 
@@ -480,7 +487,7 @@ cudaError_t bwd_impl(const AttnTensors& t, const __nv_bfloat16* dout, __nv_bfloa
 cudaError_t attention_fwd(const AttnTensors& t, cudaStream_t st, int num_sms) {
   (void)num_sms;
   if (t.S % 128) return cudaErrorInvalidValue;
-  if (!std::getenv("SEQPLAN_ISP_ATTN_MMA_SYNC")) return attention_fwd_tc(t, st);
+  if (!std::getenv("SEQPLAN_ISP_ATTN_MMA_SYNC") || t.push.p[0]) return attention_fwd_tc(t, st);
   if (t.d == 128) return fwd_impl<128>(t, st);
   if (t.d == 64) return fwd_impl<64>(t, st);
   return cudaErrorInvalidValue;

@@ -72,7 +72,7 @@ template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                        const __grid_constant__ CUtensorMap mV, __nv_bfloat16* __restrict__ out,
-                       int64_t ld_o, float* __restrict__ lse, int S, float scale_log2) {
+                       int64_t ld_o, float* __restrict__ lse, int S, float scale_log2, const AttnPush push) {
   using L = FwdSmem<D>;
   constexpr int NCH = D / 64;  // 64-wide chunks of the head dim
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -267,6 +267,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const float inv = 1.f / l_tot;
     __nv_bfloat16* orow = out + static_cast<int64_t>(q) * ld_o + h * D + half * (D / 2);
+    __nv_bfloat16* prow_out = nullptr;  // fused all-to-all: the owner rank of token q
+    if (push.p[0]) {
+      const int owner = q / push.T;
+      prow_out = static_cast<__nv_bfloat16*>(push.p[owner]) + static_cast<int64_t>(q - owner * push.T) * push.ld +
+                 push.col_o + h * D + half * (D / 2);
+    }
 #pragma unroll 1
     for (int c = 0; c < D / 64; ++c) {
       uint32_t o[32];
@@ -279,7 +285,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int e = 0; e < 4; ++e)
           pk[e] = pack_bf16(__uint_as_float(o[v * 8 + 2 * e]) * inv, __uint_as_float(o[v * 8 + 2 * e + 1]) * inv);
-        dst[v] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        const uint4 val = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        dst[v] = val;
+        if (prow_out) reinterpret_cast<uint4*>(prow_out + c * 32)[v] = val;
       }
     }
     if (half == 0) lse[static_cast<int64_t>(h) * S + q] = (m + log2f(l_tot)) * 0.6931471805599453f;
@@ -334,7 +342,7 @@ cudaError_t launch_fwd(const AttnTensors& t, cudaStream_t st) {
     return cudaErrorInvalidValue;
   const float scale_log2 = (1.0f / sqrtf(static_cast<float>(D))) * kLog2e;
   attn_fwd_tc_kernel<D><<<dim3(t.S / kBM, t.heads), kThreads, L::kBytes, st>>>(mq, mk, mv, t.o, t.ld_o, t.lse, t.S,
-                                                                               scale_log2);
+                                                                               scale_log2, t.push);
   return cudaGetLastError();
 }
 
@@ -406,7 +414,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                        const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mDO,
                        const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ dq_acc,
                        __nv_bfloat16* __restrict__ dk_out, __nv_bfloat16* __restrict__ dv_out, int64_t ld_d,
-                       int S, float scale, int dbg, long long* trace) {
+                       int S, float scale, int dbg, long long* trace, const AttnPush push) {
   using L = BwdSmem;
   constexpr int D = 128;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -631,8 +639,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tmem_ld_32x32b_x32(tDK + lo + col, a);
       tmem_ld_32x32b_x32(tDV + lo + col, b);
       tmem_ld_wait();
-      uint4* pk_out = reinterpret_cast<uint4*>(dk_out + static_cast<int64_t>(key) * ld_d + h * D + col);
-      uint4* pv_out = reinterpret_cast<uint4*>(dv_out + static_cast<int64_t>(key) * ld_d + h * D + col);
+      uint4* pk_out;
+      uint4* pv_out;
+      if (push.p[0]) {  // fused all-to-all: rows go to the owner of the key token
+        const int owner = key / push.T;
+        __nv_bfloat16* base = static_cast<__nv_bfloat16*>(push.p[owner]) +
+                              static_cast<int64_t>(key - owner * push.T) * push.ld + h * D + col;
+        pk_out = reinterpret_cast<uint4*>(base + push.col_k);
+        pv_out = reinterpret_cast<uint4*>(base + push.col_v);
+      } else {
+        pk_out = reinterpret_cast<uint4*>(dk_out + static_cast<int64_t>(key) * ld_d + h * D + col);
+        pv_out = reinterpret_cast<uint4*>(dv_out + static_cast<int64_t>(key) * ld_d + h * D + col);
+      }
 #pragma unroll
       for (int v4 = 0; v4 < 4; ++v4) {
         uint32_t x[4], y[4];
@@ -679,7 +697,7 @@ cudaError_t attention_bwd_tc(const AttnTensors& t, const __nv_bfloat16* dout, in
   const float scale = 1.0f / sqrtf(128.0f);
   attn_bwd_tc_kernel<<<dim3(t.S / kBwdKeys, t.heads), kBwdThreads, L::kBytes, st>>>(
       mq, mk, mv, mdo, t.lse, delta, dq_acc, dk, dv, ld_d, t.S, scale,
-      std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0, g_attn_trace);
+      std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0, g_attn_trace, t.push);
   return cudaGetLastError();
 }
 

@@ -98,6 +98,60 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_b
         adst[v] = make_uint4(pa[0], pa[1], pa[2], pa[3]);
       }
     }
+  } else if (EPI == EPI_BF16 && args.push[0] != nullptr) {
+    // fused all-to-all: head-aligned chunk pairs (i, i + d/2) -> owner rank, RoPE on q/k
+    const int d = args.push_d, hd = d / 2;
+    const int64_t pos = static_cast<int64_t>(args.push_rank) * args.push_T + row;
+#pragma unroll 1
+    for (int hb = 0; hb < BN; hb += d) {
+#pragma unroll 1
+      for (int c = 0; c < hd; c += 32) {
+        uint32_t lo[32], hi[32];
+        tmem_ld_32x32b_x32(t_base + hb + c, lo);
+        tmem_ld_32x32b_x32(t_base + hb + c + hd, hi);
+        tmem_ld_wait();
+        const int col = n0 + hb + c;  // global output column of the low half
+        const int part = col / args.push_H, hcol = col - part * args.push_H;
+        const int q = hcol / args.push_Hl, lc = hcol - q * args.push_Hl;
+        float fl[32], fh[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          fl[i] = __uint_as_float(lo[i]) * args.scale;
+          fh[i] = __uint_as_float(hi[i]) * args.scale;
+        }
+        if (part < args.rope_parts) {
+          const float* cp = args.rope_cos + pos * hd + c;
+          const float* sp = args.rope_sin + pos * hd + c;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 cv = *reinterpret_cast<const float4*>(cp + i);
+            const float4 sv = *reinterpret_cast<const float4*>(sp + i);
+            const float cs[4] = {cv.x, cv.y, cv.z, cv.w}, sn[4] = {sv.x, sv.y, sv.z, sv.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float a = fl[i + e], b = fh[i + e];
+              fl[i + e] = a * cs[e] - b * sn[e];
+              fh[i + e] = b * cs[e] + a * sn[e];
+            }
+          }
+        }
+        __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(args.push[q]) +
+                             (pos * args.push_parts + part) * args.push_Hl + lc;
+        uint4* d_lo = reinterpret_cast<uint4*>(dst);
+        uint4* d_hi = reinterpret_cast<uint4*>(dst + hd);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          uint32_t pl[4], ph[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            pl[e] = pack_bf16(fl[v * 8 + 2 * e], fl[v * 8 + 2 * e + 1]);
+            ph[e] = pack_bf16(fh[v * 8 + 2 * e], fh[v * 8 + 2 * e + 1]);
+          }
+          d_lo[v] = make_uint4(pl[0], pl[1], pl[2], pl[3]);
+          d_hi[v] = make_uint4(ph[0], ph[1], ph[2], ph[3]);
+        }
+      }
+    }
   } else {
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
@@ -607,6 +661,8 @@ cudaError_t gemm_launch(const GemmOperand& A, const GemmOperand& B, GemmArgs arg
   }
   if (epi == EPI_SWIGLU) bn = (args.N % 256 == 0) ? 256 : (args.N % 128 == 0 ? 128 : 0);
   if (bn == 0) return cudaErrorInvalidValue;
+  if (args.push[0] && (epi != EPI_BF16 || bn % args.push_d || args.push_H % 32 || args.push_Hl % 32))
+    return cudaErrorInvalidValue;
   const bool pair = bn == 256 && args.M % 256 == 0 && !std::getenv("SEQPLAN_GEMM_NO_PAIR");
   CUtensorMap ma, mb;
   // A: logical [M, K]; K-major storage is [M, K], MN-major storage is [K, M].

@@ -40,6 +40,15 @@ struct GemmArgs {
   float scale = 1.0f;
   int accumulate = 0;
   int interleave64 = 0;
+  // Fused Ulysses all-to-all (EPI_BF16 only): when push[0] != nullptr the [T, parts*H] tile is
+  // not stored locally; each head's columns go straight to the rank owning that head, into its
+  // head-sharded buffer [S, parts*Hl] at row rank*T + row (NVLink stores from the epilogue).
+  // RoPE (rotate-half, position = rank*T + row) is applied to parts < rope_parts on the way.
+  void* push[8] = {};
+  int push_T = 0, push_rank = 0, push_parts = 1, push_H = 0, push_Hl = 0, push_d = 128;
+  const float* rope_cos = nullptr;
+  const float* rope_sin = nullptr;
+  int rope_parts = 0;
 };
 
 int gemm_pick_bn(int N);

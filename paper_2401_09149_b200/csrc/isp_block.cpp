@@ -123,6 +123,9 @@ struct seqplan_isp_ctx {
   bool peer_opened[kMaxRanks] = {};
   size_t off_flags = 0, off_wshard[SEQPLAN_W_COUNT] = {}, off_qkv_tok = 0, off_o_heads = 0,
          off_do_tok = 0, off_dqkv_heads = 0, off_part[SEQPLAN_W_COUNT] = {};
+  // fused all-to-all (p > 1, d = 128): producers' epilogues push into these peer-writable buffers
+  bool fused_a2a = false;
+  size_t off_qkv_heads = 0, off_o_tok = 0, off_dO_heads = 0, off_dqkv_tok = 0;
   uint32_t epoch_compute = 0, epoch_comm = 0;
   uint32_t* error_flag = nullptr;  // device, in the heap flags page
 
@@ -397,6 +400,28 @@ void reduce_scatter_grad(Ctx* c, int t, cudaStream_t st) {
 // ---------------------------------------------------------------------------------
 bf16* qkv_tok_buf(Ctx* c) { return c->hp<bf16>(c->off_qkv_tok); }
 
+void set_push(Ctx* c, GemmArgs& g, size_t heap_off, int parts) {
+  for (int q = 0; q < c->world; ++q) g.push[q] = static_cast<char*>(c->peer_heap[q]) + heap_off;
+  g.push_T = static_cast<int>(c->T);
+  g.push_rank = c->rank;
+  g.push_parts = parts;
+  g.push_H = static_cast<int>(c->H);
+  g.push_Hl = static_cast<int>(c->Hl);
+  g.push_d = static_cast<int>(c->d);
+}
+
+AttnPush attn_push(Ctx* c, size_t heap_off, int64_t ld, int64_t col_o, int64_t col_q, int64_t col_k, int64_t col_v) {
+  AttnPush p{};
+  for (int q = 0; q < c->world; ++q) p.p[q] = static_cast<char*>(c->peer_heap[q]) + heap_off;
+  p.T = static_cast<int>(c->T);
+  p.ld = ld;
+  p.col_o = col_o;
+  p.col_q = col_q;
+  p.col_k = col_k;
+  p.col_v = col_v;
+  return p;
+}
+
 void fwd_issue_gathers(Ctx* c, cudaStream_t st) {
   if (c->world == 1) {
     for (int t : {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN})
@@ -428,6 +453,12 @@ void fwd_phase1(Ctx* c, const bf16* x, cudaStream_t st) {
   g.M = T; g.N = 3 * H; g.K = H;
   g.out = c->world == 1 ? static_cast<void*>(c->qkv_heads) : static_cast<void*>(qkv_tok_buf(c));
   g.ldo = 3 * H;
+  if (c->fused_a2a && !c->skip_comm()) {  // Ulysses all-to-all + RoPE fused into the epilogue (NVLink stores)
+    set_push(c, g, c->off_qkv_heads, 3);
+    g.rope_cos = c->cos_t;
+    g.rope_sin = c->sin_t;
+    g.rope_parts = 2;
+  }
   gemm(c, {c->n1, H, false}, {c->gathered[SEQPLAN_W_QKV], H, false}, g, EPI_BF16, st);
   if (c->world == 1)
     ISP_LAUNCH(1, rope_inplace(c->qkv_heads, 3 * H, T, 0, static_cast<int>(c->D), static_cast<int>(c->d), c->cos_t,
@@ -451,7 +482,7 @@ AttnTensors attn_tensors(Ctx* c) {
 }
 
 void fwd_phase2(Ctx* c, cudaStream_t st) {
-  if (c->world > 1 && !c->skip_comm()) {
+  if (c->world > 1 && !c->skip_comm() && !c->fused_a2a) {
     Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 0);
     KTimer kt(c, st, SEQPLAN_K_ALL_TO_ALL, 0, double(c->world - 1) / double(c->world) * double(c->T) * 3 * double(c->H) * 2);
     ISP_LAUNCH(1, a2a_tokens_to_heads(c->peers_at(c->off_qkv_tok), c->world, c->rank, static_cast<int>(c->T),
@@ -460,12 +491,15 @@ void fwd_phase2(Ctx* c, cudaStream_t st) {
   }
   Span sp(c, st, 0, SEQPLAN_EV_FORWARD, 1);
   KTimer kt(c, st, SEQPLAN_K_ATTN_FWD, 2.0 * double(c->S) * double(c->S) * double(c->Hl), 0);
-  ISP_LAUNCH(1, attention_fwd(attn_tensors(c), st, c->num_sms));
+  AttnTensors at = attn_tensors(c);
+  if (c->fused_a2a && !c->skip_comm())  // O rows also stream to the owner of each token
+    at.push = attn_push(c, c->off_o_tok, c->H, int64_t(c->rank) * c->Hl, 0, 0, 0);
+  ISP_LAUNCH(1, attention_fwd(at, st, c->num_sms));
 }
 
 void fwd_phase3(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
   const int T = static_cast<int>(c->T), H = static_cast<int>(c->H), I = static_cast<int>(c->I);
-  if (c->world > 1 && !c->skip_comm()) {
+  if (c->world > 1 && !c->skip_comm() && !c->fused_a2a) {
     Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 1);
     KTimer kt(c, st, SEQPLAN_K_ALL_TO_ALL, 0, double(c->world - 1) / double(c->world) * double(c->T) * 1 * double(c->H) * 2);
     ISP_LAUNCH(1, a2a_heads_to_tokens(c->peers_at(c->off_o_heads), c->world, c->rank, T, H, 1, c->o_tok, c->cos_t,
@@ -673,6 +707,7 @@ void bwd_phase1(Ctx* c, const bf16* dy, cudaStream_t st) {
     g.M = T; g.N = H; g.K = H;
     g.out = c->world == 1 ? c->dO_heads : c->hp<bf16>(c->off_do_tok);
     g.ldo = H;
+    if (c->fused_a2a && !c->skip_comm()) set_push(c, g, c->off_dO_heads, 1);
     gemm(c, {c->dh, H, false}, {c->gathered[SEQPLAN_W_O], H, true}, g, EPI_BF16, st);
   }
   release_weight(c, SEQPLAN_W_O, st);
@@ -680,7 +715,7 @@ void bwd_phase1(Ctx* c, const bf16* dy, cudaStream_t st) {
 
 void bwd_phase2(Ctx* c, cudaStream_t st) {
   const int T = static_cast<int>(c->T), H = static_cast<int>(c->H);
-  if (c->world > 1 && !c->skip_comm()) {
+  if (c->world > 1 && !c->skip_comm() && !c->fused_a2a) {
     Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 2);
     KTimer kt(c, st, SEQPLAN_K_ALL_TO_ALL, 0, double(c->world - 1) / double(c->world) * double(c->T) * 1 * double(c->H) * 2);
     ISP_LAUNCH(1, a2a_tokens_to_heads(c->peers_at(c->off_do_tok), c->world, c->rank, T, H, 1, c->dO_heads, c->cos_t,
@@ -688,6 +723,9 @@ void bwd_phase2(Ctx* c, cudaStream_t st) {
   }
   Span sp(c, st, 0, SEQPLAN_EV_GRAD_INPUT, 0);
   AttnTensors t = attn_tensors(c);
+  if (c->fused_a2a && !c->skip_comm())  // dq / dk / dv rows stream to the owner of each token
+    t.push = attn_push(c, c->off_dqkv_tok, 3 * c->H, 0, int64_t(c->rank) * c->Hl, c->H + int64_t(c->rank) * c->Hl,
+                       2 * c->H + int64_t(c->rank) * c->Hl);
   bf16* dqkv = c->world == 1 ? c->dqkv_tok : c->hp<bf16>(c->off_dqkv_heads);
   const int64_t ld = 3 * c->Hl;
   KTimer kt(c, st, SEQPLAN_K_ATTN_BWD, 4.0 * double(c->S) * double(c->S) * double(c->Hl), 0);
@@ -698,10 +736,19 @@ void bwd_phase2(Ctx* c, cudaStream_t st) {
                           c->sin_t, H, -1, st, c->num_sms));
 }
 
+// Fused all-to-all mode: the inverse RoPE of dq / dk runs on the owner after the exchange.
+void bwd_unrope_local(Ctx* c, cudaStream_t st) {
+  if (!c->fused_a2a) return;
+  ISP_LAUNCH(1, rope_inplace(c->dqkv_tok, 3 * c->H, static_cast<int>(c->T), static_cast<int>(c->rank * c->T),
+                             static_cast<int>(c->D), static_cast<int>(c->d), c->cos_t, c->sin_t, static_cast<int>(c->H),
+                             -1, st, c->num_sms));
+}
+
 void bwd_phase3(Ctx* c, const bf16* x, bf16* dx, cudaStream_t st) {
   const int T = static_cast<int>(c->T), H = static_cast<int>(c->H);
   const bool selective = !(c->flags & SEQPLAN_ISP_FLAG_FUSED_BWD);
-  if (c->world > 1 && !c->skip_comm()) {
+  bwd_unrope_local(c, st);
+  if (c->world > 1 && !c->skip_comm() && !c->fused_a2a) {
     Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 3);
     KTimer kt(c, st, SEQPLAN_K_ALL_TO_ALL, 0, double(c->world - 1) / double(c->world) * double(c->T) * 3 * double(c->H) * 2);
     ISP_LAUNCH(1, a2a_heads_to_tokens(c->peers_at(c->off_dqkv_heads), c->world, c->rank, T, H, 3, c->dqkv_tok,
@@ -753,6 +800,12 @@ void layout_heap(Ctx* c) {
     c->off_o_heads = take(size_t(c->S) * c->Hl * 2);
     c->off_do_tok = take(size_t(c->T) * c->H * 2);
     c->off_dqkv_heads = take(size_t(c->S) * 3 * c->Hl * 2);
+    if (c->fused_a2a) {
+      c->off_qkv_heads = take(size_t(c->S) * 3 * c->Hl * 2);
+      c->off_o_tok = take(size_t(c->T) * c->H * 2);
+      c->off_dO_heads = take(size_t(c->S) * c->Hl * 2);
+      c->off_dqkv_tok = take(size_t(c->T) * 3 * c->H * 2);
+    }
     for (int t : {SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_DOWN}) c->off_part[t] = take(size_t(c->numel(t)) * 2);
     c->off_part[SEQPLAN_W_GATE] = take(size_t(2 * c->I * c->H) * 2);
     c->off_part[SEQPLAN_W_NORM1] = take(size_t(c->H) * 4);
@@ -794,6 +847,7 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   }
   c->pool.set_policy(pol);
 
+  c->fused_a2a = c->world > 1 && c->d == 128 && !std::getenv("SEQPLAN_ISP_PULL_A2A");
   layout_heap(c);
   ISP_CUDA(cudaMalloc(&c->heap, c->heap_bytes));
   ISP_CUDA(cudaMemset(c->heap, 0, kFlagBytes));
@@ -820,16 +874,16 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   c->sin_t = static_cast<float*>(A(S * (c->d / 2) * 4));
   c->n1 = static_cast<bf16*>(A(T * H * 2));
   c->rstd1 = static_cast<float*>(A(T * 4));
-  c->qkv_heads = static_cast<bf16*>(A(S * 3 * Hl * 2));
-  c->o_tok = static_cast<bf16*>(A(T * H * 2));
+  c->qkv_heads = c->fused_a2a ? c->hp<bf16>(c->off_qkv_heads) : static_cast<bf16*>(A(S * 3 * Hl * 2));
+  c->o_tok = c->fused_a2a ? c->hp<bf16>(c->off_o_tok) : static_cast<bf16*>(A(T * H * 2));
   c->h = static_cast<bf16*>(A(T * H * 2, seqplan::AllocTag::MlpOutput));
   c->n2 = static_cast<bf16*>(A(T * H * 2));
   c->rstd2 = static_cast<float*>(A(T * 4));
   c->lse = static_cast<float*>(A(c->Dl * S * 4));
   c->dh = static_cast<bf16*>(A(T * H * 2));
   c->dn = static_cast<bf16*>(A(T * H * 2));
-  c->dO_heads = static_cast<bf16*>(A(S * Hl * 2));
-  c->dqkv_tok = static_cast<bf16*>(A(T * 3 * H * 2));
+  c->dO_heads = c->fused_a2a ? c->hp<bf16>(c->off_dO_heads) : static_cast<bf16*>(A(S * Hl * 2));
+  c->dqkv_tok = c->fused_a2a ? c->hp<bf16>(c->off_dqkv_tok) : static_cast<bf16*>(A(T * 3 * H * 2));
   c->delta = static_cast<float*>(A(c->Dl * S * 4));
   c->dq_acc = static_cast<float*>(A(c->Dl * S * c->d * 4));
   c->dg_scratch = static_cast<float*>(A(int64_t(rmsnorm_bwd_scratch_rows(c->num_sms)) * H * 4));
@@ -1119,7 +1173,9 @@ int seqplan_isp_fill_activation(seqplan_isp_ctx* c, uint64_t seed, int tensor_id
 }
 
 static void run_fwd(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
-  if (c->weights_dirty) {  // peers must see refreshed working shards before gathering
+  if (c->weights_dirty || c->fused_a2a) {
+    // peers must see refreshed working shards before gathering; with fused all-to-all, no
+    // peer may push into this rank's exchange buffers before its previous backward finished
     barrier(c, st, false);
     c->weights_dirty = false;
   }

@@ -33,6 +33,16 @@ cudaError_t swiglu_bwd(const __nv_bfloat16* da, const __nv_bfloat16* gu, __nv_bf
 // Causal attention over S tokens for `heads` heads of width d (64 or 128).
 // Q/K/V/O rows are `ld*` elements apart per token; head h starts at column h*d.
 // lse: fp32 [heads, S] (natural log).
+// Fused all-to-all of the attention outputs (d = 128 tcgen05 kernels): rows are global tokens
+// s; row s belongs to rank s / T and lands in that rank's token-sharded buffer (row s % T,
+// row stride ld) at column col_* (which already includes this rank's head offset).
+struct AttnPush {
+  void* p[8];
+  int T;
+  int64_t ld;
+  int64_t col_o, col_q, col_k, col_v;
+};
+
 struct AttnTensors {
   const __nv_bfloat16* q;
   const __nv_bfloat16* k;
@@ -42,6 +52,7 @@ struct AttnTensors {
   int64_t ld_o;
   float* lse;
   int S, heads, d;
+  AttnPush push;  // push.p[0] == nullptr: outputs stay local
 };
 cudaError_t attention_fwd(const AttnTensors& t, cudaStream_t st, int num_sms);
 // tcgen05/TMEM/TMA forward (attention_tc.cu); attention_fwd dispatches here.

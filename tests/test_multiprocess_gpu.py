@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _run(n, H, D, S, mode="selective"):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", f"--master-port={29500 + n + (7 if mode == 'fused' else 0)}",
+           "--master-addr=127.0.0.1", f"--master-port={29500 + n + (7 if mode == 'fused' else 0) + (20 if H == 1024 else 0)}",
            os.path.join(ROOT, "tests", "mp_parity_worker.py"), str(H), str(D), str(S), mode]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
@@ -27,10 +27,11 @@ def _run(n, H, D, S, mode="selective"):
 
 @pytest.mark.parametrize("mode", ["selective", "fused"])
 @pytest.mark.parametrize("n", [2, 4])
-def test_multiprocess_parity(n, mode):
+@pytest.mark.parametrize("H", [512, 1024])  # head dim 64 (pull all-to-all) and 128 (fused into epilogues)
+def test_multiprocess_parity(n, mode, H):
     if torch.cuda.device_count() < n:
         pytest.skip(f"needs {n} GPUs")
-    for row in _run(n, 512, 8, 1024, mode):
+    for row in _run(n, H, 8, 1024, mode):
         for k, v in row.items():
             if k not in ("rank", "timeline_events"):
                 assert v <= 1e-2, (row["rank"], k, v)
