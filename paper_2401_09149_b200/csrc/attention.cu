@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_kernel(AttnTensors t,
 // dq (bf16, row stride ld) = scale * dq_acc[h, t, :]
 template <int D>
 __global__ void attn_dq_convert_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dq,
-                                       int64_t ld, int S, int heads, float scale, const AttnPush push) {
+                                       int64_t ld, int S, int heads, float scale, const __grid_constant__ AttnPush push) {
   const int64_t n = static_cast<int64_t>(heads) * S * (D / 4);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {

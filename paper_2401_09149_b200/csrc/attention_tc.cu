@@ -21,10 +21,11 @@
 
 namespace isp {
 
+extern long long* g_attn_trace_fwd;  // development hook (seqplan_isp_debug_set_trace_fwd)
+
 namespace {
 
 constexpr int kBM = 128;      // queries per CTA
-constexpr int kBN = 64;       // keys per tile
 constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 softmax
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
@@ -44,6 +45,58 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// CW consecutive TMEM columns of this thread's lane (CW = 32 or 64), one wait by the caller.
+template <int CW>
+__device__ __forceinline__ void tmem_ld_row(uint32_t taddr, uint32_t (&r)[CW]) {
+  static_assert(CW == 32 || CW == 64, "row chunk");
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  if constexpr (CW == 64) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]),
+          "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]),
+          "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
+          "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+        : "r"(taddr + 32));
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const uint32_t (&r)[N]) {
+  static_assert(N == 16 || N == 32, "packed P row chunk");
+  if constexpr (N == 16) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+  } else {
+    tmem_st_32x32b_x32(taddr, r);
+  }
+}
+// D[tmem] (+)= A[tmem] * B[smem] (kind::f16, A K-major: lane = row, 32-bit column = 2 K elements)
+__device__ __forceinline__ void tc_mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {  // MUFU.EX2, flush-to-zero
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -54,45 +107,51 @@ __device__ __forceinline__ void named_barrier(int id, int n) {
 }
 
 template <int D>
-struct FwdSmem {
-  static constexpr int kQ = kBM * D * 2;       // D/64 chunks of [128 x 64]
-  static constexpr int kKV = kBN * D * 2;      // K (or V) tile: D/64 chunks of [64 x 64]
-  static constexpr int kP = kBM * kBN * 2;     // [128 x 64]
+struct FwdCfg {
+  static constexpr int BN = D == 128 ? 128 : 64;   // keys per tile
+  static constexpr int NS = D == 128 ? 2 : 6;      // K/V ring depth
+  static constexpr int NP = 2;                     // P lives in TMEM, aliasing the S buffer it came from
+  static constexpr int CW = BN / 2;                // S columns per softmax warp (pair split)
+  static constexpr int kQ = kBM * D * 2;           // D/64 chunks of [128 x 64]
+  static constexpr int kKV = BN * D * 2;           // K (or V) tile: D/64 chunks of [BN x 64]
+  static constexpr int kP = kBM * BN * 2;          // BN/64 chunks of [128 x 64]
   static constexpr int kOffQ = 0;
-  static constexpr int kStages = D == 128 ? 4 : 6;  // K/V ring depth (hides TMA latency)
   static constexpr int kOffK = kOffQ + kQ;
-  static constexpr int kOffV = kOffK + kStages * kKV;
-  static constexpr int kOffP = kOffV + kStages * kKV;  // 2 buffers
-  static constexpr int kOffBar = kOffP + 2 * kP;
+  static constexpr int kOffV = kOffK + NS * kKV;
+  static constexpr int kOffP = kOffV + NS * kKV;
+  static constexpr int kOffBar = kOffP;           // (no shared-memory P: the PV MMA reads P from TMEM)
   static constexpr int kBarBytes = 256;
   static constexpr int kBytes = kOffBar + kBarBytes + 6 * kBM * 4 + 1024;  // barriers + max/sum exchange
+  static constexpr int kTmemCols = D == 128 ? 512 : 256;  // S x2 at 0 / BN, O at 2 BN
+  static_assert(kBytes <= 232448, "exceeds the 227 KB per-CTA shared memory");
 };
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                        const __grid_constant__ CUtensorMap mV, __nv_bfloat16* __restrict__ out,
-                       int64_t ld_o, float* __restrict__ lse, int S, float scale_log2, const AttnPush push) {
-  using L = FwdSmem<D>;
+                       int64_t ld_o, float* __restrict__ lse, int S, float scale_log2, const __grid_constant__ AttnPush push,
+                       long long* trace) {
+  using L = FwdCfg<D>;
+  constexpr int BN = L::BN, NS = L::NS, NP = L::NP, CW = L::CW;
   constexpr int NCH = D / 64;  // 64-wide chunks of the head dim
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
-  constexpr int NS = L::kStages;
   uint64_t* q_full = bar + 0;
-  uint64_t* s_full = bar + 1;    // [2]
-  uint64_t* s_free = bar + 3;    // [2]
-  uint64_t* p_full = bar + 5;    // [2]
-  uint64_t* p_free = bar + 7;    // [2]
-  uint64_t* kv_full = bar + 9;   // [NS]
-  uint64_t* kv_empty = bar + 9 + NS;  // [NS]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9 + 2 * NS);
+  uint64_t* s_full = bar + 1;            // [2]
+  uint64_t* s_free = bar + 3;            // [2]
+  uint64_t* p_full = bar + 5;            // [NP]
+  uint64_t* p_free = bar + 5 + NP;       // [NP]
+  uint64_t* kv_full = bar + 5 + 2 * NP;  // [NS]
+  uint64_t* kv_empty = kv_full + NS;     // [NS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_empty + NS);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int qt = gridDim.x - 1 - blockIdx.x;  // heavy (late) tiles first
   const int h = blockIdx.y;
   const int q0 = qt * kBM;
-  const int n_kv = (q0 + kBM) / kBN;
+  const int n_kv = (q0 + kBM + BN - 1) / BN;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mQ);
@@ -106,18 +165,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_free[i], 256);
+    }
+    for (int i = 0; i < NP; ++i) {
       mbar_init(&p_full[i], 256);
       mbar_init(&p_free[i], 1);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<256>(tmem_slot);
+  if (warp == 1) tmem_alloc<L::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem;          // S buffers at columns 0 and 64
-  const uint32_t tO = tmem + 128;    // O at columns 128 .. 128 + D
+  const uint32_t tS = tmem;               // S buffers at columns 0 and BN
+  const uint32_t tO = tmem + 2 * BN;      // O at columns 2 BN .. 2 BN + D
 
   if (warp == 0) {
     if (lane == 0) {
@@ -130,32 +191,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (j >= NS) mbar_wait(&kv_empty[s], ((j / NS) - 1) & 1);
         mbar_arrive_expect_tx(&kv_full[s], 2 * L::kKV);
         for (int c = 0; c < NCH; ++c) {
-          tma_load_2d(smem + L::kOffK + s * L::kKV + c * kBN * 128, &mK, &kv_full[s], h * D + c * 64, j * kBN);
-          tma_load_2d(smem + L::kOffV + s * L::kKV + c * kBN * 128, &mV, &kv_full[s], h * D + c * 64, j * kBN);
+          tma_load_2d(smem + L::kOffK + s * L::kKV + c * BN * 128, &mK, &kv_full[s], h * D + c * 64, j * BN);
+          tma_load_2d(smem + L::kOffV + s * L::kKV + c * BN * 128, &mV, &kv_full[s], h * D + c * 64, j * BN);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
-      constexpr uint32_t idesc_s = make_idesc_bf16(kBM, kBN, false, false);
+      constexpr uint32_t idesc_s = make_idesc_bf16(kBM, BN, false, false);
       constexpr uint32_t idesc_o = make_idesc_bf16(kBM, D, false, true);
       const uint32_t sQ = smem_u32(smem + L::kOffQ);
       mbar_wait(q_full, 0);
       auto issue_pv = [&](int j) {
-        const int b = j & 1;
-        mbar_wait(&p_full[b], (j >> 1) & 1);
+        const int pb = j % NP;  // == j & 1 == the S/P buffer of tile j
+        mbar_wait(&p_full[pb], (j / NP) & 1);
         tc_fence_after();
-        const uint32_t sP = smem_u32(smem + L::kOffP + b * L::kP);
         const uint32_t sV = smem_u32(smem + L::kOffV + (j % NS) * L::kKV);
 #pragma unroll
-        for (int k = 0; k < kBN / 16; ++k) {
-          const uint64_t ad = make_sw128_desc(sP + k * 32, 16, 1024);
-          const uint64_t bd = make_sw128_desc(sV + k * 2048, kBN * 128, 1024);
-          tc_mma_bf16(tO, ad, bd, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
+        for (int k = 0; k < BN / 16; ++k) {  // A = P (bf16 pairs packed in TMEM columns), B = V (smem)
+          const uint64_t bd = make_sw128_desc(sV + k * 2048, BN * 128, 1024);
+          tc_mma_bf16_ts(tO, tS + pb * BN + k * 8, bd, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
         }
         tc_commit(&kv_empty[j % NS]);
-        tc_commit(&p_free[b]);
+        tc_commit(&p_free[pb]);
       };
       for (int j = 0; j < n_kv; ++j) {
         const int b = j & 1;
@@ -167,17 +226,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int k = 0; k < D / 16; ++k) {
           const int c = k / 4, kk = k % 4;
           const uint64_t ad = make_sw128_desc(sQ + c * kBM * 128 + kk * 32, 16, 1024);
-          const uint64_t bd = make_sw128_desc(sK + c * kBN * 128 + kk * 32, 16, 1024);
-          tc_mma_bf16(tS + b * kBN, ad, bd, idesc_s, k > 0 ? 1u : 0u);
+          const uint64_t bd = make_sw128_desc(sK + c * BN * 128 + kk * 32, 16, 1024);
+          tc_mma_bf16(tS + b * BN, ad, bd, idesc_s, k > 0 ? 1u : 0u);
         }
         tc_commit(&s_full[b]);
+        const bool tr = trace && blockIdx.x == 0 && blockIdx.y == 0 && j < 64;
+        if (tr) trace[j * 8 + 0] = clock64();
         if (j >= 1) issue_pv(j - 1);
+        if (tr) trace[j * 8 + 1] = clock64();
       }
       issue_pv(n_kv - 1);
     }
   } else {
     // ---------------- softmax + epilogue (warps 2..9) ----------------
-    // A warp pair per TMEM lane quadrant shares 32 query rows and splits the 64 key columns
+    // A warp pair per TMEM lane quadrant shares 32 query rows and splits the BN key columns
     // of S (and the D columns of O); the row max is exchanged through smem each tile.
     const int quad = warp & 3, half = (warp - 2) >> 2;
     const int r = quad * 32 + lane;  // query row within the tile == TMEM lane
@@ -186,33 +248,41 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* xmax = reinterpret_cast<float*>(smem + L::kOffBar + L::kBarBytes);  // [2 slots][2 halves][128 rows]
     float m = -INFINITY, l = 0.f;
     int pf_seen0 = 0, pf_seen1 = 0;  // completed p_free phases consumed per buffer (registers)
-    auto ensure_pfree = [&](int b, int count) {
-      int& seen = b ? pf_seen1 : pf_seen0;
+    auto ensure_pfree = [&](int pb, int count) {
+      int& seen = pb ? pf_seen1 : pf_seen0;
       while (seen < count) {
-        mbar_wait(&p_free[b], seen & 1);
+        mbar_wait(&p_free[pb], seen & 1);
         ++seen;
       }
     };
     for (int j = 0; j < n_kv; ++j) {
       const int b = j & 1;
+      const bool tr = trace && blockIdx.x == 0 && blockIdx.y == 0 && j < 64 && warp == 2 && lane == 0;
+      if (tr) trace[j * 8 + 2] = clock64();
       mbar_wait(&s_full[b], (j >> 1) & 1);
+      if (tr) trace[j * 8 + 3] = clock64();
       tc_fence_after();
-      uint32_t sr[32];
-      tmem_ld_32x32b_x32(tS + lane_off + b * kBN + half * 32, sr);
+      uint32_t sr[CW];
+      tmem_ld_row<CW>(tS + lane_off + b * BN + half * CW, sr);
       tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&s_free[b]);
-      const bool diag = (j + 1) * kBN > q0;  // tile may contain keys > some query of the CTA
-      float mx = -INFINITY;
+      const bool diag = (j + 1) * BN > q0;  // tile may contain keys > some query of the CTA
       if (diag) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (j * kBN + half * 32 + i > q) sr[i] = __float_as_uint(-INFINITY);
+        for (int i = 0; i < CW; ++i)
+          if (j * BN + half * CW + i > q) sr[i] = __float_as_uint(-INFINITY);
       }
+      float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(sr[i]));
+      for (int i = 0; i < CW; i += 4) {
+        mx0 = fmaxf(mx0, __uint_as_float(sr[i]));
+        mx1 = fmaxf(mx1, __uint_as_float(sr[i + 1]));
+        mx2 = fmaxf(mx2, __uint_as_float(sr[i + 2]));
+        mx3 = fmaxf(mx3, __uint_as_float(sr[i + 3]));
+      }
+      float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
       xmax[(b * 2 + half) * kBM + r] = mx;
       named_barrier(2 + quad, 64);
+      if (tr) trace[j * 8 + 4] = clock64();
       mx = fmaxf(mx, xmax[(b * 2 + (half ^ 1)) * kBM + r]) * scale_log2;
       // stale-max online softmax: correct O only when the max grows by > 2^8 (uniform across
       // the pair: both warps hold the same rows and the same m)
@@ -220,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (j == 0) {
         m = m_new;
       } else if (__any_sync(0xffffffffu, m_new > m + kRescaleThreshold)) {
-        ensure_pfree((j - 1) & 1, ((j - 1) >> 1) + 1);  // PV_{j-1} has landed in O
+        ensure_pfree((j - 1) % NP, (j - 1) / NP + 1);  // PV_{j-1} has landed in O
         tc_fence_after();
         const float alpha = fast_exp2(m - m_new);
 #pragma unroll 1
@@ -237,33 +307,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         l *= alpha;
         m = m_new;
       }
-      // P = exp2(s * scale - m) into this warp's half of the swizzled bf16 A tile
-      uint32_t pk[16];
-      float psum = 0.f;
+      // P = exp2(s * scale - m) into this warp's columns of the swizzled bf16 A tile
+      uint32_t pk[CW / 2];
+      float ps0 = 0.f, ps1 = 0.f;
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) {
+      for (int i = 0; i < CW; i += 2) {
         const float p0 = fast_exp2(fmaf(__uint_as_float(sr[i]), scale_log2, -m));
         const float p1 = fast_exp2(fmaf(__uint_as_float(sr[i + 1]), scale_log2, -m));
-        psum += p0 + p1;
+        ps0 += p0;
+        ps1 += p1;
         pk[i / 2] = pack_bf16(p0, p1);
       }
-      l += psum;
-      ensure_pfree(b, j >> 1);  // PV_{j-2} has finished reading this P buffer
-      uint8_t* prow = smem + L::kOffP + b * L::kP + r * 128;
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc)
-        *reinterpret_cast<uint4*>(prow + (((half * 4 + cc) ^ (r & 7)) * 16)) =
-            make_uint4(pk[4 * cc], pk[4 * cc + 1], pk[4 * cc + 2], pk[4 * cc + 3]);
-      fence_proxy_async();
+      l += ps0 + ps1;
+      // P (bf16 pairs) overwrites the first half of this tile's S buffer: the PV MMA reads it as
+      // its TMEM A operand; S_{j+2} is issued after PV_j, so in-order MMA execution protects it
+      const int pb = j % NP;
+      if (tr) trace[j * 8 + 5] = clock64();
+      ensure_pfree(pb, j / NP);  // consume PV_{j-2}'s completion in order (mbarrier parity bookkeeping)
+      tmem_st_cols<CW / 2>(tS + lane_off + b * BN + half * (CW / 2), pk);
+      tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&p_full[b]);
+      mbar_arrive(&s_free[b]);
+      mbar_arrive(&p_full[pb]);
+      if (tr) trace[j * 8 + 6] = clock64();
     }
     // epilogue: combine the pair's partial row sums, wait for the last PV, O / l -> bf16
     float* xsum = xmax + 4 * kBM;
     xsum[half * kBM + r] = l;
     named_barrier(2 + quad, 64);
     const float l_tot = l + xsum[(half ^ 1) * kBM + r];
-    ensure_pfree((n_kv - 1) & 1, ((n_kv - 1) >> 1) + 1);
+    ensure_pfree((n_kv - 1) % NP, (n_kv - 1) / NP + 1);
     tc_fence_after();
     const float inv = 1.f / l_tot;
     __nv_bfloat16* orow = out + static_cast<int64_t>(q) * ld_o + h * D + half * (D / 2);
@@ -297,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<256>(tmem);
+    tmem_dealloc<L::kTmemCols>(tmem);
   }
 }
 
@@ -328,7 +401,7 @@ bool map2d(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t
 
 template <int D>
 cudaError_t launch_fwd(const AttnTensors& t, cudaStream_t st) {
-  using L = FwdSmem<D>;
+  using L = FwdCfg<D>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
@@ -337,12 +410,12 @@ cudaError_t launch_fwd(const AttnTensors& t, cudaStream_t st) {
   }
   CUtensorMap mq, mk, mv;
   const int64_t cols = static_cast<int64_t>(t.heads) * D;
-  if (!map2d(&mq, t.q, t.S, cols, t.ld_qkv, kBM) || !map2d(&mk, t.k, t.S, cols, t.ld_qkv, kBN) ||
-      !map2d(&mv, t.v, t.S, cols, t.ld_qkv, kBN))
+  if (!map2d(&mq, t.q, t.S, cols, t.ld_qkv, kBM) || !map2d(&mk, t.k, t.S, cols, t.ld_qkv, L::BN) ||
+      !map2d(&mv, t.v, t.S, cols, t.ld_qkv, L::BN))
     return cudaErrorInvalidValue;
   const float scale_log2 = (1.0f / sqrtf(static_cast<float>(D))) * kLog2e;
   attn_fwd_tc_kernel<D><<<dim3(t.S / kBM, t.heads), kThreads, L::kBytes, st>>>(mq, mk, mv, t.o, t.ld_o, t.lse, t.S,
-                                                                               scale_log2, t.push);
+                                                                               scale_log2, t.push, g_attn_trace_fwd);
   return cudaGetLastError();
 }
 
@@ -414,7 +487,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                        const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mDO,
                        const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ dq_acc,
                        __nv_bfloat16* __restrict__ dk_out, __nv_bfloat16* __restrict__ dv_out, int64_t ld_d,
-                       int S, float scale, int dbg, long long* trace, const AttnPush push) {
+                       int S, float scale, int dbg, long long* trace, const __grid_constant__ AttnPush push) {
   using L = BwdSmem;
   constexpr int D = 128;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -676,7 +749,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 }  // namespace
 
 long long* g_attn_trace = nullptr;  // development: clock64 trace of CTA (0,0)
+long long* g_attn_trace_fwd = nullptr;
 extern "C" void seqplan_isp_debug_set_trace(long long* dev_buf) { g_attn_trace = dev_buf; }
+extern "C" void seqplan_isp_debug_set_trace_fwd(long long* dev_buf) { g_attn_trace_fwd = dev_buf; }
 
 // dq_acc must be zeroed and delta = rowsum(dO * O) computed before this launch.
 cudaError_t attention_bwd_tc(const AttnTensors& t, const __nv_bfloat16* dout, int64_t ld_dout, __nv_bfloat16* dk,

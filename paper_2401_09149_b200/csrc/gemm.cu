@@ -224,7 +224,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_b
 template <bool A_MN, bool B_MN, int BN, int EPI>
 __global__ void __launch_bounds__(kNumThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA,
-                   const __grid_constant__ CUtensorMap mapB, GemmArgs args) {
+                   const __grid_constant__ CUtensorMap mapB, const __grid_constant__ GemmArgs args) {
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -407,7 +407,7 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {  // arrive o
 template <bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kNumThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                    GemmArgs args) {
+                    const __grid_constant__ GemmArgs args) {
   constexpr int BN = 256, BNH = BN / 2, S = 6;
   constexpr int kABytes = BM * BK * 2, kBBytes = BNH * BK * 2, kStageBytes = kABytes + kBBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];

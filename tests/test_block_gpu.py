@@ -80,8 +80,8 @@ def test_block_p1(cuda, H, D, S):
     blk.close()
 
 
-@pytest.mark.parametrize("p", [2, 4])
-@pytest.mark.parametrize("H,D,S", [(512, 8, 1024), (1024, 8, 1024)])
+@pytest.mark.parametrize("p,H,D,S", [(2, 512, 8, 1024), (4, 512, 8, 1024), (2, 1024, 8, 1024), (4, 1024, 8, 1024),
+                                     (8, 1024, 8, 2048)])  # p = 8: the north-star degree, on one GPU
 def test_block_group(cuda, p, H, D, S):
     sh, w, x, dy, y_ref, dx_ref, g_ref = oracle_case(H, D, S)
     grp = capi.IspGroup(H, D, S, world=p)
