@@ -829,7 +829,7 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   c->T = c->S / c->world;
   c->Hl = c->H / c->world;
   c->Dl = c->D / c->world;
-  if ((c->d != 64 && c->d != 128) || c->T % 128 || c->H % 256 || c->I % 256 || (c->I / c->world) % 64 ||
+  if ((c->d != 64 && c->d != 128) || c->T % 128 || c->H % 256 || c->I % 256 || (c->I / c->world) % kGuBlock ||
       c->S % 128)
     throw IspError(SEQPLAN_ISP_ERR_UNSUPPORTED,
                    "shape not tiled by the sm_100a kernels (head dim 64/128, S/p % 128, H % 256, I % 256)");
