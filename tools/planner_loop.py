@@ -62,7 +62,7 @@ def main():
         a[0] += r["seconds"] / n
         a[1] += r["bytes"] / n
     if rank == 0:
-        prof_dir = ROOT / "profiles"
+        prof_dir = Path(os.environ.get("PLANNER_OUT", str(ROOT / "profiles")))
         prof_dir.mkdir(exist_ok=True)
         e = 2
         I = mlp_dim(H)
@@ -86,8 +86,11 @@ def main():
         with open(csv, "w") as f:
             f.write("# measured on B200 by tools/planner_loop.py (CUDA events, contended with compute)\n")
             f.write("op,participants,axis,message_bytes,bandwidth_bytes_per_sec\n")
+            # one NVSwitch box: every peer is equally close, but place_groups classifies the ps
+            # group of the single-box ISP plan as inter -> same curve on both axes
             for r in rows:
-                f.write(f"{r[0]},{r[1]},{r[2]},{int(r[3])},{r[4]:.6e}\n")
+                for axis in ("intra", "inter"):
+                    f.write(f"{r[0]},{r[1]},{axis},{int(r[3])},{r[4]:.6e}\n")
             if not rows:
                 f.write("all-gather,2,intra,1,9.0e11\n")
         exe = ROOT / "tools" / "_planner_check"
