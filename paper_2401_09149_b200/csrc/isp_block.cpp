@@ -150,6 +150,8 @@ struct seqplan_isp_ctx {
   // one stream per peer: copy-engine transfers from different peers run concurrently
   cudaStream_t peer_st[kMaxRanks] = {};
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxRanks] = {};
+  cudaEvent_t ev_tq[SEQPLAN_W_COUNT][kMaxRanks] = {};  // tensor t's shard from rank q has landed
+  bool pipelined_gather = false;                        // wait_gathered uses ev_tq (copy-engine path)
   cudaEvent_t ev_gathered[SEQPLAN_W_COUNT] = {};
   cudaEvent_t ev_wgrad[SEQPLAN_W_COUNT] = {};
   cudaEvent_t ev_comm_done = nullptr, ev_start = nullptr;
@@ -422,6 +424,58 @@ AttnPush attn_push(Ctx* c, size_t heap_off, int64_t ld, int64_t col_o, int64_t c
   return p;
 }
 
+// Copy-engine all-gather of several tensors as one pipeline: every peer's stream pulls that
+// peer's shards of all tensors back to back (no per-tensor join, so DMA setup of the next copy
+// overlaps the current one and all peers stream concurrently); a consumer waits only on the
+// per-(tensor, peer) events of the tensor it needs.
+void gather_pipelined(Ctx* c, const int* order, int n, cudaStream_t cs) {
+  const int64_t B = kGuBlock, H = c->H, rpr = c->I / c->world;
+  int todo[SEQPLAN_W_COUNT];
+  int m = 0;
+  for (int i = 0; i < n; ++i) {
+    const int t = order[i];
+    if (c->skip_comm() && c->pregathered[t]) {
+      c->gathered[t] = c->pregathered[t];
+      continue;
+    }
+    const int64_t bytes = (t == SEQPLAN_W_GATE ? 2 * c->I * c->H : c->numel(t)) * 2;
+    c->gathered[t] = static_cast<bf16*>(pool_alloc(c, bytes, seqplan::AllocTag::CommBuffer, cs));
+    todo[m++] = t;
+  }
+  if (m == 0) return;
+  double remote = 0;
+  for (int i = 0; i < m; ++i)
+    remote += double(todo[i] == SEQPLAN_W_GATE ? 2 * c->I * c->H : c->numel(todo[i])) * 2 * (c->world - 1) / c->world;
+  Span sp(c, cs, 1, SEQPLAN_EV_ALL_GATHER, todo[0]);
+  KTimer kt(c, cs, SEQPLAN_K_ALL_GATHER, 0, remote);
+  ISP_CUDA(cudaEventRecord(c->ev_fork, cs));
+  auto copy = [&](int t, int q, cudaStream_t qs) {
+    bf16* dst = c->gathered[t];
+    if (t == SEQPLAN_W_GATE) {
+      for (int which = 0; which < 2; ++which) {
+        const bf16* src = c->peer<bf16>(q, c->off_wshard[which ? SEQPLAN_W_UP : SEQPLAN_W_GATE]);
+        bf16* d0 = dst + ((q * rpr / B) * 2 * B + which * B) * H;
+        ISP_CUDA(cudaMemcpy2DAsync(d0, size_t(2 * B * H * 2), src, size_t(B * H * 2), size_t(B * H * 2),
+                                   size_t(rpr / B), cudaMemcpyDefault, qs));
+      }
+    } else {
+      const int64_t sh = c->shard(t);
+      ISP_CUDA(cudaMemcpyAsync(dst + q * sh, c->peer<bf16>(q, c->off_wshard[t]), size_t(sh * 2), cudaMemcpyDefault,
+                               qs));
+    }
+    ISP_CUDA(cudaEventRecord(c->ev_tq[t][q], qs));
+  };
+  for (int q = 0; q < c->world; ++q) {
+    if (q == c->rank) continue;
+    ISP_CUDA(cudaStreamWaitEvent(c->peer_st[q], c->ev_fork, 0));
+    for (int i = 0; i < m; ++i) copy(todo[i], q, c->peer_st[q]);
+  }
+  for (int i = 0; i < m; ++i) copy(todo[i], c->rank, cs);  // own shard: local copy
+  for (int q = 0; q < c->world; ++q)  // the comm stream rejoins before later comm work
+    if (q != c->rank) ISP_CUDA(cudaStreamWaitEvent(cs, c->ev_tq[todo[m - 1]][q], 0));
+  c->pipelined_gather = true;
+}
+
 void fwd_issue_gathers(Ctx* c, cudaStream_t st) {
   if (c->world == 1) {
     for (int t : {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN})
@@ -433,14 +487,19 @@ void fwd_issue_gathers(Ctx* c, cudaStream_t st) {
     ISP_CUDA(cudaEventRecord(c->ev_start, st));
     ISP_CUDA(cudaStreamWaitEvent(cs, c->ev_start, 0));
   }
-  for (int t : {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN}) {
-    gather_weight(c, t, cs);
-    if (!c->group_mode) ISP_CUDA(cudaEventRecord(c->ev_gathered[t], cs));
+  if (!c->group_mode) {
+    const int order[] = {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN};
+    gather_pipelined(c, order, 6, cs);
+    return;
   }
+  for (int t : {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN})
+    gather_weight(c, t, cs);
 }
 
 void wait_gathered(Ctx* c, int t, cudaStream_t st) {
-  if (c->world > 1 && !c->group_mode) ISP_CUDA(cudaStreamWaitEvent(st, c->ev_gathered[t], 0));
+  if (c->world == 1 || c->group_mode) return;
+  if (c->skip_comm() && c->gathered[t] == c->pregathered[t] && c->pregathered[t]) return;
+  for (int q = 0; q < c->world; ++q) ISP_CUDA(cudaStreamWaitEvent(st, c->ev_tq[t][q], 0));
 }
 
 void fwd_phase1(Ctx* c, const bf16* x, cudaStream_t st) {
@@ -556,10 +615,11 @@ void bwd_issue_gathers(Ctx* c, cudaStream_t st) {
     ISP_CUDA(cudaEventRecord(c->ev_start, st));
     ISP_CUDA(cudaStreamWaitEvent(cs, c->ev_start, 0));
   }
-  for (int t : order) {
-    gather_weight(c, t, cs);
-    if (!c->group_mode) ISP_CUDA(cudaEventRecord(c->ev_gathered[t], cs));
+  if (!c->group_mode) {
+    gather_pipelined(c, order, 6, cs);
+    return;
   }
+  for (int t : order) gather_weight(c, t, cs);
 }
 
 // Weight-gradient destination: fp32 grad shard directly at p = 1, bf16 partial in the heap otherwise.
@@ -893,6 +953,8 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   for (int q = 0; q < c->world; ++q) {
     ISP_CUDA(cudaStreamCreateWithFlags(&c->peer_st[q], cudaStreamNonBlocking));
     ISP_CUDA(cudaEventCreateWithFlags(&c->ev_join[q], cudaEventDisableTiming));
+    for (int t = 0; t < SEQPLAN_W_COUNT; ++t)
+      ISP_CUDA(cudaEventCreateWithFlags(&c->ev_tq[t][q], cudaEventDisableTiming));
   }
   for (int t = 0; t < SEQPLAN_W_COUNT; ++t) {
     ISP_CUDA(cudaEventCreateWithFlags(&c->ev_gathered[t], cudaEventDisableTiming));
@@ -1031,6 +1093,8 @@ void seqplan_isp_ctx_destroy(seqplan_isp_ctx* c) {
   for (int q = 0; q < kMaxRanks; ++q) {
     if (c->peer_st[q]) cudaStreamDestroy(c->peer_st[q]);
     if (c->ev_join[q]) cudaEventDestroy(c->ev_join[q]);
+    for (int t = 0; t < SEQPLAN_W_COUNT; ++t)
+      if (c->ev_tq[t][q]) cudaEventDestroy(c->ev_tq[t][q]);
   }
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   for (int t = 0; t < SEQPLAN_W_COUNT; ++t) {
