@@ -436,6 +436,7 @@ __global__ void attn_dq_convert_kernel(const float* __restrict__ dq_acc, __nv_bf
       *reinterpret_cast<uint2*>(dq + static_cast<int64_t>(tok) * ld + h * D + c4 * 4) = o;
     }
   }
+  if (push.p[0]) __threadfence_system();  // pushed rows visible before the next barrier flag
 }
 
 template <int D>

@@ -364,6 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (half == 0) lse[static_cast<int64_t>(h) * S + q] = (m + log2f(l_tot)) * 0.6931471805599453f;
+    if (push.p[0]) __threadfence_system();  // pushed rows visible before the next barrier flag
   }
 
   tc_fence_before();
@@ -736,6 +737,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         pv_out[v4] = make_uint4(y[0], y[1], y[2], y[3]);
       }
     }
+    if (push.p[0]) __threadfence_system();  // pushed rows visible before the next barrier flag
   }
 
   tc_fence_before();

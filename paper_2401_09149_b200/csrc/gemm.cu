@@ -346,6 +346,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       mbar_arrive(&tempty_bar[acc]);
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
     }
+    // remote (NVLink) stores of the fused all-to-all must be performed before the stream's
+    // next barrier flag can be observed by the peer
+    if (args.push[0]) __threadfence_system();
   }
 
   tc_fence_before();
@@ -523,6 +526,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       else mbar_arrive_leader(&tempty_bar[acc]);
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
     }
+    if (args.push[0]) __threadfence_system();  // remote stores visible before the next barrier flag
   }
 
   tc_fence_before();
