@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                        const __grid_constant__ CUtensorMap mV, __nv_bfloat16* __restrict__ out,
                        int64_t ld_o, float* __restrict__ lse, int S, float scale_log2, const __grid_constant__ AttnPush push,
-                       long long* trace) {
+                       long long* trace, int dbg) {
   using L = FwdCfg<D>;
   constexpr int BN = L::BN, NS = L::NS, NP = L::NP, CW = L::CW;
   constexpr int NCH = D / 64;  // 64-wide chunks of the head dim
@@ -262,6 +262,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&s_full[b], (j >> 1) & 1);
       if (tr) trace[j * 8 + 3] = clock64();
       tc_fence_after();
+      if (dbg == 1) {  // development: pipeline bound without the softmax math
+        ensure_pfree(j % NP, j / NP);
+        tc_fence_before();
+        mbar_arrive(&s_free[b]);
+        mbar_arrive(&p_full[j % NP]);
+        continue;
+      }
       uint32_t sr[CW];
       tmem_ld_row<CW>(tS + lane_off + b * BN + half * CW, sr);
       tmem_ld_wait();
@@ -375,6 +382,333 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------
+// CTA-pair, two-stream forward (d = 128): the production forward kernel.
+//
+// A cluster of 2 CTAs owns 4 query tiles of 128 of one head (512 queries); the leader CTA
+// issues M = 256 tcgen05.mma.cta_group::2 for two independent streams:
+//   stream A = tiles {4pp, 4pp+1} (CTA 0 / CTA 1 rows), stream B = tiles {4pp+2, 4pp+3}.
+// Per stream: S_x = Q_x K^T (each CTA holds its own Q tile and half of the 128-key K tile),
+// O_x += P_x V (P from each CTA's TMEM, each CTA holds half of V's head-dim columns).
+// TMEM per CTA: S_A | S_B | O_A | O_B (4 x 128 columns); P_x overwrites S_x as bf16 pairs.
+// The MMA order PV_A(j), S_A(j+1), PV_B(j), S_B(j+1) lets softmax A(j+1) run while the
+// tensor pipe works on stream B and vice versa, so the softmax latency is hidden whenever
+// it is below one stream's MMA time. Per 128-key tile each CTA streams 32 KB of K/V for 256
+// queries (4x less L2->SM traffic than one 128-query tile per CTA).
+// Softmax: warpgroup x (warps 4x..4x+3) owns stream x, one thread per query row with all
+// 128 columns in registers (no cross-warp max exchange); 3 of every 8 exponentials run as a
+// degree-3 polynomial on the FMA pipe, the rest on MUFU.EX2, since MUFU alone would need as
+// many cycles per tile as the MMAs.
+// Warps 0..7 softmax, warp 8 TMA, warp 9 MMA (leader only).
+// ---------------------------------------------------------------------------------
+struct Fa4Cfg {
+  static constexpr int D = 128, BN = 128, NS = 4;
+  static constexpr int kQ = kBM * D * 2;        // one Q tile: 2 chunks [128 q][64]
+  static constexpr int kKh = (BN / 2) * D * 2;  // half K tile: 2 chunks [64 keys][64]
+  static constexpr int kVh = BN * 64 * 2;       // half V tile: 1 chunk [128 keys][64 d]
+  static constexpr int kStage = kKh + kVh;
+  static constexpr int kOffQ = 0;               // Q_A, Q_B
+  static constexpr int kOffKV = kOffQ + 2 * kQ;
+  static constexpr int kOffBar = kOffKV + NS * kStage;
+  static constexpr int kBytes = kOffBar + 256 + 1024;
+  static_assert(kBytes <= 232448, "exceeds the 227 KB per-CTA shared memory");
+};
+
+__device__ __forceinline__ void tc_mma_bf16_ts_pair(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                                    uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tmem_st_x8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld_x16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// 2^x on the FMA pipe for x <= ~8: round-to-nearest split x = j + f (f in [-1/2, 1/2]) via the
+// 1.5*2^23 shifter, degree-3 polynomial for 2^f (|rel err| < 1e-3, below bf16's half ulp),
+// then j added into the exponent field. x is clamped at -125 (masked -inf -> ~2^-125).
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  constexpr float kShift = 12582912.f;  // 1.5 * 2^23
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 t = __fadd2_rn(x, make_float2(kShift, kShift));
+  const float2 jf = __fadd2_rn(t, make_float2(-kShift, -kShift));
+  const float2 f = __fadd2_rn(x, make_float2(-jf.x, -jf.y));
+  float2 p = __ffma2_rn(make_float2(0.0555041f, 0.0555041f), f, make_float2(0.2402265f, 0.2402265f));
+  p = __ffma2_rn(p, f, make_float2(0.6931472f, 0.6931472f));
+  p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_fa4_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
+                        const __grid_constant__ CUtensorMap mV, __nv_bfloat16* __restrict__ out, int64_t ld_o,
+                        float* __restrict__ lse, int S, float scale_log2, const __grid_constant__ AttnPush push,
+                        long long* trace, int dbg) {
+  using L = Fa4Cfg;
+  constexpr int D = L::D, BN = L::BN, NS = L::NS;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
+  uint64_t* q_full = bar + 0;         // leader's: the pair's 4 Q tiles
+  uint64_t* s_full = bar + 1;         // [2] local (multicast commit)
+  uint64_t* p_full = bar + 3;         // [2] leader's: 4 warps x 2 CTAs per stream
+  uint64_t* o_full = bar + 5;         // [2] local (multicast commit): last PV of the stream done
+  uint64_t* kv_full = bar + 7;        // [NS] leader's
+  uint64_t* kv_empty = kv_full + NS;  // [NS] local (multicast commit)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_empty + NS);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t crank = cluster_rank();
+  const bool leader = crank == 0;
+  const int pp = static_cast<int>(gridDim.x / 2) - 1 - static_cast<int>(blockIdx.x / 2);  // heavy groups first
+  const int h = blockIdx.y;
+  const int q0A = (4 * pp + static_cast<int>(crank)) * kBM, q0B = q0A + 2 * kBM;
+  const int nA = (4 * pp + 2) * kBM / BN, nB = nA + 2 * kBM / BN;  // key tiles per stream (its upper tile's)
+
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&mQ);
+    tma_prefetch(&mK);
+    tma_prefetch(&mV);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 8);
+      mbar_init(&o_full[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;  // S_A 0, S_B 128, O_A 256, O_B 384
+
+  if (warp == 8) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs; completion on the leader's barriers) ----------------
+      if (leader) mbar_arrive_expect_tx(q_full, 4 * L::kQ);
+      for (int x = 0; x < 2; ++x)
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d_pair(smem + L::kOffQ + x * L::kQ + c * kBM * 128, &mQ, q_full, h * D + c * 64, x ? q0B : q0A);
+      for (int j = 0; j < nB; ++j) {
+        const int s = j % NS;
+        if (j >= NS) mbar_wait(&kv_empty[s], ((j / NS) - 1) & 1);
+        if (leader) mbar_arrive_expect_tx(&kv_full[s], 2 * L::kStage);
+        uint8_t* st = smem + L::kOffKV + s * L::kStage;
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d_pair(st + c * (BN / 2) * 128, &mK, &kv_full[s], h * D + c * 64,
+                           j * BN + static_cast<int>(crank) * (BN / 2));
+        tma_load_2d_pair(st + L::kKh, &mV, &kv_full[s], h * D + static_cast<int>(crank) * 64, j * BN);
+      }
+    }
+  } else if (warp == 9) {
+    if (leader && lane == 0) {
+      // ---------------- MMA issuer (leader only) ----------------
+      constexpr uint32_t idS = make_idesc_bf16(2 * kBM, BN, false, false);
+      constexpr uint32_t idO = make_idesc_bf16(2 * kBM, D, false, true);
+      int waited = -1;
+      auto wait_kv = [&](int j) {
+        if (j > waited) {
+          mbar_wait(&kv_full[j % NS], (j / NS) & 1);
+          tc_fence_after();
+          waited = j;
+        }
+      };
+      auto issue_s = [&](int x, int j) {
+        const uint32_t sQ = smem_u32(smem + L::kOffQ + x * L::kQ);
+        const uint32_t sK = smem_u32(smem + L::kOffKV + (j % NS) * L::kStage);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const int c = k / 4, kk = k % 4;
+          tc_mma_bf16_pair(tmem + x * 128, make_sw128_desc(sQ + c * kBM * 128 + kk * 32, 16, 1024),
+                           make_sw128_desc(sK + c * (BN / 2) * 128 + kk * 32, 16, 1024), idS, k > 0 ? 1u : 0u);
+        }
+        tc_commit_pair(&s_full[x]);
+      };
+      auto issue_pv = [&](int x, int j) {
+        if (dbg != 2) mbar_wait(&p_full[x], j & 1);
+        if (trace && blockIdx.x == 0 && blockIdx.y == 0 && j < 64) trace[j * 8 + 2 * x] = clock64();
+        tc_fence_after();
+        const uint32_t sV = smem_u32(smem + L::kOffKV + (j % NS) * L::kStage + L::kKh);
+#pragma unroll
+        for (int k = 0; k < BN / 16; ++k)  // A = P_x (TMEM), B = V half (MN-major)
+          tc_mma_bf16_ts_pair(tmem + 256 + x * 128, tmem + x * 128 + k * 8,
+                              make_sw128_desc(sV + k * 2048, BN * 128, 1024), idO, (j > 0 || k > 0) ? 1u : 0u);
+        if (trace && blockIdx.x == 0 && blockIdx.y == 0 && j < 64) trace[j * 8 + 2 * x + 1] = clock64();
+      };
+      mbar_wait(q_full, 0);
+      wait_kv(0);
+      issue_s(0, 0);
+      issue_s(1, 0);
+      for (int j = 0; j < nB; ++j) {
+        if (j < nA) {
+          issue_pv(0, j);
+          if (j == nA - 1) {
+            tc_commit_pair(&o_full[0]);
+          } else {
+            wait_kv(j + 1);
+            issue_s(0, j + 1);
+          }
+        }
+        issue_pv(1, j);
+        tc_commit_pair(&kv_empty[j % NS]);
+        if (j == nB - 1) {
+          tc_commit_pair(&o_full[1]);
+        } else {
+          wait_kv(j + 1);
+          issue_s(1, j + 1);
+        }
+      }
+    }
+  } else {
+    // ---------------- softmax + epilogue: warpgroup x = stream x ----------------
+    const int x = warp >> 2, quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const int q0 = x ? q0B : q0A, q = q0 + r, n = x ? nB : nA;
+    const uint32_t lo = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t tSx = tmem + x * 128 + lo, tOx = tmem + 256 + x * 128 + lo;
+    const bool tr = trace && blockIdx.x == 0 && blockIdx.y == 0 && x == 0 && lane == 0;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n; ++j) {
+      mbar_wait(&s_full[x], j & 1);
+      tc_fence_after();
+      
+      if (dbg == 0) {
+        uint32_t sr[BN];
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t (&chunk)[32] = *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]);
+          tmem_ld_32x32b_x32(tSx + c * 32, chunk);
+        }
+        tmem_ld_wait();
+        if ((j + 1) * BN > q0) {  // tile reaches past some query of this tile: causal mask
+#pragma unroll
+          for (int i = 0; i < BN; ++i)
+            if (j * BN + i > q) sr[i] = __float_as_uint(-INFINITY);
+        }
+        float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < BN; i += 4) {
+          mx0 = fmax3f(mx0, __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
+          mx1 = fmax3f(mx1, __uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3]));
+        }
+        const float m_new = fmaxf(m, fmaxf(mx0, mx1) * scale_log2);
+        if (j == 0) {
+          m = m_new;
+        } else if (__any_sync(0xffffffffu, m_new > m + kRescaleThreshold)) {
+          // stale-max rule: O is corrected only when the row max grows by > 2^8 (warp-uniform);
+          // PV_x(j-1) has completed (it precedes S_x(j) in the tensor pipe)
+          const float alpha = fast_exp2(m - m_new);
+#pragma unroll 1
+          for (int c = 0; c < D / 16; ++c) {  // 16-column chunks: S stays live in registers
+            uint32_t o[16];
+            tmem_ld_x16(tOx + c * 16, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st_cols<16>(tOx + c * 16, o);
+          }
+          l *= alpha;
+          m = m_new;
+        }
+        const float2 sc = make_float2(scale_log2, scale_log2), nm = make_float2(-m, -m);
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < BN / 16; ++c) {  // 16 columns -> 8 packed bf16 pairs per TMEM store
+          uint32_t pk[8];
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            const float2 sv = make_float2(__uint_as_float(sr[c * 16 + i]), __uint_as_float(sr[c * 16 + i + 1]));
+            const float2 xv = __ffma2_rn(sv, sc, nm);
+            float2 pv;
+            if (i >= 10) {  // 3 of 8 pairs on the FMA pipe
+              pv = exp2_poly2(xv);
+            } else {
+              pv.x = fast_exp2(xv.x);
+              pv.y = fast_exp2(xv.y);
+            }
+            acc = __fadd2_rn(acc, pv);
+            pk[i / 2] = pack_bf16(pv.x, pv.y);
+          }
+          tmem_st_x8(tSx + c * 8, pk);
+        }
+        l += acc.x + acc.y;
+        tmem_st_wait();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (tr && j < 64) trace[j * 8 + 4 + quad] = clock64();
+      if (lane == 0) {
+        if (leader) mbar_arrive(&p_full[x]);
+        else mbar_arrive_leader(&p_full[x]);
+      }
+    }
+    // epilogue: O_x / l -> bf16 (+ push to the token owner), lse
+    mbar_wait(&o_full[x], 0);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    __nv_bfloat16* orow = out + static_cast<int64_t>(q) * ld_o + h * D;
+    __nv_bfloat16* prow_out = nullptr;
+    if (push.p[0]) {
+      const int owner = q / push.T;
+      prow_out = static_cast<__nv_bfloat16*>(push.p[owner]) + static_cast<int64_t>(q - owner * push.T) * push.ld +
+                 push.col_o + h * D;
+    }
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t o[32];
+      tmem_ld_32x32b_x32(tOx + c * 32, o);
+      tmem_ld_wait();
+      uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint32_t pk2[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          pk2[e] = pack_bf16(__uint_as_float(o[v * 8 + 2 * e]) * inv, __uint_as_float(o[v * 8 + 2 * e + 1]) * inv);
+        const uint4 val = make_uint4(pk2[0], pk2[1], pk2[2], pk2[3]);
+        dst[v] = val;
+        if (prow_out) reinterpret_cast<uint4*>(prow_out + c * 32)[v] = val;
+      }
+    }
+    lse[static_cast<int64_t>(h) * S + q] = (m + log2f(l)) * 0.6931471805599453f;
+    if (push.p[0]) __threadfence_system();  // pushed rows visible before the next barrier flag
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 9) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -416,15 +750,50 @@ cudaError_t launch_fwd(const AttnTensors& t, cudaStream_t st) {
     return cudaErrorInvalidValue;
   const float scale_log2 = (1.0f / sqrtf(static_cast<float>(D))) * kLog2e;
   attn_fwd_tc_kernel<D><<<dim3(t.S / kBM, t.heads), kThreads, L::kBytes, st>>>(mq, mk, mv, t.o, t.ld_o, t.lse, t.S,
-                                                                               scale_log2, t.push, g_attn_trace_fwd);
+                                                                               scale_log2, t.push, g_attn_trace_fwd,
+      std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0);
   return cudaGetLastError();
+}
+
+cudaError_t launch_fwd_pair(const AttnTensors& t, cudaStream_t st) {
+  using L = Fa4Cfg;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_fa4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  CUtensorMap mq, mk, mv;
+  const int64_t cols = static_cast<int64_t>(t.heads) * 128;
+  if (!map2d(&mq, t.q, t.S, cols, t.ld_qkv, kBM) || !map2d(&mk, t.k, t.S, cols, t.ld_qkv, L::BN / 2) ||
+      !map2d(&mv, t.v, t.S, cols, t.ld_qkv, L::BN))
+    return cudaErrorInvalidValue;
+  const float scale_log2 = (1.0f / sqrtf(128.0f)) * kLog2e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(t.S / (2 * kBM), t.heads);  // 2 query tiles per CTA
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = L::kBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr_[1];
+  attr_[0].id = cudaLaunchAttributeClusterDimension;
+  attr_[0].val.clusterDim.x = 2;
+  attr_[0].val.clusterDim.y = 1;
+  attr_[0].val.clusterDim.z = 1;
+  cfg.attrs = attr_;
+  cfg.numAttrs = 1;
+  const int dbg = std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0;
+  return cudaLaunchKernelEx(&cfg, attn_fwd_fa4_kernel, mq, mk, mv, t.o, t.ld_o, t.lse, t.S, scale_log2, t.push,
+                            g_attn_trace_fwd, dbg);
 }
 
 }  // namespace
 
 cudaError_t attention_fwd_tc(const AttnTensors& t, cudaStream_t st) {
   if (t.S % kBM) return cudaErrorInvalidValue;
-  if (t.d == 128) return launch_fwd<128>(t, st);
+  if (t.d == 128) {
+    if ((t.S / kBM) % 4 == 0 && !std::getenv("SEQPLAN_ISP_ATTN_SINGLE")) return launch_fwd_pair(t, st);
+    return launch_fwd<128>(t, st);
+  }
   if (t.d == 64) return launch_fwd<64>(t, st);
   return cudaErrorInvalidValue;
 }

@@ -1,3 +1,4 @@
+#include <cstdio>
 // Kernel-level C-ABI entry points used by the unit/parity tests.
 //
 // These expose the individual sm_100a kernels (GEMM, norms, attention,
@@ -62,6 +63,7 @@ extern "C" int seqplan_isp_debug_attention(const void* q, const void* k, const v
                            static_cast<__nv_bfloat16*>(dk), static_cast<__nv_bfloat16*>(dv), ld_d, delta,
                            dq_acc, st, sms);
   }
+  if (e != cudaSuccess) fprintf(stderr, "seqplan_isp_debug_attention: %s\n", cudaGetErrorString(e));
   return e == cudaSuccess ? SEQPLAN_ISP_OK : SEQPLAN_ISP_ERR_RUNTIME;
 }
 
