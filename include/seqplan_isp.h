@@ -198,6 +198,8 @@ int seqplan_isp_kernel_profile(seqplan_isp_ctx* ctx, seqplan_kernel_record* out,
 int64_t seqplan_isp_launch_count(const seqplan_isp_ctx* ctx);
 
 /* ---- kernel-level entry points (tests) ------------------------------------ */
+// Development: push all-gather rounds on the comm stream (multi-process); ms per round.
+int seqplan_isp_debug_gather_bench(seqplan_isp_ctx* ctx, int iters, int both_sets, float* ms);
 int seqplan_isp_debug_gemm(const void* a, int64_t lda, int a_mn, const void* b, int64_t ldb,
                            int b_mn, void* out, int64_t ldo, int M, int N, int K, int epi,
                            const void* resid, int64_t ldr, void* out2, int64_t ldo2, void* out_b,

@@ -240,6 +240,140 @@ __global__ void peer_barrier_kernel(PeerPtrs flags, int world, int rank, uint32_
   __threadfence_system();
 }
 
+// Push copy (all-gather of weight shards, reduce-scatter staging of gradient partials): for
+// every destination rank q (starting at rank+1 so that at any moment each GPU receives from one
+// peer) and every job, blocks of `blk` bytes are read from this rank's memory at
+// src + q*src_q + b*src_stride and stored into q's symmetric heap at dst_q + dst_off + b*dst_stride.
+// Posted NVLink writes run at link speed with few CTAs, which stay co-resident with the
+// persistent tcgen05 kernels (no shared memory, 32 registers).
+__global__ void __launch_bounds__(256) push_copy_kernel(PushJobs jobs, PeerPtrs dst, int world, int rank) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int k = 0; k < world; ++k) {
+    const int q = (rank + 1 + k) % world;
+    for (int jb = 0; jb < jobs.n; ++jb) {
+      const PushJob& J = jobs.j[jb];
+      const char* src = J.src + q * J.src_q;
+      char* dbase = static_cast<char*>(dst.p[q]) + J.dst_off;
+      const int64_t bv = J.blk / 16, total = bv * J.nblk;
+      int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+      if (J.nblk == 1) {
+        const uint4* s4 = reinterpret_cast<const uint4*>(src);
+        uint4* d4 = reinterpret_cast<uint4*>(dbase);
+        for (; i + 7 * stride < total; i += 8 * stride) {  // 128 B in flight per thread
+          uint4 v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = ld_v4(s4 + i + u * stride);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) d4[i + u * stride] = v[u];
+        }
+        for (; i < total; i += stride) d4[i] = ld_v4(s4 + i);
+      } else {
+        for (; i < total; i += stride) {
+          const int64_t b = i / bv, e = i - b * bv;
+          const uint4 v = ld_v4(src + b * J.src_stride + e * 16);
+          *reinterpret_cast<uint4*>(dbase + b * J.dst_stride + e * 16) = v;
+        }
+      }
+    }
+  }
+  __threadfence_system();  // remote stores performed before the stream's flag write
+}
+
+// Bulk-copy push (the production weight all-gather / reduce-scatter staging in multi-process
+// mode): one thread per CTA drives the TMA unit — cp.async.bulk global -> shared (mbarrier
+// completion), then cp.async.bulk shared -> peer global for every destination. Tens of such
+// CTAs keep ~1 MB in flight over NVLink with no per-byte SM instructions.
+// bcast (every job has src_q == 0): each chunk is read once and stored to all ranks.
+// 2 x 16 KB slots: the CTA fits beside a GEMM / attention-forward CTA (~198 KB) on one SM, so
+// the copy needs no SMs of its own and the persistent grids stay whole.
+constexpr int kBulkChunk = 16384, kBulkSlots = 2;
+constexpr int kBulkSmem = kBulkChunk * kBulkSlots + 64;
+
+__device__ __forceinline__ void bulk_g2s(uint32_t smem, const void* g, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem),
+               "l"(g), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* g, uint32_t smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(smem), "r"(bytes) : "memory");
+}
+
+struct ChunkRef {
+  const char* src;
+  char* dst_rel;  // offset within the destination heap (added to dst.p[q])
+  uint32_t bytes;
+};
+
+__global__ void __launch_bounds__(32) push_bulk_kernel(PushJobs jobs, PeerPtrs dst, int world, int rank, int bcast) {
+  extern __shared__ __align__(128) uint8_t sm_raw[];
+  if (threadIdx.x != 0) return;
+  uint8_t* buf = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 127) & ~uintptr_t(127));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(buf + kBulkChunk * kBulkSlots);
+  for (int i = 0; i < kBulkSlots; ++i) mbar_init(&bars[i], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  // item space: per job, nblk x ceil(blk / chunk) chunks; per destination unless bcast
+  int64_t cpb[2], njob_items[2], per_dest = 0;
+  for (int j = 0; j < jobs.n; ++j) {
+    cpb[j] = (jobs.j[j].blk + kBulkChunk - 1) / kBulkChunk;
+    njob_items[j] = cpb[j] * jobs.j[j].nblk;
+    per_dest += njob_items[j];
+  }
+  const int ndest = bcast ? 1 : world;
+  const int64_t total = per_dest * ndest;
+  auto item = [&](int64_t it, int& qsel) {
+    const int k = static_cast<int>(it / per_dest);
+    int64_t r = it - k * per_dest;
+    qsel = bcast ? -1 : (rank + 1 + k) % world;
+    int j = 0;
+    if (jobs.n > 1 && r >= njob_items[0]) {
+      r -= njob_items[0];
+      j = 1;
+    }
+    const PushJob& J = jobs.j[j];
+    const int64_t b = r / cpb[j], c = r - b * cpb[j];
+    const int64_t off = c * kBulkChunk;
+    ChunkRef ref;
+    ref.src = J.src + (qsel < 0 ? 0 : qsel * J.src_q) + b * J.src_stride + off;
+    ref.dst_rel = reinterpret_cast<char*>(J.dst_off + b * J.dst_stride + off);
+    ref.bytes = static_cast<uint32_t>(J.blk - off < kBulkChunk ? J.blk - off : kBulkChunk);
+    return ref;
+  };
+  // this CTA's items: it = blockIdx.x + n * gridDim.x
+  const int64_t mine = total > blockIdx.x ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const uint32_t sbase = smem_u32(buf), bbase = smem_u32(bars);
+  auto issue_load = [&](int64_t n) {
+    int qs;
+    const ChunkRef r = item(blockIdx.x + n * gridDim.x, qs);
+    const int slot = static_cast<int>(n % kBulkSlots);
+    mbar_arrive_expect_tx(&bars[slot], r.bytes);
+    bulk_g2s(sbase + slot * kBulkChunk, r.src, r.bytes, bbase + slot * 8);
+  };
+  for (int64_t n = 0; n < mine && n < kBulkSlots - 1; ++n) issue_load(n);
+  for (int64_t n = 0; n < mine; ++n) {
+    const int slot = static_cast<int>(n % kBulkSlots);
+    mbar_wait(&bars[slot], static_cast<uint32_t>((n / kBulkSlots) & 1));
+    int qs;
+    const ChunkRef r = item(blockIdx.x + n * gridDim.x, qs);
+    if (qs < 0) {
+      for (int k = 0; k < world; ++k) {
+        const int q = (rank + 1 + k) % world;
+        bulk_s2g(static_cast<char*>(dst.p[q]) + reinterpret_cast<uintptr_t>(r.dst_rel), sbase + slot * kBulkChunk, r.bytes);
+      }
+    } else {
+      bulk_s2g(static_cast<char*>(dst.p[qs]) + reinterpret_cast<uintptr_t>(r.dst_rel), sbase + slot * kBulkChunk, r.bytes);
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    // refill: the slot of item n+kBulkSlots-1 was last used by item n-1, whose stores must have
+    // finished reading it (at most the current group still reading)
+    if (n + kBulkSlots - 1 < mine) {
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      issue_load(n + kBulkSlots - 1);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
+  __threadfence_system();
+}
+
 int ctas(int64_t work, int threads, int cap) {
   const int64_t b = (work + threads - 1) / threads;
   return static_cast<int>(b < cap ? (b > 0 ? b : 1) : cap);
@@ -308,6 +442,29 @@ cudaError_t a2a_heads_to_tokens(const PeerPtrs& src, int world, int rank, int T,
   const int64_t work = static_cast<int64_t>(T) * parts * (H / d) * (d / 16);
   a2a_to_tokens_kernel<<<ctas(work, 256, num_ctas), 256, 0, st>>>(src, world, rank, T, H, parts, d,
                                                                    dst, cos_t, sin_t, rope_parts);
+  return cudaGetLastError();
+}
+
+cudaError_t push_copy(const PushJobs& jobs, const PeerPtrs& dst, int world, int rank, cudaStream_t st, int num_ctas) {
+  for (int j = 0; j < jobs.n; ++j) {
+    const PushJob& J = jobs.j[j];
+    if (J.blk % 16 || J.src_stride % 16 || J.dst_stride % 16 || J.dst_off % 16 || J.src_q % 16 ||
+        reinterpret_cast<uintptr_t>(J.src) % 16)
+      return cudaErrorInvalidValue;
+  }
+  if (num_ctas < 0) {  // bulk-copy (TMA) kernel on -num_ctas dedicated CTAs
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(push_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem + 128);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    int bcast = 1;
+    for (int j = 0; j < jobs.n; ++j) bcast &= jobs.j[j].src_q == 0;
+    push_bulk_kernel<<<-num_ctas, 32, kBulkSmem + 128, st>>>(jobs, dst, world, rank, bcast);
+    return cudaGetLastError();
+  }
+  push_copy_kernel<<<num_ctas, 256, 0, st>>>(jobs, dst, world, rank);
   return cudaGetLastError();
 }
 

@@ -549,7 +549,8 @@ cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArg
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int tiles = (args.M / BM) * (args.N / BN);
-  const int grid = tiles < g_num_sms ? tiles : g_num_sms;
+  const int sms = args.sm_budget > 0 && args.sm_budget < g_num_sms ? args.sm_budget : g_num_sms;
+  const int grid = tiles < sms ? tiles : sms;
   kern<<<grid, kNumThreads, Cfg::kSmemBytes, stream>>>(ma, mb, args);
   return cudaGetLastError();
 }
@@ -570,7 +571,8 @@ cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const Gemm
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int tiles = (args.M / 256) * (args.N / 256);
-  const int clusters = tiles < g_num_sms / 2 ? tiles : g_num_sms / 2;
+  const int sms = args.sm_budget > 0 && args.sm_budget < g_num_sms ? args.sm_budget : g_num_sms;
+  const int clusters = tiles < sms / 2 ? tiles : sms / 2;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * clusters);
   cfg.blockDim = dim3(kNumThreads);

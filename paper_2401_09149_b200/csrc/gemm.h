@@ -49,6 +49,9 @@ struct GemmArgs {
   const float* rope_cos = nullptr;
   const float* rope_sin = nullptr;
   int rope_parts = 0;
+  // persistent-grid size limit (0 = every SM): SMs held by concurrent bulk-copy comm kernels
+  // are left out so no CTA of the persistent grid waits for them
+  int sm_budget = 0;
 };
 
 int gemm_pick_bn(int N);

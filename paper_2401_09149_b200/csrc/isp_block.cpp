@@ -127,6 +127,15 @@ struct seqplan_isp_ctx {
   bool fused_a2a = false;
   size_t off_qkv_heads = 0, off_o_tok = 0, off_dO_heads = 0, off_dqkv_tok = 0;
   uint32_t epoch_compute = 0, epoch_comm = 0;
+  // push-mode weight traffic (multi-process): every rank stores its shards into the peers'
+  // pinned comm double buffer (set 0 = forward gather, set 1 = backward re-gather; the
+  // reference's pinned comm pool, cost.hpp:147 / mempool.hpp pinned policy) and its gradient
+  // partial slices into the owners' staging slots; per-(tensor, source) epoch flags order them
+  size_t off_gath[2][SEQPLAN_W_COUNT] = {}, off_stage[SEQPLAN_W_COUNT] = {};
+  uint32_t step_epoch = 0;
+  int gather_set = 0;
+  bool push_primed = false;  // SKIP_COMM: buffers filled by one real step, then reused
+  int comm_ctas = -96;  // < 0: bulk-copy (TMA) push kernel with -comm_ctas CTAs
   uint32_t* error_flag = nullptr;  // device, in the heap flags page
 
   // ---- device pool (subsystem 5) and persistent buffers ----
@@ -166,6 +175,8 @@ struct seqplan_isp_ctx {
   // SEQPLAN_ISP_FLAG_SKIP_COMM: weights gathered once and kept (measurement of exposed comm)
   bf16* pregathered[SEQPLAN_W_COUNT] = {};
   bool skip_comm() const { return (flags & SEQPLAN_ISP_FLAG_SKIP_COMM) && world > 1; }
+  bool push_mode() const { return world > 1 && !group_mode; }
+  bool push_skip() const { return skip_comm() && push_primed; }
 
   // timeline
   struct TEv {
@@ -369,6 +380,10 @@ void gather_weight(Ctx* c, int t, cudaStream_t st) {
 }
 
 void release_weight(Ctx* c, int t, cudaStream_t st) {
+  if (c->push_mode()) {  // pinned set buffers: nothing to free
+    c->gathered[t] = nullptr;
+    return;
+  }
   if (c->skip_comm()) {
     c->pregathered[t] = c->gathered[t];
     c->gathered[t] = nullptr;
@@ -476,6 +491,132 @@ void gather_pipelined(Ctx* c, const int* order, int n, cudaStream_t cs) {
   c->pipelined_gather = true;
 }
 
+// ---- push-mode collectives (multi-process) -------------------------------------------
+// Flag slots in the heap flags page (uint32 index): AG [512 + (set*8 + t)*8 + src],
+// RS [640 + t*8 + src]; a slot holds the step epoch of the last completed transfer.
+size_t ag_flag(const Ctx* c, int set, int t, int src) {
+  return c->off_flags + sizeof(uint32_t) * (512 + (set * 8 + t) * 8 + src);
+}
+size_t rs_flag(const Ctx* c, int t, int src) { return c->off_flags + sizeof(uint32_t) * (640 + t * 8 + src); }
+
+// After the push kernel on stream cs: publish this rank's epoch into every peer's slot
+// (cuStreamWriteValue32 is preceded by a system-wide fence).
+void signal_peers(Ctx* c, cudaStream_t cs, size_t slot_off) {
+  const MemOps& mo = memops();
+  for (int q = 0; q < c->world; ++q) {
+    if (q == c->rank) continue;
+    auto dst = reinterpret_cast<CUdeviceptr>(c->peer<uint32_t>(q, slot_off));
+    if (!mo.ok() || mo.write(reinterpret_cast<CUstream>(cs), dst, c->step_epoch, 0) != CUDA_SUCCESS)
+      throw IspError(SEQPLAN_ISP_ERR_RUNTIME, "cuStreamWriteValue32 to a peer failed");
+  }
+}
+// Stream st waits until every peer q published the current epoch into slot_of(q).
+template <typename F>
+void wait_peers(Ctx* c, cudaStream_t st, F&& slot_of) {
+  const MemOps& mo = memops();
+  for (int q = 0; q < c->world; ++q) {
+    if (q == c->rank) continue;
+    auto mine = reinterpret_cast<CUdeviceptr>(c->hp<uint32_t>(slot_of(q)));
+    if (!mo.ok() || mo.wait(reinterpret_cast<CUstream>(st), mine, c->step_epoch, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+      throw IspError(SEQPLAN_ISP_ERR_RUNTIME, "cuStreamWaitValue32 failed");
+  }
+}
+
+// All-gather of tensor t (gate|up together) by pushing this rank's shard into slot `rank` of
+// every rank's set buffer (own slot: local copy).
+void push_gather(Ctx* c, int set, int t, cudaStream_t cs) {
+  PushJobs J{};
+  const int64_t r = c->rank;
+  int64_t bytes = 0;
+  if (t == SEQPLAN_W_GATE) {
+    const int64_t B = kGuBlock, H = c->H, rpr = c->I / c->world;
+    for (int which = 0; which < 2; ++which) {
+      PushJob& j = J.j[which];
+      j.src = reinterpret_cast<const char*>(c->wshard(which ? SEQPLAN_W_UP : SEQPLAN_W_GATE));
+      j.src_q = 0;
+      j.dst_off = int64_t(c->off_gath[set][t]) + ((r * rpr / B) * 2 * B + which * B) * H * 2;
+      j.blk = B * H * 2;
+      j.src_stride = B * H * 2;
+      j.dst_stride = 2 * B * H * 2;
+      j.nblk = rpr / B;
+    }
+    J.n = 2;
+    bytes = 2 * rpr * H * 2;
+  } else {
+    const int64_t sh = c->shard(t);
+    J.j[0] = PushJob{reinterpret_cast<const char*>(c->wshard(t)), 0, int64_t(c->off_gath[set][t]) + r * sh * 2, sh * 2,
+                     0, 0, 1};
+    J.n = 1;
+    bytes = sh * 2;
+  }
+  KTimer kt(c, cs, SEQPLAN_K_ALL_GATHER, 0, double(c->world - 1) * double(bytes));
+  ISP_LAUNCH(1, push_copy(J, c->peers_at(0), c->world, c->rank, cs, c->comm_ctas));
+  signal_peers(c, cs, ag_flag(c, set, t, c->rank));
+}
+
+// The set's buffers become this pass's gathered weights; with push == true the pushes of the
+// given tensors are issued on the comm stream (in order).
+void push_gather_set(Ctx* c, int set, const int* order, int n, bool push) {
+  for (int i = 0; i < n; ++i) c->gathered[order[i]] = c->hp<bf16>(c->off_gath[set][order[i]]);
+  if (!push) return;
+  Span sp(c, c->comm, 1, SEQPLAN_EV_ALL_GATHER, set);
+  for (int i = 0; i < n; ++i) push_gather(c, set, order[i], c->comm);
+}
+
+// Reduce-scatter staging of tensor t's partial: slice q of this rank's partial -> slot `rank`
+// of owner q's staging buffer, then the owner's flag. (Own slice: local copy.)
+void push_rs(Ctx* c, int t, cudaStream_t cs) {
+  PushJobs J{};
+  const int64_t r = c->rank, H = c->H, p = c->world;
+  const char* part = c->hp<char>(c->off_part[t]);
+  int64_t bytes = 0;
+  if (t == SEQPLAN_W_GATE) {
+    const int64_t B = kGuBlock, rpr = c->I / p, slot = 2 * rpr * H * 2;  // [gate rpr x H | up rpr x H]
+    for (int which = 0; which < 2; ++which) {
+      PushJob& j = J.j[which];
+      j.src = part + which * B * H * 2;
+      j.src_q = (rpr / B) * 2 * B * H * 2;
+      j.dst_off = int64_t(c->off_stage[t]) + r * slot + which * rpr * H * 2;
+      j.blk = B * H * 2;
+      j.src_stride = 2 * B * H * 2;
+      j.dst_stride = B * H * 2;
+      j.nblk = rpr / B;
+    }
+    J.n = 2;
+    bytes = slot;
+  } else {
+    const bool norm = (t == SEQPLAN_W_NORM1 || t == SEQPLAN_W_NORM2);
+    const int64_t esz = norm ? 4 : 2, sh = c->shard(t);
+    J.j[0] = PushJob{part, sh * esz, int64_t(c->off_stage[t]) + r * sh * esz, sh * esz, 0, 0, 1};
+    J.n = 1;
+    bytes = sh * esz;
+  }
+  Span sp(c, cs, 1, SEQPLAN_EV_REDUCE_SCATTER, t);
+  KTimer kt(c, cs, SEQPLAN_K_REDUCE_SCATTER, 0, double(p - 1) * double(bytes));
+  ISP_LAUNCH(1, push_copy(J, c->peers_at(0), c->world, c->rank, cs, c->comm_ctas));
+  signal_peers(c, cs, rs_flag(c, t, c->rank));
+}
+
+// Owner side: wait for every peer's slice, then the fp32 reduction + cast/scale (fixed rank order).
+void reduce_pushed(Ctx* c, int t, cudaStream_t st) {
+  wait_peers(c, st, [&](int q) { return rs_flag(c, t, q); });
+  PeerPtrs src{};
+  const bool norm = (t == SEQPLAN_W_NORM1 || t == SEQPLAN_W_NORM2);
+  if (t == SEQPLAN_W_GATE) {
+    const int64_t half = (c->I / c->world) * c->H, slot = 2 * half;
+    bf16* stg = c->hp<bf16>(c->off_stage[t]);
+    for (int q = 0; q < c->world; ++q) src.p[q] = stg + q * slot;
+    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, half, false, 1.0f, 0, c->grad[SEQPLAN_W_GATE], st, c->num_sms * 4));
+    for (int q = 0; q < c->world; ++q) src.p[q] = stg + q * slot + half;
+    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, half, false, 1.0f, 0, c->grad[SEQPLAN_W_UP], st, c->num_sms * 4));
+  } else {
+    const int64_t sh = c->shard(t), esz = norm ? 4 : 2;
+    char* stg = c->hp<char>(c->off_stage[t]);
+    for (int q = 0; q < c->world; ++q) src.p[q] = stg + q * sh * esz;
+    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, sh, norm, 1.0f, 0, c->grad[t], st, c->num_sms * 4));
+  }
+}
+
 void fwd_issue_gathers(Ctx* c, cudaStream_t st) {
   if (c->world == 1) {
     for (int t : {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN})
@@ -486,6 +627,18 @@ void fwd_issue_gathers(Ctx* c, cudaStream_t st) {
   if (!c->group_mode) {  // comm stream starts after the caller's prior work
     ISP_CUDA(cudaEventRecord(c->ev_start, st));
     ISP_CUDA(cudaStreamWaitEvent(cs, c->ev_start, 0));
+  }
+  if (c->push_mode()) {
+    // forward set, then the backward re-gather into the second set (its buffers are free since
+    // the step-start barrier), so the backward never waits for weights
+    const int fo[] = {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN};
+    const int bo[] = {SEQPLAN_W_DOWN, SEQPLAN_W_GATE, SEQPLAN_W_NORM2, SEQPLAN_W_O, SEQPLAN_W_QKV, SEQPLAN_W_NORM1};
+    c->gather_set = 0;
+    push_gather_set(c, 1, bo, 6, false);
+    push_gather_set(c, 0, fo, 6, !c->push_skip());
+    if (!c->push_skip()) push_gather_set(c, 1, bo, 6, true);
+    for (int t : fo) c->gathered[t] = c->hp<bf16>(c->off_gath[0][t]);
+    return;
   }
   if (!c->group_mode) {
     const int order[] = {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN};
@@ -498,6 +651,10 @@ void fwd_issue_gathers(Ctx* c, cudaStream_t st) {
 
 void wait_gathered(Ctx* c, int t, cudaStream_t st) {
   if (c->world == 1 || c->group_mode) return;
+  if (c->push_mode()) {
+    if (!c->push_skip()) wait_peers(c, st, [&](int q) { return ag_flag(c, c->gather_set, t, q); });
+    return;
+  }
   if (c->skip_comm() && c->gathered[t] == c->pregathered[t] && c->pregathered[t]) return;
   for (int q = 0; q < c->world; ++q) ISP_CUDA(cudaStreamWaitEvent(st, c->ev_tq[t][q], 0));
 }
@@ -610,6 +767,11 @@ void bwd_issue_gathers(Ctx* c, cudaStream_t st) {
     for (int t : order) gather_weight(c, t, st);
     return;
   }
+  if (c->push_mode()) {  // pushed at the start of the step (fwd_issue_gathers)
+    c->gather_set = 1;
+    for (int t : order) c->gathered[t] = c->hp<bf16>(c->off_gath[1][t]);
+    return;
+  }
   cudaStream_t cs = c->group_mode ? st : c->comm;
   if (!c->group_mode) {
     ISP_CUDA(cudaEventRecord(c->ev_start, st));
@@ -700,6 +862,10 @@ void schedule_rs(Ctx* c, int t, cudaStream_t st) {
   if (c->world == 1 || c->group_mode || c->skip_comm()) return;
   ISP_CUDA(cudaEventRecord(c->ev_wgrad[t], st));
   ISP_CUDA(cudaStreamWaitEvent(c->comm, c->ev_wgrad[t], 0));
+  if (c->push_mode()) {
+    push_rs(c, t, c->comm);
+    return;
+  }
   barrier(c, c->comm, true);
   stage_rs(c, t, c->comm);
 }
@@ -870,6 +1036,13 @@ void layout_heap(Ctx* c) {
     c->off_part[SEQPLAN_W_GATE] = take(size_t(2 * c->I * c->H) * 2);
     c->off_part[SEQPLAN_W_NORM1] = take(size_t(c->H) * 4);
     c->off_part[SEQPLAN_W_NORM2] = take(size_t(c->H) * 4);
+    for (int set = 0; set < 2; ++set)
+      for (int t : {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN})
+        c->off_gath[set][t] = take(size_t(t == SEQPLAN_W_GATE ? 2 * c->I * c->H : c->numel(t)) * 2);
+    for (int t : {SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_DOWN}) c->off_stage[t] = take(size_t(c->numel(t)) * 2);
+    c->off_stage[SEQPLAN_W_GATE] = take(size_t(2 * c->I * c->H) * 2);
+    c->off_stage[SEQPLAN_W_NORM1] = take(size_t(c->H) * 4);
+    c->off_stage[SEQPLAN_W_NORM2] = take(size_t(c->H) * 4);
   }
   c->heap_bytes = off;
 }
@@ -908,6 +1081,7 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   c->pool.set_policy(pol);
 
   c->fused_a2a = c->world > 1 && c->d == 128 && !std::getenv("SEQPLAN_ISP_PULL_A2A");
+  if (const char* e = std::getenv("SEQPLAN_ISP_COMM_CTAS")) c->comm_ctas = std::atoi(e) ? std::atoi(e) : -96;
   layout_heap(c);
   ISP_CUDA(cudaMalloc(&c->heap, c->heap_bytes));
   ISP_CUDA(cudaMemset(c->heap, 0, kFlagBytes));
@@ -1237,7 +1411,8 @@ int seqplan_isp_fill_activation(seqplan_isp_ctx* c, uint64_t seed, int tensor_id
 }
 
 static void run_fwd(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
-  if (c->weights_dirty || c->fused_a2a) {
+  ++c->step_epoch;
+  if (c->weights_dirty || c->fused_a2a || c->push_mode()) {
     // peers must see refreshed working shards before gathering; with fused all-to-all, no
     // peer may push into this rank's exchange buffers before its previous backward finished
     barrier(c, st, false);
@@ -1265,12 +1440,18 @@ static void run_bwd(Ctx* c, const bf16* x, const bf16* dy, bf16* dx, cudaStream_
     bwd_reduce_all(c, st);
   } else if (c->world > 1) {
     // reduce the staged slices (fp32 accumulate, cast/scale) and join the comm stream
-    for (int t : {SEQPLAN_W_DOWN, SEQPLAN_W_GATE, SEQPLAN_W_NORM2, SEQPLAN_W_O, SEQPLAN_W_QKV, SEQPLAN_W_NORM1})
-      reduce_staged(c, t, st);
+    for (int t : {SEQPLAN_W_DOWN, SEQPLAN_W_GATE, SEQPLAN_W_NORM2, SEQPLAN_W_O, SEQPLAN_W_QKV, SEQPLAN_W_NORM1}) {
+      if (c->push_mode()) {
+        if (!c->skip_comm()) reduce_pushed(c, t, st);
+      } else {
+        reduce_staged(c, t, st);
+      }
+    }
     ISP_CUDA(cudaEventRecord(c->ev_comm_done, c->comm));
     ISP_CUDA(cudaStreamWaitEvent(st, c->ev_comm_done, 0));
   }
   c->pool.step_boundary();
+  if (c->push_mode()) c->push_primed = true;
 }
 
 int seqplan_isp_block_fwd(seqplan_isp_ctx* c, const void* x, void* y, void* stream) {
@@ -1374,6 +1555,38 @@ int seqplan_isp_kernel_profile(seqplan_isp_ctx* c, seqplan_kernel_record* out, i
 }
 
 int64_t seqplan_isp_launch_count(const seqplan_isp_ctx* c) { return c ? c->launches : -1; }
+
+// Development: `iters` rounds of (comm-lane barrier, push all-gather of the forward set [and the
+// backward set], wait for every peer's flags) on the comm stream; *ms = time per round.
+int seqplan_isp_debug_gather_bench(seqplan_isp_ctx* c, int iters, int both_sets, float* ms) {
+  if (!c || !ms || !c->push_mode()) return SEQPLAN_ISP_ERR_INVALID;
+  try {
+    ISP_CUDA(cudaSetDevice(c->device));
+    ISP_CUDA(cudaDeviceSynchronize());
+    const int fo[] = {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN};
+    cudaEvent_t e0, e1;
+    ISP_CUDA(cudaEventCreate(&e0));
+    ISP_CUDA(cudaEventCreate(&e1));
+    for (int it = -1; it < iters; ++it) {
+      if (it == 0) ISP_CUDA(cudaEventRecord(e0, c->comm));
+      ++c->step_epoch;
+      barrier(c, c->comm, true);
+      for (int set = 0; set < (both_sets ? 2 : 1); ++set) {
+        push_gather_set(c, set, fo, 6, true);
+        for (int t : fo) wait_peers(c, c->comm, [&](int q) { return ag_flag(c, set, t, q); });
+      }
+    }
+    ISP_CUDA(cudaEventRecord(e1, c->comm));
+    ISP_CUDA(cudaEventSynchronize(e1));
+    ISP_CUDA(cudaEventElapsedTime(ms, e0, e1));
+    *ms /= iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  } catch (const IspError& e) {
+    return fail(c, e);
+  }
+  return SEQPLAN_ISP_OK;
+}
 
 int seqplan_isp_pool_stats(seqplan_isp_ctx* c, seqplan_step_stats* out) {
   if (!c || !out) return SEQPLAN_ISP_ERR_INVALID;

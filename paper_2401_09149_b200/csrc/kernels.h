@@ -100,6 +100,19 @@ cudaError_t a2a_tokens_to_heads(const PeerPtrs& src, int world, int rank, int T,
 cudaError_t a2a_heads_to_tokens(const PeerPtrs& src, int world, int rank, int T, int H, int parts,
                                 __nv_bfloat16* dst, const float* cos_t, const float* sin_t, int d,
                                 int rope_parts, cudaStream_t st, int num_ctas);
+// Push copy over peer memory: for every rank q (this rank included, as a local copy) and job,
+// nblk blocks of blk bytes: dst_q[dst_off + b*dst_stride] <- src[q*src_q + b*src_stride].
+// All-gather: src_q = 0 (the same shard to everyone), dst_off = this rank's slot.
+// Reduce-scatter staging: src_q = owner q's slice stride, dst_off = this rank's slot.
+struct PushJob {
+  const char* src;
+  int64_t src_q, dst_off, blk, src_stride, dst_stride, nblk;
+};
+struct PushJobs {
+  PushJob j[2];
+  int n;
+};
+cudaError_t push_copy(const PushJobs& jobs, const PeerPtrs& dst, int world, int rank, cudaStream_t st, int num_ctas);
 // Cross-GPU barrier over system-scope flags in every rank's heap. epoch increases by one per
 // call; a rank spins (bounded, ~20 s) until all peers have published `epoch`.
 cudaError_t peer_barrier(const PeerPtrs& flags, int world, int rank, uint32_t epoch,
