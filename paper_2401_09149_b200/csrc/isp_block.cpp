@@ -175,7 +175,10 @@ struct seqplan_isp_ctx {
   // SEQPLAN_ISP_FLAG_SKIP_COMM: weights gathered once and kept (measurement of exposed comm)
   bf16* pregathered[SEQPLAN_W_COUNT] = {};
   bool skip_comm() const { return (flags & SEQPLAN_ISP_FLAG_SKIP_COMM) && world > 1; }
-  bool push_mode() const { return world > 1 && !group_mode; }
+  // push (bulk-copy) weight traffic for p >= 4; at p = 2 the copy engines' pull is faster
+  // (measured: 7B-4K/32K at p = 2, CE 2-7 % ahead; at p = 4 push +25 %). SEQPLAN_ISP_PUSH=0/1 forces.
+  int push_pref = -1;
+  bool push_mode() const { return world > 1 && !group_mode && (push_pref >= 0 ? push_pref == 1 : world >= 4); }
   bool push_skip() const { return skip_comm() && push_primed; }
 
   // timeline
@@ -1081,6 +1084,7 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   c->pool.set_policy(pol);
 
   c->fused_a2a = c->world > 1 && c->d == 128 && !std::getenv("SEQPLAN_ISP_PULL_A2A");
+  if (const char* e = std::getenv("SEQPLAN_ISP_PUSH")) c->push_pref = std::atoi(e) ? 1 : 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_COMM_CTAS")) c->comm_ctas = std::atoi(e) ? std::atoi(e) : -96;
   layout_heap(c);
   ISP_CUDA(cudaMalloc(&c->heap, c->heap_bytes));

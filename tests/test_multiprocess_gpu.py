@@ -14,11 +14,12 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _run(n, H, D, S, mode="selective"):
+def _run(n, H, D, S, mode="selective", env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", f"--master-port={29500 + n + (7 if mode == 'fused' else 0) + (20 if H == 1024 else 0)}",
+           "--master-addr=127.0.0.1", f"--master-port={29500 + n + (7 if mode == 'fused' else 0) + (20 if H == 1024 else 0) + (40 + 3 * int(env.get('SEQPLAN_ISP_PUSH', '0')) if env else 0)}",
            os.path.join(ROOT, "tests", "mp_parity_worker.py"), str(H), str(D), str(S), mode]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                       env={**os.environ, **(env or {})})
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     rows = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(rows) == n
@@ -36,3 +37,15 @@ def test_multiprocess_parity(n, mode, H):
             if k not in ("rank", "timeline_events"):
                 assert v <= 1e-2, (row["rank"], k, v)
         assert row["timeline_events"] > 0
+
+
+@pytest.mark.parametrize("push", ["0", "1"])
+def test_multiprocess_parity_forced_transport(push):
+    """Both weight-traffic transports at p = 2: copy-engine pull (default at p = 2) and the
+    bulk-copy push into the pinned double buffer (default at p >= 4)."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    for row in _run(2, 1024, 8, 1024, "selective", env={"SEQPLAN_ISP_PUSH": push}):
+        for k, v in row.items():
+            if k not in ("rank", "timeline_events"):
+                assert v <= 1e-2, (row["rank"], k, v)
