@@ -829,9 +829,9 @@ struct BwdSmem {
   static constexpr int kOffK = 0;
   static constexpr int kOffV = kOffK + kKV;
   static constexpr int kOffQ = kOffV + kKV;           // stage s: Q at kOffQ + s*kStage, dO at +kQ
-  static constexpr int kOffP = kOffQ + kStages * kStage;
-  static constexpr int kOffDS = kOffP + kP;
-  static constexpr int kOffBar = kOffDS + kP;
+  static constexpr int kOffDS = kOffQ + kStages * kStage;  // dS^T (bf16, SW128): B operand of dQ^T
+  static constexpr int kOffLD = kOffDS + kP;          // stage s: lse[64] | delta[64] (fp32), bulk-loaded
+  static constexpr int kOffBar = kOffLD + kStages * 512;
   static constexpr int kBytes = kOffBar + 256 + 1024;
   static_assert(kBytes <= 232448, "exceeds the 227 KB per-CTA shared memory");
 };
@@ -900,7 +900,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // TMEM: S^T 0 | dP^T 64 | dK 128 | dV 256 | dQ^T 384 (64) | P^T bf16 448 (32) | dS^T bf16 480 (32)
   const uint32_t tS = tmem, tP = tmem + 64, tDK = tmem + 128, tDV = tmem + 256, tDQ = tmem + 384;
+  const uint32_t tPT = tmem + 448, tDST = tmem + 480;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -913,11 +915,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int i = 0; i < nq; ++i) {
         const int s = i % NS, q0 = (qi0 + i) * kBwdQ;
         if (i >= NS) mbar_wait(&q_empty[s], ((i / NS) - 1) & 1);
-        mbar_arrive_expect_tx(&q_full[s], 2 * L::kQ);
+        mbar_arrive_expect_tx(&q_full[s], 2 * L::kQ + 512);
         for (int c = 0; c < 2; ++c) {
           tma_load_2d(smem + L::kOffQ + s * L::kStage + c * kBwdQ * 128, &mQ, &q_full[s], h * D + c * 64, q0);
           tma_load_2d(smem + L::kOffQ + s * L::kStage + L::kQ + c * kBwdQ * 128, &mDO, &q_full[s], h * D + c * 64, q0);
         }
+        bulk_load(smem + L::kOffLD + s * 512, lse + static_cast<int64_t>(h) * S + q0, 256, &q_full[s]);
+        bulk_load(smem + L::kOffLD + s * 512 + 256, delta + static_cast<int64_t>(h) * S + q0, 256, &q_full[s]);
       }
     }
   } else if (warp == 1) {
@@ -927,7 +931,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       constexpr uint32_t id_g = make_idesc_bf16(kBwdKeys, D, false, true);       // dV, dK
       constexpr uint32_t id_q = make_idesc_bf16(D, kBwdQ, true, true);           // dQ^T
       const uint32_t sK = smem_u32(smem + L::kOffK), sV = smem_u32(smem + L::kOffV);
-      const uint32_t sP = smem_u32(smem + L::kOffP), sDS = smem_u32(smem + L::kOffDS);
+      const uint32_t sDS = smem_u32(smem + L::kOffDS);
       mbar_wait(kv_full, 0);
       auto grads = [&](int j) {
         const int s = j % NS;
@@ -936,11 +940,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_fence_after();
         const uint32_t sQ = smem_u32(smem + L::kOffQ + s * L::kStage), sDO = sQ + L::kQ;
 #pragma unroll
-        for (int k = 0; k < kBwdQ / 16; ++k) {
-          tc_mma_bf16(tDV, make_sw128_desc(sP + k * 32, 16, 1024), make_sw128_desc(sDO + k * 2048, kBwdQ * 128, 1024),
-                      id_g, (j > 0 || k > 0) ? 1u : 0u);
-          tc_mma_bf16(tDK, make_sw128_desc(sDS + k * 32, 16, 1024), make_sw128_desc(sQ + k * 2048, kBwdQ * 128, 1024),
-                      id_g, (j > 0 || k > 0) ? 1u : 0u);
+        for (int k = 0; k < kBwdQ / 16; ++k) {  // A = P^T / dS^T from TMEM (16 queries = 8 columns)
+          tc_mma_bf16_ts(tDV, tPT + k * 8, make_sw128_desc(sDO + k * 2048, kBwdQ * 128, 1024), id_g,
+                         (j > 0 || k > 0) ? 1u : 0u);
+          tc_mma_bf16_ts(tDK, tDST + k * 8, make_sw128_desc(sQ + k * 2048, kBwdQ * 128, 1024), id_g,
+                         (j > 0 || k > 0) ? 1u : 0u);
         }
 #pragma unroll
         for (int k = 0; k < kBwdKeys / 16; ++k)
@@ -981,6 +985,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait(dq_full, j & 1);
       tc_fence_after();
       uint32_t v0[32], v1[32];
+      if (dbg == 12) {  // development: pipeline bound without the dQ reductions
+        tc_fence_before();
+        mbar_arrive(dq_free);
+        continue;
+      }
       tmem_ld_32x32b_x32(tDQ + lo, v0);
       tmem_ld_32x32b_x32(tDQ + lo + 32, v1);
       tmem_ld_wait();
@@ -1004,15 +1013,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int r = quad * 32 + lane;  // key row
     const uint32_t lo = static_cast<uint32_t>(quad * 32) << 16;
     const int key = k0 + r;
-    const float* lse_h = lse + static_cast<int64_t>(h) * S + half * 32;
-    const float* del_h = delta + static_cast<int64_t>(h) * S + half * 32;
     for (int i = 0; i < nq; ++i) {
       const int q0 = (qi0 + i) * kBwdQ;
       const bool tr = trace && blockIdx.x == 0 && blockIdx.y == 0 && i < 64 && warp == 2 && lane == 0;
       if (tr) trace[i * 8 + 2] = clock64();
       mbar_wait(s_full, i & 1);
+      mbar_wait(&q_full[i % NS], (i / NS) & 1);  // lse / delta of this tile are in shared memory
       if (tr) trace[i * 8 + 3] = clock64();
       tc_fence_after();
+      if (dbg >= 11) {  // development: pipeline bound without the P / dS math
+        tc_fence_before();
+        mbar_arrive(s_free);
+        if (i >= 1) mbar_wait(p_free, (i - 1) & 1);
+        tc_fence_before();
+        mbar_arrive(p_full);
+        continue;
+      }
       const bool diag = q0 < k0 + kBwdKeys;
       uint32_t pk[16], dk[16];
 #pragma unroll
@@ -1031,10 +1047,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               "=r"(pv[14]), "=r"(pv[15])
             : "r"(tP + lo + half * 32 + hc * 16));
         float4 l4[4], d4[4];
+        const float* lsm = reinterpret_cast<const float*>(smem + L::kOffLD + (i % NS) * 512) + half * 32 + hc * 16;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          l4[k] = __ldg(reinterpret_cast<const float4*>(lse_h + q0 + hc * 16) + k);
-          d4[k] = __ldg(reinterpret_cast<const float4*>(del_h + q0 + hc * 16) + k);
+        for (int k = 0; k < 4; ++k) {  // warp-uniform addresses: shared-memory broadcasts
+          l4[k] = reinterpret_cast<const float4*>(lsm)[k];
+          d4[k] = reinterpret_cast<const float4*>(lsm + 64)[k];
         }
         tmem_ld_wait();
         const float* lr = reinterpret_cast<const float*>(l4);
@@ -1059,14 +1076,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (tr) trace[i * 8 + 4] = clock64();
       if (i >= 1) mbar_wait(p_free, (i - 1) & 1);  // gradient MMAs of tile i-1 released P^T / dS^T
       if (tr) trace[i * 8 + 5] = clock64();
-      uint8_t* prow = smem + L::kOffP + r * 128;
+      // P^T, dS^T (bf16 pairs) into TMEM: the A operands of dV / dK; dS^T also into shared
+      // memory (SW128) as the B operand of dQ^T
+      tmem_st_cols<16>(tPT + lo + half * 16, pk);
+      tmem_st_cols<16>(tDST + lo + half * 16, dk);
       uint8_t* drow = smem + L::kOffDS + r * 128;
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
         const int chunk = (half * 4 + cc) ^ (r & 7);
-        *reinterpret_cast<uint4*>(prow + chunk * 16) = make_uint4(pk[4 * cc], pk[4 * cc + 1], pk[4 * cc + 2], pk[4 * cc + 3]);
         *reinterpret_cast<uint4*>(drow + chunk * 16) = make_uint4(dk[4 * cc], dk[4 * cc + 1], dk[4 * cc + 2], dk[4 * cc + 3]);
       }
+      tmem_st_wait();
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(p_full);
