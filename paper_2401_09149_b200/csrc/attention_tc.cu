@@ -1031,29 +1031,23 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
       const bool diag = q0 < k0 + kBwdKeys;
       uint32_t pk[16], dk[16];
+      // S^T and dP^T of this warp's 32 query columns into registers, then release the TMEM
+      // buffers at once so the next tile's S^T / dP^T MMAs overlap this tile's math
+      uint32_t sv[32], pv[32];
+      tmem_ld_32x32b_x32(tS + lo + half * 32, sv);
+      tmem_ld_32x32b_x32(tP + lo + half * 32, pv);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(s_free);
+      const float* lsm = reinterpret_cast<const float*>(smem + L::kOffLD + (i % NS) * 512) + half * 32;
 #pragma unroll
       for (int hc = 0; hc < 2; ++hc) {
-        uint32_t sv[16], pv[16];
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(sv[0]), "=r"(sv[1]), "=r"(sv[2]), "=r"(sv[3]), "=r"(sv[4]), "=r"(sv[5]), "=r"(sv[6]),
-              "=r"(sv[7]), "=r"(sv[8]), "=r"(sv[9]), "=r"(sv[10]), "=r"(sv[11]), "=r"(sv[12]), "=r"(sv[13]),
-              "=r"(sv[14]), "=r"(sv[15])
-            : "r"(tS + lo + half * 32 + hc * 16));
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(pv[0]), "=r"(pv[1]), "=r"(pv[2]), "=r"(pv[3]), "=r"(pv[4]), "=r"(pv[5]), "=r"(pv[6]),
-              "=r"(pv[7]), "=r"(pv[8]), "=r"(pv[9]), "=r"(pv[10]), "=r"(pv[11]), "=r"(pv[12]), "=r"(pv[13]),
-              "=r"(pv[14]), "=r"(pv[15])
-            : "r"(tP + lo + half * 32 + hc * 16));
         float4 l4[4], d4[4];
-        const float* lsm = reinterpret_cast<const float*>(smem + L::kOffLD + (i % NS) * 512) + half * 32 + hc * 16;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {  // warp-uniform addresses: shared-memory broadcasts
-          l4[k] = reinterpret_cast<const float4*>(lsm)[k];
-          d4[k] = reinterpret_cast<const float4*>(lsm + 64)[k];
+          l4[k] = reinterpret_cast<const float4*>(lsm + hc * 16)[k];
+          d4[k] = reinterpret_cast<const float4*>(lsm + 64 + hc * 16)[k];
         }
-        tmem_ld_wait();
         const float* lr = reinterpret_cast<const float*>(l4);
         const float* dr = reinterpret_cast<const float*>(d4);
 #pragma unroll
@@ -1062,17 +1056,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int qc = half * 32 + hc * 16 + c + e;
-            float p = fast_exp2(fmaf(__uint_as_float(sv[c + e]), scale_log2, -lr[c + e] * kLog2e));
+            float p = fast_exp2(fmaf(__uint_as_float(sv[hc * 16 + c + e]), scale_log2, -lr[c + e] * kLog2e));
             if (diag && key > q0 + qc) p = 0.f;
             p2[e] = p;
-            d2[e] = p * (__uint_as_float(pv[c + e]) - dr[c + e]);
+            d2[e] = p * (__uint_as_float(pv[hc * 16 + c + e]) - dr[c + e]);
           }
           pk[hc * 8 + c / 2] = pack_bf16(p2[0], p2[1]);
           dk[hc * 8 + c / 2] = pack_bf16(d2[0], d2[1]);
         }
       }
-      tc_fence_before();
-      mbar_arrive(s_free);
       if (tr) trace[i * 8 + 4] = clock64();
       if (i >= 1) mbar_wait(p_free, (i - 1) & 1);  // gradient MMAs of tile i-1 released P^T / dS^T
       if (tr) trace[i * 8 + 5] = clock64();

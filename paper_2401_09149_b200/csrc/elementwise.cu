@@ -179,20 +179,31 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_bwd_kernel(
   }
 }
 
-// dg[j] += sum_b part[b, j]
-__global__ void column_sum_kernel(const float* __restrict__ part, int rows, int H, float* __restrict__ dg) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= H) return;
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-  int b = 0;
-  for (; b + 4 <= rows; b += 4) {
-    s0 += part[static_cast<int64_t>(b) * H + j];
-    s1 += part[static_cast<int64_t>(b + 1) * H + j];
-    s2 += part[static_cast<int64_t>(b + 2) * H + j];
-    s3 += part[static_cast<int64_t>(b + 3) * H + j];
+// dg[j] += sum_b part[b, j]: one CTA per 32 columns, 32 row groups (warp w sums rows w, w+32, ...
+// with its lanes on consecutive columns: 128-B coalesced rows), then the 32 group sums are added
+// in fixed order through shared memory — deterministic, and 128 CTAs instead of H/128 long loops.
+__global__ void __launch_bounds__(1024) column_sum_kernel(const float* __restrict__ part, int rows, int H,
+                                                          float* __restrict__ dg) {
+  __shared__ float red[32][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + lane;
+  float s0 = 0.f, s1 = 0.f;
+  if (j < H) {
+    int b = w;
+    for (; b + 32 < rows; b += 64) {
+      s0 += part[static_cast<int64_t>(b) * H + j];
+      s1 += part[static_cast<int64_t>(b + 32) * H + j];
+    }
+    if (b < rows) s0 += part[static_cast<int64_t>(b) * H + j];
   }
-  for (; b < rows; ++b) s0 += part[static_cast<int64_t>(b) * H + j];
-  dg[j] += (s0 + s1) + (s2 + s3);
+  red[w][lane] = s0 + s1;
+  __syncthreads();
+  if (w == 0 && j < H) {
+    float t = 0.f;
+#pragma unroll 8
+    for (int g = 0; g < 32; ++g) t += red[g][lane];
+    dg[j] += t;
+  }
 }
 
 // In-place rotate-half RoPE on the q and k parts of token rows (ld elements apart).
@@ -319,7 +330,7 @@ cudaError_t rmsnorm_bwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const fl
     ISP_NORM_CASE(5) ISP_NORM_CASE(6) ISP_NORM_CASE(7) ISP_NORM_CASE(8)
 #undef ISP_NORM_CASE
   }
-  if (dg_scratch) column_sum_kernel<<<(H + 127) / 128, 128, 0, st>>>(dg_scratch, grid, H, dg);
+  if (dg_scratch) column_sum_kernel<<<(H + 31) / 32, 1024, 0, st>>>(dg_scratch, grid, H, dg);
   return cudaGetLastError();
 }
 

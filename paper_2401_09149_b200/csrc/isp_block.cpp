@@ -135,7 +135,11 @@ struct seqplan_isp_ctx {
   uint32_t step_epoch = 0;
   int gather_set = 0;
   bool push_primed = false;  // SKIP_COMM: buffers filled by one real step, then reused
-  int comm_ctas = -96;  // < 0: bulk-copy (TMA) push kernel with -comm_ctas CTAs
+  int comm_ctas = -96;  // < 0: bulk-copy (TMA) push kernel with -comm_ctas CTAs (all-gathers)
+  // reduce-scatter staging: each chunk goes to one destination, so the bulk kernel (one load in
+  // flight per CTA) is load-latency bound there; 16-B vector stores from 256-thread CTAs
+  // (128 B in flight per thread, no shared memory: they co-reside with every compute kernel)
+  int rs_ctas = 128;
   uint32_t* error_flag = nullptr;  // device, in the heap flags page
 
   // ---- device pool (subsystem 5) and persistent buffers ----
@@ -596,7 +600,7 @@ void push_rs(Ctx* c, int t, cudaStream_t cs) {
   }
   Span sp(c, cs, 1, SEQPLAN_EV_REDUCE_SCATTER, t);
   KTimer kt(c, cs, SEQPLAN_K_REDUCE_SCATTER, 0, double(p - 1) * double(bytes));
-  ISP_LAUNCH(1, push_copy(J, c->peers_at(0), c->world, c->rank, cs, c->comm_ctas));
+  ISP_LAUNCH(1, push_copy(J, c->peers_at(0), c->world, c->rank, cs, c->rs_ctas));
   signal_peers(c, cs, rs_flag(c, t, c->rank));
 }
 
@@ -1085,6 +1089,7 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
 
   c->fused_a2a = c->world > 1 && c->d == 128 && !std::getenv("SEQPLAN_ISP_PULL_A2A");
   if (const char* e = std::getenv("SEQPLAN_ISP_PUSH")) c->push_pref = std::atoi(e) ? 1 : 0;
+  if (const char* e = std::getenv("SEQPLAN_ISP_RS_CTAS")) c->rs_ctas = std::atoi(e) ? std::atoi(e) : 128;
   if (const char* e = std::getenv("SEQPLAN_ISP_COMM_CTAS")) c->comm_ctas = std::atoi(e) ? std::atoi(e) : -96;
   layout_heap(c);
   ISP_CUDA(cudaMalloc(&c->heap, c->heap_bytes));
