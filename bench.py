@@ -197,6 +197,9 @@ def run_reference(args):
 
 
 def main():
+    import faulthandler
+    import signal
+    faulthandler.register(signal.SIGUSR1, all_threads=True)  # `kill -USR1` dumps where a run hangs
     args = parse()
     if args.impl == "reference":
         run_reference(args)

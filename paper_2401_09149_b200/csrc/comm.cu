@@ -286,8 +286,8 @@ __global__ void __launch_bounds__(256) push_copy_kernel(PushJobs jobs, PeerPtrs 
 // bcast (every job has src_q == 0): each chunk is read once and stored to all ranks.
 // 2 x 16 KB slots: the CTA fits beside a GEMM / attention-forward CTA (~198 KB) on one SM, so
 // the copy needs no SMs of its own and the persistent grids stay whole.
-constexpr int kBulkChunk = 16384, kBulkSlots = 2;
-constexpr int kBulkSmem = kBulkChunk * kBulkSlots + 64;
+template <int CH, int NS>
+constexpr int bulk_smem() { return CH * NS + 64 + 128; }
 
 __device__ __forceinline__ void bulk_g2s(uint32_t smem, const void* g, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem),
@@ -304,6 +304,7 @@ struct ChunkRef {
   uint32_t bytes;
 };
 
+template <int kBulkChunk, int kBulkSlots>
 __global__ void __launch_bounds__(32) push_bulk_kernel(PushJobs jobs, PeerPtrs dst, int world, int rank, int bcast) {
   extern __shared__ __align__(128) uint8_t sm_raw[];
   if (threadIdx.x != 0) return;
@@ -445,23 +446,36 @@ cudaError_t a2a_heads_to_tokens(const PeerPtrs& src, int world, int rank, int T,
   return cudaGetLastError();
 }
 
-cudaError_t push_copy(const PushJobs& jobs, const PeerPtrs& dst, int world, int rank, cudaStream_t st, int num_ctas) {
+cudaError_t push_copy(const PushJobs& jobs, const PeerPtrs& dst, int world, int rank, cudaStream_t st, int num_ctas,
+                      int kind) {
   for (int j = 0; j < jobs.n; ++j) {
     const PushJob& J = jobs.j[j];
     if (J.blk % 16 || J.src_stride % 16 || J.dst_stride % 16 || J.dst_off % 16 || J.src_q % 16 ||
         reinterpret_cast<uintptr_t>(J.src) % 16)
       return cudaErrorInvalidValue;
   }
-  if (num_ctas < 0) {  // bulk-copy (TMA) kernel on -num_ctas dedicated CTAs
+  int bcast = 1;
+  for (int j = 0; j < jobs.n; ++j) bcast &= jobs.j[j].src_q == 0;
+  if (kind == kPushBulk) {  // 2 x 16 KB slots: co-resides with a ~198 KB GEMM / attention CTA
+    constexpr int sm = bulk_smem<16384, 2>();
     static bool attr = false;
     if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(push_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem + 128);
+      cudaError_t e = cudaFuncSetAttribute(push_bulk_kernel<16384, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    int bcast = 1;
-    for (int j = 0; j < jobs.n; ++j) bcast &= jobs.j[j].src_q == 0;
-    push_bulk_kernel<<<-num_ctas, 32, kBulkSmem + 128, st>>>(jobs, dst, world, rank, bcast);
+    push_bulk_kernel<16384, 2><<<num_ctas, 32, sm, st>>>(jobs, dst, world, rank, bcast);
+    return cudaGetLastError();
+  }
+  if (kind == kPushBulkWide) {  // 4 x 32 KB slots: an SM of its own per CTA
+    constexpr int sm = bulk_smem<32768, 4>();
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(push_bulk_kernel<32768, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    push_bulk_kernel<32768, 4><<<num_ctas, 32, sm, st>>>(jobs, dst, world, rank, bcast);
     return cudaGetLastError();
   }
   push_copy_kernel<<<num_ctas, 256, 0, st>>>(jobs, dst, world, rank);

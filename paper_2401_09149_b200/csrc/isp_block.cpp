@@ -135,11 +135,12 @@ struct seqplan_isp_ctx {
   uint32_t step_epoch = 0;
   int gather_set = 0;
   bool push_primed = false;  // SKIP_COMM: buffers filled by one real step, then reused
-  int comm_ctas = -96;  // < 0: bulk-copy (TMA) push kernel with -comm_ctas CTAs (all-gathers)
+  int ag_ctas = 96, ag_kind = kPushBulk;  // all-gathers: bulk-copy push, one chunk stored to every rank
   // reduce-scatter staging: each chunk goes to one destination, so the bulk kernel (one load in
   // flight per CTA) is load-latency bound there; 16-B vector stores from 256-thread CTAs
   // (128 B in flight per thread, no shared memory: they co-reside with every compute kernel)
   int rs_ctas = 128;
+  int gemm_sm_budget = 0;  // > 0 when the all-gather holds SMs of its own (kPushBulkWide)
   uint32_t* error_flag = nullptr;  // device, in the heap flags page
 
   // ---- device pool (subsystem 5) and persistent buffers ----
@@ -290,7 +291,9 @@ void gemm(Ctx* c, const GemmOperand& A, const GemmOperand& B, const GemmArgs& ar
   const double out_bytes = (epi == EPI_F32 ? 4.0 : 2.0) * M * N * (epi == EPI_SWIGLU ? 1.5 : 1.0);
   KTimer kt(c, st, SEQPLAN_K_GEMM, 2.0 * M * N * K, 2.0 * (M * K + N * K) + out_bytes);
   c->launches += 1;
-  cudaError_t e = gemm_launch(A, B, args, epi, st);
+  GemmArgs a = args;
+  if (c->push_mode() && c->gemm_sm_budget > 0) a.sm_budget = c->gemm_sm_budget;
+  cudaError_t e = gemm_launch(A, B, a, epi, st);
   if (e == cudaErrorInvalidValue)
     throw IspError(SEQPLAN_ISP_ERR_UNSUPPORTED, "GEMM shape not tiled by the sm_100a kernel (M%128, N%128, K%64)");
   ISP_CUDA(e);
@@ -557,7 +560,7 @@ void push_gather(Ctx* c, int set, int t, cudaStream_t cs) {
     bytes = sh * 2;
   }
   KTimer kt(c, cs, SEQPLAN_K_ALL_GATHER, 0, double(c->world - 1) * double(bytes));
-  ISP_LAUNCH(1, push_copy(J, c->peers_at(0), c->world, c->rank, cs, c->comm_ctas));
+  ISP_LAUNCH(1, push_copy(J, c->peers_at(0), c->world, c->rank, cs, c->ag_ctas, c->ag_kind));
   signal_peers(c, cs, ag_flag(c, set, t, c->rank));
 }
 
@@ -600,7 +603,7 @@ void push_rs(Ctx* c, int t, cudaStream_t cs) {
   }
   Span sp(c, cs, 1, SEQPLAN_EV_REDUCE_SCATTER, t);
   KTimer kt(c, cs, SEQPLAN_K_REDUCE_SCATTER, 0, double(p - 1) * double(bytes));
-  ISP_LAUNCH(1, push_copy(J, c->peers_at(0), c->world, c->rank, cs, c->rs_ctas));
+  ISP_LAUNCH(1, push_copy(J, c->peers_at(0), c->world, c->rank, cs, c->rs_ctas, kPushLsu));
   signal_peers(c, cs, rs_flag(c, t, c->rank));
 }
 
@@ -1090,7 +1093,9 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   c->fused_a2a = c->world > 1 && c->d == 128 && !std::getenv("SEQPLAN_ISP_PULL_A2A");
   if (const char* e = std::getenv("SEQPLAN_ISP_PUSH")) c->push_pref = std::atoi(e) ? 1 : 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_RS_CTAS")) c->rs_ctas = std::atoi(e) ? std::atoi(e) : 128;
-  if (const char* e = std::getenv("SEQPLAN_ISP_COMM_CTAS")) c->comm_ctas = std::atoi(e) ? std::atoi(e) : -96;
+  if (const char* e = std::getenv("SEQPLAN_ISP_AG_CTAS")) c->ag_ctas = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("SEQPLAN_ISP_AG_KIND")) c->ag_kind = std::atoi(e);
+  if (c->ag_kind == kPushBulkWide) c->gemm_sm_budget = c->num_sms - c->ag_ctas;
   layout_heap(c);
   ISP_CUDA(cudaMalloc(&c->heap, c->heap_bytes));
   ISP_CUDA(cudaMemset(c->heap, 0, kFlagBytes));

@@ -112,7 +112,12 @@ struct PushJobs {
   PushJob j[2];
   int n;
 };
-cudaError_t push_copy(const PushJobs& jobs, const PeerPtrs& dst, int world, int rank, cudaStream_t st, int num_ctas);
+// kind: kPushLsu (16-B vector stores, 256-thread CTAs, no shared memory), kPushBulk (one thread
+// driving cp.async.bulk through 2 x 16 KB slots: co-resident with compute CTAs), kPushBulkWide
+// (4 x 32 KB slots: one SM per CTA).
+enum PushKind : int { kPushLsu = 0, kPushBulk = 1, kPushBulkWide = 2 };
+cudaError_t push_copy(const PushJobs& jobs, const PeerPtrs& dst, int world, int rank, cudaStream_t st, int num_ctas,
+                      int kind);
 // Cross-GPU barrier over system-scope flags in every rank's heap. epoch increases by one per
 // call; a rank spins (bounded, ~20 s) until all peers have published `epoch`.
 cudaError_t peer_barrier(const PeerPtrs& flags, int world, int rank, uint32_t epoch,

@@ -37,7 +37,7 @@ def main():
         incoming = (1 + both) * psi * 2 * (world - 1) / world
         if rank == 0:
             print(f"p={world} sets={1 + both}: {t.item():.3f} ms/round, {incoming / t.item() / 1e6:.0f} GB/s incoming "
-                  f"per GPU (comm_ctas={os.environ.get('SEQPLAN_ISP_COMM_CTAS', 'default')})", flush=True)
+                  f"per GPU (ag kind={os.environ.get('SEQPLAN_ISP_AG_KIND', 'default')} ctas={os.environ.get('SEQPLAN_ISP_AG_CTAS', 'default')})", flush=True)
     blk.close()
     dist.barrier()
     dist.destroy_process_group()
