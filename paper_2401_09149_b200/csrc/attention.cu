@@ -467,6 +467,12 @@ cudaError_t bwd_impl(const AttnTensors& t, const __nv_bfloat16* dout, __nv_bfloa
     set = true;
   }
   const float scale = 1.0f / sqrtf(static_cast<float>(D));
+  if (D == 128 && t.S % 256 == 0 && !std::getenv("SEQPLAN_ISP_ATTN_MMA_SYNC") && std::getenv("SEQPLAN_ISP_ATTN_SPLIT_BWD")) {
+    // split tcgen05 backward: dK/dV kernel + CTA-pair dQ kernel (no dq_acc, no atomics). Opt-in:
+    // measured 2.41 ms vs 1.7 ms fused at S = 16K x 8 heads (dK/dV 894 TF/s, dQ 699 TF/s)
+    attn_delta_kernel<D><<<num_sms * 8, 256, 0, st>>>(t.o, t.ld_o, dout, delta, t.S, t.heads);
+    return attention_bwd_split_tc(t, dout, t.ld_o, dq, dk, dv, ld_d, delta, st);
+  }
   cudaError_t e = cudaMemsetAsync(dq_acc, 0, sizeof(float) * static_cast<size_t>(t.heads) * t.S * D, st);
   if (e != cudaSuccess) return e;
   attn_delta_kernel<D><<<num_sms * 8, 256, 0, st>>>(t.o, t.ld_o, dout, delta, t.S, t.heads);

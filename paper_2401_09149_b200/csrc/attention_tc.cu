@@ -852,12 +852,16 @@ __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.w
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-__global__ void __launch_bounds__(kBwdThreads, 1)
+// kDQ = false: the dK/dV kernel of the split backward (dQ comes from attn_bwd_dq_pair_kernel):
+// no dQ^T MMA / warps / atomics, and K lives in TMEM so S^T = K Q^T is a TS MMA.
+template <bool kDQ>
+__global__ void __launch_bounds__(kDQ ? kBwdThreads : 320, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                        const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mDO,
                        const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ dq_acc,
                        __nv_bfloat16* __restrict__ dk_out, __nv_bfloat16* __restrict__ dv_out, int64_t ld_d,
-                       int S, float scale, int dbg, long long* trace, const __grid_constant__ AttnPush push) {
+                       int S, float scale, int dbg, long long* trace, const __grid_constant__ AttnPush push,
+                       const __nv_bfloat16* __restrict__ kg, int64_t ld_k) {
   using L = BwdSmem;
   constexpr int D = 128;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -874,7 +878,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* dkv_full = bar + 7;
   uint64_t* q_full = bar + 8;        // [NS]
   uint64_t* q_empty = bar + 8 + NS;  // [NS]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8 + 2 * NS);
+  uint64_t* k_tm = bar + 8 + 2 * NS;  // !kDQ: K rows written into TMEM by the P/dS warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9 + 2 * NS);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int kt = blockIdx.x, h = blockIdx.y;
@@ -893,6 +898,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(dq_full, 1);
     mbar_init(dq_free, 128);
     mbar_init(dkv_full, 1);
+    mbar_init(k_tm, 256);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -900,16 +906,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM: S^T 0 | dP^T 64 | dK 128 | dV 256 | dQ^T 384 (64) | P^T bf16 448 (32) | dS^T bf16 480 (32)
+  // TMEM, kDQ:  S^T 0 | dP^T 64 | dK 128 | dV 256 | dQ^T 384 (64) | P^T bf16 448 (32) | dS^T bf16 480 (32)
+  //       !kDQ: S^T 0 | dP^T 64 | dK 128 | dV 256 | P^T bf16 384 (32) | dS^T bf16 416 (32) | K bf16 448 (64)
   const uint32_t tS = tmem, tP = tmem + 64, tDK = tmem + 128, tDV = tmem + 256, tDQ = tmem + 384;
-  const uint32_t tPT = tmem + 448, tDST = tmem + 480;
+  const uint32_t tPT = tmem + (kDQ ? 448 : 384), tDST = tmem + (kDQ ? 480 : 416), tK = tmem + 448;
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
-      mbar_arrive_expect_tx(kv_full, 2 * L::kKV);
+      mbar_arrive_expect_tx(kv_full, (kDQ ? 2 : 1) * L::kKV);
       for (int c = 0; c < 2; ++c) {
-        tma_load_2d(smem + L::kOffK + c * kBwdKeys * 128, &mK, kv_full, h * D + c * 64, k0);
+        if constexpr (kDQ) tma_load_2d(smem + L::kOffK + c * kBwdKeys * 128, &mK, kv_full, h * D + c * 64, k0);
         tma_load_2d(smem + L::kOffV + c * kBwdKeys * 128, &mV, kv_full, h * D + c * 64, k0);
       }
       for (int i = 0; i < nq; ++i) {
@@ -933,10 +940,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint32_t sK = smem_u32(smem + L::kOffK), sV = smem_u32(smem + L::kOffV);
       const uint32_t sDS = smem_u32(smem + L::kOffDS);
       mbar_wait(kv_full, 0);
+      if constexpr (!kDQ) mbar_wait(k_tm, 0);
       auto grads = [&](int j) {
         const int s = j % NS;
         mbar_wait(p_full, j & 1);
-        if (j >= 1) mbar_wait(dq_free, (j - 1) & 1);
+        if (kDQ && j >= 1) mbar_wait(dq_free, (j - 1) & 1);
         tc_fence_after();
         const uint32_t sQ = smem_u32(smem + L::kOffQ + s * L::kStage), sDO = sQ + L::kQ;
 #pragma unroll
@@ -946,13 +954,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           tc_mma_bf16_ts(tDK, tDST + k * 8, make_sw128_desc(sQ + k * 2048, kBwdQ * 128, 1024), id_g,
                          (j > 0 || k > 0) ? 1u : 0u);
         }
+        if constexpr (kDQ) {
 #pragma unroll
-        for (int k = 0; k < kBwdKeys / 16; ++k)
-          tc_mma_bf16(tDQ, make_sw128_desc(sK + k * 2048, kBwdKeys * 128, 1024),
-                      make_sw128_desc(sDS + k * 2048, kBwdQ * 128, 1024), id_q, k > 0 ? 1u : 0u);
+          for (int k = 0; k < kBwdKeys / 16; ++k)
+            tc_mma_bf16(tDQ, make_sw128_desc(sK + k * 2048, kBwdKeys * 128, 1024),
+                        make_sw128_desc(sDS + k * 2048, kBwdQ * 128, 1024), id_q, k > 0 ? 1u : 0u);
+        }
         tc_commit(&q_empty[s]);
         tc_commit(p_free);
-        tc_commit(dq_full);
+        if constexpr (kDQ) tc_commit(dq_full);
       };
       for (int i = 0; i < nq; ++i) {
         const int s = i % NS;
@@ -963,8 +973,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const int c = k / 4, kk = k % 4;
-          tc_mma_bf16(tS, make_sw128_desc(sK + c * kBwdKeys * 128 + kk * 32, 16, 1024),
-                      make_sw128_desc(sQ + c * kBwdQ * 128 + kk * 32, 16, 1024), id_s, k > 0 ? 1u : 0u);
+          if constexpr (kDQ)
+            tc_mma_bf16(tS, make_sw128_desc(sK + c * kBwdKeys * 128 + kk * 32, 16, 1024),
+                        make_sw128_desc(sQ + c * kBwdQ * 128 + kk * 32, 16, 1024), id_s, k > 0 ? 1u : 0u);
+          else  // A = K from TMEM (16 head dims = 8 columns)
+            tc_mma_bf16_ts(tS, tK + k * 8, make_sw128_desc(sQ + c * kBwdQ * 128 + kk * 32, 16, 1024), id_s,
+                           k > 0 ? 1u : 0u);
           tc_mma_bf16(tP, make_sw128_desc(sV + c * kBwdKeys * 128 + kk * 32, 16, 1024),
                       make_sw128_desc(sDO + c * kBwdQ * 128 + kk * 32, 16, 1024), id_s, k > 0 ? 1u : 0u);
         }
@@ -976,7 +990,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       grads(nq - 1);
       tc_commit(dkv_full);
     }
-  } else if (warp >= 10) {
+  } else if (kDQ && warp >= 10) {
     // ---------------- dQ warps 10..13: dQ^T (lane = head dim) -> fp32 reductions ----------------
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
@@ -1013,6 +1027,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int r = quad * 32 + lane;  // key row
     const uint32_t lo = static_cast<uint32_t>(quad * 32) << 16;
     const int key = k0 + r;
+    if constexpr (!kDQ) {  // K row of this key into TMEM (this warp's 64 head dims): the S^T A operand
+      const uint4* src = reinterpret_cast<const uint4*>(kg + static_cast<int64_t>(key) * ld_k + h * D + half * 64);
+      uint32_t kr[32];
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const uint4 u = src[v];
+        kr[4 * v] = u.x; kr[4 * v + 1] = u.y; kr[4 * v + 2] = u.z; kr[4 * v + 3] = u.w;
+      }
+      tmem_st_32x32b_x32(tK + lo + half * 32, kr);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(k_tm);
+    }
     for (int i = 0; i < nq; ++i) {
       const int q0 = (qi0 + i) * kBwdQ;
       const bool tr = trace && blockIdx.x == 0 && blockIdx.y == 0 && i < 64 && warp == 2 && lane == 0;
@@ -1072,14 +1099,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       // memory (SW128) as the B operand of dQ^T
       tmem_st_cols<16>(tPT + lo + half * 16, pk);
       tmem_st_cols<16>(tDST + lo + half * 16, dk);
-      uint8_t* drow = smem + L::kOffDS + r * 128;
+      if constexpr (kDQ) {
+        uint8_t* drow = smem + L::kOffDS + r * 128;
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        const int chunk = (half * 4 + cc) ^ (r & 7);
-        *reinterpret_cast<uint4*>(drow + chunk * 16) = make_uint4(dk[4 * cc], dk[4 * cc + 1], dk[4 * cc + 2], dk[4 * cc + 3]);
+        for (int cc = 0; cc < 4; ++cc) {
+          const int chunk = (half * 4 + cc) ^ (r & 7);
+          *reinterpret_cast<uint4*>(drow + chunk * 16) =
+              make_uint4(dk[4 * cc], dk[4 * cc + 1], dk[4 * cc + 2], dk[4 * cc + 3]);
+        }
       }
       tmem_st_wait();
-      fence_proxy_async();
+      if constexpr (kDQ) fence_proxy_async();
       tc_fence_before();
       mbar_arrive(p_full);
       if (tr) trace[i * 8 + 6] = clock64();
@@ -1129,12 +1159,292 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   }
 }
 
+// =====================================================================================
+// Split backward, dQ part: CTA-pair kernel (d = 128), no atomics.
+//
+// A cluster owns 2 query tiles of 128 (CTA c: tile 2pp + c) of one head and walks 64-key tiles.
+// Q and dO rows live in TMEM (each CTA's own 128 rows, bf16 pairs) as the A operands of the
+// M = 256 pair MMAs S = Q K^T and dP = dO V^T (each CTA holds half of the tile's K and V rows);
+// S and dP are double-buffered in TMEM so the next tile's MMAs overlap this tile's
+// P = exp2(S*scale - lse), dS = P (dP - delta) (one thread per query row, no cross-thread
+// reduction); dS (bf16) overwrites its own S columns and is the A operand of dQ += dS K
+// (each CTA holds half of K's head-dim columns). dQ accumulates in TMEM; the epilogue scales,
+// converts and stores (or pushes to the owner rank) each query row once.
+// TMEM per CTA: Q 0 (64) | dO 64 (64) | S[2] 128, 192 | dP[2] 256, 320 | dQ 384 (128).
+// Warps 0..7 dS math (warp pair per lane quadrant, 32 keys each), warp 8 TMA, warp 9 MMA.
+// =====================================================================================
+struct DqCfg {
+  static constexpr int D = 128, BN = 64, NS = 4;
+  static constexpr int kKr = (BN / 2) * D * 2;  // K rows half: 2 chunks [32 keys][64]
+  static constexpr int kVr = (BN / 2) * D * 2;  // V rows half
+  static constexpr int kKc = BN * 64 * 2;       // K head-dim half: 1 chunk [64 keys][64 d]
+  static constexpr int kStage = kKr + kVr + kKc;
+  static constexpr int kOffBar = NS * kStage;
+  static constexpr int kBytes = kOffBar + 256 + 1024;
+  static_assert(kBytes <= 232448, "exceeds the 227 KB per-CTA shared memory");
+};
+
+__global__ void __launch_bounds__(320, 1)
+    attn_bwd_dq_pair_kernel(const __grid_constant__ CUtensorMap mKr, const __grid_constant__ CUtensorMap mVr,
+                            const __grid_constant__ CUtensorMap mKc, const __nv_bfloat16* __restrict__ qg,
+                            int64_t ld_q, const __nv_bfloat16* __restrict__ dog, int64_t ld_do,
+                            const float* __restrict__ lse, const float* __restrict__ delta,
+                            __nv_bfloat16* __restrict__ dq_out, int64_t ld_dq, int S, float scale,
+                            const __grid_constant__ AttnPush push) {
+  using L = DqCfg;
+  constexpr int D = L::D, BN = L::BN, NS = L::NS;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
+  uint64_t* qo_full = bar + 0;         // leader's: Q / dO rows of both CTAs in TMEM (8 warps x 2)
+  uint64_t* s_full = bar + 1;          // [2] local (multicast commit)
+  uint64_t* p_full = bar + 3;          // [2] leader's: dS of the buffer written (8 warps x 2)
+  uint64_t* o_full = bar + 5;          // local (multicast commit): last dQ MMA done
+  uint64_t* kv_full = bar + 6;         // [NS] leader's
+  uint64_t* kv_empty = kv_full + NS;   // [NS] local (multicast commit)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_empty + NS);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t crank = cluster_rank();
+  const bool leader = crank == 0;
+  const int pp = static_cast<int>(gridDim.x / 2) - 1 - static_cast<int>(blockIdx.x / 2);  // heavy pairs first
+  const int h = blockIdx.y;
+  const int q0 = (2 * pp + static_cast<int>(crank)) * kBM;
+  const int n = (2 * pp + 2) * kBM / BN;  // key tiles of the upper query tile (both CTAs)
+
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&mKr);
+    tma_prefetch(&mVr);
+    tma_prefetch(&mKc);
+    mbar_init(qo_full, 16);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 16);
+    }
+    mbar_init(o_full, 1);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tQ = tmem, tDO = tmem + 64, tSb = tmem + 128, tDPb = tmem + 256, tDQ = tmem + 384;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs; completion on the leader's barriers) ----------------
+      const int ch = static_cast<int>(crank);
+      for (int j = 0; j < n; ++j) {
+        const int s = j % NS;
+        if (j >= NS) mbar_wait(&kv_empty[s], ((j / NS) - 1) & 1);
+        if (leader) mbar_arrive_expect_tx(&kv_full[s], 2 * L::kStage);
+        uint8_t* st = smem + s * L::kStage;
+        for (int c = 0; c < 2; ++c) {
+          tma_load_2d_pair(st + c * (BN / 2) * 128, &mKr, &kv_full[s], h * D + c * 64, j * BN + ch * (BN / 2));
+          tma_load_2d_pair(st + L::kKr + c * (BN / 2) * 128, &mVr, &kv_full[s], h * D + c * 64, j * BN + ch * (BN / 2));
+        }
+        tma_load_2d_pair(st + L::kKr + L::kVr, &mKc, &kv_full[s], h * D + ch * 64, j * BN);
+      }
+    }
+  } else if (warp == 9) {
+    if (leader && lane == 0) {
+      // ---------------- MMA issuer (leader only) ----------------
+      constexpr uint32_t idS = make_idesc_bf16(2 * kBM, BN, false, false);  // S, dP: N = keys
+      constexpr uint32_t idQ = make_idesc_bf16(2 * kBM, D, false, true);    // dQ: N = head dim, B MN-major
+      auto issue_dq = [&](int i) {
+        const int b = i & 1;
+        mbar_wait(&p_full[b], (i >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sKc = smem_u32(smem + (i % NS) * L::kStage + L::kKr + L::kVr);
+#pragma unroll
+        for (int k = 0; k < BN / 16; ++k)  // dS packed: keys 0..31 in columns 0..15, keys 32..63 in 32..47
+          tc_mma_bf16_ts_pair(tDQ, tSb + b * 64 + (k >> 1) * 32 + (k & 1) * 8,
+                              make_sw128_desc(sKc + k * 2048, BN * 128, 1024), idQ, (i > 0 || k > 0) ? 1u : 0u);
+        tc_commit_pair(&kv_empty[i % NS]);
+      };
+      mbar_wait(qo_full, 0);
+      for (int j = 0; j < n; ++j) {
+        const int b = j & 1;
+        mbar_wait(&kv_full[j % NS], (j / NS) & 1);
+        tc_fence_after();
+        const uint32_t sKr = smem_u32(smem + (j % NS) * L::kStage), sVr = sKr + L::kKr;
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const int c = k / 4, kk = k % 4;
+          tc_mma_bf16_ts_pair(tSb + b * 64, tQ + k * 8, make_sw128_desc(sKr + c * (BN / 2) * 128 + kk * 32, 16, 1024),
+                              idS, k > 0 ? 1u : 0u);
+        }
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const int c = k / 4, kk = k % 4;
+          tc_mma_bf16_ts_pair(tDPb + b * 64, tDO + k * 8,
+                              make_sw128_desc(sVr + c * (BN / 2) * 128 + kk * 32, 16, 1024), idS, k > 0 ? 1u : 0u);
+        }
+        tc_commit_pair(&s_full[b]);
+        if (j >= 1) issue_dq(j - 1);
+      }
+      issue_dq(n - 1);
+      tc_commit_pair(o_full);
+    }
+  } else {
+    // ---------------- dS warps 0..7 ----------------
+    const int quad = warp & 3, half = warp >> 2;
+    const int r = quad * 32 + lane;
+    const int q = q0 + r;
+    const uint32_t lo = static_cast<uint32_t>(quad * 32) << 16;
+    auto arrive_leader = [&](uint64_t* bar_) {
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(bar_);
+        else mbar_arrive_leader(bar_);
+      }
+    };
+    {  // Q and dO rows of this query (this warp's 64 head dims) into TMEM
+      uint32_t v[32];
+      const uint4* sq = reinterpret_cast<const uint4*>(qg + static_cast<int64_t>(q) * ld_q + h * D + half * 64);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint4 u = sq[i];
+        v[4 * i] = u.x; v[4 * i + 1] = u.y; v[4 * i + 2] = u.z; v[4 * i + 3] = u.w;
+      }
+      tmem_st_32x32b_x32(tQ + lo + half * 32, v);
+      const uint4* sd = reinterpret_cast<const uint4*>(dog + static_cast<int64_t>(q) * ld_do + h * D + half * 64);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint4 u = sd[i];
+        v[4 * i] = u.x; v[4 * i + 1] = u.y; v[4 * i + 2] = u.z; v[4 * i + 3] = u.w;
+      }
+      tmem_st_32x32b_x32(tDO + lo + half * 32, v);
+      tmem_st_wait();
+      tc_fence_before();
+      arrive_leader(qo_full);
+    }
+    const float scale_log2 = scale * kLog2e;
+    const float lse2 = lse[static_cast<int64_t>(h) * S + q] * kLog2e;
+    const float dl = delta[static_cast<int64_t>(h) * S + q];
+    for (int j = 0; j < n; ++j) {
+      const int b = j & 1;
+      mbar_wait(&s_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t sv[32], pv[32];
+      tmem_ld_32x32b_x32(tSb + b * 64 + lo + half * 32, sv);
+      tmem_ld_32x32b_x32(tDPb + b * 64 + lo + half * 32, pv);
+      tmem_ld_wait();
+      const int key0 = j * BN + half * 32;
+      const bool diag = key0 + 31 > q0;  // some key of this chunk may lie past some query of the tile
+      uint32_t dk[16];
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) {
+        float d2[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          float p = fast_exp2(fmaf(__uint_as_float(sv[c + e]), scale_log2, -lse2));
+          if (diag && key0 + c + e > q) p = 0.f;
+          d2[e] = p * (__uint_as_float(pv[c + e]) - dl);
+        }
+        dk[c / 2] = pack_bf16(d2[0], d2[1]);
+      }
+      // dS over this warp's own (already read) S columns: the A operand of dQ += dS K
+      tmem_st_cols<16>(tSb + b * 64 + lo + half * 32, dk);
+      tmem_st_wait();
+      tc_fence_before();
+      arrive_leader(&p_full[b]);
+    }
+    // epilogue: dQ * scale -> bf16 row (or pushed to the owner rank of token q)
+    mbar_wait(o_full, 0);
+    tc_fence_after();
+    __nv_bfloat16* row = dq_out + static_cast<int64_t>(q) * ld_dq + h * D + half * 64;
+    if (push.p[0]) {
+      const int owner = q / push.T;
+      row = static_cast<__nv_bfloat16*>(push.p[owner]) + static_cast<int64_t>(q - owner * push.T) * push.ld +
+            push.col_q + h * D + half * 64;
+    }
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      uint32_t o[32];
+      tmem_ld_32x32b_x32(tDQ + lo + half * 64 + c * 32, o);
+      tmem_ld_wait();
+      uint4* dst = reinterpret_cast<uint4*>(row + c * 32);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint32_t pk2[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          pk2[e] = pack_bf16(__uint_as_float(o[v * 8 + 2 * e]) * scale, __uint_as_float(o[v * 8 + 2 * e + 1]) * scale);
+        dst[v] = make_uint4(pk2[0], pk2[1], pk2[2], pk2[3]);
+      }
+    }
+    if (push.p[0]) __threadfence_system();  // pushed rows visible before the next barrier flag
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 9) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
 }  // namespace
 
 long long* g_attn_trace = nullptr;  // development: clock64 trace of CTA (0,0)
 long long* g_attn_trace_fwd = nullptr;
 extern "C" void seqplan_isp_debug_set_trace(long long* dev_buf) { g_attn_trace = dev_buf; }
 extern "C" void seqplan_isp_debug_set_trace_fwd(long long* dev_buf) { g_attn_trace_fwd = dev_buf; }
+
+// Split backward (d = 128, S / 256 integral): dK/dV kernel (K in TMEM, no dQ) + CTA-pair dQ kernel.
+// delta = rowsum(dO * O) must be computed before; dq is written (or pushed) in bf16, no dq_acc.
+cudaError_t attention_bwd_split_tc(const AttnTensors& t, const __nv_bfloat16* dout, int64_t ld_dout, __nv_bfloat16* dq,
+                                   __nv_bfloat16* dk, __nv_bfloat16* dv, int64_t ld_d, const float* delta,
+                                   cudaStream_t st) {
+  if (t.d != 128 || t.S % 256) return cudaErrorInvalidValue;
+  using L = BwdSmem;
+  using Q = DqCfg;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(attn_bwd_dq_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::kBytes);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  CUtensorMap mq, mk, mv, mdo, mkr, mvr, mkc;
+  const int64_t cols = static_cast<int64_t>(t.heads) * 128;
+  if (!map2d(&mq, t.q, t.S, cols, t.ld_qkv, kBwdQ) || !map2d(&mk, t.k, t.S, cols, t.ld_qkv, kBwdKeys) ||
+      !map2d(&mv, t.v, t.S, cols, t.ld_qkv, kBwdKeys) || !map2d(&mdo, dout, t.S, cols, ld_dout, kBwdQ) ||
+      !map2d(&mkr, t.k, t.S, cols, t.ld_qkv, Q::BN / 2) || !map2d(&mvr, t.v, t.S, cols, t.ld_qkv, Q::BN / 2) ||
+      !map2d(&mkc, t.k, t.S, cols, t.ld_qkv, Q::BN))
+    return cudaErrorInvalidValue;
+  const float scale = 1.0f / sqrtf(128.0f);
+  const int dbg = std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0;
+  AttnPush kv_push = t.push;  // dK / dV rows
+  attn_bwd_tc_kernel<false><<<dim3(t.S / kBwdKeys, t.heads), 320, L::kBytes, st>>>(
+      mq, mk, mv, mdo, t.lse, delta, nullptr, dk, dv, ld_d, t.S, scale, dbg, g_attn_trace, kv_push, t.k, t.ld_qkv);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(t.S / kBM, t.heads);
+  cfg.blockDim = dim3(320);
+  cfg.dynamicSmemBytes = Q::kBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, attn_bwd_dq_pair_kernel, mkr, mvr, mkc, t.q, t.ld_qkv, dout, ld_dout, t.lse, delta, dq,
+                            ld_d, t.S, scale, t.push);
+}
 
 // dq_acc must be zeroed and delta = rowsum(dO * O) computed before this launch.
 cudaError_t attention_bwd_tc(const AttnTensors& t, const __nv_bfloat16* dout, int64_t ld_dout, __nv_bfloat16* dk,
@@ -1143,7 +1453,7 @@ cudaError_t attention_bwd_tc(const AttnTensors& t, const __nv_bfloat16* dout, in
   using L = BwdSmem;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -1153,9 +1463,10 @@ cudaError_t attention_bwd_tc(const AttnTensors& t, const __nv_bfloat16* dout, in
       !map2d(&mv, t.v, t.S, cols, t.ld_qkv, kBwdKeys) || !map2d(&mdo, dout, t.S, cols, ld_dout, kBwdQ))
     return cudaErrorInvalidValue;
   const float scale = 1.0f / sqrtf(128.0f);
-  attn_bwd_tc_kernel<<<dim3(t.S / kBwdKeys, t.heads), kBwdThreads, L::kBytes, st>>>(
+  attn_bwd_tc_kernel<true><<<dim3(t.S / kBwdKeys, t.heads), kBwdThreads, L::kBytes, st>>>(
       mq, mk, mv, mdo, t.lse, delta, dq_acc, dk, dv, ld_d, t.S, scale,
-      std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0, g_attn_trace, t.push);
+      std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0, g_attn_trace, t.push, t.k,
+      t.ld_qkv);
   return cudaGetLastError();
 }
 

@@ -24,8 +24,14 @@ def torch_attention(q, k, v):  # [S, h, d] fp32, causal
     return torch.einsum("hqk,khd->qhd", p, v), lse
 
 
+@pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("S,heads,d", [(256, 2, 64), (512, 3, 128), (1024, 1, 128), (384, 2, 64)])
-def test_attention_fwd_bwd(cuda, S, heads, d):
+def test_attention_fwd_bwd(cuda, S, heads, d, split, monkeypatch):
+    # split: the opt-in two-kernel backward (dK/dV kernel + CTA-pair dQ kernel), d = 128 only
+    if split and d != 128:
+        pytest.skip("split backward is d = 128")
+    if split:
+        monkeypatch.setenv("SEQPLAN_ISP_ATTN_SPLIT_BWD", "1")
     torch.manual_seed(S + d)
     Hl = heads * d
     qkv = torch.randn(S, 3 * Hl, device=cuda).bfloat16()

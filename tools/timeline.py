@@ -33,7 +33,7 @@ def main():
         blk.fwd(x, y)
         blk.bwd(x, dx)
     torch.cuda.synchronize()
-    if rank == 0:
+    if rank == int(os.environ.get("TIMELINE_RANK", 0)):
         ev = blk.timeline()
         comp = [e for e in ev if e["stream"] == 0]
         comm = [e for e in ev if e["stream"] == 1]
