@@ -171,6 +171,17 @@ int seqplan_isp_get_grad_shard(seqplan_isp_ctx* ctx, int tensor, float* host, in
 /* Device pointer of the fp32 gradient shard (stream-ordered after block_bwd). */
 int seqplan_isp_grad_shard_ptr(seqplan_isp_ctx* ctx, int tensor, float** dev_ptr);
 
+/* Optimizer step after the path (T_update of estimate_step, cost.hpp:292-294):
+ * AdamW (torch.optim.AdamW rule: decoupled weight decay, bias-corrected moments) on every fp32
+ * master shard with the gradient shard of the last block_bwd; the moment shards live in the device
+ * pool (created zero on the first call); the bf16 working shards are refreshed in the same pass.
+ * With ISP (dp = 1, oss = 1, gs = 1) there is no optimizer-state collective. step >= 1. */
+typedef struct seqplan_adamw_params {
+  double lr, beta1, beta2, eps, weight_decay;
+  int64_t step;
+} seqplan_adamw_params;
+int seqplan_isp_adamw_step(seqplan_isp_ctx* ctx, const seqplan_adamw_params* params, void* stream);
+
 /* Synthetic index-keyed bf16 activations for tokens [r*S/p, (r+1)*S/p) of tensor id. */
 int seqplan_isp_fill_activation(seqplan_isp_ctx* ctx, uint64_t seed, int tensor_id, void* dev_out,
                                 void* stream);

@@ -123,3 +123,20 @@ def rope_table(S: int, d: int, base: float = 10000.0):
     s = np.empty((S, d // 2), np.float32)
     lib().ob_rope_table(S, d, base, _fp(c), _fp(s))
     return c, s
+
+
+def adamw(w, g, m, v, step: int, lr: float, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
+          weight_decay: float = 0.0):
+    """One AdamW update of an fp32 shard (torch.optim.AdamW rule: decoupled weight decay, then
+    bias-corrected first/second moments). The optimizer step after the path (SURVEY.md §8f item 2);
+    the reference prices it only, as T_update = optimizer-state bytes / 1 TB/s (cost.hpp:292-294).
+    Returns (w, m, v) as new float32 arrays; computed in float64."""
+    w = np.asarray(w, np.float64); g = np.asarray(g, np.float64)
+    m = np.asarray(m, np.float64); v = np.asarray(v, np.float64)
+    w = w - lr * weight_decay * w
+    m = beta1 * m + (1 - beta1) * g
+    v = beta2 * v + (1 - beta2) * g * g
+    mh = m / (1 - beta1 ** step)
+    vh = v / (1 - beta2 ** step)
+    w = w - lr * mh / (np.sqrt(vh) + eps)
+    return w.astype(np.float32), m.astype(np.float32), v.astype(np.float32)

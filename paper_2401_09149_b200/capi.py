@@ -34,6 +34,10 @@ class PolicyC(ctypes.Structure):
                 ("grad_premap", ctypes.c_int32), ("capacity", c_i64)]
 
 
+class AdamWC(ctypes.Structure):
+    _fields_ = [("lr", c_d), ("beta1", c_d), ("beta2", c_d), ("eps", c_d), ("weight_decay", c_d), ("step", c_i64)]
+
+
 class StepStatsC(ctypes.Structure):
     _fields_ = [(n, c_i64) for n in ("reserved", "allocated", "free_cached", "fragmented",
                                      "peak_reserved", "peak_fragmented", "peak_allocated")]
@@ -109,6 +113,8 @@ _EXTRA_SIGS = [
     ("seqplan_isp_timeline", c_int, [c_vp, P(EventC), P(c_i64)]),
     ("seqplan_isp_kernel_profile", c_int, [c_vp, P(KernelRecC), P(c_i64), c_int]),
     ("seqplan_isp_launch_count", c_i64, [c_vp]),
+    ("seqplan_isp_adamw_step", c_int, [c_vp, P(AdamWC), c_vp]),
+    ("seqplan_isp_debug_gather_bench", c_int, [c_vp, c_int, c_int, P(ctypes.c_float)]),
     ("seqplan_isp_debug_attention", c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_int, c_int, c_int,
                                             c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     ("seqplan_isp_debug_rmsnorm", c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_f,
@@ -209,6 +215,11 @@ class IspBlock:
         a = np.empty(self.shard_numel(t), np.float32)
         check(lib().seqplan_isp_get_grad_shard(self.h, t, a.ctypes.data, a.size), self.h, "get_grad_shard")
         return a
+
+    def adamw_step(self, lr, step, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, stream=None):
+        """AdamW on every fp32 master shard; refreshes the bf16 working shards."""
+        p = AdamWC(lr, beta1, beta2, eps, weight_decay, step)
+        check(lib().seqplan_isp_adamw_step(self.h, ctypes.byref(p), _stream_handle(stream)), self.h, "adamw_step")
 
     def fill_activation(self, seed, tid, out, stream=None):
         check(lib().seqplan_isp_fill_activation(self.h, seed, tid, out.data_ptr(), _stream_handle(stream)),

@@ -296,6 +296,46 @@ cudaError_t keyed_fill(uint64_t seed, int tensor_id, int64_t offset, int64_t n, 
   return cudaGetLastError();
 }
 
+// AdamW on one fp32 master shard (decoupled weight decay, bias-corrected moments, the update
+// rule of torch.optim.AdamW), fused with the refresh of the bf16 working shard. 4 elements per
+// thread (16-B vectors); n % 4 == 0 (every shard is a multiple of 8 elements).
+__global__ void adamw_kernel(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ m,
+                             float* __restrict__ v, __nv_bfloat16* __restrict__ wb, int64_t n4, AdamWArgs a) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 W = reinterpret_cast<float4*>(w)[i];
+    const float4 G = reinterpret_cast<const float4*>(g)[i];
+    float4 M = reinterpret_cast<float4*>(m)[i], V = reinterpret_cast<float4*>(v)[i];
+    float* pw = &W.x;
+    const float* pg = &G.x;
+    float* pm = &M.x;
+    float* pv = &V.x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      pw[e] -= a.lr * a.weight_decay * pw[e];
+      pm[e] = a.beta1 * pm[e] + (1.f - a.beta1) * pg[e];
+      pv[e] = a.beta2 * pv[e] + (1.f - a.beta2) * pg[e] * pg[e];
+      const float mh = pm[e] * a.inv_bc1, vh = pv[e] * a.inv_bc2;
+      pw[e] -= a.lr * mh / (sqrtf(vh) + a.eps);
+    }
+    reinterpret_cast<float4*>(w)[i] = W;
+    reinterpret_cast<float4*>(m)[i] = M;
+    reinterpret_cast<float4*>(v)[i] = V;
+    uint2 b;
+    b.x = pack_bf16(W.x, W.y);
+    b.y = pack_bf16(W.z, W.w);
+    reinterpret_cast<uint2*>(wb)[i] = b;
+  }
+}
+
+cudaError_t adamw_step(float* w, const float* g, float* m, float* v, __nv_bfloat16* wb, int64_t n, const AdamWArgs& a,
+                       cudaStream_t st, int num_sms) {
+  if (n % 4) return cudaErrorInvalidValue;
+  if (n == 0) return cudaSuccess;
+  adamw_kernel<<<grid_for(n / 4, 256, num_sms), 256, 0, st>>>(w, g, m, v, wb, n / 4, a);
+  return cudaGetLastError();
+}
+
 cudaError_t cast_f32_bf16(const float* in, __nv_bfloat16* out, int64_t n, cudaStream_t st,
                           int num_sms) {
   if (n <= 0) return cudaSuccess;

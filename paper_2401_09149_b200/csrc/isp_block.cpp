@@ -147,6 +147,8 @@ struct seqplan_isp_ctx {
   DevicePool pool;
   float* master[SEQPLAN_W_COUNT] = {};
   float* grad[SEQPLAN_W_COUNT] = {};
+  float* adam_m[SEQPLAN_W_COUNT] = {};  // optimizer moments (seqplan_isp_adamw_step), lazily created
+  float* adam_v[SEQPLAN_W_COUNT] = {};
   bf16* wgu_local = nullptr;  // p = 1: interleaved gate|up working copy
   float* cos_t = nullptr;
   float* sin_t = nullptr;
@@ -1359,6 +1361,45 @@ int seqplan_isp_init_weights(seqplan_isp_ctx* c, uint64_t seed) {
       refresh_working(c, t, nullptr);
     }
     ISP_CUDA(cudaDeviceSynchronize());
+  } catch (const IspError& e) {
+    return fail(c, e);
+  }
+  return SEQPLAN_ISP_OK;
+}
+
+int seqplan_isp_adamw_step(seqplan_isp_ctx* c, const seqplan_adamw_params* p, void* stream) {
+  if (!c || !p || p->step < 1 || !(p->lr >= 0) || !(p->beta1 >= 0 && p->beta1 < 1) || !(p->beta2 >= 0 && p->beta2 < 1) ||
+      !(p->eps > 0))
+    return SEQPLAN_ISP_ERR_INVALID;
+  try {
+    ISP_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    AdamWArgs a;
+    a.lr = static_cast<float>(p->lr);
+    a.beta1 = static_cast<float>(p->beta1);
+    a.beta2 = static_cast<float>(p->beta2);
+    a.eps = static_cast<float>(p->eps);
+    a.weight_decay = static_cast<float>(p->weight_decay);
+    a.inv_bc1 = static_cast<float>(1.0 / (1.0 - std::pow(p->beta1, double(p->step))));
+    a.inv_bc2 = static_cast<float>(1.0 / (1.0 - std::pow(p->beta2, double(p->step))));
+    for (int t = 0; t < SEQPLAN_W_COUNT; ++t) {
+      const int64_t n = c->shard(t);
+      if (!c->adam_m[t]) {
+        c->adam_m[t] = static_cast<float*>(pool_alloc(c, n * 4, seqplan::AllocTag::Other, st));
+        c->adam_v[t] = static_cast<float*>(pool_alloc(c, n * 4, seqplan::AllocTag::Other, st));
+        ISP_CUDA(cudaMemsetAsync(c->adam_m[t], 0, size_t(n) * 4, st));
+        ISP_CUDA(cudaMemsetAsync(c->adam_v[t], 0, size_t(n) * 4, st));
+      }
+      ISP_LAUNCH(1, adamw_step(c->master[t], c->grad[t], c->adam_m[t], c->adam_v[t], c->wshard(t), n, a, st,
+                               c->num_sms));
+      if (c->world == 1 && (t == SEQPLAN_W_GATE || t == SEQPLAN_W_UP)) {  // interleaved gate|up working copy
+        const int64_t rows = c->I, cols = c->H, B = kGuBlock;
+        ISP_CUDA(cudaMemcpy2DAsync(c->wgu_local + (t == SEQPLAN_W_UP ? B : 0) * cols, size_t(2 * B * cols * 2),
+                                   c->wshard(t), size_t(B * cols * 2), size_t(B * cols * 2), size_t(rows / B),
+                                   cudaMemcpyDeviceToDevice, st));
+      }
+    }
+    c->weights_dirty = true;  // peers gather the new working shards after the next barrier
   } catch (const IspError& e) {
     return fail(c, e);
   }

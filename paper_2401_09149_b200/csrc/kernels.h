@@ -12,6 +12,13 @@ uint64_t keyed_stream_base(uint64_t seed, int tensor_id);
 cudaError_t keyed_fill(uint64_t seed, int tensor_id, int64_t offset, int64_t n, double mean,
                        double stdv, float* out_f32, __nv_bfloat16* out_bf16, cudaStream_t st,
                        int num_sms);
+// AdamW (torch.optim.AdamW update rule) on an fp32 master shard with its fp32 gradient and moment
+// shards, writing the refreshed bf16 working shard in the same pass.
+struct AdamWArgs {
+  float lr, beta1, beta2, eps, weight_decay, inv_bc1, inv_bc2;  // inv_bc = 1 / (1 - beta^step)
+};
+cudaError_t adamw_step(float* w, const float* g, float* m, float* v, __nv_bfloat16* wb, int64_t n, const AdamWArgs& a,
+                       cudaStream_t st, int num_sms);
 cudaError_t cast_f32_bf16(const float* in, __nv_bfloat16* out, int64_t n, cudaStream_t st,
                           int num_sms);
 cudaError_t rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* y,
