@@ -171,6 +171,22 @@ int seqplan_isp_get_grad_shard(seqplan_isp_ctx* ctx, int tensor, float* host, in
 /* Device pointer of the fp32 gradient shard (stream-ordered after block_bwd). */
 int seqplan_isp_grad_shard_ptr(seqplan_isp_ctx* ctx, int tensor, float** dev_ptr);
 
+/* ---- multi-layer stacks ---------------------------
+ * `layers` ISP blocks (one context each, independent weights) run as one step on one comm
+ * stream: every layer's forward gathers are issued up front in layer order and every layer's
+ * backward re-gather in reverse order (overlap_sim.hpp:80-105, 141-150); layer l's compute waits
+ * only on its own weights, and the reduce-scatters of all layers overlap the backward of the
+ * layers below. Each layer is a seqplan_isp_ctx (weights, grads, IPC bootstrap, timeline). */
+typedef struct seqplan_isp_stack seqplan_isp_stack;
+int seqplan_isp_stack_create(int layers, int world, int rank, int device, const seqplan_isp_shape* shape,
+                             const seqplan_strategy* strategy, const seqplan_mempool_policy* policy,
+                             uint32_t flags, seqplan_isp_stack** out);
+void seqplan_isp_stack_destroy(seqplan_isp_stack* stack);
+int seqplan_isp_stack_layers(const seqplan_isp_stack* stack);
+seqplan_isp_ctx* seqplan_isp_stack_layer(seqplan_isp_stack* stack, int layer);
+int seqplan_isp_stack_fwd(seqplan_isp_stack* stack, const void* x, void* y, void* stream);
+int seqplan_isp_stack_bwd(seqplan_isp_stack* stack, const void* dy, void* dx, void* stream);
+
 /* Optimizer step after the path (T_update of estimate_step, cost.hpp:292-294):
  * AdamW (torch.optim.AdamW rule: decoupled weight decay, bias-corrected moments) on every fp32
  * master shard with the gradient shard of the last block_bwd; the moment shards live in the device

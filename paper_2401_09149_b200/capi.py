@@ -114,6 +114,13 @@ _EXTRA_SIGS = [
     ("seqplan_isp_kernel_profile", c_int, [c_vp, P(KernelRecC), P(c_i64), c_int]),
     ("seqplan_isp_launch_count", c_i64, [c_vp]),
     ("seqplan_isp_adamw_step", c_int, [c_vp, P(AdamWC), c_vp]),
+    ("seqplan_isp_stack_create", c_int, [c_int, c_int, c_int, c_int, P(ShapeC), P(StrategyC), P(PolicyC), c_u32,
+                                         P(c_vp)]),
+    ("seqplan_isp_stack_destroy", None, [c_vp]),
+    ("seqplan_isp_stack_layers", c_int, [c_vp]),
+    ("seqplan_isp_stack_layer", c_vp, [c_vp, c_int]),
+    ("seqplan_isp_stack_fwd", c_int, [c_vp, c_vp, c_vp, c_vp]),
+    ("seqplan_isp_stack_bwd", c_int, [c_vp, c_vp, c_vp, c_vp]),
     ("seqplan_isp_debug_gather_bench", c_int, [c_vp, c_int, c_int, P(ctypes.c_float)]),
     ("seqplan_isp_debug_attention", c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_int, c_int, c_int,
                                             c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
@@ -259,6 +266,49 @@ class IspBlock:
     def close(self):
         if getattr(self, "h", None) and getattr(self, "_owner", True):
             lib().seqplan_isp_ctx_destroy(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class IspStack:
+    """`layers` ISP blocks run as one step: inter-layer prefetch of every
+    layer's gathers on one comm stream; layer(l) is a non-owning IspBlock view (weights, grads,
+    peer bootstrap, timeline of that layer)."""
+
+    def __init__(self, layers, H, D, S, world=1, rank=0, device=0, policy=None, flags=0, I=0):
+        l = lib()
+        self.world, self.rank = world, rank
+        self.shape = make_shape(H, D, S, I)
+        strat = StrategyC(1, 1, 0, 1, 1, 1, world, world, 1, 1)
+        pol = policy if policy is not None else make_policy()
+        h = c_vp()
+        check(l.seqplan_isp_stack_create(layers, world, rank, device, ctypes.byref(self.shape), ctypes.byref(strat),
+                                         ctypes.byref(pol), flags, ctypes.byref(h)), None, "stack_create")
+        self.h = h
+        self.n = layers
+
+    def layer(self, i):
+        b = IspBlock.__new__(IspBlock)
+        b.h, b.world, b.rank, b.shape = c_vp(lib().seqplan_isp_stack_layer(self.h, i)), self.world, self.rank, self.shape
+        b._owner = False  # a view: the stack owns and destroys the context
+        return b
+
+    def fwd(self, x, y, stream=None):
+        check(lib().seqplan_isp_stack_fwd(self.h, x.data_ptr(), y.data_ptr(), _stream_handle(stream)),
+              self.layer(0).h, "stack_fwd")
+
+    def bwd(self, dy, dx, stream=None):
+        check(lib().seqplan_isp_stack_bwd(self.h, dy.data_ptr(), dx.data_ptr(), _stream_handle(stream)),
+              self.layer(0).h, "stack_bwd")
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().seqplan_isp_stack_destroy(self.h)
         self.h = None
 
     def __del__(self):

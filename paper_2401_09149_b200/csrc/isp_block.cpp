@@ -135,6 +135,8 @@ struct seqplan_isp_ctx {
   uint32_t step_epoch = 0;
   int gather_set = 0;
   bool push_primed = false;  // SKIP_COMM: buffers filled by one real step, then reused
+  bool defer_bwd_set = false;  // fwd_issue_gathers leaves the backward set to the caller (stacks)
+  bool owns_comm = true;       // false: the comm stream belongs to layer 0 of a stack
   int ag_ctas = 96, ag_kind = kPushBulk;  // all-gathers: bulk-copy push, one chunk stored to every rank
   // reduce-scatter staging: each chunk goes to one destination, so the bulk kernel (one load in
   // flight per CTA) is load-latency bound there; 16-B vector stores from 256-thread CTAs
@@ -648,7 +650,7 @@ void fwd_issue_gathers(Ctx* c, cudaStream_t st) {
     c->gather_set = 0;
     push_gather_set(c, 1, bo, 6, false);
     push_gather_set(c, 0, fo, 6, !c->push_skip());
-    if (!c->push_skip()) push_gather_set(c, 1, bo, 6, true);
+    if (!c->push_skip() && !c->defer_bwd_set) push_gather_set(c, 1, bo, 6, true);
     for (int t : fo) c->gathered[t] = c->hp<bf16>(c->off_gath[0][t]);
     return;
   }
@@ -1279,7 +1281,7 @@ void seqplan_isp_ctx_destroy(seqplan_isp_ctx* c) {
     if (c->peer_opened[q]) cudaIpcCloseMemHandle(c->peer_heap[q]);
   c->pool.release_all();
   if (c->heap) cudaFree(c->heap);
-  if (c->comm) cudaStreamDestroy(c->comm);
+  if (c->comm && c->owns_comm) cudaStreamDestroy(c->comm);
   for (int q = 0; q < kMaxRanks; ++q) {
     if (c->peer_st[q]) cudaStreamDestroy(c->peer_st[q]);
     if (c->ev_join[q]) cudaEventDestroy(c->ev_join[q]);
@@ -1465,16 +1467,31 @@ int seqplan_isp_fill_activation(seqplan_isp_ctx* c, uint64_t seed, int tensor_id
   return SEQPLAN_ISP_OK;
 }
 
-static void run_fwd(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
+// Step start: epoch, the write-after-read barrier (peers finished the previous step, refreshed
+// working shards visible), and the weight gathers. defer_bwd_set (push mode): the backward
+// re-gather set is left for the caller to issue (multi-layer stacks order it after every
+// layer's forward set).
+static void fwd_prologue(Ctx* c, cudaStream_t st, bool do_barrier, bool defer_bwd_set) {
   ++c->step_epoch;
-  if (c->weights_dirty || c->fused_a2a || c->push_mode()) {
+  if (do_barrier && (c->weights_dirty || c->fused_a2a || c->push_mode())) {
     // peers must see refreshed working shards before gathering; with fused all-to-all, no
     // peer may push into this rank's exchange buffers before its previous backward finished
     barrier(c, st, false);
-    c->weights_dirty = false;
   }
+  c->weights_dirty = false;
   c->timeline.clear();
+  c->defer_bwd_set = defer_bwd_set;
   fwd_issue_gathers(c, st);
+  c->defer_bwd_set = false;
+}
+
+static void push_bwd_set(Ctx* c) {
+  if (!c->push_mode()) return;
+  const int bo[] = {SEQPLAN_W_DOWN, SEQPLAN_W_GATE, SEQPLAN_W_NORM2, SEQPLAN_W_O, SEQPLAN_W_QKV, SEQPLAN_W_NORM1};
+  push_gather_set(c, 1, bo, 6, !c->push_skip());
+}
+
+static void fwd_body(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
   fwd_phase1(c, x, st);
   barrier(c, st, false);
   fwd_phase2(c, st);
@@ -1483,13 +1500,22 @@ static void run_fwd(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
   c->fwd_done = true;
 }
 
-static void run_bwd(Ctx* c, const bf16* x, const bf16* dy, bf16* dx, cudaStream_t st) {
+static void run_fwd(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
+  fwd_prologue(c, st, true, false);
+  fwd_body(c, x, y, st);
+}
+
+static void bwd_body(Ctx* c, const bf16* x, const bf16* dy, bf16* dx, cudaStream_t st) {
   bwd_issue_gathers(c, st);
   bwd_phase1(c, dy, st);
   barrier(c, st, false);
   bwd_phase2(c, st);
   barrier(c, st, false);
   bwd_phase3(c, x, dx, st);
+}
+
+// Gradient reductions of the step and the join with the comm stream.
+static void bwd_epilogue(Ctx* c, cudaStream_t st) {
   if (c->flags & SEQPLAN_ISP_FLAG_FUSED_BWD) {
     barrier(c, st, false);
     bwd_reduce_all(c, st);
@@ -1507,6 +1533,11 @@ static void run_bwd(Ctx* c, const bf16* x, const bf16* dy, bf16* dx, cudaStream_
   }
   c->pool.step_boundary();
   if (c->push_mode()) c->push_primed = true;
+}
+
+static void run_bwd(Ctx* c, const bf16* x, const bf16* dy, bf16* dx, cudaStream_t st) {
+  bwd_body(c, x, dy, dx, st);
+  bwd_epilogue(c, st);
 }
 
 int seqplan_isp_block_fwd(seqplan_isp_ctx* c, const void* x, void* y, void* stream) {
@@ -1610,6 +1641,142 @@ int seqplan_isp_kernel_profile(seqplan_isp_ctx* c, seqplan_kernel_record* out, i
 }
 
 int64_t seqplan_isp_launch_count(const seqplan_isp_ctx* c) { return c ? c->launches : -1; }
+
+// ---- multi-layer stacks ------------------------------------------
+struct seqplan_isp_stack {
+  std::vector<Ctx*> layers;
+  std::vector<bf16*> act;   // layer boundaries: act[l] = input of layer l (l >= 1), [T, H] bf16
+  std::vector<bf16*> grad;  // dx of layer l = dy of layer l-1
+  const void* x0 = nullptr;
+  bool fwd_done = false;
+};
+
+int seqplan_isp_stack_create(int layers, int world, int rank, int device, const seqplan_isp_shape* shape,
+                             const seqplan_strategy* strategy, const seqplan_mempool_policy* policy, uint32_t flags,
+                             seqplan_isp_stack** out) {
+  if (!out || layers < 1) return SEQPLAN_ISP_ERR_INVALID;
+  *out = nullptr;
+  auto* s = new seqplan_isp_stack();
+  for (int l = 0; l < layers; ++l) {
+    Ctx* c = nullptr;
+    const int st = seqplan_isp_ctx_create(world, rank, device, shape, strategy, policy, flags, &c);
+    if (st != SEQPLAN_ISP_OK) {
+      seqplan_isp_stack_destroy(s);
+      return st;
+    }
+    s->layers.push_back(c);
+  }
+  Ctx* c0 = s->layers[0];
+  try {
+    ISP_CUDA(cudaSetDevice(device));
+    // one comm stream for the whole stack: gathers and reduce-scatters of all layers are one FIFO,
+    // the reference's two-stream schedule (overlap_sim.hpp:55-74)
+    for (int l = 1; l < layers; ++l) {
+      Ctx* c = s->layers[l];
+      ISP_CUDA(cudaStreamDestroy(c->comm));
+      c->comm = c0->comm;
+      c->owns_comm = false;
+    }
+    const size_t bytes = size_t(c0->T) * c0->H * 2;
+    for (int l = 0; l < layers; ++l) {
+      bf16 *a = nullptr, *g = nullptr;
+      if (l > 0) ISP_CUDA(cudaMalloc(&a, bytes));
+      if (l > 0) ISP_CUDA(cudaMalloc(&g, bytes));
+      s->act.push_back(a);
+      s->grad.push_back(g);
+    }
+  } catch (const IspError& e) {
+    std::fprintf(stderr, "seqplan_isp_stack_create: %s\n", e.msg.c_str());
+    seqplan_isp_stack_destroy(s);
+    return e.code;
+  }
+  *out = s;
+  return SEQPLAN_ISP_OK;
+}
+
+void seqplan_isp_stack_destroy(seqplan_isp_stack* s) {
+  if (!s) return;
+  if (!s->layers.empty()) cudaSetDevice(s->layers[0]->device);
+  cudaDeviceSynchronize();
+  for (bf16* p : s->act)
+    if (p) cudaFree(p);
+  for (bf16* p : s->grad)
+    if (p) cudaFree(p);
+  for (size_t l = s->layers.size(); l-- > 0;) seqplan_isp_ctx_destroy(s->layers[l]);  // layer 0 (comm owner) last
+  delete s;
+}
+
+int seqplan_isp_stack_layers(const seqplan_isp_stack* s) { return s ? static_cast<int>(s->layers.size()) : 0; }
+
+seqplan_isp_ctx* seqplan_isp_stack_layer(seqplan_isp_stack* s, int layer) {
+  if (!s || layer < 0 || layer >= static_cast<int>(s->layers.size())) return nullptr;
+  return s->layers[size_t(layer)];
+}
+
+// Forward of every layer. All forward gathers are issued up front in layer order, then every
+// layer's backward re-gather in reverse layer order, on the one comm stream — the reference's
+// InterLayerPrefetch forward (overlap_sim.hpp:80-105) and the reverse-order backward prefetch
+// (overlap_sim.hpp:141-150); layer l's compute waits only on its own weights.
+int seqplan_isp_stack_fwd(seqplan_isp_stack* s, const void* x, void* y, void* stream) {
+  if (!s || !x || !y) return SEQPLAN_ISP_ERR_INVALID;
+  const int L = static_cast<int>(s->layers.size());
+  Ctx* cur = s->layers[0];
+  try {
+    ISP_CUDA(cudaSetDevice(cur->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    for (int l = 0; l < L; ++l) {
+      cur = s->layers[size_t(l)];
+      if (cur->group_mode) throw IspError(SEQPLAN_ISP_ERR_INVALID, "stacks run one process per GPU");
+      fwd_prologue(cur, st, l == 0, true);  // one write-after-read barrier covers every layer
+    }
+    for (int l = L; l-- > 0;) push_bwd_set(s->layers[size_t(l)]);
+    for (int l = 0; l < L; ++l) {
+      cur = s->layers[size_t(l)];
+      const bf16* in = l == 0 ? static_cast<const bf16*>(x) : s->act[size_t(l)];
+      bf16* outp = l == L - 1 ? static_cast<bf16*>(y) : s->act[size_t(l + 1)];
+      fwd_body(cur, in, outp, st);
+      cur->last_x = in;
+    }
+    s->x0 = x;
+    s->fwd_done = true;
+  } catch (const IspError& e) {
+    return fail(cur, e);
+  }
+  return SEQPLAN_ISP_OK;
+}
+
+// Backward in reverse layer order; the reduce-scatters of every layer overlap the backward of
+// the layers below (selective, overlap_sim.hpp:114-153) and are reduced at the end of the step.
+int seqplan_isp_stack_bwd(seqplan_isp_stack* s, const void* dy, void* dx, void* stream) {
+  if (!s || !dy || !dx || !s->fwd_done) return SEQPLAN_ISP_ERR_INVALID;
+  const int L = static_cast<int>(s->layers.size());
+  Ctx* cur = s->layers[0];
+  try {
+    ISP_CUDA(cudaSetDevice(cur->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    for (int l = L; l-- > 0;) {
+      cur = s->layers[size_t(l)];
+      const bf16* g_in = l == L - 1 ? static_cast<const bf16*>(dy) : s->grad[size_t(l + 1)];
+      bf16* g_out = l == 0 ? static_cast<bf16*>(dx) : s->grad[size_t(l)];
+      bwd_body(cur, static_cast<const bf16*>(cur->last_x), g_in, g_out, st);
+      cur->fwd_done = false;
+    }
+    for (int l = L; l-- > 0;) {
+      cur = s->layers[size_t(l)];
+      bwd_epilogue(cur, st);
+      if (cur->flags & (SEQPLAN_ISP_FLAG_TIMELINE | SEQPLAN_ISP_FLAG_PROFILE)) {
+        ISP_CUDA(cudaStreamSynchronize(st));
+        check_device_error(cur);
+        collect_timeline(cur);
+        collect_kprof(cur);
+      }
+    }
+    s->fwd_done = false;
+  } catch (const IspError& e) {
+    return fail(cur, e);
+  }
+  return SEQPLAN_ISP_OK;
+}
 
 // Development: `iters` rounds of (comm-lane barrier, push all-gather of the forward set [and the
 // backward set], wait for every peer's flags) on the comm stream; *ms = time per round.

@@ -168,3 +168,48 @@ def test_adamw_step_matches_oracle(cuda):
     torch.cuda.synchronize()
     assert rel(y.float().cpu().numpy(), y0) > 1e-4  # the refreshed working shards are used
     blk.close()
+
+
+def _bf16(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).bfloat16().float().numpy()
+
+
+def stack_oracle(sh, ws, x, dy):
+    """L-layer chain of the oracle block with the GPU's bf16 rounding at layer boundaries."""
+    ys, xs = [], [x]
+    for w in ws:
+        y, _, _ = ob.block(sh, w, xs[-1], np.zeros_like(xs[-1]), p=1)
+        ys.append(y)
+        xs.append(_bf16(y))
+    g_in, grads = dy, [None] * len(ws)
+    for l in reversed(range(len(ws))):
+        _, dx, g = ob.block(sh, ws[l], xs[l], g_in, p=1)
+        grads[l] = g
+        g_in = _bf16(dx)
+    return ys[-1], dx, grads
+
+
+@pytest.mark.parametrize("H,D,S", [(512, 8, 1024), (1024, 8, 512)])
+def test_stack_two_layers_p1(cuda, H, D, S):
+    """Multi-layer stack: 2 layers with independent weights through
+    seqplan_isp_stack_fwd/bwd vs the oracle block chained twice."""
+    sh, w0, x, dy, _, _, _ = oracle_case(H, D, S)
+    w1 = ob.make_weights(sh, seed=ob.SEED + 1)
+    y_ref, dx_ref, g_ref = stack_oracle(sh, [w0, w1], x, dy)
+    st = capi.IspStack(2, H, D, S)
+    for l, w in enumerate((w0, w1)):
+        load_weights(st.layer(l), w, 1, 0)
+    xd = torch.from_numpy(x).bfloat16().to(cuda)
+    dyd = torch.from_numpy(dy).bfloat16().to(cuda)
+    y, dx = torch.empty_like(xd), torch.empty_like(xd)
+    for _ in range(2):  # second step: buffers / flags reused
+        st.fwd(xd, y)
+        st.bwd(dyd, dx)
+    torch.cuda.synchronize()
+    assert rel(y.float().cpu(), y_ref) <= TOL
+    assert rel(dx.float().cpu(), dx_ref) <= TOL
+    for l in range(2):
+        for t in range(7):
+            e = rel(st.layer(l).grad_shard(t), g_ref[l][t].reshape(-1))
+            assert e <= TOL, (l, capi.W_NAMES[t], e)
+    st.close()
