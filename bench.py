@@ -279,36 +279,70 @@ def main():
     clocks = clk.summary()
 
     # ---- end to end through the public API with host buffers ----
+    # Every step copies its own inputs x, dy from pinned host memory and reads its result dx back.
+    # The loop is the one a training job runs: inputs are double-buffered, step i+1's H2D copies run
+    # on a copy stream while step i computes, and step i's D2H overlaps step i+1. The timed region
+    # spans the first copy-in to the last copy-out (all copies of all steps are inside it).
     e2e = None
     if not args.no_e2e:
         hx = torch.empty(T, H, dtype=torch.bfloat16).pin_memory()
         hdy = torch.empty_like(hx).pin_memory()
-        hdx = torch.empty_like(hx).pin_memory()
+        hdx = [torch.empty_like(hx).pin_memory() for _ in range(2)]
         hx.copy_(x.cpu())
         hdy.copy_(dy.cpu())
+        xb, dyb, dxb = [x, torch.empty_like(x)], [dy, torch.empty_like(dy)], [dx, torch.empty_like(dx)]
+        copy_in, copy_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        in_ready = [torch.cuda.Event() for _ in range(2)]
+        step_done = [torch.cuda.Event() for _ in range(2)]
+        for ev in step_done:
+            ev.record(stream)
 
-        copy_stream = torch.cuda.Stream(device=dev)
-        dy_ready = torch.cuda.Event()
+        def issue_in(i):
+            b = i % 2
+            copy_in.wait_event(step_done[b])  # step i-2 is done with this buffer pair
+            with torch.cuda.stream(copy_in):
+                xb[b].copy_(hx, non_blocking=True)
+                dyb[b].copy_(hdy, non_blocking=True)
+                in_ready[b].record(copy_in)
 
-        def e2e_step():
-            # this step's inputs come from pinned host memory: x before the forward, dy on a
-            # side stream overlapping the forward; the result dx is read back every step
-            x.copy_(hx, non_blocking=True)
-            copy_stream.wait_stream(stream)
-            with torch.cuda.stream(copy_stream):
-                dy.copy_(hdy, non_blocking=True)
-                dy_ready.record(copy_stream)
-            blk.fwd(x, y, stream)
-            stream.wait_event(dy_ready)
-            blk.bwd(dy, dx, stream)
-            hdx.copy_(dx, non_blocking=True)
+        def run(i):
+            b = i % 2
+            stream.wait_event(in_ready[b])
+            blk.fwd(xb[b], y, stream)
+            blk.bwd(dyb[b], dxb[b], stream)
+            step_done[b].record(stream)
+            copy_out.wait_event(step_done[b])
+            with torch.cuda.stream(copy_out):
+                hdx[b].copy_(dxb[b], non_blocking=True)
+
+        def e2e_loop(n):
+            issue_in(0)
+            for i in range(n):
+                if i + 1 < n:
+                    issue_in(i + 1)
+                run(i)
+            stream.wait_stream(copy_out)
 
         with torch.cuda.stream(stream):
-            e2e_step()
-        ms_e2e = timed(e2e_step, args.steps)
+            e2e_loop(2)
+        sync_all()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            flush.fill_(1)
+            e0.record(stream)
+            copy_in.wait_event(e0)
+            e2e_loop(args.steps)
+            e1.record(stream)
+        sync_all()
+        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
         nb = T * H * 2
         e2e = {"value": S / (ms_e2e / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": 2 * nb,
-               "d2h_bytes_per_step": nb, "ms_per_step": ms_e2e}
+               "d2h_bytes_per_step": nb, "ms_per_step": ms_e2e,
+               "pipelining": "double-buffered inputs: step i+1's H2D and step i's D2H overlap compute",
+               "l2": "flushed once before the loop; per-step working set (weights, activations) > L2"}
 
     # ---- profiled pass: per-kernel CUDA events (not the headline number) ----
     blk.close()
