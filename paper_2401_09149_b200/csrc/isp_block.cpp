@@ -1094,7 +1094,12 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   }
   c->pool.set_policy(pol);
 
-  c->fused_a2a = c->world > 1 && c->d == 128 && !std::getenv("SEQPLAN_ISP_PULL_A2A");
+  // Ulysses all-to-all: SM pull kernels after the producer (default), or fused into the producers'
+  // epilogues as 16-B remote stores (SEQPLAN_ISP_FUSED_A2A=1). Measured at p = 2/4: the pull is
+  // 3-7 % faster end to end (7B-4K/32K) — per-thread 16-B NVLink stores from 32 different rows
+  // per warp instruction slow the QKV GEMM and attention epilogues more than the exchange costs.
+  const char* fa = std::getenv("SEQPLAN_ISP_FUSED_A2A");
+  c->fused_a2a = c->world > 1 && c->d == 128 && fa && std::atoi(fa) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_PUSH")) c->push_pref = std::atoi(e) ? 1 : 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_RS_CTAS")) c->rs_ctas = std::atoi(e) ? std::atoi(e) : 128;
   if (const char* e = std::getenv("SEQPLAN_ISP_AG_CTAS")) c->ag_ctas = std::max(1, std::atoi(e));

@@ -80,9 +80,14 @@ def test_block_p1(cuda, H, D, S):
     blk.close()
 
 
+@pytest.mark.parametrize("fused_a2a", [False, True])
 @pytest.mark.parametrize("p,H,D,S", [(2, 512, 8, 1024), (4, 512, 8, 1024), (2, 1024, 8, 1024), (4, 1024, 8, 1024),
                                      (8, 1024, 8, 2048)])  # p = 8: the north-star degree, on one GPU
-def test_block_group(cuda, p, H, D, S):
+def test_block_group(cuda, p, H, D, S, fused_a2a, monkeypatch):
+    if fused_a2a and H // D != 128:
+        pytest.skip("the fused all-to-all is for head dim 128")
+    if fused_a2a:  # the all-to-all fused into the producers' epilogues
+        monkeypatch.setenv("SEQPLAN_ISP_FUSED_A2A", "1")
     sh, w, x, dy, y_ref, dx_ref, g_ref = oracle_case(H, D, S)
     grp = capi.IspGroup(H, D, S, world=p)
     blocks = [grp.rank(r) for r in range(p)]

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _run(n, H, D, S, mode="selective", env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", f"--master-port={29500 + n + (7 if mode == 'fused' else 0) + (20 if H == 1024 else 0) + (40 + 3 * int(env.get('SEQPLAN_ISP_PUSH', '0')) if env else 0)}",
+           "--master-addr=127.0.0.1", f"--master-port={29500 + n + (7 if mode == 'fused' else 0) + (20 if H == 1024 else 0) + (40 + 3 * int(env.get('SEQPLAN_ISP_PUSH', '0')) + 5 * int(env.get('SEQPLAN_ISP_FUSED_A2A', '0')) if env else 0)}",
            os.path.join(ROOT, "tests", "mp_parity_worker.py"), str(H), str(D), str(S), mode]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
                        env={**os.environ, **(env or {})})
@@ -37,6 +37,17 @@ def test_multiprocess_parity(n, mode, H):
             if k not in ("rank", "timeline_events"):
                 assert v <= 1e-2, (row["rank"], k, v)
         assert row["timeline_events"] > 0
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_multiprocess_parity_fused_a2a(n):
+    """The Ulysses all-to-all fused into the producers' epilogues (SEQPLAN_ISP_FUSED_A2A=1)."""
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    for row in _run(n, 1024, 8, 1024, "selective", env={"SEQPLAN_ISP_FUSED_A2A": "1"}):
+        for k, v in row.items():
+            if k not in ("rank", "timeline_events"):
+                assert v <= 1e-2, (row["rank"], k, v)
 
 
 @pytest.mark.parametrize("push", ["0", "1"])
