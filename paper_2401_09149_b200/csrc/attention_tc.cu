@@ -854,7 +854,10 @@ __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.syn
 
 // kDQ = false: the dK/dV kernel of the split backward (dQ comes from attn_bwd_dq_pair_kernel):
 // no dQ^T MMA / warps / atomics, and K lives in TMEM so S^T = K Q^T is a TS MMA.
-template <bool kDQ>
+// kKT (fused kernel): K also lives in TMEM (S^T as a TS MMA, 32 KB less shared-memory operand
+// traffic per tile); P^T / dS^T then share the dQ^T columns, so the P/dS warps also wait for the
+// dQ warps to have drained dQ^T of the previous tile before writing them.
+template <bool kDQ, bool kKT = !kDQ>
 __global__ void __launch_bounds__(kDQ ? kBwdThreads : 320, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                        const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mDO,
@@ -908,8 +911,9 @@ __global__ void __launch_bounds__(kDQ ? kBwdThreads : 320, 1)
   const uint32_t tmem = *tmem_slot;
   // TMEM, kDQ:  S^T 0 | dP^T 64 | dK 128 | dV 256 | dQ^T 384 (64) | P^T bf16 448 (32) | dS^T bf16 480 (32)
   //       !kDQ: S^T 0 | dP^T 64 | dK 128 | dV 256 | P^T bf16 384 (32) | dS^T bf16 416 (32) | K bf16 448 (64)
+  //  kDQ && kKT: S^T 0 | dP^T 64 | dK 128 | dV 256 | dQ^T 384 (64) = P^T 384 | dS^T 416 | K bf16 448 (64)
   const uint32_t tS = tmem, tP = tmem + 64, tDK = tmem + 128, tDV = tmem + 256, tDQ = tmem + 384;
-  const uint32_t tPT = tmem + (kDQ ? 448 : 384), tDST = tmem + (kDQ ? 480 : 416), tK = tmem + 448;
+  const uint32_t tPT = tmem + (kDQ && !kKT ? 448 : 384), tDST = tmem + (kDQ && !kKT ? 480 : 416), tK = tmem + 448;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -940,7 +944,7 @@ __global__ void __launch_bounds__(kDQ ? kBwdThreads : 320, 1)
       const uint32_t sK = smem_u32(smem + L::kOffK), sV = smem_u32(smem + L::kOffV);
       const uint32_t sDS = smem_u32(smem + L::kOffDS);
       mbar_wait(kv_full, 0);
-      if constexpr (!kDQ) mbar_wait(k_tm, 0);
+      if constexpr (kKT) mbar_wait(k_tm, 0);
       auto grads = [&](int j) {
         const int s = j % NS;
         mbar_wait(p_full, j & 1);
@@ -973,7 +977,7 @@ __global__ void __launch_bounds__(kDQ ? kBwdThreads : 320, 1)
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const int c = k / 4, kk = k % 4;
-          if constexpr (kDQ)
+          if constexpr (!kKT)
             tc_mma_bf16(tS, make_sw128_desc(sK + c * kBwdKeys * 128 + kk * 32, 16, 1024),
                         make_sw128_desc(sQ + c * kBwdQ * 128 + kk * 32, 16, 1024), id_s, k > 0 ? 1u : 0u);
           else  // A = K from TMEM (16 head dims = 8 columns)
@@ -1027,7 +1031,7 @@ __global__ void __launch_bounds__(kDQ ? kBwdThreads : 320, 1)
     const int r = quad * 32 + lane;  // key row
     const uint32_t lo = static_cast<uint32_t>(quad * 32) << 16;
     const int key = k0 + r;
-    if constexpr (!kDQ) {  // K row of this key into TMEM (this warp's 64 head dims): the S^T A operand
+    if constexpr (kKT) {  // K row of this key into TMEM (this warp's 64 head dims): the S^T A operand
       const uint4* src = reinterpret_cast<const uint4*>(kg + static_cast<int64_t>(key) * ld_k + h * D + half * 64);
       uint32_t kr[32];
 #pragma unroll
@@ -1094,6 +1098,7 @@ __global__ void __launch_bounds__(kDQ ? kBwdThreads : 320, 1)
       }
       if (tr) trace[i * 8 + 4] = clock64();
       if (i >= 1) mbar_wait(p_free, (i - 1) & 1);  // gradient MMAs of tile i-1 released P^T / dS^T
+      if (kDQ && kKT && i >= 1) mbar_wait(dq_free, (i - 1) & 1);  // dQ^T of tile i-1 drained (shared columns)
       if (tr) trace[i * 8 + 5] = clock64();
       // P^T, dS^T (bf16 pairs) into TMEM: the A operands of dV / dK; dS^T also into shared
       // memory (SW128) as the B operand of dQ^T
@@ -1410,7 +1415,7 @@ cudaError_t attention_bwd_split_tc(const AttnTensors& t, const __nv_bfloat16* do
   using Q = DqCfg;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_bwd_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_tc_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(attn_bwd_dq_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::kBytes);
     if (e != cudaSuccess) return e;
@@ -1426,7 +1431,7 @@ cudaError_t attention_bwd_split_tc(const AttnTensors& t, const __nv_bfloat16* do
   const float scale = 1.0f / sqrtf(128.0f);
   const int dbg = std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0;
   AttnPush kv_push = t.push;  // dK / dV rows
-  attn_bwd_tc_kernel<false><<<dim3(t.S / kBwdKeys, t.heads), 320, L::kBytes, st>>>(
+  attn_bwd_tc_kernel<false, true><<<dim3(t.S / kBwdKeys, t.heads), 320, L::kBytes, st>>>(
       mq, mk, mv, mdo, t.lse, delta, nullptr, dk, dv, ld_d, t.S, scale, dbg, g_attn_trace, kv_push, t.k, t.ld_qkv);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -1453,7 +1458,9 @@ cudaError_t attention_bwd_tc(const AttnTensors& t, const __nv_bfloat16* dout, in
   using L = BwdSmem;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_bwd_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_tc_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(attn_bwd_tc_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -1463,7 +1470,10 @@ cudaError_t attention_bwd_tc(const AttnTensors& t, const __nv_bfloat16* dout, in
       !map2d(&mv, t.v, t.S, cols, t.ld_qkv, kBwdKeys) || !map2d(&mdo, dout, t.S, cols, ld_dout, kBwdQ))
     return cudaErrorInvalidValue;
   const float scale = 1.0f / sqrtf(128.0f);
-  attn_bwd_tc_kernel<true><<<dim3(t.S / kBwdKeys, t.heads), kBwdThreads, L::kBytes, st>>>(
+  const char* kt_env = std::getenv("SEQPLAN_ISP_BWD_KTMEM");
+  // K resident in TMEM (kKT) measured no faster (634 vs 639 TF/s at 32K): opt-in only
+  auto kern = (kt_env && std::atoi(kt_env) != 0) ? attn_bwd_tc_kernel<true, true> : attn_bwd_tc_kernel<true, false>;
+  kern<<<dim3(t.S / kBwdKeys, t.heads), kBwdThreads, L::kBytes, st>>>(
       mq, mk, mv, mdo, t.lse, delta, dq_acc, dk, dv, ld_d, t.S, scale,
       std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0, g_attn_trace, t.push, t.k,
       t.ld_qkv);
