@@ -160,6 +160,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fused-bwd", action="store_true")
+    ap.add_argument("--recompute", action="store_true", help="a = 1: activation recomputation (SURVEY.md §8f item 3)")
     return ap.parse_args()
 
 
@@ -215,6 +216,10 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # NCCL is plumbing only (IPC-handle exchange, barriers, max over ranks); keep its version
+        # banner off stdout, where the one JSON line goes
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+            os.environ["NCCL_DEBUG"] = "WARN"
         dist.init_process_group("nccl", device_id=dev)
     cfg = CONFIGS[args.config]
     H, D, S = cfg["H"], cfg["D"], cfg["S"]
@@ -222,7 +227,8 @@ def main():
     flags = capi.FLAG_FUSED_BWD if args.fused_bwd else 0
 
     def make_ctx(extra_flags=0):
-        blk = capi.IspBlock(H, D, S, world=world, rank=rank, device=local, flags=flags | extra_flags)
+        blk = capi.IspBlock(H, D, S, world=world, rank=rank, device=local, flags=flags | extra_flags,
+                            recompute=args.recompute)
         if world > 1:
             handles = [None] * world
             dist.all_gather_object(handles, blk.ipc_handle())
@@ -409,7 +415,8 @@ def main():
                                    f"SwiGLU), H={H}, heads={D}, I={mlp_dim(H)}, S={S}, b=1",
                        "parallelism": f"isp sp=ps={world}", "global_batch_tokens": S, "seq_len": S,
                        "l2": "flushed between timed steps (256 MiB write); working set > L2",
-                       "bwd_policy": "fused" if args.fused_bwd else "selective"},
+                       "bwd_policy": "fused" if args.fused_bwd else "selective",
+                       "recompute": int(args.recompute)},
             "exposed_comm_pct": None if exposed is None else 100.0 * exposed,
             "block_roofline": {"t_roof_ms": t_roof * 1e3, "bound": "tensor" if t_comp >= t_nvl else "nvlink",
                                "frac": (t_roof * 1e3) / ms, "flops": block_flops(H, S),

@@ -65,6 +65,7 @@ enum {
   SEQPLAN_ISP_FLAG_TIMELINE = 1u << 2,     /* record CUDA-event timeline                            */
   SEQPLAN_ISP_FLAG_SKIP_COMM = 1u << 3,    /* measurement only: collectives become no-ops           */
   SEQPLAN_ISP_FLAG_PROFILE = 1u << 4,      /* per-kernel CUDA events (seqplan_isp_kernel_profile)    */
+  SEQPLAN_ISP_FLAG_RECOMPUTE = 1u << 5,    /* a = 1 (Strategy::recompute) where no strategy is given */
 };
 
 /* Kernel classes of the per-kernel profile. */
@@ -215,6 +216,10 @@ int seqplan_isp_block_bwd(seqplan_isp_ctx* ctx, const void* dy, void* dx, void* 
 
 /* ---- observability ------------------------------------------------------ */
 int seqplan_isp_pool_stats(seqplan_isp_ctx* ctx, seqplan_step_stats* out);
+/* The reference's model of this pool: run_mempool(trace, policy) (mempool.hpp:285-387) over the
+ * alloc/free trace the device pool recorded (peak_* over the whole trace, the rest at its end);
+ * *n_ops receives the trace length. A stack's layers share layer 0's pool. */
+int seqplan_isp_pool_replay(seqplan_isp_ctx* ctx, seqplan_step_stats* out, int64_t* n_ops);
 /* Copies up to *n events of the last fwd/bwd pair; *n receives the count. */
 int seqplan_isp_timeline(seqplan_isp_ctx* ctx, seqplan_timeline_event* events, int64_t* n);
 

@@ -60,6 +60,7 @@ STATUS = {0: "ok", 1: "invalid argument", 2: "runtime error", 3: "out of memory"
 W_NORM1, W_QKV, W_O, W_NORM2, W_GATE, W_UP, W_DOWN = range(7)
 W_NAMES = ["norm1", "qkv", "o", "norm2", "gate", "up", "down"]
 FLAG_NO_OVERLAP, FLAG_FUSED_BWD, FLAG_TIMELINE, FLAG_SKIP_COMM, FLAG_PROFILE = 1, 2, 4, 8, 16
+FLAG_RECOMPUTE = 32  # a = 1 where no Strategy is passed (group mode)
 EV_NAMES = ["forward", "grad_input", "grad_weight", "all_gather", "reduce_scatter", "all_to_all"]
 
 
@@ -110,6 +111,7 @@ _EXTRA_SIGS = [
     ("seqplan_isp_block_fwd", c_int, [c_vp, c_vp, c_vp, c_vp]),
     ("seqplan_isp_block_bwd", c_int, [c_vp, c_vp, c_vp, c_vp]),
     ("seqplan_isp_pool_stats", c_int, [c_vp, P(StepStatsC)]),
+    ("seqplan_isp_pool_replay", c_int, [c_vp, P(StepStatsC), P(c_i64)]),
     ("seqplan_isp_timeline", c_int, [c_vp, P(EventC), P(c_i64)]),
     ("seqplan_isp_kernel_profile", c_int, [c_vp, P(KernelRecC), P(c_i64), c_int]),
     ("seqplan_isp_launch_count", c_i64, [c_vp]),
@@ -176,11 +178,11 @@ class IspBlock:
     Thin ctypes wrapper; every call goes through the C ABI of include/seqplan_isp.h.
     """
 
-    def __init__(self, H, D, S, world=1, rank=0, device=0, policy=None, flags=0, I=0):
+    def __init__(self, H, D, S, world=1, rank=0, device=0, policy=None, flags=0, I=0, recompute=False):
         l = lib()
         self.world, self.rank = world, rank
         self.shape = make_shape(H, D, S, I)
-        strat = StrategyC(1, 1, 0, 1, 1, 1, world, world, 1, 1)
+        strat = StrategyC(1, 1, int(recompute), 1, 1, 1, world, world, 1, 1)
         pol = policy if policy is not None else make_policy()
         h = c_vp()
         st = l.seqplan_isp_ctx_create(world, rank, device, ctypes.byref(self.shape), ctypes.byref(strat),
@@ -245,6 +247,15 @@ class IspBlock:
         check(lib().seqplan_isp_pool_stats(self.h, ctypes.byref(s)), self.h, "pool_stats")
         return {n: getattr(s, n) for n, _ in StepStatsC._fields_}
 
+    def pool_replay(self):
+        """run_mempool (mempool.hpp:285-387) over the device pool's own recorded trace."""
+        s = StepStatsC()
+        n = c_i64(0)
+        check(lib().seqplan_isp_pool_replay(self.h, ctypes.byref(s), ctypes.byref(n)), self.h, "pool_replay")
+        d = {k: getattr(s, k) for k, _ in StepStatsC._fields_}
+        d["trace_ops"] = n.value
+        return d
+
     def timeline(self):
         n = c_i64(0)
         lib().seqplan_isp_timeline(self.h, None, ctypes.byref(n))
@@ -280,11 +291,11 @@ class IspStack:
     layer's gathers on one comm stream; layer(l) is a non-owning IspBlock view (weights, grads,
     peer bootstrap, timeline of that layer)."""
 
-    def __init__(self, layers, H, D, S, world=1, rank=0, device=0, policy=None, flags=0, I=0):
+    def __init__(self, layers, H, D, S, world=1, rank=0, device=0, policy=None, flags=0, I=0, recompute=False):
         l = lib()
         self.world, self.rank = world, rank
         self.shape = make_shape(H, D, S, I)
-        strat = StrategyC(1, 1, 0, 1, 1, 1, world, world, 1, 1)
+        strat = StrategyC(1, 1, int(recompute), 1, 1, 1, world, world, 1, 1)
         pol = policy if policy is not None else make_policy()
         h = c_vp()
         check(l.seqplan_isp_stack_create(layers, world, rank, device, ctypes.byref(self.shape), ctypes.byref(strat),

@@ -6,8 +6,15 @@
 // request size and never released while the context lives. The policy knobs are
 // MempoolPolicy's (mempool.hpp:137-142):
 //   pinned_comm_pool : comm buffers (gathered weights) rotate through a dedicated
-//                      double buffer sized 2 x largest request, never touching the
+//                      double buffer (the first request reserves 2 slots of its size, more
+//                      slots only when every slot is busy or too small), never touching the
 //                      general pool (cost.hpp:147 other_buffers);
+//   consolidate_every_k_mlp : MLP outputs (the per-layer checkpoints of the a = 1 regime) are
+//                      packed k to a region of k x size (mempool.hpp:345-352). The reference
+//                      never returns a packed region (its consolidated_reserved grows every
+//                      step); here a region whose k slots are all free is
+//                      recycled by the next packed request of the same size. Within one step
+//                      the two agree byte for byte; across steps the device stays flat;
 //   grad_premap      : gradient shards live in one arena reserved up front;
 //   capacity         : reserved bytes above it count as OOM events.
 // Every alloc/free is recorded as a seqplan::Trace, so run_mempool(trace, policy)
@@ -20,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -57,10 +65,14 @@ public:
         bytes = round_up(bytes);
         const std::int64_t id = next_id_++;
         trace_.ops.push_back(seqplan::TraceOp::alloc(id, bytes, tag));
+        if (++size_seen_[bytes] == 2 && (threshold_ == 0 || bytes < threshold_)) threshold_ = bytes;
         void* ptr = nullptr;
         Live lv{id, bytes, tag, Where::General, 0, 0};
         if (policy_.pinned_comm_pool && tag == seqplan::AllocTag::CommBuffer) {
             ptr = pinned_alloc(bytes, stream, lv);
+        } else if (policy_.consolidate_every_k_mlp > 0 && tag == seqplan::AllocTag::MlpOutput) {
+            ptr = packed_alloc(bytes, stream, lv);
+            if (!ptr) return nullptr;
         } else if (policy_.grad_premap && tag == seqplan::AllocTag::Grad && grad_arena_) {
             if (grad_used_ + bytes > grad_arena_bytes_) return fail("grad arena exhausted");
             ptr = static_cast<char*>(grad_arena_) + grad_used_;
@@ -68,6 +80,7 @@ public:
             lv.offset = grad_used_;
             grad_used_ += bytes;
             grad_alloc_ += bytes;
+            ++grad_live_;
         } else {
             const bool fresh = pool_.alloc(id, bytes);
             const auto w = pool_.where(id);
@@ -107,7 +120,19 @@ public:
                 break;
             case Where::Grad:
                 grad_alloc_ -= lv.bytes;
+                if (--grad_live_ == 0) grad_used_ = 0;  // bump arena: rewinds when empty
                 break;
+            case Where::Packed: {
+                Region& r = regions_[lv.segment];
+                r.used[static_cast<std::size_t>(lv.offset)] = false;
+                packed_alloc_ -= lv.bytes;
+                if (!host_only_) {
+                    cudaEventRecord(r.ev, stream);
+                    r.ev_valid = true;
+                    r.last_stream = stream;
+                }
+                break;
+            }
         }
         snapshot();
     }
@@ -133,7 +158,13 @@ public:
             if (grad_arena_) cudaFree(grad_arena_);
             for (auto& e : pending_) cudaEventDestroy(e.ev);
             for (auto& s : pinned_slots_) if (s.ev) cudaEventDestroy(s.ev);
+            for (auto& r : regions_) {
+                if (r.ptr) cudaFree(r.ptr);
+                if (r.ev) cudaEventDestroy(r.ev);
+            }
         }
+        regions_.clear();
+        open_ = -1;
         segments_.clear();
         pinned_slots_.clear();
         pending_.clear();
@@ -141,7 +172,7 @@ public:
     }
 
 private:
-    enum class Where { General, Pinned, Grad };
+    enum class Where { General, Pinned, Grad, Packed };
     struct Live {
         std::int64_t id, bytes;
         seqplan::AllocTag tag;
@@ -159,6 +190,16 @@ private:
         void* ptr = nullptr;
         std::int64_t bytes = 0;
         bool busy = false;
+        cudaStream_t last_stream = nullptr;
+        cudaEvent_t ev = nullptr;
+        bool ev_valid = false;
+    };
+
+    struct Region {  // consolidated MLP-output region: k slots of `slot` bytes
+        void* ptr = nullptr;
+        std::int64_t slot = 0;
+        std::vector<bool> used;
+        std::int64_t handed_out = 0;  // slots ever handed out (the reference's packed_slots)
         cudaStream_t last_stream = nullptr;
         cudaEvent_t ev = nullptr;
         bool ev_valid = false;
@@ -194,12 +235,67 @@ private:
             slot->bytes = bytes;
             if (!host_only_) cudaEventCreateWithFlags(&slot->ev, cudaEventDisableTiming);
             pinned_reserved_ += bytes;
+            if (pinned_slots_.size() == 1) {  // the first request reserves the double buffer (2 x size)
+                PinnedSlot twin{};
+                if (!reserve_raw(bytes, &twin.ptr)) return fail("pinned comm slot allocation failed");
+                twin.bytes = bytes;
+                if (!host_only_) cudaEventCreateWithFlags(&twin.ev, cudaEventDisableTiming);
+                pinned_reserved_ += bytes;
+                pinned_slots_.push_back(twin);
+                slot = &pinned_slots_.front();
+            }
         }
         slot->busy = true;
         if (!host_only_ && slot->ev_valid && slot->last_stream != stream) cudaStreamWaitEvent(stream, slot->ev, 0);
         pinned_alloc_ += bytes;
         lv.offset = static_cast<std::int64_t>(slot - pinned_slots_.data());
         return slot->ptr;
+    }
+
+    // Consolidation: the open region (slots never handed out yet) first, as the reference fills
+    // it; then any fully idle region of the same slot size (recycled); else a new k-slot region.
+    void* packed_alloc(std::int64_t bytes, cudaStream_t stream, Live& lv) {
+        const std::int64_t k = policy_.consolidate_every_k_mlp;
+        Region* reg = nullptr;
+        std::size_t slot = 0;
+        if (open_ >= 0 && regions_[static_cast<std::size_t>(open_)].slot == bytes &&
+            regions_[static_cast<std::size_t>(open_)].handed_out < k) {
+            reg = &regions_[static_cast<std::size_t>(open_)];
+            slot = static_cast<std::size_t>(reg->handed_out++);
+        }
+        if (!reg) {
+            for (auto& r : regions_) {
+                bool idle = r.slot == bytes;
+                for (bool u : r.used) idle = idle && !u;
+                if (idle && r.handed_out >= k) {
+                    reg = &r;
+                    r.handed_out = 1;  // the region reopens; slot 0 first, as when it was new
+                    slot = 0;
+                    break;
+                }
+            }
+        }
+        if (!reg) {
+            regions_.push_back(Region{});
+            reg = &regions_.back();
+            if (!reserve_raw(k * bytes, &reg->ptr)) {
+                regions_.pop_back();
+                return fail("consolidated region allocation failed");
+            }
+            reg->slot = bytes;
+            reg->used.assign(static_cast<std::size_t>(k), false);
+            reg->handed_out = 1;
+            if (!host_only_) cudaEventCreateWithFlags(&reg->ev, cudaEventDisableTiming);
+            packed_reserved_ += k * bytes;
+        }
+        open_ = reg - regions_.data();
+        reg->used[slot] = true;
+        if (!host_only_ && reg->ev_valid && reg->last_stream != stream) cudaStreamWaitEvent(stream, reg->ev, 0);
+        packed_alloc_ += bytes;
+        lv.where = Where::Packed;
+        lv.segment = static_cast<std::size_t>(reg - regions_.data());
+        lv.offset = static_cast<std::int64_t>(slot);
+        return static_cast<char*>(reg->ptr) + static_cast<std::int64_t>(slot) * bytes;
     }
 
     void record_pinned_release(const Live& lv, cudaStream_t stream) {
@@ -238,14 +334,15 @@ private:
 
     Stats snapshot() {
         std::int64_t cached = 0, frag = 0;
-        const std::int64_t threshold = trace_.smallest_recurring_request();
+        const std::int64_t threshold = threshold_;  // == trace_.smallest_recurring_request(), kept incrementally
         pool_.free_space(threshold, cached, frag);
         Stats& s = stats_;
         const std::int64_t pinned_res = pinned_reserved_;
         const std::int64_t grad_res = grad_arena_bytes_;
-        s.reserved = pool_.reserved() + pinned_res + grad_res;
-        s.allocated = pool_.allocated() + pinned_alloc_ + grad_alloc_;
-        s.free_cached = cached + (pinned_res - pinned_alloc_) + (grad_res - grad_alloc_);
+        s.reserved = pool_.reserved() + pinned_res + grad_res + packed_reserved_;
+        s.allocated = pool_.allocated() + pinned_alloc_ + grad_alloc_ + packed_alloc_;
+        s.free_cached = cached + (pinned_res - pinned_alloc_) + (grad_res - grad_alloc_) +
+                        (packed_reserved_ - packed_alloc_);
         s.fragmented = frag;
         s.peak_reserved = std::max(s.peak_reserved, s.reserved);
         s.peak_fragmented = std::max(s.peak_fragmented, s.fragmented);
@@ -258,13 +355,18 @@ private:
     seqplan::Trace trace_;
     std::vector<void*> segments_;
     std::vector<PinnedSlot> pinned_slots_;
+    std::vector<Region> regions_;
+    std::map<std::int64_t, int> size_seen_;
+    std::int64_t threshold_ = 0;
+    std::ptrdiff_t open_ = -1;  // the region packed requests currently fill
+    std::int64_t packed_reserved_ = 0, packed_alloc_ = 0;
     std::vector<Pending> pending_;
     std::unordered_map<void*, Live> live_;
     std::vector<Stats> per_step_;
     Stats stats_;
     std::string error_;
     void* grad_arena_ = nullptr;
-    std::int64_t grad_arena_bytes_ = 0, grad_used_ = 0, grad_alloc_ = 0;
+    std::int64_t grad_arena_bytes_ = 0, grad_used_ = 0, grad_alloc_ = 0, grad_live_ = 0;
     std::int64_t pinned_reserved_ = 0, pinned_alloc_ = 0;
     std::int64_t next_id_ = 0;
     std::int64_t host_cursor_ = 0;

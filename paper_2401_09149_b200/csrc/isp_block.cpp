@@ -146,7 +146,13 @@ struct seqplan_isp_ctx {
   uint32_t* error_flag = nullptr;  // device, in the heap flags page
 
   // ---- device pool (subsystem 5) and persistent buffers ----
-  DevicePool pool;
+  DevicePool own_pool;
+  DevicePool* pool = &own_pool;  // a stack's layers share layer 0's pool
+  bool owns_pool = true;
+  bool recompute = false;        // a = 1: only the block input survives the forward
+  bool recomputing = false;      // inside the backward's forward recomputation
+  bool acts_live = false;        // saved activations currently allocated
+  bool scratch_live = false;     // backward scratch currently allocated
   float* master[SEQPLAN_W_COUNT] = {};
   float* grad[SEQPLAN_W_COUNT] = {};
   float* adam_m[SEQPLAN_W_COUNT] = {};  // optimizer moments (seqplan_isp_adamw_step), lazily created
@@ -235,8 +241,8 @@ namespace {
 using Ctx = seqplan_isp_ctx;
 
 void* pool_alloc(Ctx* c, int64_t bytes, seqplan::AllocTag tag, cudaStream_t st) {
-  void* p = c->pool.alloc(bytes, tag, st);
-  if (!p) throw IspError(SEQPLAN_ISP_ERR_OOM, "device pool: " + c->pool.error());
+  void* p = c->pool->alloc(bytes, tag, st);
+  if (!p) throw IspError(SEQPLAN_ISP_ERR_OOM, "device pool: " + c->pool->error());
   return p;
 }
 
@@ -403,7 +409,7 @@ void release_weight(Ctx* c, int t, cudaStream_t st) {
     c->gathered[t] = nullptr;
     return;
   }
-  if (c->world > 1 && c->gathered[t]) c->pool.free(c->gathered[t], st);
+  if (c->world > 1 && c->gathered[t]) c->pool->free(c->gathered[t], st);
   c->gathered[t] = nullptr;
 }
 
@@ -744,7 +750,7 @@ void fwd_phase3(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
     g.resid = x; g.ldr = H;
     gemm(c, {c->o_tok, H, false}, {c->gathered[SEQPLAN_W_O], H, false}, g, EPI_BF16_RESID, st);
   }
-  release_weight(c, SEQPLAN_W_O, st);
+  if (!c->recomputing) release_weight(c, SEQPLAN_W_O, st);
   wait_gathered(c, SEQPLAN_W_NORM2, st);
   ISP_LAUNCH(1, rmsnorm_fwd(c->h, c->gathered[SEQPLAN_W_NORM2], c->n2, c->rstd2, T, H, c->eps, st, c->num_sms));
   c->gu = static_cast<bf16*>(pool_alloc(c, int64_t(T) * 2 * I * 2, seqplan::AllocTag::MlpIntermediate, st));
@@ -757,6 +763,8 @@ void fwd_phase3(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
     g.out2 = c->a; g.ldo2 = I;
     gemm(c, {c->n2, H, false}, {c->gathered[SEQPLAN_W_GATE], H, false}, g, EPI_SWIGLU, st);
   }
+  // recomputation (a = 1) stops here: y is not needed again and the weights stay for the backward
+  if (c->recomputing) return;
   release_weight(c, SEQPLAN_W_GATE, st);
   wait_gathered(c, SEQPLAN_W_DOWN, st);
   {
@@ -776,14 +784,17 @@ void fwd_phase3(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
 // backward phases
 // ---------------------------------------------------------------------------------
 void bwd_issue_gathers(Ctx* c, cudaStream_t st) {
-  const int order[] = {SEQPLAN_W_DOWN, SEQPLAN_W_GATE, SEQPLAN_W_NORM2, SEQPLAN_W_O, SEQPLAN_W_QKV, SEQPLAN_W_NORM1};
+  // a = 1: the recomputed forward consumes the re-gathered weights first, in forward order
+  const int bwd_order[] = {SEQPLAN_W_DOWN, SEQPLAN_W_GATE, SEQPLAN_W_NORM2, SEQPLAN_W_O, SEQPLAN_W_QKV, SEQPLAN_W_NORM1};
+  const int rec_order[] = {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN};
+  const int* order = c->recompute ? rec_order : bwd_order;
   if (c->world == 1) {
-    for (int t : order) gather_weight(c, t, st);
+    for (int i = 0; i < 6; ++i) gather_weight(c, order[i], st);
     return;
   }
   if (c->push_mode()) {  // pushed at the start of the step (fwd_issue_gathers)
     c->gather_set = 1;
-    for (int t : order) c->gathered[t] = c->hp<bf16>(c->off_gath[1][t]);
+    for (int i = 0; i < 6; ++i) c->gathered[order[i]] = c->hp<bf16>(c->off_gath[1][order[i]]);
     return;
   }
   cudaStream_t cs = c->group_mode ? st : c->comm;
@@ -795,7 +806,7 @@ void bwd_issue_gathers(Ctx* c, cudaStream_t st) {
     gather_pipelined(c, order, 6, cs);
     return;
   }
-  for (int t : order) gather_weight(c, t, cs);
+  for (int i = 0; i < 6; ++i) gather_weight(c, order[i], cs);
 }
 
 // Weight-gradient destination: fp32 grad shard directly at p = 1, bf16 partial in the heap otherwise.
@@ -868,7 +879,7 @@ void reduce_staged(Ctx* c, int t, cudaStream_t st) {
     for (int q = 0; q < c->world; ++q) src.p[q] = stg + q * sh * esz;
     ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, sh, norm, 1.0f, 0, c->grad[t], st, c->num_sms * 4));
   }
-  c->pool.free(c->stage[t], st);
+  c->pool->free(c->stage[t], st);
   c->stage[t] = nullptr;
 }
 
@@ -903,13 +914,13 @@ void bwd_phase1(Ctx* c, const bf16* dy, cudaStream_t st) {
     gemm(c, {dy, H, false}, {c->gathered[SEQPLAN_W_DOWN], I, true}, g, EPI_BF16, st);
   }
   release_weight(c, SEQPLAN_W_DOWN, st);
-  c->pool.free(c->a, st);
+  c->pool->free(c->a, st);
   c->a = nullptr;
   // ---- SwiGLU backward ----
   bf16* dgu = static_cast<bf16*>(pool_alloc(c, int64_t(T) * 2 * I * 2, seqplan::AllocTag::MlpIntermediate, st));
   ISP_LAUNCH(1, swiglu_bwd(da, c->gu, dgu, T, I, st, c->num_sms));
-  c->pool.free(da, st);
-  c->pool.free(c->gu, st);
+  c->pool->free(da, st);
+  c->pool->free(c->gu, st);
   c->gu = nullptr;
   // ---- gate|up ----
   wait_gathered(c, SEQPLAN_W_GATE, st);
@@ -926,7 +937,7 @@ void bwd_phase1(Ctx* c, const bf16* dy, cudaStream_t st) {
     gemm(c, {dgu, 2 * I, false}, {c->gathered[SEQPLAN_W_GATE], H, true}, g, EPI_BF16, st);
   }
   release_weight(c, SEQPLAN_W_GATE, st);
-  c->pool.free(dgu, st);
+  c->pool->free(dgu, st);
   // ---- norm2 backward: dh = dy + d(norm2) ----
   wait_gathered(c, SEQPLAN_W_NORM2, st);
   float* dg2 = c->world == 1 ? c->grad[SEQPLAN_W_NORM2] : c->hp<float>(c->off_part[SEQPLAN_W_NORM2]);
@@ -1061,7 +1072,68 @@ void layout_heap(Ctx* c) {
   c->heap_bytes = off;
 }
 
-void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy* policy) {
+// Saved activations of the forward (needed by the backward) and the backward's scratch.
+// a = 0: allocated once at setup and kept. a = 1 (activation recomputation, SURVEY.md §8f
+// item 3; cost.hpp:139 (34 - 32a)): allocated at the start of each pass and freed at its end, so
+// between passes only the block input (the checkpoint) is live, and in a stack, whose layers
+// share one pool, one layer's workspace is recycled by the next.
+void alloc_acts(Ctx* c, cudaStream_t st) {
+  if (c->acts_live) return;
+  const int64_t T = c->T, H = c->H, S = c->S, Hl = c->Hl;
+  auto A = [&](int64_t bytes) { return pool_alloc(c, bytes, seqplan::AllocTag::Other, st); };
+  c->n1 = static_cast<bf16*>(A(T * H * 2));
+  c->rstd1 = static_cast<float*>(A(T * 4));
+  c->qkv_heads = c->fused_a2a ? c->hp<bf16>(c->off_qkv_heads) : static_cast<bf16*>(A(S * 3 * Hl * 2));
+  c->o_tok = c->fused_a2a ? c->hp<bf16>(c->off_o_tok) : static_cast<bf16*>(A(T * H * 2));
+  c->h = static_cast<bf16*>(A(T * H * 2));
+  c->n2 = static_cast<bf16*>(A(T * H * 2));
+  c->rstd2 = static_cast<float*>(A(T * 4));
+  c->lse = static_cast<float*>(A(c->Dl * S * 4));
+  c->acts_live = true;
+}
+
+void alloc_scratch(Ctx* c, cudaStream_t st) {
+  if (c->scratch_live) return;
+  const int64_t T = c->T, H = c->H, S = c->S, Hl = c->Hl;
+  auto A = [&](int64_t bytes) { return pool_alloc(c, bytes, seqplan::AllocTag::Other, st); };
+  c->dh = static_cast<bf16*>(A(T * H * 2));
+  c->dn = static_cast<bf16*>(A(T * H * 2));
+  c->dO_heads = c->fused_a2a ? c->hp<bf16>(c->off_dO_heads) : static_cast<bf16*>(A(S * Hl * 2));
+  c->dqkv_tok = c->fused_a2a ? c->hp<bf16>(c->off_dqkv_tok) : static_cast<bf16*>(A(T * 3 * H * 2));
+  c->delta = static_cast<float*>(A(c->Dl * S * 4));
+  c->dq_acc = static_cast<float*>(A(c->Dl * S * c->d * 4));
+  c->dg_scratch = static_cast<float*>(A(int64_t(rmsnorm_bwd_scratch_rows(c->num_sms)) * H * 4));
+  c->scratch_live = true;
+}
+
+void free_acts(Ctx* c, cudaStream_t st) {
+  if (!c->acts_live) return;
+  for (void* p : {static_cast<void*>(c->n1), static_cast<void*>(c->rstd1), static_cast<void*>(c->h),
+                  static_cast<void*>(c->n2), static_cast<void*>(c->rstd2), static_cast<void*>(c->lse)})
+    c->pool->free(p, st);
+  if (!c->fused_a2a) {
+    c->pool->free(c->qkv_heads, st);
+    c->pool->free(c->o_tok, st);
+  }
+  for (bf16* p : {c->gu, c->a})
+    if (p) c->pool->free(p, st);
+  c->gu = c->a = nullptr;
+  c->acts_live = false;
+}
+
+void free_scratch(Ctx* c, cudaStream_t st) {
+  if (!c->scratch_live) return;
+  for (void* p : {static_cast<void*>(c->dh), static_cast<void*>(c->dn), static_cast<void*>(c->delta),
+                  static_cast<void*>(c->dq_acc), static_cast<void*>(c->dg_scratch)})
+    c->pool->free(p, st);
+  if (!c->fused_a2a) {
+    c->pool->free(c->dO_heads, st);
+    c->pool->free(c->dqkv_tok, st);
+  }
+  c->scratch_live = false;
+}
+
+void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy* policy, int premap_layers) {
   c->H = shape->hidden_dim;
   c->D = shape->heads;
   c->S = shape->seq_len;
@@ -1092,7 +1164,7 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
     pol.pinned_comm_pool = true;
     pol.grad_premap = true;
   }
-  c->pool.set_policy(pol);
+  if (c->owns_pool) c->pool->set_policy(pol);
 
   // Ulysses all-to-all: SM pull kernels after the producer (default), or fused into the producers'
   // epilogues as 16-B remote stores (SEQPLAN_ISP_FUSED_A2A=1). Measured at p = 2/4: the pull is
@@ -1116,7 +1188,9 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   const cudaStream_t s0 = nullptr;
   int64_t grad_bytes = 0;
   for (int t = 0; t < SEQPLAN_W_COUNT; ++t) grad_bytes += (c->shard(t) * 4 + 511) / 512 * 512;
-  if (!c->pool.premap_grads(grad_bytes)) throw IspError(SEQPLAN_ISP_ERR_OOM, "grad arena");
+  // a stack's pool owner pre-maps the gradient arena of every layer (grad_premap)
+  if (c->owns_pool && !c->pool->premap_grads(grad_bytes * premap_layers))
+    throw IspError(SEQPLAN_ISP_ERR_OOM, "grad arena");
   for (int t = 0; t < SEQPLAN_W_COUNT; ++t) {
     c->master[t] = static_cast<float*>(pool_alloc(c, c->shard(t) * 4, seqplan::AllocTag::Other, s0));
     c->grad[t] = static_cast<float*>(pool_alloc(c, c->shard(t) * 4, seqplan::AllocTag::Grad, s0));
@@ -1129,21 +1203,11 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   };
   c->cos_t = static_cast<float*>(A(S * (c->d / 2) * 4));
   c->sin_t = static_cast<float*>(A(S * (c->d / 2) * 4));
-  c->n1 = static_cast<bf16*>(A(T * H * 2));
-  c->rstd1 = static_cast<float*>(A(T * 4));
-  c->qkv_heads = c->fused_a2a ? c->hp<bf16>(c->off_qkv_heads) : static_cast<bf16*>(A(S * 3 * Hl * 2));
-  c->o_tok = c->fused_a2a ? c->hp<bf16>(c->off_o_tok) : static_cast<bf16*>(A(T * H * 2));
-  c->h = static_cast<bf16*>(A(T * H * 2, seqplan::AllocTag::MlpOutput));
-  c->n2 = static_cast<bf16*>(A(T * H * 2));
-  c->rstd2 = static_cast<float*>(A(T * 4));
-  c->lse = static_cast<float*>(A(c->Dl * S * 4));
-  c->dh = static_cast<bf16*>(A(T * H * 2));
-  c->dn = static_cast<bf16*>(A(T * H * 2));
-  c->dO_heads = c->fused_a2a ? c->hp<bf16>(c->off_dO_heads) : static_cast<bf16*>(A(S * Hl * 2));
-  c->dqkv_tok = c->fused_a2a ? c->hp<bf16>(c->off_dqkv_tok) : static_cast<bf16*>(A(T * 3 * H * 2));
-  c->delta = static_cast<float*>(A(c->Dl * S * 4));
-  c->dq_acc = static_cast<float*>(A(c->Dl * S * c->d * 4));
-  c->dg_scratch = static_cast<float*>(A(int64_t(rmsnorm_bwd_scratch_rows(c->num_sms)) * H * 4));
+  (void)T; (void)H; (void)Hl;
+  if (!c->recompute) {  // a = 0: the forward's saved tensors and the backward scratch live in the context
+    alloc_acts(c, s0);
+    alloc_scratch(c, s0);
+  }
 
   ISP_CUDA(cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking));
   ISP_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
@@ -1176,7 +1240,7 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
     ISP_CUDA(cudaMemcpy(c->cos_t, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice));
     ISP_CUDA(cudaMemcpy(c->sin_t, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice));
   }
-  c->pool.step_boundary();
+  c->pool->step_boundary();
 }
 
 // Refresh the bf16 working shard(s) from the fp32 master of tensor t.
@@ -1241,9 +1305,19 @@ void check_device_error(Ctx* c) {
 // =====================================================================================
 extern "C" {
 
+static int create_ctx(int world, int rank, int device, const seqplan_isp_shape* shape,
+                      const seqplan_strategy* strategy, const seqplan_mempool_policy* policy, uint32_t flags,
+                      DevicePool* shared_pool, int premap_layers, seqplan_isp_ctx** out);
+
 int seqplan_isp_ctx_create(int world, int rank, int device, const seqplan_isp_shape* shape,
                            const seqplan_strategy* strategy, const seqplan_mempool_policy* policy,
                            uint32_t flags, seqplan_isp_ctx** out) {
+  return create_ctx(world, rank, device, shape, strategy, policy, flags, nullptr, 1, out);
+}
+
+static int create_ctx(int world, int rank, int device, const seqplan_isp_shape* shape,
+                      const seqplan_strategy* strategy, const seqplan_mempool_policy* policy, uint32_t flags,
+                      DevicePool* shared_pool, int premap_layers, seqplan_isp_ctx** out) {
   if (!out || !shape) return SEQPLAN_ISP_ERR_INVALID;
   *out = nullptr;
   if (rank < 0 || rank >= world) return SEQPLAN_ISP_ERR_INVALID;
@@ -1258,7 +1332,7 @@ int seqplan_isp_ctx_create(int world, int rank, int device, const seqplan_isp_sh
     m.seq_len = shape->seq_len; m.global_batch_tokens = shape->seq_len * s.micro_batch * s.micro_batch_num * s.dp;
     seqplan::ClusterConfig cl{world, world, 0};
     if (!seqplan::validate(s, m, cl).ok() || s.sp != world || s.ps != world || s.tp != 1 || s.pp != 1 ||
-        s.dp != 1 || s.recompute != 0)
+        s.dp != 1 || (s.recompute != 0 && s.recompute != 1))
       return SEQPLAN_ISP_ERR_INVALID;
   }
   Ctx* c = new Ctx();
@@ -1266,8 +1340,13 @@ int seqplan_isp_ctx_create(int world, int rank, int device, const seqplan_isp_sh
   c->rank = rank;
   c->device = device;
   c->flags = flags;
+  c->recompute = (strategy && strategy->recompute == 1) || (flags & SEQPLAN_ISP_FLAG_RECOMPUTE);
+  if (shared_pool) {
+    c->pool = shared_pool;
+    c->owns_pool = false;
+  }
   try {
-    setup(c, shape, policy);
+    setup(c, shape, policy, premap_layers);
   } catch (const IspError& e) {
     const int code = e.code;
     std::fprintf(stderr, "seqplan_isp_ctx_create: %s\n", e.msg.c_str());
@@ -1284,7 +1363,7 @@ void seqplan_isp_ctx_destroy(seqplan_isp_ctx* c) {
   cudaDeviceSynchronize();
   for (int q = 0; q < c->world; ++q)
     if (c->peer_opened[q]) cudaIpcCloseMemHandle(c->peer_heap[q]);
-  c->pool.release_all();
+  if (c->owns_pool) c->pool->release_all();  // a stack's layers free their memory with layer 0's pool
   if (c->heap) cudaFree(c->heap);
   if (c->comm && c->owns_comm) cudaStreamDestroy(c->comm);
   for (int q = 0; q < kMaxRanks; ++q) {
@@ -1497,11 +1576,13 @@ static void push_bwd_set(Ctx* c) {
 }
 
 static void fwd_body(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
+  alloc_acts(c, st);
   fwd_phase1(c, x, st);
   barrier(c, st, false);
   fwd_phase2(c, st);
   barrier(c, st, false);
   fwd_phase3(c, x, y, st);
+  if (c->recompute) free_acts(c, st);  // a = 1: only x (the checkpoint) outlives the forward
   c->fwd_done = true;
 }
 
@@ -1510,13 +1591,33 @@ static void run_fwd(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
   fwd_body(c, x, y, st);
 }
 
+// a = 1: the forward is re-run from the checkpoint x on the backward's re-gathered weights
+// (the reference's passes = 3 + a, cost.hpp:227), minus the down projection whose output y
+// the backward never reads.
+static void recompute_fwd(Ctx* c, const bf16* x, cudaStream_t st) {
+  alloc_acts(c, st);
+  c->recomputing = true;
+  fwd_phase1(c, x, st);
+  barrier(c, st, false);
+  fwd_phase2(c, st);
+  barrier(c, st, false);
+  fwd_phase3(c, x, nullptr, st);
+  c->recomputing = false;
+}
+
 static void bwd_body(Ctx* c, const bf16* x, const bf16* dy, bf16* dx, cudaStream_t st) {
   bwd_issue_gathers(c, st);
+  if (c->recompute) recompute_fwd(c, x, st);
+  alloc_scratch(c, st);
   bwd_phase1(c, dy, st);
   barrier(c, st, false);
   bwd_phase2(c, st);
   barrier(c, st, false);
   bwd_phase3(c, x, dx, st);
+  if (c->recompute) {
+    free_acts(c, st);
+    free_scratch(c, st);
+  }
 }
 
 // Gradient reductions of the step and the join with the comm stream.
@@ -1536,7 +1637,7 @@ static void bwd_epilogue(Ctx* c, cudaStream_t st) {
     ISP_CUDA(cudaEventRecord(c->ev_comm_done, c->comm));
     ISP_CUDA(cudaStreamWaitEvent(st, c->ev_comm_done, 0));
   }
-  c->pool.step_boundary();
+  if (c->owns_pool) c->pool->step_boundary();
   if (c->push_mode()) c->push_primed = true;
 }
 
@@ -1590,10 +1691,12 @@ int seqplan_isp_group_fwd(seqplan_isp_ctx** cs, int world, const void* const* x,
       cs[r]->weights_dirty = false;
       fwd_issue_gathers(cs[r], st);
     }
+    for (int r = 0; r < world; ++r) alloc_acts(cs[r], st);
     for (int r = 0; r < world; ++r) fwd_phase1(cs[r], static_cast<const bf16*>(x[r]), st);
     for (int r = 0; r < world; ++r) fwd_phase2(cs[r], st);
     for (int r = 0; r < world; ++r) {
       fwd_phase3(cs[r], static_cast<const bf16*>(x[r]), static_cast<bf16*>(y[r]), st);
+      if (cs[r]->recompute) free_acts(cs[r], st);
       cs[r]->fwd_done = true;
       cs[r]->last_x = x[r];
     }
@@ -1611,13 +1714,30 @@ int seqplan_isp_group_bwd(seqplan_isp_ctx** cs, int world, const void* const* dy
     for (int r = 0; r < world; ++r)
       if (!cs[r]->fwd_done) throw IspError(SEQPLAN_ISP_ERR_INVALID, "group_bwd without group_fwd");
     for (int r = 0; r < world; ++r) bwd_issue_gathers(cs[r], st);
+    if (cs[0]->recompute) {  // a = 1: every rank's forward again, in lock-step
+      for (int r = 0; r < world; ++r) {
+        alloc_acts(cs[r], st);
+        cs[r]->recomputing = true;
+      }
+      for (int r = 0; r < world; ++r) fwd_phase1(cs[r], static_cast<const bf16*>(cs[r]->last_x), st);
+      for (int r = 0; r < world; ++r) fwd_phase2(cs[r], st);
+      for (int r = 0; r < world; ++r) {
+        fwd_phase3(cs[r], static_cast<const bf16*>(cs[r]->last_x), nullptr, st);
+        cs[r]->recomputing = false;
+      }
+    }
+    for (int r = 0; r < world; ++r) alloc_scratch(cs[r], st);
     for (int r = 0; r < world; ++r) bwd_phase1(cs[r], static_cast<const bf16*>(dy[r]), st);
     for (int r = 0; r < world; ++r) bwd_phase2(cs[r], st);
     for (int r = 0; r < world; ++r)
       bwd_phase3(cs[r], static_cast<const bf16*>(cs[r]->last_x), static_cast<bf16*>(dx[r]), st);
     for (int r = 0; r < world; ++r) {
       bwd_reduce_all(cs[r], st);
-      cs[r]->pool.step_boundary();
+      if (cs[r]->recompute) {
+        free_acts(cs[r], st);
+        free_scratch(cs[r], st);
+      }
+      cs[r]->pool->step_boundary();
       cs[r]->fwd_done = false;
     }
     if (cs[0]->flags & (SEQPLAN_ISP_FLAG_TIMELINE | SEQPLAN_ISP_FLAG_PROFILE)) {
@@ -1650,8 +1770,12 @@ int64_t seqplan_isp_launch_count(const seqplan_isp_ctx* c) { return c ? c->launc
 // ---- multi-layer stacks ------------------------------------------
 struct seqplan_isp_stack {
   std::vector<Ctx*> layers;
-  std::vector<bf16*> act;   // layer boundaries: act[l] = input of layer l (l >= 1), [T, H] bf16
-  std::vector<bf16*> grad;  // dx of layer l = dy of layer l-1
+  // layer boundaries, [T, H] bf16 from the shared pool: act[l] = input of layer l (l >= 1), the
+  // checkpoint kept from the forward to layer l's backward (AllocTag::MlpOutput, packed k to a
+  // region under consolidate_every_k_mlp, mempool.hpp:345-352); grad[l] = dx of layer l = dy of
+  // layer l-1, live from layer l's backward to layer l-1's
+  std::vector<bf16*> act;
+  std::vector<bf16*> grad;
   const void* x0 = nullptr;
   bool fwd_done = false;
 };
@@ -1664,7 +1788,10 @@ int seqplan_isp_stack_create(int layers, int world, int rank, int device, const 
   auto* s = new seqplan_isp_stack();
   for (int l = 0; l < layers; ++l) {
     Ctx* c = nullptr;
-    const int st = seqplan_isp_ctx_create(world, rank, device, shape, strategy, policy, flags, &c);
+    // one device pool for the stack (layer 0's): checkpoints, a = 1 workspaces and the gradient
+    // arena of every layer (pre-mapped by the owner) share it, as in the reference's trace
+    DevicePool* shared = l == 0 ? nullptr : s->layers[0]->pool;
+    const int st = create_ctx(world, rank, device, shape, strategy, policy, flags, shared, l == 0 ? layers : 1, &c);
     if (st != SEQPLAN_ISP_OK) {
       seqplan_isp_stack_destroy(s);
       return st;
@@ -1682,14 +1809,8 @@ int seqplan_isp_stack_create(int layers, int world, int rank, int device, const 
       c->comm = c0->comm;
       c->owns_comm = false;
     }
-    const size_t bytes = size_t(c0->T) * c0->H * 2;
-    for (int l = 0; l < layers; ++l) {
-      bf16 *a = nullptr, *g = nullptr;
-      if (l > 0) ISP_CUDA(cudaMalloc(&a, bytes));
-      if (l > 0) ISP_CUDA(cudaMalloc(&g, bytes));
-      s->act.push_back(a);
-      s->grad.push_back(g);
-    }
+    s->act.assign(size_t(layers), nullptr);
+    s->grad.assign(size_t(layers), nullptr);
   } catch (const IspError& e) {
     std::fprintf(stderr, "seqplan_isp_stack_create: %s\n", e.msg.c_str());
     seqplan_isp_stack_destroy(s);
@@ -1703,10 +1824,6 @@ void seqplan_isp_stack_destroy(seqplan_isp_stack* s) {
   if (!s) return;
   if (!s->layers.empty()) cudaSetDevice(s->layers[0]->device);
   cudaDeviceSynchronize();
-  for (bf16* p : s->act)
-    if (p) cudaFree(p);
-  for (bf16* p : s->grad)
-    if (p) cudaFree(p);
   for (size_t l = s->layers.size(); l-- > 0;) seqplan_isp_ctx_destroy(s->layers[l]);  // layer 0 (comm owner) last
   delete s;
 }
@@ -1735,9 +1852,12 @@ int seqplan_isp_stack_fwd(seqplan_isp_stack* s, const void* x, void* y, void* st
       fwd_prologue(cur, st, l == 0, true);  // one write-after-read barrier covers every layer
     }
     for (int l = L; l-- > 0;) push_bwd_set(s->layers[size_t(l)]);
+    const int64_t bytes = s->layers[0]->T * s->layers[0]->H * 2;
     for (int l = 0; l < L; ++l) {
       cur = s->layers[size_t(l)];
       const bf16* in = l == 0 ? static_cast<const bf16*>(x) : s->act[size_t(l)];
+      if (l < L - 1 && !s->act[size_t(l + 1)])
+        s->act[size_t(l + 1)] = static_cast<bf16*>(pool_alloc(cur, bytes, seqplan::AllocTag::MlpOutput, st));
       bf16* outp = l == L - 1 ? static_cast<bf16*>(y) : s->act[size_t(l + 1)];
       fwd_body(cur, in, outp, st);
       cur->last_x = in;
@@ -1759,12 +1879,22 @@ int seqplan_isp_stack_bwd(seqplan_isp_stack* s, const void* dy, void* dx, void* 
   try {
     ISP_CUDA(cudaSetDevice(cur->device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t bytes = s->layers[0]->T * s->layers[0]->H * 2;
     for (int l = L; l-- > 0;) {
       cur = s->layers[size_t(l)];
       const bf16* g_in = l == L - 1 ? static_cast<const bf16*>(dy) : s->grad[size_t(l + 1)];
+      if (l > 0) s->grad[size_t(l)] = static_cast<bf16*>(pool_alloc(cur, bytes, seqplan::AllocTag::Other, st));
       bf16* g_out = l == 0 ? static_cast<bf16*>(dx) : s->grad[size_t(l)];
       bwd_body(cur, static_cast<const bf16*>(cur->last_x), g_in, g_out, st);
       cur->fwd_done = false;
+      if (l > 0) {  // the checkpoint of layer l is consumed
+        cur->pool->free(s->act[size_t(l)], st);
+        s->act[size_t(l)] = nullptr;
+      }
+      if (l < L - 1) {
+        cur->pool->free(s->grad[size_t(l + 1)], st);
+        s->grad[size_t(l + 1)] = nullptr;
+      }
     }
     for (int l = L; l-- > 0;) {
       cur = s->layers[size_t(l)];
@@ -1817,7 +1947,7 @@ int seqplan_isp_debug_gather_bench(seqplan_isp_ctx* c, int iters, int both_sets,
 
 int seqplan_isp_pool_stats(seqplan_isp_ctx* c, seqplan_step_stats* out) {
   if (!c || !out) return SEQPLAN_ISP_ERR_INVALID;
-  const auto s = c->pool.stats();
+  const auto s = c->pool->stats();
   out->reserved = s.reserved;
   out->allocated = s.allocated;
   out->free_cached = s.free_cached;
@@ -1825,6 +1955,26 @@ int seqplan_isp_pool_stats(seqplan_isp_ctx* c, seqplan_step_stats* out) {
   out->peak_reserved = s.peak_reserved;
   out->peak_fragmented = s.peak_fragmented;
   out->peak_allocated = s.peak_allocated;
+  return SEQPLAN_ISP_OK;
+}
+
+int seqplan_isp_pool_replay(seqplan_isp_ctx* c, seqplan_step_stats* out, int64_t* n_ops) {
+  if (!c || !out) return SEQPLAN_ISP_ERR_INVALID;
+  try {
+    const seqplan::FragmentationReport r = c->pool->replay();
+    const seqplan::StepStats last = r.per_step.empty() ? seqplan::StepStats{} : r.per_step.back();
+    out->reserved = last.reserved;
+    out->allocated = last.allocated;
+    out->free_cached = last.free_cached;
+    out->fragmented = last.fragmented;
+    out->peak_reserved = r.peak_reserved;
+    out->peak_fragmented = r.peak_fragmented;
+    out->peak_allocated = 0;
+    if (n_ops) *n_ops = static_cast<int64_t>(c->pool->trace().ops.size());
+  } catch (const std::exception& e) {
+    c->last_error = e.what();
+    return SEQPLAN_ISP_ERR_INVALID;
+  }
   return SEQPLAN_ISP_OK;
 }
 

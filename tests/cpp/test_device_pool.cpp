@@ -3,6 +3,7 @@
 // the pool's own recorded trace (mempool.hpp:285-387), for every policy combination.
 #include <cstdio>
 #include <random>
+#include <unordered_map>
 #include <vector>
 
 #include "../../paper_2401_09149_b200/csrc/device_pool.h"
@@ -49,6 +50,50 @@ int main() {
             for (const auto& st : rep.per_step)
                 if (st.reserved != st.allocated + st.free_cached + st.fragmented) ++failures;
         }
+    }
+    // The a = 1 trace of the reference (synthesize_trace) fed op by op to the device pool, under
+    // every policy incl. consolidate-every-3 and grad pre-map: one step reserves exactly what
+    // run_mempool reserves; over 3 steps the device recycles its packed regions (flat), while the
+    // reference's consolidated_reserved grows.
+    {
+      for (int cfg = 0; cfg < 2; ++cfg) {  // 7B-32K L32 and 20B-128K L60 at p = 8
+        seqplan::ModelConfig m;
+        m.hidden_dim = cfg ? 5120 : 4096; m.layers = cfg ? 60 : 32; m.heads = cfg ? 40 : 32; m.vocab = 1;
+        m.seq_len = cfg ? 131072 : 32768; m.global_batch_tokens = m.seq_len; m.bytes_per_element = 2;
+        seqplan::ClusterConfig cl;
+        cl.total_gpus = 8; cl.gpus_per_node = 8; cl.gpu_memory_capacity = std::int64_t(180) << 30;
+        for (int steps : {1, 3}) {
+            seqplan::Strategy s;
+            s.micro_batch_num = steps; s.recompute = 1; s.sp = 8; s.ps = 8;
+            m.global_batch_tokens = m.seq_len * steps;
+            const seqplan::Trace tr = seqplan::synthesize_trace(m, s, cl);
+            for (int pol_i = 0; pol_i < 8; ++pol_i) {
+                seqplan::MempoolPolicy pol;
+                pol.pinned_comm_pool = pol_i & 1;
+                pol.consolidate_every_k_mlp = (pol_i & 2) ? 3 : 0;
+                pol.grad_premap = pol_i & 4;
+                isp::DevicePool pool;
+                pool.set_host_only(true);
+                pool.set_policy(pol);
+                if (pol.grad_premap) pool.premap_grads(seqplan::run_mempool(tr, pol).per_step.empty() ? 0 :
+                                                       m.seq_len / 8 * m.hidden_dim * 2);
+                std::unordered_map<std::int64_t, void*> ptr;
+                for (const auto& op : tr.ops) {
+                    if (op.kind == seqplan::TraceOp::Kind::Alloc) ptr[op.id] = pool.alloc(op.size, op.tag, nullptr);
+                    else if (op.kind == seqplan::TraceOp::Kind::Free) pool.free(ptr[op.id], nullptr);
+                    else pool.step_boundary();
+                }
+                const auto rep = seqplan::run_mempool(tr, pol);
+                const std::int64_t dev = pool.stats().peak_reserved, ref = rep.peak_reserved;
+                const bool ok = steps == 1 ? dev == ref : (dev <= ref && (pol.consolidate_every_k_mlp ? dev < ref : dev == ref));
+                if (!ok) {
+                    std::printf("synth trace steps %d policy %d: device peak %lld reference %lld\n", steps, pol_i,
+                                (long long)dev, (long long)ref);
+                    ++failures;
+                }
+            }
+        }
+      }
     }
     std::printf("device pool vs run_mempool: %s\n", failures ? "FAIL" : "ok");
     return failures ? 1 : 0;

@@ -26,6 +26,7 @@ def bf16(a):
 
 def main():
     H, D, S, L = (int(v) for v in sys.argv[1:5])
+    recompute = len(sys.argv) > 5 and sys.argv[5] == "recompute"
     world, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -36,7 +37,9 @@ def main():
     x = torch.from_numpy(ob.make_activation(sh, ob.TID_X)).bfloat16()
     dy = torch.from_numpy(ob.make_activation(sh, ob.TID_DY)).bfloat16()
     T = S // world
-    st = capi.IspStack(L, H, D, S, world=world, rank=rank, device=local, flags=capi.FLAG_TIMELINE)
+    pol = capi.make_policy(consolidate=2) if recompute else None
+    st = capi.IspStack(L, H, D, S, world=world, rank=rank, device=local, flags=capi.FLAG_TIMELINE,
+                       recompute=recompute, policy=pol)
     for l in range(L):
         blk = st.layer(l)
         bootstrap_peers(blk, world)

@@ -218,3 +218,110 @@ def test_stack_two_layers_p1(cuda, H, D, S):
             e = rel(st.layer(l).grad_shard(t), g_ref[l][t].reshape(-1))
             assert e <= TOL, (l, capi.W_NAMES[t], e)
     st.close()
+
+
+def stack_oracle_n(sh, ws, x, dy):
+    """The oracle block chained len(ws) times, with the GPU's bf16 rounding at layer boundaries."""
+    def bf16(a):
+        return torch.from_numpy(np.ascontiguousarray(a, np.float32)).bfloat16().float().numpy()
+    xs = [x]
+    for w in ws:
+        yl, _, _ = ob.block(sh, w, xs[-1], np.zeros_like(xs[-1]), p=1)
+        xs.append(bf16(yl))
+    g_in, grads = dy, [None] * len(ws)
+    for l in reversed(range(len(ws))):
+        _, dxl, g = ob.block(sh, ws[l], xs[l], g_in, p=1)
+        grads[l] = g
+        g_in = bf16(dxl)
+    return yl, dxl, grads
+
+
+@pytest.mark.parametrize("H,D,S", [(512, 8, 1024), (1024, 8, 512)])
+def test_block_recompute_p1(cuda, H, D, S):
+    """Activation recomputation (a = 1; cost.hpp:139, 227): only the block
+    input survives the forward, the backward re-runs the forward on the re-gathered weights.
+    Same results as the oracle; far fewer bytes live between the passes than at a = 0."""
+    sh, w, x, dy, y_ref, dx_ref, g_ref = oracle_case(H, D, S)
+    xd = torch.from_numpy(x).bfloat16().to(cuda)
+    dyd = torch.from_numpy(dy).bfloat16().to(cuda)
+    live = {}
+    for a in (0, 1):
+        blk = capi.IspBlock(H, D, S, world=1, recompute=bool(a))
+        load_weights(blk, w, 1, 0)
+        y, dx = torch.empty_like(xd), torch.empty_like(xd)
+        for _ in range(2):
+            blk.fwd(xd, y)
+            torch.cuda.synchronize()
+            live[a] = blk.pool_stats()["allocated"]
+            blk.bwd(dyd, dx)
+        torch.cuda.synchronize()
+        assert rel(y.float().cpu(), y_ref) <= TOL
+        assert rel(dx.float().cpu(), dx_ref) <= TOL
+        check_grads([blk], g_ref, 1)
+        blk.close()
+    T = S
+    saved = T * H * 2 * 5 + S * 3 * H * 2  # n1, o, h, n2, a|gu (>= 1 of them), qkv heads
+    assert live[0] - live[1] >= saved, live
+
+
+@pytest.mark.parametrize("p", [2, 4])
+def test_block_group_recompute(cuda, p):
+    """a = 1 in group mode (p ranks on one GPU): the recomputed forward repeats both all-to-alls."""
+    H, D, S = 1024, 8, 1024
+    sh, w, x, dy, y_ref, dx_ref, g_ref = oracle_case(H, D, S)
+    grp = capi.IspGroup(H, D, S, world=p, flags=capi.FLAG_RECOMPUTE)
+    blocks = [grp.rank(r) for r in range(p)]
+    T = S // p
+    for r, b in enumerate(blocks):
+        load_weights(b, w, p, r)
+    xs = [torch.from_numpy(x[r * T:(r + 1) * T]).bfloat16().to(cuda) for r in range(p)]
+    dys = [torch.from_numpy(dy[r * T:(r + 1) * T]).bfloat16().to(cuda) for r in range(p)]
+    ys = [torch.empty_like(v) for v in xs]
+    dxs = [torch.empty_like(v) for v in xs]
+    for _ in range(2):
+        grp.fwd(xs, ys)
+        grp.bwd(dys, dxs)
+    torch.cuda.synchronize()
+    assert rel(torch.cat(ys).float().cpu(), y_ref) <= TOL
+    assert rel(torch.cat(dxs).float().cpu(), dx_ref) <= TOL
+    check_grads(blocks, g_ref, p)
+    grp.close()
+
+
+def test_stack_recompute_consolidated_pool(cuda):
+    """4-layer stack at a = 1 with checkpoints packed two to a region (consolidate_every_k_mlp = 2)
+    and the gradient arena pre-mapped: parity with the oracle chain, and the device pool
+    reserves exactly what the reference's run_mempool reserves over the pool's own trace in the
+    first step; afterwards the device recycles its packed regions (flat) while the reference's
+    never-returned regions grow."""
+    H, D, S, L = 512, 8, 1024, 4
+    sh, w0, x, dy, _, _, _ = oracle_case(H, D, S)
+    ws = [w0] + [ob.make_weights(sh, seed=ob.SEED + l) for l in range(1, L)]
+    y_ref, dx_ref, g_ref = stack_oracle_n(sh, ws, x, dy)
+    pol = capi.make_policy(pinned=False, consolidate=2, premap=True)
+    st = capi.IspStack(L, H, D, S, policy=pol, recompute=True)
+    for l, w in enumerate(ws):
+        load_weights(st.layer(l), w, 1, 0)
+    xd = torch.from_numpy(x).bfloat16().to(cuda)
+    dyd = torch.from_numpy(dy).bfloat16().to(cuda)
+    y, dx = torch.empty_like(xd), torch.empty_like(xd)
+    st.fwd(xd, y)
+    st.bwd(dyd, dx)
+    torch.cuda.synchronize()
+    dev1, rep1 = st.layer(0).pool_stats(), st.layer(0).pool_replay()
+    assert dev1["peak_reserved"] == rep1["peak_reserved"], (dev1, rep1)
+    assert dev1["reserved"] == dev1["allocated"] + dev1["free_cached"] + dev1["fragmented"]
+    for _ in range(2):
+        st.fwd(xd, y)
+        st.bwd(dyd, dx)
+    torch.cuda.synchronize()
+    dev3, rep3 = st.layer(0).pool_stats(), st.layer(0).pool_replay()
+    assert dev3["peak_reserved"] == dev1["peak_reserved"]
+    assert rep3["peak_reserved"] > dev3["peak_reserved"]
+    assert rel(y.float().cpu(), y_ref) <= TOL
+    assert rel(dx.float().cpu(), dx_ref) <= TOL
+    for l in range(L):
+        for t in range(7):
+            e = rel(st.layer(l).grad_shard(t), g_ref[l][t].reshape(-1))
+            assert e <= TOL, (l, capi.W_NAMES[t], e)
+    st.close()

@@ -81,3 +81,25 @@ def test_multiprocess_stack_parity(n, push):
         for k, v in row.items():
             if k != "rank":
                 assert v <= 1e-2, (row["rank"], k, v)
+
+
+@pytest.mark.parametrize("push", ["0", "1"])
+@pytest.mark.parametrize("n", [2, 4])
+def test_multiprocess_stack_recompute_parity(n, push):
+    """Activation recomputation (a = 1) in a 2-layer stack over real peers:
+    each layer's backward re-runs its forward from the checkpoint on the re-gathered weights;
+    checkpoints packed two to a region (consolidate_every_k_mlp = 2); both transports."""
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={29580 + n + 10 * int(push)}",
+           os.path.join(ROOT, "tests", "mp_stack_worker.py"), "1024", "8", "1024", "2", "recompute"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                       env={**os.environ, "SEQPLAN_ISP_PUSH": push})
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    rows = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(rows) == n
+    for row in rows:
+        for k, v in row.items():
+            if k != "rank":
+                assert v <= 1e-2, (row["rank"], k, v)

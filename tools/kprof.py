@@ -22,7 +22,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     H, D, S = cfg["H"], cfg["D"], cfg["S"]
     T = S // world
-    blk = capi.IspBlock(H, D, S, world=world, rank=rank, device=local, flags=capi.FLAG_PROFILE)
+    blk = capi.IspBlock(H, D, S, world=world, rank=rank, device=local, flags=capi.FLAG_PROFILE | (capi.FLAG_SKIP_COMM if os.environ.get("KPROF_SKIP") == "1" else 0))
     bootstrap_peers(blk, world)
     blk.init_weights(SEED)
     x = torch.empty(T, H, device="cuda", dtype=torch.bfloat16)
