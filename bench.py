@@ -351,6 +351,13 @@ def main():
                "l2": "flushed once before the loop; per-step working set (weights, activations) > L2"}
 
     # ---- profiled pass: per-kernel CUDA events (not the headline number) ----
+    # HBM: the device pool's own accounting (peak reserved / fragmented) and the
+    # device-wide high-water mark of this process
+    ps = blk.pool_stats()
+    free_b, total_b = torch.cuda.mem_get_info(dev)
+    memory = {"pool_peak_reserved_bytes": ps["peak_reserved"], "pool_peak_fragmented_bytes": ps["peak_fragmented"],
+              "pool_peak_allocated_bytes": ps["peak_allocated"], "device_used_bytes": total_b - free_b,
+              "device_total_bytes": total_b}
     blk.close()
     pblk = make_ctx(capi.FLAG_PROFILE)
     with torch.cuda.stream(stream):
@@ -433,6 +440,7 @@ def main():
             "kernel_breakdown_ms": {k: v["s"] / nprof * 1e3 for k, v in by.items()},
             "gpu_launches": int(launches),
             "clocks": clocks,
+            "memory": memory,
             "e2e": e2e,
         }
         if world == 1 and not args.no_cpu_baseline:

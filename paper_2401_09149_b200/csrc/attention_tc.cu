@@ -148,8 +148,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_empty + NS);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int qt = gridDim.x - 1 - blockIdx.x;  // heavy (late) tiles first
-  const int h = blockIdx.y;
+  // longest-first over the whole grid (blocks dispatch in linear-index order): the heavy late
+  // query tiles of every head go first, so no heavy tile of the last head trails the grid
+  const int lin = static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x);
+  const int qt = static_cast<int>(gridDim.x) - 1 - lin / static_cast<int>(gridDim.y);
+  const int h = lin % static_cast<int>(gridDim.y);
   const int q0 = qt * kBM;
   const int n_kv = (q0 + kBM + BN - 1) / BN;
 
@@ -479,8 +482,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t crank = cluster_rank();
   const bool leader = crank == 0;
-  const int pp = static_cast<int>(gridDim.x / 2) - 1 - static_cast<int>(blockIdx.x / 2);  // heavy groups first
-  const int h = blockIdx.y;
+  // longest-first over the whole grid: cluster (pair) lp in dispatch order takes the heaviest
+  // remaining query group of head lp % heads
+  const int lp = static_cast<int>((blockIdx.y * gridDim.x + blockIdx.x) / 2);
+  const int pp = static_cast<int>(gridDim.x / 2) - 1 - lp / static_cast<int>(gridDim.y);
+  const int h = lp % static_cast<int>(gridDim.y);
   const int q0A = (4 * pp + static_cast<int>(crank)) * kBM, q0B = q0A + 2 * kBM;
   const int nA = (4 * pp + 2) * kBM / BN, nB = nA + 2 * kBM / BN;  // key tiles per stream (its upper tile's)
 
@@ -885,7 +891,9 @@ __global__ void __launch_bounds__(kDQ ? kBwdThreads : 320, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9 + 2 * NS);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int kt = blockIdx.x, h = blockIdx.y;
+  // longest-first over the whole grid: key tile 0 (the most query tiles) of every head first
+  const int lin = static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x);
+  const int kt = lin / static_cast<int>(gridDim.y), h = lin % static_cast<int>(gridDim.y);
   const int k0 = kt * kBwdKeys;
   const int qi0 = k0 / kBwdQ, nq = S / kBwdQ - qi0;
   const float scale_log2 = scale * kLog2e;
@@ -1212,8 +1220,9 @@ __global__ void __launch_bounds__(320, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t crank = cluster_rank();
   const bool leader = crank == 0;
-  const int pp = static_cast<int>(gridDim.x / 2) - 1 - static_cast<int>(blockIdx.x / 2);  // heavy pairs first
-  const int h = blockIdx.y;
+  const int lp = static_cast<int>((blockIdx.y * gridDim.x + blockIdx.x) / 2);  // longest-first, all heads
+  const int pp = static_cast<int>(gridDim.x / 2) - 1 - lp / static_cast<int>(gridDim.y);
+  const int h = lp % static_cast<int>(gridDim.y);
   const int q0 = (2 * pp + static_cast<int>(crank)) * kBM;
   const int n = (2 * pp + 2) * kBM / BN;  // key tiles of the upper query tile (both CTAs)
 
