@@ -148,11 +148,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_empty + NS);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // longest-first over the whole grid (blocks dispatch in linear-index order): the heavy late
-  // query tiles of every head go first, so no heavy tile of the last head trails the grid
+  // longest-first inside each L2-sized head group (grid: x tiles, y heads per group, z groups;
+  // lpt_grid): the heavy late query tiles of every head of the group go first
   const int lin = static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x);
   const int qt = static_cast<int>(gridDim.x) - 1 - lin / static_cast<int>(gridDim.y);
-  const int h = lin % static_cast<int>(gridDim.y);
+  const int h = static_cast<int>(blockIdx.z * gridDim.y) + lin % static_cast<int>(gridDim.y);
   const int q0 = qt * kBM;
   const int n_kv = (q0 + kBM + BN - 1) / BN;
 
@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // remaining query group of head lp % heads
   const int lp = static_cast<int>((blockIdx.y * gridDim.x + blockIdx.x) / 2);
   const int pp = static_cast<int>(gridDim.x / 2) - 1 - lp / static_cast<int>(gridDim.y);
-  const int h = lp % static_cast<int>(gridDim.y);
+  const int h = static_cast<int>(blockIdx.z * gridDim.y) + lp % static_cast<int>(gridDim.y);
   const int q0A = (4 * pp + static_cast<int>(crank)) * kBM, q0B = q0A + 2 * kBM;
   const int nA = (4 * pp + 2) * kBM / BN, nB = nA + 2 * kBM / BN;  // key tiles per stream (its upper tile's)
 
@@ -740,6 +740,18 @@ bool map2d(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Longest-first dispatch inside L2-sized head groups: grid (tiles, G, heads / G). Blocks
+// dispatch in linear-index order, so within a group the heaviest causal tiles of all G heads go
+// first (no heavy tile of the last head trails the grid), and the groups run one after another
+// so the K/V (forward) or Q/dO (backward) streams in flight, G * S * d * 4 bytes, stay in L2.
+dim3 lpt_grid(int tiles_x, int heads, int S, int d) {
+  const int64_t per_head = int64_t(S) * d * 4;
+  int g = 1;
+  for (int c = 1; c <= heads; ++c)
+    if (heads % c == 0 && c * per_head <= (int64_t(48) << 20)) g = c;
+  return dim3(tiles_x, g, heads / g);
+}
+
 template <int D>
 cudaError_t launch_fwd(const AttnTensors& t, cudaStream_t st) {
   using L = FwdCfg<D>;
@@ -755,7 +767,7 @@ cudaError_t launch_fwd(const AttnTensors& t, cudaStream_t st) {
       !map2d(&mv, t.v, t.S, cols, t.ld_qkv, L::BN))
     return cudaErrorInvalidValue;
   const float scale_log2 = (1.0f / sqrtf(static_cast<float>(D))) * kLog2e;
-  attn_fwd_tc_kernel<D><<<dim3(t.S / kBM, t.heads), kThreads, L::kBytes, st>>>(mq, mk, mv, t.o, t.ld_o, t.lse, t.S,
+  attn_fwd_tc_kernel<D><<<lpt_grid(t.S / kBM, t.heads, t.S, D), kThreads, L::kBytes, st>>>(mq, mk, mv, t.o, t.ld_o, t.lse, t.S,
                                                                                scale_log2, t.push, g_attn_trace_fwd,
       std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0);
   return cudaGetLastError();
@@ -776,7 +788,7 @@ cudaError_t launch_fwd_pair(const AttnTensors& t, cudaStream_t st) {
     return cudaErrorInvalidValue;
   const float scale_log2 = (1.0f / sqrtf(128.0f)) * kLog2e;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(t.S / (2 * kBM), t.heads);  // 2 query tiles per CTA
+  cfg.gridDim = lpt_grid(t.S / (2 * kBM), t.heads, t.S, 128);  // 2 query tiles per CTA
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = L::kBytes;
   cfg.stream = st;
@@ -893,7 +905,8 @@ __global__ void __launch_bounds__(kDQ ? kBwdThreads : 320, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // longest-first over the whole grid: key tile 0 (the most query tiles) of every head first
   const int lin = static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x);
-  const int kt = lin / static_cast<int>(gridDim.y), h = lin % static_cast<int>(gridDim.y);
+  const int kt = lin / static_cast<int>(gridDim.y);
+  const int h = static_cast<int>(blockIdx.z * gridDim.y) + lin % static_cast<int>(gridDim.y);
   const int k0 = kt * kBwdKeys;
   const int qi0 = k0 / kBwdQ, nq = S / kBwdQ - qi0;
   const float scale_log2 = scale * kLog2e;
@@ -1222,7 +1235,7 @@ __global__ void __launch_bounds__(320, 1)
   const bool leader = crank == 0;
   const int lp = static_cast<int>((blockIdx.y * gridDim.x + blockIdx.x) / 2);  // longest-first, all heads
   const int pp = static_cast<int>(gridDim.x / 2) - 1 - lp / static_cast<int>(gridDim.y);
-  const int h = lp % static_cast<int>(gridDim.y);
+  const int h = static_cast<int>(blockIdx.z * gridDim.y) + lp % static_cast<int>(gridDim.y);
   const int q0 = (2 * pp + static_cast<int>(crank)) * kBM;
   const int n = (2 * pp + 2) * kBM / BN;  // key tiles of the upper query tile (both CTAs)
 
@@ -1440,12 +1453,12 @@ cudaError_t attention_bwd_split_tc(const AttnTensors& t, const __nv_bfloat16* do
   const float scale = 1.0f / sqrtf(128.0f);
   const int dbg = std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0;
   AttnPush kv_push = t.push;  // dK / dV rows
-  attn_bwd_tc_kernel<false, true><<<dim3(t.S / kBwdKeys, t.heads), 320, L::kBytes, st>>>(
+  attn_bwd_tc_kernel<false, true><<<lpt_grid(t.S / kBwdKeys, t.heads, t.S, 128), 320, L::kBytes, st>>>(
       mq, mk, mv, mdo, t.lse, delta, nullptr, dk, dv, ld_d, t.S, scale, dbg, g_attn_trace, kv_push, t.k, t.ld_qkv);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(t.S / kBM, t.heads);
+  cfg.gridDim = lpt_grid(t.S / kBM, t.heads, t.S, 128);
   cfg.blockDim = dim3(320);
   cfg.dynamicSmemBytes = Q::kBytes;
   cfg.stream = st;
@@ -1482,7 +1495,7 @@ cudaError_t attention_bwd_tc(const AttnTensors& t, const __nv_bfloat16* dout, in
   const char* kt_env = std::getenv("SEQPLAN_ISP_BWD_KTMEM");
   // K resident in TMEM (kKT) measured no faster (634 vs 639 TF/s at 32K): opt-in only
   auto kern = (kt_env && std::atoi(kt_env) != 0) ? attn_bwd_tc_kernel<true, true> : attn_bwd_tc_kernel<true, false>;
-  kern<<<dim3(t.S / kBwdKeys, t.heads), kBwdThreads, L::kBytes, st>>>(
+  kern<<<lpt_grid(t.S / kBwdKeys, t.heads, t.S, 128), kBwdThreads, L::kBytes, st>>>(
       mq, mk, mv, mdo, t.lse, delta, dq_acc, dk, dv, ld_d, t.S, scale,
       std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0, g_attn_trace, t.push, t.k,
       t.ld_qkv);

@@ -366,11 +366,18 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 // smem and accumulate into each CTA's own TMEM (128 lanes x BN). Per-SM smem traffic per MMA
 // halves vs the single-CTA kernel, which is what lets the tensor pipe run near peak.
 // ---------------------------------------------------------------------------
-template <bool A_MN, bool B_MN, int EPI>
+// BN = 256 (production) or 128 (SEQPLAN_GEMM_PAIR_BN=128, development; see gemm_launch).
+template <int BN>
+struct PairCfg {
+  static constexpr int BNH = BN / 2, S = BN == 256 ? 6 : 8;
+  static constexpr int kSmem = S * (BM * BK * 2 + BNH * BK * 2) + 1024 + 512;
+};
+
+template <bool A_MN, bool B_MN, int EPI, int BN>
 __global__ void __launch_bounds__(kNumThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                     const __grid_constant__ GemmArgs args) {
-  constexpr int BN = 256, BNH = BN / 2, S = 6;
+  constexpr int BNH = PairCfg<BN>::BNH, S = PairCfg<BN>::S;
   constexpr int kABytes = BM * BK * 2, kBBytes = BNH * BK * 2, kStageBytes = kABytes + kBBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -555,10 +562,10 @@ cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArg
   return cudaGetLastError();
 }
 
-template <bool A_MN, bool B_MN, int EPI>
+template <bool A_MN, bool B_MN, int EPI, int BN>
 cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& args, cudaStream_t stream) {
-  constexpr int kSmem = 6 * (BM * BK * 2 + 128 * BK * 2) + 1024 + 512;
-  auto kern = gemm_tc2_kernel<A_MN, B_MN, EPI>;
+  constexpr int kSmem = PairCfg<BN>::kSmem;
+  auto kern = gemm_tc2_kernel<A_MN, B_MN, EPI, BN>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
@@ -570,7 +577,7 @@ cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const Gemm
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int tiles = (args.M / 256) * (args.N / 256);
+  const int tiles = (args.M / 256) * (args.N / BN);
   const int sms = args.sm_budget > 0 && args.sm_budget < g_num_sms ? args.sm_budget : g_num_sms;
   const int clusters = tiles < sms / 2 ? tiles : sms / 2;
   cudaLaunchConfig_t cfg{};
@@ -588,16 +595,17 @@ cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const Gemm
   return cudaLaunchKernelEx(&cfg, kern, ma, mb, args);
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, int BN>
 cudaError_t dispatch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, int epi, cudaStream_t st) {
   switch (epi) {
-    case EPI_BF16: return launch_pair<A_MN, B_MN, EPI_BF16>(ma, mb, a, st);
-    case EPI_BF16_RESID: return launch_pair<A_MN, B_MN, EPI_BF16_RESID>(ma, mb, a, st);
-    case EPI_SWIGLU: return launch_pair<A_MN, B_MN, EPI_SWIGLU>(ma, mb, a, st);
-    case EPI_F32: return launch_pair<A_MN, B_MN, EPI_F32>(ma, mb, a, st);
+    case EPI_BF16: return launch_pair<A_MN, B_MN, EPI_BF16, BN>(ma, mb, a, st);
+    case EPI_BF16_RESID: return launch_pair<A_MN, B_MN, EPI_BF16_RESID, BN>(ma, mb, a, st);
+    case EPI_SWIGLU: return launch_pair<A_MN, B_MN, EPI_SWIGLU, BN>(ma, mb, a, st);
+    case EPI_F32: return launch_pair<A_MN, B_MN, EPI_F32, BN>(ma, mb, a, st);
   }
   return cudaErrorInvalidValue;
 }
+
 
 template <bool A_MN, bool B_MN, int BN>
 cudaError_t dispatch_epi(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a,
@@ -629,20 +637,37 @@ cudaError_t gemm_launch(const GemmOperand& A, const GemmOperand& B, GemmArgs arg
   if (args.push[0] && (epi != EPI_BF16 || bn % args.push_d || args.push_H % 32 || args.push_Hl % 32))
     return cudaErrorInvalidValue;
   const bool pair = bn == 256 && args.M % 256 == 0 && !std::getenv("SEQPLAN_GEMM_NO_PAIR");
+  // pair tile width: 256 x 256. 256 x 128 tiles (SEQPLAN_GEMM_PAIR_BN=128, development) fill the
+  // last wave better (4096 x 4096: 512 tiles = 6.9 waves of 74 pairs instead of 3.46) but
+  // measured ~30 % slower per FLOP on B200 (1000-1070 vs 1410-1550 TF/s, 7B shapes): twice the
+  // operand bytes per MMA cycle, which L2 cannot feed to all 148 SMs.
+  int pbn = 256;
+  if (pair) {
+    if (const char* f = std::getenv("SEQPLAN_GEMM_PAIR_BN")) pbn = std::atoi(f) == 128 ? 128 : 256;
+    if (args.push[0] && pbn % args.push_d) pbn = 256;
+  }
   CUtensorMap ma, mb;
   // A: logical [M, K]; K-major storage is [M, K], MN-major storage is [K, M].
   bool ok = A.mn_major ? make_map(&ma, A.ptr, args.K, args.M, A.ld, 64)
                        : make_map(&ma, A.ptr, args.M, args.K, A.ld, BM);
   ok = ok && (B.mn_major ? make_map(&mb, B.ptr, args.K, args.N, B.ld, 64)
-                         : make_map(&mb, B.ptr, args.N, args.K, B.ld, pair ? bn / 2 : bn));
+                         : make_map(&mb, B.ptr, args.N, args.K, B.ld, pair ? pbn / 2 : bn));
   if (!ok) return cudaErrorInvalidValue;
   const int code = (A.mn_major ? 2 : 0) | (B.mn_major ? 1 : 0);
+  if (pair && pbn == 128) {
+    switch (code) {
+      case 0: return dispatch_pair<false, false, 128>(ma, mb, args, epi, stream);
+      case 1: return dispatch_pair<false, true, 128>(ma, mb, args, epi, stream);
+      case 2: return dispatch_pair<true, false, 128>(ma, mb, args, epi, stream);
+      case 3: return dispatch_pair<true, true, 128>(ma, mb, args, epi, stream);
+    }
+  }
   if (pair) {
     switch (code) {
-      case 0: return dispatch_pair<false, false>(ma, mb, args, epi, stream);
-      case 1: return dispatch_pair<false, true>(ma, mb, args, epi, stream);
-      case 2: return dispatch_pair<true, false>(ma, mb, args, epi, stream);
-      case 3: return dispatch_pair<true, true>(ma, mb, args, epi, stream);
+      case 0: return dispatch_pair<false, false, 256>(ma, mb, args, epi, stream);
+      case 1: return dispatch_pair<false, true, 256>(ma, mb, args, epi, stream);
+      case 2: return dispatch_pair<true, false, 256>(ma, mb, args, epi, stream);
+      case 3: return dispatch_pair<true, true, 256>(ma, mb, args, epi, stream);
     }
   }
   if (bn == 256) {

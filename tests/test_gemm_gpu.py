@@ -87,3 +87,32 @@ def test_gemm_large(cuda):
     torch.cuda.synchronize()
     ref = A.float() @ B.float().t()
     assert rel_l2(out, ref) < 4e-3
+
+
+@pytest.mark.parametrize("pbn", ["128", "256"])
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False), (True, True)])
+def test_gemm_pair_tile_widths(cuda, pbn, a_mn, b_mn, monkeypatch):
+    """CTA-pair kernel with 256 x 128 and 256 x 256 tiles, every operand layout and epilogue."""
+    monkeypatch.setenv("SEQPLAN_GEMM_PAIR_BN", pbn)
+    M, N, K = 768, 1280, 448
+    A, B, R = _rand(M, K, dev=cuda), _rand(N, K, dev=cuda), _rand(M, N, dev=cuda)
+    a_store = A.t().contiguous() if a_mn else A
+    b_store = B.t().contiguous() if b_mn else B
+    out = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    capi.debug_gemm(a_store, b_store, out, M, N, K, a_mn=a_mn, b_mn=b_mn, epi=1, resid=R, scale=0.5)
+    torch.cuda.synchronize()
+    assert rel_l2(out, 0.5 * (A.float() @ B.float().t()) + R.float()) < 4e-3
+    o32 = torch.full((M, N), 1.0, device=cuda)
+    capi.debug_gemm(a_store, b_store, o32, M, N, K, a_mn=a_mn, b_mn=b_mn, epi=3, scale=0.25, accumulate=True)
+    torch.cuda.synchronize()
+    assert rel_l2(o32 - 1.0, 0.25 * (A.float() @ B.float().t())) < 2e-3
+    I = 640  # gate|up interleaved in 32-row blocks, SwiGLU epilogue
+    Wg, Wu = _rand(I, K, dev=cuda), _rand(I, K, dev=cuda)
+    Wgu = torch.stack([Wg.view(I // 32, 32, K), Wu.view(I // 32, 32, K)], 1).reshape(2 * I, K)
+    gu = torch.empty(M, 2 * I, device=cuda, dtype=torch.bfloat16)
+    a = torch.empty(M, I, device=cuda, dtype=torch.bfloat16)
+    capi.debug_gemm(A, Wgu, gu, M, 2 * I, K, epi=2, out2=a)
+    torch.cuda.synchronize()
+    g = A.float() @ Wg.float().t()
+    u = A.float() @ Wu.float().t()
+    assert rel_l2(a, torch.nn.functional.silu(g) * u) < 1e-2
