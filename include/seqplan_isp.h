@@ -76,6 +76,7 @@ enum {
   SEQPLAN_K_ALL_GATHER = 3,
   SEQPLAN_K_REDUCE_SCATTER = 4,
   SEQPLAN_K_ALL_TO_ALL = 5,
+  SEQPLAN_K_ELEMENTWISE = 6, /* RMSNorm fwd/bwd, RoPE, SwiGLU bwd (HBM-bound) */
 };
 
 typedef struct {

@@ -52,7 +52,7 @@ class KernelRecC(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("flops", c_d), ("bytes", c_d), ("seconds", c_d)]
 
 
-K_NAMES = ["gemm", "attn_fwd", "attn_bwd", "all_gather", "reduce_scatter", "all_to_all"]
+K_NAMES = ["gemm", "attn_fwd", "attn_bwd", "all_gather", "reduce_scatter", "all_to_all", "elementwise"]
 
 STATUS = {0: "ok", 1: "invalid argument", 2: "runtime error", 3: "out of memory",
           4: "unsupported"}

@@ -21,6 +21,9 @@
 #include <cstdlib>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+#include <unordered_map>
+
 #include "common.cuh"
 #include "gemm.h"
 
@@ -60,18 +63,38 @@ struct TileSched {
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
 
-// TMEM accumulator tile (this thread's row, BN columns) -> global, fused epilogue.
+// 32 accumulator columns of this thread's row from TMEM, plus the fp32 partials other K-ranges
+// of a split tile left in the workspace (np of them, `pstride` floats apart).
+__device__ __forceinline__ void ld_acc(uint32_t taddr, uint32_t (&r)[32], const float* part, int64_t pstride,
+                                       int np) {
+  tmem_ld_32x32b_x32(taddr, r);
+  tmem_ld_wait();
+  for (int q = 0; q < np; ++q) {
+    const float4* pp = reinterpret_cast<const float4*>(part + q * pstride);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const float4 a = __ldcg(pp + v);
+      r[4 * v] = __float_as_uint(__uint_as_float(r[4 * v]) + a.x);
+      r[4 * v + 1] = __float_as_uint(__uint_as_float(r[4 * v + 1]) + a.y);
+      r[4 * v + 2] = __float_as_uint(__uint_as_float(r[4 * v + 2]) + a.z);
+      r[4 * v + 3] = __float_as_uint(__uint_as_float(r[4 * v + 3]) + a.w);
+    }
+  }
+}
+
+// TMEM accumulator tile (this thread's row, BN columns) -> global, fused epilogue. part/np: the
+// fp32 partial rows of a split tile to add (part + col addresses column col of the row).
 template <int BN, int EPI>
-__device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_base, int row, int n0) {
+__device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_base, int row, int n0,
+                                              const float* part = nullptr, int64_t pstride = 0, int np = 0) {
   if constexpr (EPI == EPI_SWIGLU) {
     // kGuBlock(=32)-column blocks alternate gate / up: pair chunk 2j (gate) with 2j+1 (up).
 #pragma unroll 1
     for (int pr = 0; pr < BN / 64; ++pr) {
       const int cg = pr * 64;  // gate column within tile
       uint32_t g[32], u[32];
-      tmem_ld_32x32b_x32(t_base + cg, g);
-      tmem_ld_32x32b_x32(t_base + cg + kGuBlock, u);
-      tmem_ld_wait();
+      ld_acc(t_base + cg, g, part + cg, pstride, np);
+      ld_acc(t_base + cg + kGuBlock, u, part + cg + kGuBlock, pstride, np);
       __nv_bfloat16* gu_row = reinterpret_cast<__nv_bfloat16*>(args.out) +
                               static_cast<int64_t>(row) * args.ldo + n0;
       __nv_bfloat16* a_row = args.out2 + static_cast<int64_t>(row) * args.ldo2 + (n0 / 2 + pr * 32);
@@ -107,9 +130,8 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_b
 #pragma unroll 1
       for (int c = 0; c < hd; c += 32) {
         uint32_t lo[32], hi[32];
-        tmem_ld_32x32b_x32(t_base + hb + c, lo);
-        tmem_ld_32x32b_x32(t_base + hb + c + hd, hi);
-        tmem_ld_wait();
+        ld_acc(t_base + hb + c, lo, part + hb + c, pstride, np);
+        ld_acc(t_base + hb + c + hd, hi, part + hb + c + hd, pstride, np);
         const int col = n0 + hb + c;  // global output column of the low half
         const int part = col / args.push_H, hcol = col - part * args.push_H;
         const int q = hcol / args.push_Hl, lc = hcol - q * args.push_Hl;
@@ -156,8 +178,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_b
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
       uint32_t r[32];
-      tmem_ld_32x32b_x32(t_base + c * 32, r);
-      tmem_ld_wait();
+      ld_acc(t_base + c * 32, r, part + c * 32, pstride, np);
       const int col = n0 + c * 32;
       if constexpr (EPI == EPI_F32) {
         float* dst;
@@ -393,6 +414,19 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
   TileSched sched{args.M / (2 * BM), args.N / BN, (args.M / (2 * BM)) * (args.N / BN)};
   const int num_kb = args.K / BK;
+  // work units: split_base whole tiles, then split_L tiles x split_s K-ranges (the last wave)
+  const int n_units = args.split_L > 0 ? args.split_base + args.split_L * args.split_s : sched.num_tiles;
+  auto unit = [&](int u, int& tile, int& kb0, int& kb1, int& j, int& p) {
+    if (u < args.split_base || args.split_L == 0) {
+      tile = u; kb0 = 0; kb1 = num_kb; j = -1; p = 0;
+    } else {
+      const int v = u - args.split_base;
+      j = v / args.split_s; p = v % args.split_s;
+      tile = args.split_base + j;
+      kb0 = num_kb * p / args.split_s;
+      kb1 = num_kb * (p + 1) / args.split_s;
+    }
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mapA);
@@ -420,11 +454,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int t = cid; t < sched.num_tiles; t += ncl) {
+      for (int u = cid; u < n_units; u += ncl) {
+        int t, kb0, kb1, j, p;
+        unit(u, t, kb0, kb1, j, p);
         int mb, nb;
         sched.coords(t, mb, nb);
         const int m0 = mb * 2 * BM + static_cast<int>(crank) * BM, n0 = nb * BN + static_cast<int>(crank) * BNH;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* sa = smem + s * kStageBytes;
           uint8_t* sb = sa + kABytes;
@@ -452,11 +488,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       uint32_t ph = 0;
       int acc = 0;
       uint32_t acc_ph = 0;
-      for (int t = cid; t < sched.num_tiles; t += ncl) {
+      for (int u = cid; u < n_units; u += ncl) {
+        int t, kb0, kb1, j, p;
+        unit(u, t, kb0, kb1, j, p);
         mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[s], ph);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + s * kStageBytes);
@@ -465,7 +503,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = A_MN ? make_sw128_desc(sa + k * 2048, 8192, 1024) : make_sw128_desc(sa + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? make_sw128_desc(sb + k * 2048, 8192, 1024) : make_sw128_desc(sb + k * 32, 16, 1024);
-            tc_mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            tc_mma_bf16_pair(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           }
           tc_commit_pair(&empty_bar[s]);
           if (++s == S) { s = 0; ph ^= 1; }
@@ -478,15 +516,60 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     const int lane_grp = warp & 3;
     int acc = 0;
     uint32_t acc_ph = 0;
-    for (int t = cid; t < sched.num_tiles; t += ncl) {
+    __shared__ uint32_t split_order;
+    const int lrow = lane_grp * 32 + lane;  // this thread's row within the CTA's 128
+    for (int u = cid; u < n_units; u += ncl) {
+      int t, kb0, kb1, j, p;
+      unit(u, t, kb0, kb1, j, p);
       int mb, nb;
       sched.coords(t, mb, nb);
-      const int row = mb * 2 * BM + static_cast<int>(crank) * BM + lane_grp * 32 + lane;
+      const int row = mb * 2 * BM + static_cast<int>(crank) * BM + lrow;
       const int n0 = nb * BN;
       mbar_wait(&tfull_bar[acc], acc_ph);
       tc_fence_after();
       const uint32_t t_base = tmem_base + (static_cast<uint32_t>(lane_grp * 32) << 16) + acc * BN;
-      epilogue_tile<BN, EPI>(args, t_base, row, n0);
+      if (j < 0) {
+        epilogue_tile<BN, EPI>(args, t_base, row, n0);
+      } else {
+        // split tile: arrival order decides who finishes it (no unit ever waits for one that has
+        // not arrived, so the partial wave cannot deadlock on unscheduled clusters)
+        const int sm1 = args.split_s - 1;
+        const int64_t slot_f = int64_t(2) * 128 * BN;  // floats per (slot, both CTAs)
+        uint32_t* cnt = args.split_cnt + j * 2 + crank;
+        uint32_t* rdy = args.split_ready + (int64_t(j) * sm1) * 2 + crank;
+        float* ws = args.split_ws + (int64_t(j) * sm1) * slot_f + (int64_t(crank) * 128 + lrow) * BN;
+        if (threadIdx.x == 64) split_order = atomicAdd(cnt, 1u);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const uint32_t order = split_order;
+        if (static_cast<int>(order) < sm1) {  // not last: leave the fp32 partial in slot `order`
+          float* dst = ws + int64_t(order) * slot_f;
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(t_base + c * 32, r);
+            tmem_ld_wait();
+            float4* d4 = reinterpret_cast<float4*>(dst + c * 32);
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+              __stcg(d4 + v, make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                         __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3])));
+          }
+          __threadfence();
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (threadIdx.x == 64) st_release_sys(rdy + int64_t(order) * 2, 1u);
+        } else {  // last: wait for the others' partials, reset the flags, fused epilogue on the sum
+          if (threadIdx.x == 64) {
+            for (int q = 0; q < sm1; ++q)
+              while (ld_acquire_sys(rdy + int64_t(q) * 2) == 0u) {
+              }
+            for (int q = 0; q < sm1; ++q) rdy[int64_t(q) * 2] = 0u;
+            *cnt = 0u;
+            __threadfence();
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          epilogue_tile<BN, EPI>(args, t_base, row, n0, ws, slot_f, sm1);
+        }
+      }
       tc_fence_before();
       if (leader) mbar_arrive(&tempty_bar[acc]);
       else mbar_arrive_leader(&tempty_bar[acc]);
@@ -562,6 +645,45 @@ cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArg
   return cudaGetLastError();
 }
 
+// Split-K of the last partial wave. With `tiles` = w * clusters + L (0 < L <= clusters / 2), the
+// L trailing tiles would leave most CTA pairs idle for a whole tile time; cut each into
+// s = min(4, clusters / L) K-ranges instead (>= 8 K-blocks each), so the last wave takes ~1/s
+// of a tile time. 4096 x 4096 outputs: 256 tiles = 3 waves + 34 -> 3 + 1/2 waves.
+// Workspace (fp32 partials, arrival counters, ready flags) per stream, allocated once.
+struct SplitWs {
+  float* ws = nullptr;
+  uint32_t* flags = nullptr;
+};
+void split_last_wave(GemmArgs& a, int tiles, int clusters, int num_kb, cudaStream_t st) {
+  a.split_base = 0; a.split_L = 0; a.split_s = 1;
+  // opt-in (SEQPLAN_GEMM_SPLIT=1): measured neutral on the 7B block (4.327 vs 4.327 ms/step at
+  // S = 4K; per GEMM -6 % .. +3.5 %): the partial last wave runs faster per tile than a full one
+  // (fewer clusters share L2 bandwidth), so the idle-slot loss is smaller than the tile count says
+  const char* on = std::getenv("SEQPLAN_GEMM_SPLIT");
+  if (!on || std::atoi(on) == 0 || tiles <= clusters) return;
+  const int L = tiles % clusters;
+  if (L == 0 || 2 * L > clusters) return;
+  int sp = std::min(4, clusters / L);
+  while (sp > 1 && num_kb / sp < 8) --sp;
+  if (sp < 2) return;
+  constexpr int kMaxSlots = 74;                 // L * (s - 1) <= clusters - L < 74
+  constexpr size_t kSlotBytes = 2 * 128 * 256 * 4;  // one (tile, K-range) partial, both CTAs
+  static std::unordered_map<cudaStream_t, SplitWs> per_stream;
+  SplitWs& w = per_stream[st];
+  if (!w.ws) {
+    if (cudaMalloc(&w.ws, kMaxSlots * kSlotBytes) != cudaSuccess) { w.ws = nullptr; return; }
+    if (cudaMalloc(&w.flags, 4 * 1024 * sizeof(uint32_t)) != cudaSuccess) { cudaFree(w.ws); w.ws = nullptr; return; }
+    cudaMemsetAsync(w.flags, 0, 4 * 1024 * sizeof(uint32_t), st);
+  }
+  if (L * (sp - 1) > kMaxSlots) return;
+  a.split_base = tiles - L;
+  a.split_L = L;
+  a.split_s = sp;
+  a.split_ws = w.ws;
+  a.split_cnt = w.flags;            // [L][2]
+  a.split_ready = w.flags + 2048;   // [L][s-1][2]
+}
+
 template <bool A_MN, bool B_MN, int EPI, int BN>
 cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& args, cudaStream_t stream) {
   constexpr int kSmem = PairCfg<BN>::kSmem;
@@ -580,6 +702,8 @@ cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const Gemm
   const int tiles = (args.M / 256) * (args.N / BN);
   const int sms = args.sm_budget > 0 && args.sm_budget < g_num_sms ? args.sm_budget : g_num_sms;
   const int clusters = tiles < sms / 2 ? tiles : sms / 2;
+  GemmArgs a2 = args;
+  split_last_wave(a2, tiles, clusters, args.K / BK, stream);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * clusters);
   cfg.blockDim = dim3(kNumThreads);
@@ -592,7 +716,7 @@ cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const Gemm
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, ma, mb, args);
+  return cudaLaunchKernelEx(&cfg, kern, ma, mb, a2);
 }
 
 template <bool A_MN, bool B_MN, int BN>

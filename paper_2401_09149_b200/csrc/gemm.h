@@ -52,6 +52,14 @@ struct GemmArgs {
   // persistent-grid size limit (0 = every SM): SMs held by concurrent bulk-copy comm kernels
   // are left out so no CTA of the persistent grid waits for them
   int sm_budget = 0;
+  // Split-K of the last partial wave (CTA-pair kernel; set by gemm_launch, not by callers): the
+  // first split_base tiles run whole; each of the remaining split_L tiles is cut into split_s
+  // K-ranges run concurrently in the last wave. Finishers but the last leave fp32 partials in
+  // split_ws and raise their ready flag; the last adds them and runs the fused epilogue.
+  int split_base = 0, split_L = 0, split_s = 1;
+  float* split_ws = nullptr;
+  uint32_t* split_cnt = nullptr;    // [L][2] arrivals per (tile, CTA of the pair); self-resetting
+  uint32_t* split_ready = nullptr;  // [L][s-1][2] partial p of (tile, CTA) written; self-resetting
 };
 
 int gemm_pick_bn(int N);

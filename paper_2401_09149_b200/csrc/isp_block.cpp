@@ -296,6 +296,13 @@ struct KTimer {
     c->launches += (n);     \
   } while (0)
 
+// HBM-bound elementwise kernels: timed under SEQPLAN_ISP_FLAG_PROFILE with their algorithmic bytes.
+#define ISP_EW(n, bytes, expr)                                         \
+  do {                                                                 \
+    KTimer kt_ew_(c, st, SEQPLAN_K_ELEMENTWISE, 0, double(bytes));     \
+    ISP_LAUNCH(n, expr);                                               \
+  } while (0)
+
 void gemm(Ctx* c, const GemmOperand& A, const GemmOperand& B, const GemmArgs& args, int epi, cudaStream_t st) {
   const double M = args.M, N = args.N, K = args.K;
   const double out_bytes = (epi == EPI_F32 ? 4.0 : 2.0) * M * N * (epi == EPI_SWIGLU ? 1.5 : 1.0);
@@ -683,7 +690,7 @@ void fwd_phase1(Ctx* c, const bf16* x, cudaStream_t st) {
   Span sp(c, st, 0, SEQPLAN_EV_FORWARD, 0);
   const int T = static_cast<int>(c->T), H = static_cast<int>(c->H);
   wait_gathered(c, SEQPLAN_W_NORM1, st);
-  ISP_LAUNCH(1, rmsnorm_fwd(x, c->gathered[SEQPLAN_W_NORM1], c->n1, c->rstd1, T, H, c->eps, st, c->num_sms));
+  ISP_EW(1, 4.0 * T * H, rmsnorm_fwd(x, c->gathered[SEQPLAN_W_NORM1], c->n1, c->rstd1, T, H, c->eps, st, c->num_sms));
   wait_gathered(c, SEQPLAN_W_QKV, st);
   GemmArgs g;
   g.M = T; g.N = 3 * H; g.K = H;
@@ -697,7 +704,7 @@ void fwd_phase1(Ctx* c, const bf16* x, cudaStream_t st) {
   }
   gemm(c, {c->n1, H, false}, {c->gathered[SEQPLAN_W_QKV], H, false}, g, EPI_BF16, st);
   if (c->world == 1)
-    ISP_LAUNCH(1, rope_inplace(c->qkv_heads, 3 * H, T, 0, static_cast<int>(c->D), static_cast<int>(c->d), c->cos_t,
+    ISP_EW(1, 8.0 * T * H, rope_inplace(c->qkv_heads, 3 * H, T, 0, static_cast<int>(c->D), static_cast<int>(c->d), c->cos_t,
                           c->sin_t, H, +1, st, c->num_sms));
 }
 
@@ -752,7 +759,7 @@ void fwd_phase3(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
   }
   if (!c->recomputing) release_weight(c, SEQPLAN_W_O, st);
   wait_gathered(c, SEQPLAN_W_NORM2, st);
-  ISP_LAUNCH(1, rmsnorm_fwd(c->h, c->gathered[SEQPLAN_W_NORM2], c->n2, c->rstd2, T, H, c->eps, st, c->num_sms));
+  ISP_EW(1, 4.0 * T * H, rmsnorm_fwd(c->h, c->gathered[SEQPLAN_W_NORM2], c->n2, c->rstd2, T, H, c->eps, st, c->num_sms));
   c->gu = static_cast<bf16*>(pool_alloc(c, int64_t(T) * 2 * I * 2, seqplan::AllocTag::MlpIntermediate, st));
   c->a = static_cast<bf16*>(pool_alloc(c, int64_t(T) * I * 2, seqplan::AllocTag::MlpIntermediate, st));
   wait_gathered(c, SEQPLAN_W_GATE, st);
@@ -918,7 +925,7 @@ void bwd_phase1(Ctx* c, const bf16* dy, cudaStream_t st) {
   c->a = nullptr;
   // ---- SwiGLU backward ----
   bf16* dgu = static_cast<bf16*>(pool_alloc(c, int64_t(T) * 2 * I * 2, seqplan::AllocTag::MlpIntermediate, st));
-  ISP_LAUNCH(1, swiglu_bwd(da, c->gu, dgu, T, I, st, c->num_sms));
+  ISP_EW(1, 10.0 * T * I, swiglu_bwd(da, c->gu, dgu, T, I, st, c->num_sms));
   c->pool->free(da, st);
   c->pool->free(c->gu, st);
   c->gu = nullptr;
@@ -942,7 +949,7 @@ void bwd_phase1(Ctx* c, const bf16* dy, cudaStream_t st) {
   wait_gathered(c, SEQPLAN_W_NORM2, st);
   float* dg2 = c->world == 1 ? c->grad[SEQPLAN_W_NORM2] : c->hp<float>(c->off_part[SEQPLAN_W_NORM2]);
   ISP_CUDA(cudaMemsetAsync(dg2, 0, sizeof(float) * H, st));
-  ISP_LAUNCH(2, rmsnorm_bwd(c->h, c->gathered[SEQPLAN_W_NORM2], c->rstd2, c->dn, dy, c->dh, dg2, T, H, st, c->num_sms, c->dg_scratch));
+  ISP_EW(2, 8.0 * T * H, rmsnorm_bwd(c->h, c->gathered[SEQPLAN_W_NORM2], c->rstd2, c->dn, dy, c->dh, dg2, T, H, st, c->num_sms, c->dg_scratch));
   release_weight(c, SEQPLAN_W_NORM2, st);
   if (selective) schedule_rs(c, SEQPLAN_W_NORM2, st);
   // ---- output projection ----
@@ -983,7 +990,7 @@ void bwd_phase2(Ctx* c, cudaStream_t st) {
   ISP_LAUNCH(3, attention_bwd(t, c->dO_heads, dqkv, dqkv + c->Hl, dqkv + 2 * c->Hl, ld, c->delta, c->dq_acc, st,
                          c->num_sms));
   if (c->world == 1)
-    ISP_LAUNCH(1, rope_inplace(c->dqkv_tok, 3 * H, T, 0, static_cast<int>(c->D), static_cast<int>(c->d), c->cos_t,
+    ISP_EW(1, 8.0 * T * H, rope_inplace(c->dqkv_tok, 3 * H, T, 0, static_cast<int>(c->D), static_cast<int>(c->d), c->cos_t,
                           c->sin_t, H, -1, st, c->num_sms));
 }
 
@@ -1022,7 +1029,7 @@ void bwd_phase3(Ctx* c, const bf16* x, bf16* dx, cudaStream_t st) {
   wait_gathered(c, SEQPLAN_W_NORM1, st);
   float* dg1 = c->world == 1 ? c->grad[SEQPLAN_W_NORM1] : c->hp<float>(c->off_part[SEQPLAN_W_NORM1]);
   ISP_CUDA(cudaMemsetAsync(dg1, 0, sizeof(float) * H, st));
-  ISP_LAUNCH(2, rmsnorm_bwd(x, c->gathered[SEQPLAN_W_NORM1], c->rstd1, c->dn, c->dh, dx, dg1, T, H, st, c->num_sms, c->dg_scratch));
+  ISP_EW(2, 8.0 * T * H, rmsnorm_bwd(x, c->gathered[SEQPLAN_W_NORM1], c->rstd1, c->dn, c->dh, dx, dg1, T, H, st, c->num_sms, c->dg_scratch));
   release_weight(c, SEQPLAN_W_NORM1, st);
   if (selective) schedule_rs(c, SEQPLAN_W_NORM1, st);
 }

@@ -116,3 +116,26 @@ def test_gemm_pair_tile_widths(cuda, pbn, a_mn, b_mn, monkeypatch):
     g = A.float() @ Wg.float().t()
     u = A.float() @ Wu.float().t()
     assert rel_l2(a, torch.nn.functional.silu(g) * u) < 1e-2
+
+
+@pytest.mark.parametrize("M,N,K", [(4096, 4096, 4096), (4096, 12288, 1024), (2048, 14336, 2048)])
+@pytest.mark.parametrize("epi", [0, 1, 3])
+def test_gemm_split_last_wave(cuda, M, N, K, epi, monkeypatch):
+    """Tile counts that leave a partial last wave (256 = 3 x 74 + 34, 768 = 10 x 74 + 28,
+    448 = 6 x 74 + 4) take the split-K path: the trailing tiles' K-ranges run concurrently and the
+    last finisher adds the others' fp32 partials before the fused epilogue. Also run twice to
+    check the self-resetting arrival flags."""
+    monkeypatch.setenv("SEQPLAN_GEMM_SPLIT", "1")
+    A, B, R = _rand(M, K, dev=cuda), _rand(N, K, dev=cuda), _rand(M, N, dev=cuda)
+    ref = A.float() @ B.float().t()
+    for _ in range(2):
+        if epi == 3:
+            out = torch.full((M, N), 1.0, device=cuda)
+            capi.debug_gemm(A, B, out, M, N, K, epi=3, scale=0.5, accumulate=True)
+            torch.cuda.synchronize()
+            assert rel_l2(out - 1.0, 0.5 * ref) < 2e-3
+        else:
+            out = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+            capi.debug_gemm(A, B, out, M, N, K, epi=epi, resid=R if epi == 1 else None)
+            torch.cuda.synchronize()
+            assert rel_l2(out, ref + (R.float() if epi == 1 else 0)) < 4e-3
