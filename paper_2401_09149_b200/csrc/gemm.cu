@@ -121,6 +121,53 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_b
         adst[v] = make_uint4(pa[0], pa[1], pa[2], pa[3]);
       }
     }
+  } else if constexpr (EPI == EPI_SWIGLU_BWD) {
+    // SwiGLU backward fused into the down-projection dgrad: this 32-column chunk of da covers one
+    // kGuBlock of I, i.e. gate columns [64 b, 64 b + 32) and up columns [64 b + 32, 64 b + 64) of gu
+    // gu rows are read from HBM by one thread per row: the next chunk's 128 B are loaded while
+    // this chunk is computed (8 x 16-B loads in flight per thread), or the epilogue, not the MMA,
+    // bounds the tile
+    const __nv_bfloat16* gu_row = args.resid + static_cast<int64_t>(row) * args.ldr;
+    uint4 nxt[8];
+    {
+      const uint4* src = reinterpret_cast<const uint4*>(gu_row + static_cast<int64_t>(n0 / kGuBlock) * 2 * kGuBlock);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) nxt[v] = __ldcs(src + v);
+    }
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      uint4 cur[8];
+#pragma unroll
+      for (int v = 0; v < 8; ++v) cur[v] = nxt[v];
+      const int64_t gcol = static_cast<int64_t>((n0 + c * 32) / kGuBlock) * 2 * kGuBlock;
+      if (c + 1 < BN / 32) {
+        const uint4* src = reinterpret_cast<const uint4*>(gu_row + gcol + 2 * kGuBlock);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) nxt[v] = __ldcs(src + v);
+      }
+      uint32_t r[32];
+      ld_acc(t_base + c * 32, r, part + c * 32, pstride, np);
+      uint4* gdst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.out) +
+                                             static_cast<int64_t>(row) * args.ldo + gcol);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const uint4 g4 = cur[v], u4 = cur[v + 4];
+        const uint32_t gw[4] = {g4.x, g4.y, g4.z, g4.w}, uw[4] = {u4.x, u4.y, u4.z, u4.w};
+        uint32_t pg[4], pu[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 g = unpack_bf16(gw[e]), u = unpack_bf16(uw[e]);
+          // da rounded to bf16 exactly as the unfused path stored it
+          const float2 da = unpack_bf16(pack_bf16(__uint_as_float(r[v * 8 + 2 * e]) * args.scale,
+                                                  __uint_as_float(r[v * 8 + 2 * e + 1]) * args.scale));
+          const float s0 = 1.f / (1.f + __expf(-g.x)), s1 = 1.f / (1.f + __expf(-g.y));
+          pg[e] = pack_bf16(da.x * u.x * s0 * (1.f + g.x * (1.f - s0)), da.y * u.y * s1 * (1.f + g.y * (1.f - s1)));
+          pu[e] = pack_bf16(da.x * g.x * s0, da.y * g.y * s1);
+        }
+        __stcs(gdst + v, make_uint4(pg[0], pg[1], pg[2], pg[3]));
+        __stcs(gdst + v + 4, make_uint4(pu[0], pu[1], pu[2], pu[3]));
+      }
+    }
   } else if (EPI == EPI_BF16 && args.push[0] != nullptr) {
     // fused all-to-all: head-aligned chunk pairs (i, i + d/2) -> owner rank, RoPE on q/k
     const int d = args.push_d, hd = d / 2;
@@ -726,6 +773,7 @@ cudaError_t dispatch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const Ge
     case EPI_BF16_RESID: return launch_pair<A_MN, B_MN, EPI_BF16_RESID, BN>(ma, mb, a, st);
     case EPI_SWIGLU: return launch_pair<A_MN, B_MN, EPI_SWIGLU, BN>(ma, mb, a, st);
     case EPI_F32: return launch_pair<A_MN, B_MN, EPI_F32, BN>(ma, mb, a, st);
+    case EPI_SWIGLU_BWD: return launch_pair<A_MN, B_MN, EPI_SWIGLU_BWD, BN>(ma, mb, a, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -739,6 +787,7 @@ cudaError_t dispatch_epi(const CUtensorMap& ma, const CUtensorMap& mb, const Gem
     case EPI_BF16_RESID: return launch_t<A_MN, B_MN, BN, EPI_BF16_RESID>(ma, mb, a, st);
     case EPI_SWIGLU: return launch_t<A_MN, B_MN, BN, EPI_SWIGLU>(ma, mb, a, st);
     case EPI_F32: return launch_t<A_MN, B_MN, BN, EPI_F32>(ma, mb, a, st);
+    case EPI_SWIGLU_BWD: return launch_t<A_MN, B_MN, BN, EPI_SWIGLU_BWD>(ma, mb, a, st);
   }
   return cudaErrorInvalidValue;
 }

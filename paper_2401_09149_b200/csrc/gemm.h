@@ -17,6 +17,8 @@ enum GemmEpilogue : int {
   EPI_BF16_RESID = 1,  // out(bf16) = scale * acc + resid(bf16)
   EPI_SWIGLU = 2,      // out(bf16) = acc (gate/up interleaved by kGuBlock cols); out2 = silu(g) * u
   EPI_F32 = 3,         // out(f32) (+)= scale * acc; optional kGuBlock-row gate/up de-interleave
+  EPI_SWIGLU_BWD = 4,  // da = bf16(scale * acc) (N = I columns); out(bf16) = dgu, kGuBlock-col
+                       // interleaved gate|up grads from da and the saved gu passed as resid [M, 2N]
 };
 
 // One GEMM operand. Logical shape is [rows, K] (A: rows = M, B: rows = N).

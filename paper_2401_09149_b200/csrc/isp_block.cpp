@@ -150,6 +150,7 @@ struct seqplan_isp_ctx {
   DevicePool* pool = &own_pool;  // a stack's layers share layer 0's pool
   bool owns_pool = true;
   bool recompute = false;        // a = 1: only the block input survives the forward
+  bool fuse_swiglu_bwd = false;  // SEQPLAN_ISP_FUSE_SWIGLU_BWD=1 (development)
   bool recomputing = false;      // inside the backward's forward recomputation
   bool acts_live = false;        // saved activations currently allocated
   bool scratch_live = false;     // backward scratch currently allocated
@@ -174,8 +175,14 @@ struct seqplan_isp_ctx {
   // one stream per peer: copy-engine transfers from different peers run concurrently
   cudaStream_t peer_st[kMaxRanks] = {};
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxRanks] = {};
-  cudaEvent_t ev_tq[SEQPLAN_W_COUNT][kMaxRanks] = {};  // tensor t's shard from rank q has landed
+  // tensor t's shard from rank q has landed: [0] the forward set, [1] the backward re-gather
+  cudaEvent_t ev_tq[2][SEQPLAN_W_COUNT][kMaxRanks] = {};
   bool pipelined_gather = false;                        // wait_gathered uses ev_tq (copy-engine path)
+  int evset = 0;                                        // which ev_tq set the current pass waits on
+  // copy-engine mode: the backward re-gather is issued at step start right behind the forward
+  // set (the comm stream is idle during the forward), into its own CommBuffers
+  bf16* pre_bwd[SEQPLAN_W_COUNT] = {};
+  bool bwd_prefetched = false;
   cudaEvent_t ev_gathered[SEQPLAN_W_COUNT] = {};
   cudaEvent_t ev_wgrad[SEQPLAN_W_COUNT] = {};
   cudaEvent_t ev_comm_done = nullptr, ev_start = nullptr;
@@ -305,7 +312,8 @@ struct KTimer {
 
 void gemm(Ctx* c, const GemmOperand& A, const GemmOperand& B, const GemmArgs& args, int epi, cudaStream_t st) {
   const double M = args.M, N = args.N, K = args.K;
-  const double out_bytes = (epi == EPI_F32 ? 4.0 : 2.0) * M * N * (epi == EPI_SWIGLU ? 1.5 : 1.0);
+  const double out_bytes = (epi == EPI_F32 ? 4.0 : 2.0) * M * N *
+                           (epi == EPI_SWIGLU ? 1.5 : epi == EPI_SWIGLU_BWD ? 4.0 : 1.0);
   KTimer kt(c, st, SEQPLAN_K_GEMM, 2.0 * M * N * K, 2.0 * (M * K + N * K) + out_bytes);
   c->launches += 1;
   GemmArgs a = args;
@@ -470,18 +478,20 @@ AttnPush attn_push(Ctx* c, size_t heap_off, int64_t ld, int64_t col_o, int64_t c
 // peer's shards of all tensors back to back (no per-tensor join, so DMA setup of the next copy
 // overlaps the current one and all peers stream concurrently); a consumer waits only on the
 // per-(tensor, peer) events of the tensor it needs.
-void gather_pipelined(Ctx* c, const int* order, int n, cudaStream_t cs) {
+// set 0: into gathered[] (this pass); set 1: the backward re-gather prefetched into pre_bwd[].
+void gather_pipelined(Ctx* c, const int* order, int n, cudaStream_t cs, int set = 0) {
   const int64_t B = kGuBlock, H = c->H, rpr = c->I / c->world;
+  bf16** dsts = set ? c->pre_bwd : c->gathered;
   int todo[SEQPLAN_W_COUNT];
   int m = 0;
   for (int i = 0; i < n; ++i) {
     const int t = order[i];
     if (c->skip_comm() && c->pregathered[t]) {
-      c->gathered[t] = c->pregathered[t];
+      dsts[t] = c->pregathered[t];
       continue;
     }
     const int64_t bytes = (t == SEQPLAN_W_GATE ? 2 * c->I * c->H : c->numel(t)) * 2;
-    c->gathered[t] = static_cast<bf16*>(pool_alloc(c, bytes, seqplan::AllocTag::CommBuffer, cs));
+    dsts[t] = static_cast<bf16*>(pool_alloc(c, bytes, seqplan::AllocTag::CommBuffer, cs));
     todo[m++] = t;
   }
   if (m == 0) return;
@@ -492,7 +502,7 @@ void gather_pipelined(Ctx* c, const int* order, int n, cudaStream_t cs) {
   KTimer kt(c, cs, SEQPLAN_K_ALL_GATHER, 0, remote);
   ISP_CUDA(cudaEventRecord(c->ev_fork, cs));
   auto copy = [&](int t, int q, cudaStream_t qs) {
-    bf16* dst = c->gathered[t];
+    bf16* dst = dsts[t];
     if (t == SEQPLAN_W_GATE) {
       for (int which = 0; which < 2; ++which) {
         const bf16* src = c->peer<bf16>(q, c->off_wshard[which ? SEQPLAN_W_UP : SEQPLAN_W_GATE]);
@@ -505,7 +515,7 @@ void gather_pipelined(Ctx* c, const int* order, int n, cudaStream_t cs) {
       ISP_CUDA(cudaMemcpyAsync(dst + q * sh, c->peer<bf16>(q, c->off_wshard[t]), size_t(sh * 2), cudaMemcpyDefault,
                                qs));
     }
-    ISP_CUDA(cudaEventRecord(c->ev_tq[t][q], qs));
+    ISP_CUDA(cudaEventRecord(c->ev_tq[set][t][q], qs));
   };
   for (int q = 0; q < c->world; ++q) {
     if (q == c->rank) continue;
@@ -514,7 +524,7 @@ void gather_pipelined(Ctx* c, const int* order, int n, cudaStream_t cs) {
   }
   for (int i = 0; i < m; ++i) copy(todo[i], c->rank, cs);  // own shard: local copy
   for (int q = 0; q < c->world; ++q)  // the comm stream rejoins before later comm work
-    if (q != c->rank) ISP_CUDA(cudaStreamWaitEvent(cs, c->ev_tq[todo[m - 1]][q], 0));
+    if (q != c->rank) ISP_CUDA(cudaStreamWaitEvent(cs, c->ev_tq[set][todo[m - 1]][q], 0));
   c->pipelined_gather = true;
 }
 
@@ -644,6 +654,22 @@ void reduce_pushed(Ctx* c, int t, cudaStream_t st) {
   }
 }
 
+// Backward re-gather order: the backward's first consumer first; a = 1 re-runs the forward
+// first, so forward order then.
+const int* bwd_gather_order(const Ctx* c) {
+  static const int bwd_order[] = {SEQPLAN_W_DOWN, SEQPLAN_W_GATE, SEQPLAN_W_NORM2, SEQPLAN_W_O, SEQPLAN_W_QKV, SEQPLAN_W_NORM1};
+  static const int rec_order[] = {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN};
+  return c->recompute ? rec_order : bwd_order;
+}
+
+// Copy-engine mode: queue the backward re-gather on the comm stream behind the forward set (no SM
+// is used; the comm stream is otherwise idle until the first reduce-scatter).
+void prefetch_bwd_set(Ctx* c) {
+  if (c->world == 1 || c->group_mode || c->push_mode() || c->skip_comm() || c->bwd_prefetched) return;
+  gather_pipelined(c, bwd_gather_order(c), 6, c->comm, 1);
+  c->bwd_prefetched = true;
+}
+
 void fwd_issue_gathers(Ctx* c, cudaStream_t st) {
   if (c->world == 1) {
     for (int t : {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN})
@@ -669,7 +695,9 @@ void fwd_issue_gathers(Ctx* c, cudaStream_t st) {
   }
   if (!c->group_mode) {
     const int order[] = {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN};
+    c->evset = 0;
     gather_pipelined(c, order, 6, cs);
+    if (!c->defer_bwd_set) prefetch_bwd_set(c);
     return;
   }
   for (int t : {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN})
@@ -683,7 +711,7 @@ void wait_gathered(Ctx* c, int t, cudaStream_t st) {
     return;
   }
   if (c->skip_comm() && c->gathered[t] == c->pregathered[t] && c->pregathered[t]) return;
-  for (int q = 0; q < c->world; ++q) ISP_CUDA(cudaStreamWaitEvent(st, c->ev_tq[t][q], 0));
+  for (int q = 0; q < c->world; ++q) ISP_CUDA(cudaStreamWaitEvent(st, c->ev_tq[c->evset][t][q], 0));
 }
 
 void fwd_phase1(Ctx* c, const bf16* x, cudaStream_t st) {
@@ -792,9 +820,17 @@ void fwd_phase3(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
 // ---------------------------------------------------------------------------------
 void bwd_issue_gathers(Ctx* c, cudaStream_t st) {
   // a = 1: the recomputed forward consumes the re-gathered weights first, in forward order
-  const int bwd_order[] = {SEQPLAN_W_DOWN, SEQPLAN_W_GATE, SEQPLAN_W_NORM2, SEQPLAN_W_O, SEQPLAN_W_QKV, SEQPLAN_W_NORM1};
-  const int rec_order[] = {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN};
-  const int* order = c->recompute ? rec_order : bwd_order;
+  const int* order = bwd_gather_order(c);
+  if (c->bwd_prefetched) {  // copy-engine re-gather already queued at step start
+    for (int i = 0; i < 6; ++i) {
+      c->gathered[order[i]] = c->pre_bwd[order[i]];
+      c->pre_bwd[order[i]] = nullptr;
+    }
+    c->evset = 1;
+    c->bwd_prefetched = false;
+    return;
+  }
+  c->evset = 0;
   if (c->world == 1) {
     for (int i = 0; i < 6; ++i) gather_weight(c, order[i], st);
     return;
@@ -907,26 +943,38 @@ void bwd_phase1(Ctx* c, const bf16* dy, cudaStream_t st) {
   const bool selective = !(c->flags & SEQPLAN_ISP_FLAG_FUSED_BWD);
   // ---- down projection: G-W first (its RS overlaps the rest), then G-X ----
   wait_gathered(c, SEQPLAN_W_DOWN, st);
-  bf16* da = static_cast<bf16*>(pool_alloc(c, int64_t(T) * I * 2, seqplan::AllocTag::MlpIntermediate, st));
   {
     Span sp(c, st, 0, SEQPLAN_EV_GRAD_WEIGHT, 3);
     wgrad(c, SEQPLAN_W_DOWN, {dy, H, true}, {c->a, I, true}, H, I, T, st);
   }
   if (selective) schedule_rs(c, SEQPLAN_W_DOWN, st);
-  {
+  // ---- down dgrad, then the SwiGLU backward. SEQPLAN_ISP_FUSE_SWIGLU_BWD=1 computes dgu in the
+  // GEMM epilogue from da (never stored) and gu instead: measured no faster at 7B-4K (0.322 ms
+  // fused vs 0.242 + 0.084 ms; the one-row-per-thread gu/dgu traffic slows the epilogue enough to
+  // stall the MMAs), so the separate HBM-bound kernel stays the default ----
+  bf16* dgu = static_cast<bf16*>(pool_alloc(c, int64_t(T) * 2 * I * 2, seqplan::AllocTag::MlpIntermediate, st));
+  if (c->fuse_swiglu_bwd) {
     Span sp(c, st, 0, SEQPLAN_EV_GRAD_INPUT, 3);
     GemmArgs g;
     g.M = T; g.N = I; g.K = H;
-    g.out = da; g.ldo = I;
-    gemm(c, {dy, H, false}, {c->gathered[SEQPLAN_W_DOWN], I, true}, g, EPI_BF16, st);
+    g.out = dgu; g.ldo = 2 * I;
+    g.resid = c->gu; g.ldr = 2 * I;
+    gemm(c, {dy, H, false}, {c->gathered[SEQPLAN_W_DOWN], I, true}, g, EPI_SWIGLU_BWD, st);
+  } else {
+    bf16* da = static_cast<bf16*>(pool_alloc(c, int64_t(T) * I * 2, seqplan::AllocTag::MlpIntermediate, st));
+    {
+      Span sp(c, st, 0, SEQPLAN_EV_GRAD_INPUT, 3);
+      GemmArgs g;
+      g.M = T; g.N = I; g.K = H;
+      g.out = da; g.ldo = I;
+      gemm(c, {dy, H, false}, {c->gathered[SEQPLAN_W_DOWN], I, true}, g, EPI_BF16, st);
+    }
+    ISP_EW(1, 10.0 * T * I, swiglu_bwd(da, c->gu, dgu, T, I, st, c->num_sms));
+    c->pool->free(da, st);
   }
   release_weight(c, SEQPLAN_W_DOWN, st);
   c->pool->free(c->a, st);
   c->a = nullptr;
-  // ---- SwiGLU backward ----
-  bf16* dgu = static_cast<bf16*>(pool_alloc(c, int64_t(T) * 2 * I * 2, seqplan::AllocTag::MlpIntermediate, st));
-  ISP_EW(1, 10.0 * T * I, swiglu_bwd(da, c->gu, dgu, T, I, st, c->num_sms));
-  c->pool->free(da, st);
   c->pool->free(c->gu, st);
   c->gu = nullptr;
   // ---- gate|up ----
@@ -1180,6 +1228,7 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   const char* fa = std::getenv("SEQPLAN_ISP_FUSED_A2A");
   c->fused_a2a = c->world > 1 && c->d == 128 && fa && std::atoi(fa) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_PUSH")) c->push_pref = std::atoi(e) ? 1 : 0;
+  if (const char* e = std::getenv("SEQPLAN_ISP_FUSE_SWIGLU_BWD")) c->fuse_swiglu_bwd = std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_RS_CTAS")) c->rs_ctas = std::atoi(e) ? std::atoi(e) : 128;
   if (const char* e = std::getenv("SEQPLAN_ISP_AG_CTAS")) c->ag_ctas = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("SEQPLAN_ISP_AG_KIND")) c->ag_kind = std::atoi(e);
@@ -1222,7 +1271,7 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
     ISP_CUDA(cudaStreamCreateWithFlags(&c->peer_st[q], cudaStreamNonBlocking));
     ISP_CUDA(cudaEventCreateWithFlags(&c->ev_join[q], cudaEventDisableTiming));
     for (int t = 0; t < SEQPLAN_W_COUNT; ++t)
-      ISP_CUDA(cudaEventCreateWithFlags(&c->ev_tq[t][q], cudaEventDisableTiming));
+      for (int set = 0; set < 2; ++set) ISP_CUDA(cudaEventCreateWithFlags(&c->ev_tq[set][t][q], cudaEventDisableTiming));
   }
   for (int t = 0; t < SEQPLAN_W_COUNT; ++t) {
     ISP_CUDA(cudaEventCreateWithFlags(&c->ev_gathered[t], cudaEventDisableTiming));
@@ -1377,7 +1426,8 @@ void seqplan_isp_ctx_destroy(seqplan_isp_ctx* c) {
     if (c->peer_st[q]) cudaStreamDestroy(c->peer_st[q]);
     if (c->ev_join[q]) cudaEventDestroy(c->ev_join[q]);
     for (int t = 0; t < SEQPLAN_W_COUNT; ++t)
-      if (c->ev_tq[t][q]) cudaEventDestroy(c->ev_tq[t][q]);
+      for (int set = 0; set < 2; ++set)
+        if (c->ev_tq[set][t][q]) cudaEventDestroy(c->ev_tq[set][t][q]);
   }
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   for (int t = 0; t < SEQPLAN_W_COUNT; ++t) {
@@ -1577,7 +1627,10 @@ static void fwd_prologue(Ctx* c, cudaStream_t st, bool do_barrier, bool defer_bw
 }
 
 static void push_bwd_set(Ctx* c) {
-  if (!c->push_mode()) return;
+  if (!c->push_mode()) {
+    prefetch_bwd_set(c);
+    return;
+  }
   const int bo[] = {SEQPLAN_W_DOWN, SEQPLAN_W_GATE, SEQPLAN_W_NORM2, SEQPLAN_W_O, SEQPLAN_W_QKV, SEQPLAN_W_NORM1};
   push_gather_set(c, 1, bo, 6, !c->push_skip());
 }

@@ -139,3 +139,24 @@ def test_gemm_split_last_wave(cuda, M, N, K, epi, monkeypatch):
             capi.debug_gemm(A, B, out, M, N, K, epi=epi, resid=R if epi == 1 else None)
             torch.cuda.synchronize()
             assert rel_l2(out, ref + (R.float() if epi == 1 else 0)) < 4e-3
+
+
+@pytest.mark.parametrize("M,I,K", [(256, 384, 256), (512, 1024, 320)])
+def test_gemm_swiglu_bwd_epilogue(cuda, M, I, K):
+    """Down-projection dgrad with the SwiGLU backward fused into the epilogue (EPI_SWIGLU_BWD):
+    da = dy Wd (bf16-rounded, never stored) -> dgu (gate|up interleaved in 32-column blocks) from
+    the saved gu; matches the unfused formula on the same bf16 inputs."""
+    A, B = _rand(M, K, dev=cuda), _rand(I, K, dev=cuda)
+    gu = _rand(M, 2 * I, dev=cuda)
+    dgu = torch.empty(M, 2 * I, device=cuda, dtype=torch.bfloat16)
+    capi.debug_gemm(A, B, dgu, M, I, K, epi=4, resid=gu)
+    torch.cuda.synchronize()
+    da = (A.float() @ B.float().t()).bfloat16().float()
+    guv = gu.float().view(M, I // 32, 2, 32)
+    g, u = guv[:, :, 0].reshape(M, I), guv[:, :, 1].reshape(M, I)
+    sg = torch.sigmoid(g)
+    dg = da * u * sg * (1 + g * (1 - sg))
+    du = da * g * sg
+    out = dgu.float().view(M, I // 32, 2, 32)
+    assert rel_l2(out[:, :, 0].reshape(M, I), dg) < 1e-2
+    assert rel_l2(out[:, :, 1].reshape(M, I), du) < 1e-2
