@@ -151,6 +151,7 @@ struct seqplan_isp_ctx {
   bool owns_pool = true;
   bool recompute = false;        // a = 1: only the block input survives the forward
   bool fuse_swiglu_bwd = false;  // SEQPLAN_ISP_FUSE_SWIGLU_BWD=1 (development)
+  bool no_bwd_prefetch = false;  // SEQPLAN_ISP_BWD_PREFETCH=0: copy-engine re-gather at backward start
   bool recomputing = false;      // inside the backward's forward recomputation
   bool acts_live = false;        // saved activations currently allocated
   bool scratch_live = false;     // backward scratch currently allocated
@@ -665,7 +666,8 @@ const int* bwd_gather_order(const Ctx* c) {
 // Copy-engine mode: queue the backward re-gather on the comm stream behind the forward set (no SM
 // is used; the comm stream is otherwise idle until the first reduce-scatter).
 void prefetch_bwd_set(Ctx* c) {
-  if (c->world == 1 || c->group_mode || c->push_mode() || c->skip_comm() || c->bwd_prefetched) return;
+  if (c->world == 1 || c->group_mode || c->push_mode() || c->skip_comm() || c->bwd_prefetched || c->no_bwd_prefetch)
+    return;
   gather_pipelined(c, bwd_gather_order(c), 6, c->comm, 1);
   c->bwd_prefetched = true;
 }
@@ -1229,6 +1231,7 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   c->fused_a2a = c->world > 1 && c->d == 128 && fa && std::atoi(fa) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_PUSH")) c->push_pref = std::atoi(e) ? 1 : 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_FUSE_SWIGLU_BWD")) c->fuse_swiglu_bwd = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SEQPLAN_ISP_BWD_PREFETCH")) c->no_bwd_prefetch = std::atoi(e) == 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_RS_CTAS")) c->rs_ctas = std::atoi(e) ? std::atoi(e) : 128;
   if (const char* e = std::getenv("SEQPLAN_ISP_AG_CTAS")) c->ag_ctas = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("SEQPLAN_ISP_AG_KIND")) c->ag_kind = std::atoi(e);
