@@ -168,8 +168,10 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_b
         __stcs(gdst + v + 4, make_uint4(pu[0], pu[1], pu[2], pu[3]));
       }
     }
-  } else if (EPI == EPI_BF16 && args.push[0] != nullptr) {
-    // fused all-to-all: head-aligned chunk pairs (i, i + d/2) -> owner rank, RoPE on q/k
+  } else if (EPI == EPI_BF16 && (args.push[0] != nullptr || args.rope_parts > 0)) {
+    // head-aligned chunk pairs (i, i + d/2), RoPE on parts < rope_parts at position
+    // push_rank * push_T + row; stored locally (out, token layout), or with push[] set pushed to
+    // the rank owning the head (fused all-to-all)
     const int d = args.push_d, hd = d / 2;
     const int64_t pos = static_cast<int64_t>(args.push_rank) * args.push_T + row;
 #pragma unroll 1
@@ -204,8 +206,9 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_b
             }
           }
         }
-        __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(args.push[q]) +
-                             (pos * args.push_parts + part) * args.push_Hl + lc;
+        __nv_bfloat16* dst = args.push[0] != nullptr
+                                 ? static_cast<__nv_bfloat16*>(args.push[q]) + (pos * args.push_parts + part) * args.push_Hl + lc
+                                 : reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<int64_t>(row) * args.ldo + col;
         uint4* d_lo = reinterpret_cast<uint4*>(dst);
         uint4* d_hi = reinterpret_cast<uint4*>(dst + hd);
 #pragma unroll
@@ -807,7 +810,8 @@ cudaError_t gemm_launch(const GemmOperand& A, const GemmOperand& B, GemmArgs arg
   }
   if (epi == EPI_SWIGLU) bn = (args.N % 256 == 0) ? 256 : (args.N % 128 == 0 ? 128 : 0);
   if (bn == 0) return cudaErrorInvalidValue;
-  if (args.push[0] && (epi != EPI_BF16 || bn % args.push_d || args.push_H % 32 || args.push_Hl % 32))
+  if ((args.push[0] || args.rope_parts > 0) &&
+      (epi != EPI_BF16 || bn % args.push_d || args.push_H % 32 || args.push_Hl % 32))
     return cudaErrorInvalidValue;
   const bool pair = bn == 256 && args.M % 256 == 0 && !std::getenv("SEQPLAN_GEMM_NO_PAIR");
   // pair tile width: 256 x 256. 256 x 128 tiles (SEQPLAN_GEMM_PAIR_BN=128, development) fill the
@@ -817,7 +821,7 @@ cudaError_t gemm_launch(const GemmOperand& A, const GemmOperand& B, GemmArgs arg
   int pbn = 256;
   if (pair) {
     if (const char* f = std::getenv("SEQPLAN_GEMM_PAIR_BN")) pbn = std::atoi(f) == 128 ? 128 : 256;
-    if (args.push[0] && pbn % args.push_d) pbn = 256;
+    if ((args.push[0] || args.rope_parts > 0) && pbn % args.push_d) pbn = 256;
   }
   CUtensorMap ma, mb;
   // A: logical [M, K]; K-major storage is [M, K], MN-major storage is [K, M].

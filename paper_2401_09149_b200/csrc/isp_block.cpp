@@ -152,6 +152,7 @@ struct seqplan_isp_ctx {
   bool recompute = false;        // a = 1: only the block input survives the forward
   bool fuse_swiglu_bwd = false;  // SEQPLAN_ISP_FUSE_SWIGLU_BWD=1 (development)
   bool no_bwd_prefetch = false;  // SEQPLAN_ISP_BWD_PREFETCH=0: copy-engine re-gather at backward start
+  bool ce_a2a = false;           // Ulysses all-to-all on the copy engines (SEQPLAN_ISP_A2A_CE)
   bool recomputing = false;      // inside the backward's forward recomputation
   bool acts_live = false;        // saved activations currently allocated
   bool scratch_live = false;     // backward scratch currently allocated
@@ -475,6 +476,28 @@ AttnPush attn_push(Ctx* c, size_t heap_off, int64_t ld, int64_t col_o, int64_t c
   return p;
 }
 
+// Ulysses all-to-all on the copy engines: one strided 2-D copy per source rank, each peer's on
+// its own stream (no SM is used, the compute stream only waits). Rows are (token, part) pairs:
+// token layout [T, parts*H] rows have pitch H, head layout [S, parts*Hl] rows pitch Hl.
+// tokens -> heads: dst rows (q*T + t, part) <- rank q's (t, part) columns [rank*Hl, +Hl).
+void a2a_ce_to_heads(Ctx* c, size_t src_off, int parts, bf16* dst, cudaStream_t st) {
+  const int64_t T = c->T, H = c->H, Hl = c->Hl;
+  fan_out(c, st, [&](int q, cudaStream_t qs) {
+    const bf16* src = c->peer<bf16>(q, src_off) + c->rank * Hl;
+    ISP_CUDA(cudaMemcpy2DAsync(dst + q * T * parts * Hl, size_t(Hl * 2), src, size_t(H * 2), size_t(Hl * 2),
+                               size_t(T * parts), cudaMemcpyDefault, qs));
+  });
+}
+// heads -> tokens: dst (t, part) columns [q*Hl, +Hl) <- rank q's rows (rank*T + t, part).
+void a2a_ce_to_tokens(Ctx* c, size_t src_off, int parts, bf16* dst, cudaStream_t st) {
+  const int64_t T = c->T, H = c->H, Hl = c->Hl;
+  fan_out(c, st, [&](int q, cudaStream_t qs) {
+    const bf16* src = c->peer<bf16>(q, src_off) + c->rank * T * parts * Hl;
+    ISP_CUDA(cudaMemcpy2DAsync(dst + q * Hl, size_t(H * 2), src, size_t(Hl * 2), size_t(Hl * 2),
+                               size_t(T * parts), cudaMemcpyDefault, qs));
+  });
+}
+
 // Copy-engine all-gather of several tensors as one pipeline: every peer's stream pulls that
 // peer's shards of all tensors back to back (no per-tensor join, so DMA setup of the next copy
 // overlaps the current one and all peers stream concurrently); a consumer waits only on the
@@ -731,11 +754,18 @@ void fwd_phase1(Ctx* c, const bf16* x, cudaStream_t st) {
     g.rope_cos = c->cos_t;
     g.rope_sin = c->sin_t;
     g.rope_parts = 2;
+  } else if (c->world == 1 || c->ce_a2a) {  // RoPE in the epilogue, token layout kept locally
+    g.push_T = T;
+    g.push_rank = c->rank;
+    g.push_parts = 3;
+    g.push_H = H;
+    g.push_Hl = static_cast<int>(c->Hl);
+    g.push_d = static_cast<int>(c->d);
+    g.rope_cos = c->cos_t;
+    g.rope_sin = c->sin_t;
+    g.rope_parts = 2;
   }
   gemm(c, {c->n1, H, false}, {c->gathered[SEQPLAN_W_QKV], H, false}, g, EPI_BF16, st);
-  if (c->world == 1)
-    ISP_EW(1, 8.0 * T * H, rope_inplace(c->qkv_heads, 3 * H, T, 0, static_cast<int>(c->D), static_cast<int>(c->d), c->cos_t,
-                          c->sin_t, H, +1, st, c->num_sms));
 }
 
 AttnTensors attn_tensors(Ctx* c) {
@@ -755,7 +785,11 @@ AttnTensors attn_tensors(Ctx* c) {
 }
 
 void fwd_phase2(Ctx* c, cudaStream_t st) {
-  if (c->world > 1 && !c->skip_comm() && !c->fused_a2a) {
+  if (c->world > 1 && !c->skip_comm() && c->ce_a2a) {
+    Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 0);
+    KTimer kt(c, st, SEQPLAN_K_ALL_TO_ALL, 0, double(c->world - 1) / double(c->world) * double(c->T) * 3 * double(c->H) * 2);
+    a2a_ce_to_heads(c, c->off_qkv_tok, 3, c->qkv_heads, st);
+  } else if (c->world > 1 && !c->skip_comm() && !c->fused_a2a) {
     Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 0);
     KTimer kt(c, st, SEQPLAN_K_ALL_TO_ALL, 0, double(c->world - 1) / double(c->world) * double(c->T) * 3 * double(c->H) * 2);
     ISP_LAUNCH(1, a2a_tokens_to_heads(c->peers_at(c->off_qkv_tok), c->world, c->rank, static_cast<int>(c->T),
@@ -772,7 +806,11 @@ void fwd_phase2(Ctx* c, cudaStream_t st) {
 
 void fwd_phase3(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
   const int T = static_cast<int>(c->T), H = static_cast<int>(c->H), I = static_cast<int>(c->I);
-  if (c->world > 1 && !c->skip_comm() && !c->fused_a2a) {
+  if (c->world > 1 && !c->skip_comm() && c->ce_a2a) {
+    Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 1);
+    KTimer kt(c, st, SEQPLAN_K_ALL_TO_ALL, 0, double(c->world - 1) / double(c->world) * double(c->T) * 1 * double(c->H) * 2);
+    a2a_ce_to_tokens(c, c->off_o_heads, 1, c->o_tok, st);
+  } else if (c->world > 1 && !c->skip_comm() && !c->fused_a2a) {
     Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 1);
     KTimer kt(c, st, SEQPLAN_K_ALL_TO_ALL, 0, double(c->world - 1) / double(c->world) * double(c->T) * 1 * double(c->H) * 2);
     ISP_LAUNCH(1, a2a_heads_to_tokens(c->peers_at(c->off_o_heads), c->world, c->rank, T, H, 1, c->o_tok, c->cos_t,
@@ -1023,7 +1061,11 @@ void bwd_phase1(Ctx* c, const bf16* dy, cudaStream_t st) {
 
 void bwd_phase2(Ctx* c, cudaStream_t st) {
   const int T = static_cast<int>(c->T), H = static_cast<int>(c->H);
-  if (c->world > 1 && !c->skip_comm() && !c->fused_a2a) {
+  if (c->world > 1 && !c->skip_comm() && c->ce_a2a) {
+    Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 2);
+    KTimer kt(c, st, SEQPLAN_K_ALL_TO_ALL, 0, double(c->world - 1) / double(c->world) * double(c->T) * 1 * double(c->H) * 2);
+    a2a_ce_to_heads(c, c->off_do_tok, 1, c->dO_heads, st);
+  } else if (c->world > 1 && !c->skip_comm() && !c->fused_a2a) {
     Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 2);
     KTimer kt(c, st, SEQPLAN_K_ALL_TO_ALL, 0, double(c->world - 1) / double(c->world) * double(c->T) * 1 * double(c->H) * 2);
     ISP_LAUNCH(1, a2a_tokens_to_heads(c->peers_at(c->off_do_tok), c->world, c->rank, T, H, 1, c->dO_heads, c->cos_t,
@@ -1056,7 +1098,16 @@ void bwd_phase3(Ctx* c, const bf16* x, bf16* dx, cudaStream_t st) {
   const int T = static_cast<int>(c->T), H = static_cast<int>(c->H);
   const bool selective = !(c->flags & SEQPLAN_ISP_FLAG_FUSED_BWD);
   bwd_unrope_local(c, st);
-  if (c->world > 1 && !c->skip_comm() && !c->fused_a2a) {
+  if (c->world > 1 && !c->skip_comm() && c->ce_a2a) {
+    {
+      Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 3);
+      KTimer kt(c, st, SEQPLAN_K_ALL_TO_ALL, 0, double(c->world - 1) / double(c->world) * double(c->T) * 3 * double(c->H) * 2);
+      a2a_ce_to_tokens(c, c->off_dqkv_heads, 3, c->dqkv_tok, st);
+    }
+    ISP_EW(1, 8.0 * T * H, rope_inplace(c->dqkv_tok, 3 * c->H, T, static_cast<int>(c->rank * c->T),
+                                         static_cast<int>(c->D), static_cast<int>(c->d), c->cos_t, c->sin_t, H, -1,
+                                         st, c->num_sms));
+  } else if (c->world > 1 && !c->skip_comm() && !c->fused_a2a) {
     Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 3);
     KTimer kt(c, st, SEQPLAN_K_ALL_TO_ALL, 0, double(c->world - 1) / double(c->world) * double(c->T) * 3 * double(c->H) * 2);
     ISP_LAUNCH(1, a2a_heads_to_tokens(c->peers_at(c->off_dqkv_heads), c->world, c->rank, T, H, 3, c->dqkv_tok,
@@ -1232,6 +1283,7 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   if (const char* e = std::getenv("SEQPLAN_ISP_PUSH")) c->push_pref = std::atoi(e) ? 1 : 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_FUSE_SWIGLU_BWD")) c->fuse_swiglu_bwd = std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_BWD_PREFETCH")) c->no_bwd_prefetch = std::atoi(e) == 0;
+  if (const char* e = std::getenv("SEQPLAN_ISP_A2A_CE")) c->ce_a2a = c->world > 1 && !c->fused_a2a && std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_RS_CTAS")) c->rs_ctas = std::atoi(e) ? std::atoi(e) : 128;
   if (const char* e = std::getenv("SEQPLAN_ISP_AG_CTAS")) c->ag_ctas = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("SEQPLAN_ISP_AG_KIND")) c->ag_kind = std::atoi(e);

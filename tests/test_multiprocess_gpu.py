@@ -103,3 +103,17 @@ def test_multiprocess_stack_recompute_parity(n, push):
         for k, v in row.items():
             if k != "rank":
                 assert v <= 1e-2, (row["rank"], k, v)
+
+
+@pytest.mark.parametrize("n", [2, 4])
+@pytest.mark.parametrize("H", [512, 1024])
+def test_multiprocess_parity_ce_a2a(n, H):
+    """Ulysses all-to-all on the copy engines (SEQPLAN_ISP_A2A_CE=1): one strided 2-D copy per
+    source rank, RoPE applied in the QKV GEMM epilogue before the exchange, inverse RoPE after
+    the backward exchange; head dim 64 and 128."""
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    for row in _run(n, H, 8, 1024, "selective", env={"SEQPLAN_ISP_A2A_CE": "1"}):
+        for k, v in row.items():
+            if k not in ("rank", "timeline_events"):
+                assert v <= 1e-2, (row["rank"], k, v)
