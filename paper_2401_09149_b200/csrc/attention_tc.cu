@@ -1102,19 +1102,30 @@ __global__ void __launch_bounds__(kDQ ? kBwdThreads : 320, 1)
         }
         const float* lr = reinterpret_cast<const float*>(l4);
         const float* dr = reinterpret_cast<const float*>(d4);
+        // packed f32x2 math (FFMA2/FMUL2/FADD2), and 3 of 8 exponential pairs as a polynomial on
+        // the FMA pipe (exp2_poly2, as in the forward): MUFU.EX2 alone needs 512 cycles per tile
 #pragma unroll
         for (int c = 0; c < 16; c += 2) {
-          float p2[2], d2[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int qc = half * 32 + hc * 16 + c + e;
-            float p = fast_exp2(fmaf(__uint_as_float(sv[hc * 16 + c + e]), scale_log2, -lr[c + e] * kLog2e));
-            if (diag && key > q0 + qc) p = 0.f;
-            p2[e] = p;
-            d2[e] = p * (__uint_as_float(pv[hc * 16 + c + e]) - dr[c + e]);
+          const float2 s2 = make_float2(__uint_as_float(sv[hc * 16 + c]), __uint_as_float(sv[hc * 16 + c + 1]));
+          const float2 nl = __fmul2_rn(make_float2(lr[c], lr[c + 1]), make_float2(-kLog2e, -kLog2e));
+          const float2 x = __ffma2_rn(s2, make_float2(scale_log2, scale_log2), nl);
+          float2 p;
+          if (c >= 10) {
+            p = exp2_poly2(x);
+          } else {
+            p.x = fast_exp2(x.x);
+            p.y = fast_exp2(x.y);
           }
-          pk[hc * 8 + c / 2] = pack_bf16(p2[0], p2[1]);
-          dk[hc * 8 + c / 2] = pack_bf16(d2[0], d2[1]);
+          if (diag) {
+            const int qc = q0 + half * 32 + hc * 16 + c;
+            if (key > qc) p.x = 0.f;
+            if (key > qc + 1) p.y = 0.f;
+          }
+          const float2 dd = __fadd2_rn(make_float2(__uint_as_float(pv[hc * 16 + c]), __uint_as_float(pv[hc * 16 + c + 1])),
+                                       make_float2(-dr[c], -dr[c + 1]));
+          const float2 d = __fmul2_rn(p, dd);
+          pk[hc * 8 + c / 2] = pack_bf16(p.x, p.y);
+          dk[hc * 8 + c / 2] = pack_bf16(d.x, d.y);
         }
       }
       if (tr) trace[i * 8 + 4] = clock64();

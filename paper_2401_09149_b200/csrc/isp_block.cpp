@@ -153,6 +153,7 @@ struct seqplan_isp_ctx {
   bool fuse_swiglu_bwd = false;  // SEQPLAN_ISP_FUSE_SWIGLU_BWD=1 (development)
   bool no_bwd_prefetch = false;  // SEQPLAN_ISP_BWD_PREFETCH=0: copy-engine re-gather at backward start
   bool ce_a2a = false;           // Ulysses all-to-all on the copy engines (SEQPLAN_ISP_A2A_CE)
+  bool rs_ce = false;            // push mode: reduce-scatter staged by the copy engines (SEQPLAN_ISP_RS_CE)
   bool recomputing = false;      // inside the backward's forward recomputation
   bool acts_live = false;        // saved activations currently allocated
   bool scratch_live = false;     // backward scratch currently allocated
@@ -970,7 +971,7 @@ void schedule_rs(Ctx* c, int t, cudaStream_t st) {
   if (c->world == 1 || c->group_mode || c->skip_comm()) return;
   ISP_CUDA(cudaEventRecord(c->ev_wgrad[t], st));
   ISP_CUDA(cudaStreamWaitEvent(c->comm, c->ev_wgrad[t], 0));
-  if (c->push_mode()) {
+  if (c->push_mode() && !c->rs_ce) {
     push_rs(c, t, c->comm);
     return;
   }
@@ -1283,6 +1284,7 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   if (const char* e = std::getenv("SEQPLAN_ISP_PUSH")) c->push_pref = std::atoi(e) ? 1 : 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_FUSE_SWIGLU_BWD")) c->fuse_swiglu_bwd = std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_BWD_PREFETCH")) c->no_bwd_prefetch = std::atoi(e) == 0;
+  if (const char* e = std::getenv("SEQPLAN_ISP_RS_CE")) c->rs_ce = std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_A2A_CE")) c->ce_a2a = c->world > 1 && !c->fused_a2a && std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_RS_CTAS")) c->rs_ctas = std::atoi(e) ? std::atoi(e) : 128;
   if (const char* e = std::getenv("SEQPLAN_ISP_AG_CTAS")) c->ag_ctas = std::max(1, std::atoi(e));
@@ -1743,7 +1745,7 @@ static void bwd_epilogue(Ctx* c, cudaStream_t st) {
   } else if (c->world > 1) {
     // reduce the staged slices (fp32 accumulate, cast/scale) and join the comm stream
     for (int t : {SEQPLAN_W_DOWN, SEQPLAN_W_GATE, SEQPLAN_W_NORM2, SEQPLAN_W_O, SEQPLAN_W_QKV, SEQPLAN_W_NORM1}) {
-      if (c->push_mode()) {
+      if (c->push_mode() && !c->rs_ce) {
         if (!c->skip_comm()) reduce_pushed(c, t, st);
       } else {
         reduce_staged(c, t, st);
