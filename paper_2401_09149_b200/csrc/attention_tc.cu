@@ -1034,47 +1034,17 @@ __global__ void __launch_bounds__(kDQ ? kBwdThreads : 320, 1)
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(dq_free);
-      if (dbg == 21) {  // development A/B: scalar reductions, one query row of 32 head dims per instruction
-        float* dst = dq_acc + (static_cast<int64_t>(h) * S + (qi0 + j) * kBwdQ) * D + r;
+      // a warp instruction covers 32 consecutive floats (one query row, 32 head dims). 16-B vector
+      // REDs after a 4 x 4 lane transpose (4 queries x 128 B per instruction) measured ~10 % slower
+      // for the whole kernel (S = 16K: 3.54 vs 3.20 ms)
+      float* dst = dq_acc + (static_cast<int64_t>(h) * S + (qi0 + j) * kBwdQ) * D + r;
 #pragma unroll
-        for (int c = 0; c < 32; ++c)
-          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(dst + c * D), "f"(__uint_as_float(v0[c]) * scale) : "memory");
+      for (int c = 0; c < 32; ++c)
+        asm volatile("red.global.add.f32 [%0], %1;" ::"l"(dst + c * D), "f"(__uint_as_float(v0[c]) * scale) : "memory");
 #pragma unroll
-        for (int c = 0; c < 32; ++c)
-          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(dst + (32 + c) * D), "f"(__uint_as_float(v1[c]) * scale)
-                       : "memory");
-        continue;
-      }
-      // 16-B vector reductions: a 4 x 4 transpose inside each group of 4 lanes (two shuffle
-      // stages) turns "lane = head dim, registers = queries" into "lane = query, 4 consecutive head
-      // dims", so one REDG.F32x4 replaces four scalar ones (a quarter of the LSU instructions; the
-      // dQ reductions are the largest removable cost of this kernel, profiles/r1c_attn_bwd_analysis.md)
-      const int m4 = lane & 3;
-      float* dbase = dq_acc + (static_cast<int64_t>(h) * S + (qi0 + j) * kBwdQ) * D + quad * 32 + (lane & ~3);
-      auto flush = [&](const uint32_t(&v)[32], int qoff) {
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          float a0 = __uint_as_float(v[4 * b]) * scale, a1 = __uint_as_float(v[4 * b + 1]) * scale;
-          float a2 = __uint_as_float(v[4 * b + 2]) * scale, a3 = __uint_as_float(v[4 * b + 3]) * scale;
-          {
-            const bool hi = m4 & 1;
-            const float r0 = __shfl_xor_sync(0xffffffffu, hi ? a0 : a1, 1);
-            const float r2 = __shfl_xor_sync(0xffffffffu, hi ? a2 : a3, 1);
-            if (hi) { a0 = r0; a2 = r2; } else { a1 = r0; a3 = r2; }
-          }
-          {
-            const bool hi = m4 & 2;
-            const float r0 = __shfl_xor_sync(0xffffffffu, hi ? a0 : a2, 2);
-            const float r1 = __shfl_xor_sync(0xffffffffu, hi ? a1 : a3, 2);
-            if (hi) { a0 = r0; a1 = r1; } else { a2 = r0; a3 = r1; }
-          }
-          float* dst = dbase + static_cast<int64_t>(qoff + 4 * b + m4) * D;
-          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(a0), "f"(a1), "f"(a2), "f"(a3)
-                       : "memory");
-        }
-      };
-      flush(v0, 0);
-      flush(v1, 32);
+      for (int c = 0; c < 32; ++c)
+        asm volatile("red.global.add.f32 [%0], %1;" ::"l"(dst + (32 + c) * D), "f"(__uint_as_float(v1[c]) * scale)
+                     : "memory");
     }
   } else {
     // ---------------- P^T / dS^T warps 2..9 ----------------

@@ -154,6 +154,7 @@ struct seqplan_isp_ctx {
   bool no_bwd_prefetch = false;  // SEQPLAN_ISP_BWD_PREFETCH=0: copy-engine re-gather at backward start
   bool ce_a2a = false;           // Ulysses all-to-all on the copy engines (SEQPLAN_ISP_A2A_CE)
   bool rs_ce = false;            // push mode: reduce-scatter staged by the copy engines (SEQPLAN_ISP_RS_CE)
+  bool qkv_slice = true;         // QKV GEMM sliced by weight-shard source (SEQPLAN_ISP_QKV_SLICE=0 turns off)
   bool recomputing = false;      // inside the backward's forward recomputation
   bool acts_live = false;        // saved activations currently allocated
   bool scratch_live = false;     // backward scratch currently allocated
@@ -745,6 +746,28 @@ void fwd_phase1(Ctx* c, const bf16* x, cudaStream_t st) {
   const int T = static_cast<int>(c->T), H = static_cast<int>(c->H);
   wait_gathered(c, SEQPLAN_W_NORM1, st);
   ISP_EW(1, 4.0 * T * H, rmsnorm_fwd(x, c->gathered[SEQPLAN_W_NORM1], c->n1, c->rstd1, T, H, c->eps, st, c->num_sms));
+  const int64_t n_own = 3 * c->H / c->world;  // rows of Wqkv in each rank's shard
+  if (c->world > 1 && !c->group_mode && !c->fused_a2a && !c->ce_a2a && !c->skip_comm() && c->qkv_slice &&
+      n_own % 128 == 0) {
+    // The step's first gather consumer, sliced by weight-shard source: this rank's own rows of
+    // Wqkv are multiplied straight from its working shard while the peers' rows are in flight,
+    // the rest once they have landed (unsliced, the GEMM waits for every shard).
+    const int64_t r0 = c->rank * n_own;
+    bf16* out = qkv_tok_buf(c);
+    auto slice = [&](const bf16* w, int64_t col0, int64_t ncols) {
+      if (ncols <= 0) return;
+      GemmArgs g;
+      g.M = T; g.N = static_cast<int>(ncols); g.K = H;
+      g.out = out + col0; g.ldo = 3 * H;
+      gemm(c, {c->n1, H, false}, {w, H, false}, g, EPI_BF16, st);
+    };
+    slice(c->wshard(SEQPLAN_W_QKV), r0, n_own);
+    wait_gathered(c, SEQPLAN_W_QKV, st);
+    const bf16* wq = c->gathered[SEQPLAN_W_QKV];
+    slice(wq, 0, r0);
+    slice(wq + (r0 + n_own) * H, r0 + n_own, 3 * H - r0 - n_own);
+    return;
+  }
   wait_gathered(c, SEQPLAN_W_QKV, st);
   GemmArgs g;
   g.M = T; g.N = 3 * H; g.K = H;
@@ -1285,6 +1308,7 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   if (const char* e = std::getenv("SEQPLAN_ISP_FUSE_SWIGLU_BWD")) c->fuse_swiglu_bwd = std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_BWD_PREFETCH")) c->no_bwd_prefetch = std::atoi(e) == 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_RS_CE")) c->rs_ce = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SEQPLAN_ISP_QKV_SLICE")) c->qkv_slice = std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_A2A_CE")) c->ce_a2a = c->world > 1 && !c->fused_a2a && std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_RS_CTAS")) c->rs_ctas = std::atoi(e) ? std::atoi(e) : 128;
   if (const char* e = std::getenv("SEQPLAN_ISP_AG_CTAS")) c->ag_ctas = std::max(1, std::atoi(e));
