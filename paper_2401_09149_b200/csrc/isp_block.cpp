@@ -154,7 +154,7 @@ struct seqplan_isp_ctx {
   bool no_bwd_prefetch = false;  // SEQPLAN_ISP_BWD_PREFETCH=0: copy-engine re-gather at backward start
   bool ce_a2a = false;           // Ulysses all-to-all on the copy engines (SEQPLAN_ISP_A2A_CE)
   bool rs_ce = false;            // push mode: reduce-scatter staged by the copy engines (SEQPLAN_ISP_RS_CE)
-  bool qkv_slice = true;         // QKV GEMM sliced by weight-shard source (SEQPLAN_ISP_QKV_SLICE=0 turns off)
+  bool qkv_slice = true;         // QKV GEMM sliced by weight-shard source (SEQPLAN_ISP_QKV_SLICE=0 turns off; +1.1 % at 4K p = 2, neutral at p = 4)
   bool recomputing = false;      // inside the backward's forward recomputation
   bool acts_live = false;        // saved activations currently allocated
   bool scratch_live = false;     // backward scratch currently allocated
