@@ -13,6 +13,8 @@
 // system-scope flag barrier separates producer and consumer phases.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "gemm.h"
 #include "kernels.h"
@@ -160,6 +162,7 @@ __device__ __forceinline__ void rotate8(uint4& lo, uint4& hi, const float* c, co
 // Token-sharded [T, parts*H] on every rank -> head-sharded [S, parts*Hl] on this rank.
 // Work unit: (global token s, part, local head, 8-element group j of the low half); optional
 // RoPE on parts < rope_parts at global position s. 32-bit index math (units < 2^31).
+template <int kU>
 __global__ void __launch_bounds__(256) a2a_to_heads_kernel(PeerPtrs src, int world, int rank, int T, int H,
                                                            int parts, int d, __nv_bfloat16* __restrict__ dst,
                                                            const float* __restrict__ cos_t,
@@ -168,27 +171,46 @@ __global__ void __launch_bounds__(256) a2a_to_heads_kernel(PeerPtrs src, int wor
   const int per_part = heads_l * g8;
   const int per_row = parts * per_part;
   const int total = T * world * per_row;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int s = i / per_row;
-    int rem = i - s * per_row;
-    const int part = rem / per_part;
-    rem -= part * per_part;
-    const int hl = rem / g8, j = (rem - hl * g8) * 8;
-    const int q = s / T, t = s - q * T;
-    const __nv_bfloat16* sp = static_cast<const __nv_bfloat16*>(src.p[q]) +
-                              (static_cast<int64_t>(t) * parts + part) * H + rank * Hl + hl * d + j;
-    __nv_bfloat16* dp = dst + (static_cast<int64_t>(s) * parts + part) * Hl + hl * d + j;
-    uint4 lo = ld_v4(sp), hi = ld_v4(sp + half);
-    if (part < rope_parts) {
-      const int64_t cs = static_cast<int64_t>(s) * half + j;
-      rotate8(lo, hi, cos_t + cs, sin_t + cs, 1.f);
+  const int stride = gridDim.x * blockDim.x;
+  // kU units per thread per round, all 2*kU remote loads issued before any store (NVLink latency
+  // needs bytes in flight; one unit at a time leaves the exchange latency-bound)
+  for (int i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < total; i0 += kU * stride) {
+    uint4 lo[kU], hi[kU];
+    __nv_bfloat16* dp[kU];
+    int spos[kU], part_u[kU], j_u[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * stride;
+      dp[u] = nullptr;
+      if (i >= total) continue;
+      const int s = i / per_row;
+      int rem = i - s * per_row;
+      const int part = rem / per_part;
+      rem -= part * per_part;
+      const int hl = rem / g8, j = (rem - hl * g8) * 8;
+      const int q = s / T, t = s - q * T;
+      const __nv_bfloat16* sp = static_cast<const __nv_bfloat16*>(src.p[q]) +
+                                (static_cast<int64_t>(t) * parts + part) * H + rank * Hl + hl * d + j;
+      dp[u] = dst + (static_cast<int64_t>(s) * parts + part) * Hl + hl * d + j;
+      spos[u] = s; part_u[u] = part; j_u[u] = j;
+      lo[u] = ld_v4(sp);
+      hi[u] = ld_v4(sp + half);
     }
-    *reinterpret_cast<uint4*>(dp) = lo;
-    *reinterpret_cast<uint4*>(dp + half) = hi;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (!dp[u]) continue;
+      if (part_u[u] < rope_parts) {
+        const int64_t cs = static_cast<int64_t>(spos[u]) * half + j_u[u];
+        rotate8(lo[u], hi[u], cos_t + cs, sin_t + cs, 1.f);
+      }
+      *reinterpret_cast<uint4*>(dp[u]) = lo[u];
+      *reinterpret_cast<uint4*>(dp[u] + half) = hi[u];
+    }
   }
 }
 
 // Head-sharded [S, parts*Hl] on every rank -> token-sharded [T, parts*H] on this rank.
+template <int kU>
 __global__ void __launch_bounds__(256) a2a_to_tokens_kernel(PeerPtrs src, int world, int rank, int T, int H,
                                                             int parts, int d, __nv_bfloat16* __restrict__ dst,
                                                             const float* __restrict__ cos_t,
@@ -197,25 +219,42 @@ __global__ void __launch_bounds__(256) a2a_to_tokens_kernel(PeerPtrs src, int wo
   const int per_part = heads * g8;
   const int per_row = parts * per_part;
   const int total = T * per_row;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int t = i / per_row;
-    int rem = i - t * per_row;
-    const int part = rem / per_part;
-    rem -= part * per_part;
-    const int hg = rem / g8, j = (rem - hg * g8) * 8;  // hg = global head
-    const int q = hg / heads_l;                        // owner rank of that head
-    const int hl = hg - q * heads_l;
-    const int s = rank * T + t;                        // global position
-    const __nv_bfloat16* sp = static_cast<const __nv_bfloat16*>(src.p[q]) +
-                              (static_cast<int64_t>(s) * parts + part) * Hl + hl * d + j;
-    __nv_bfloat16* dp = dst + (static_cast<int64_t>(t) * parts + part) * H + hg * d + j;
-    uint4 lo = ld_v4(sp), hi = ld_v4(sp + half);
-    if (part < rope_parts) {
-      const int64_t cs = static_cast<int64_t>(s) * half + j;
-      rotate8(lo, hi, cos_t + cs, sin_t + cs, -1.f);
+  const int stride = gridDim.x * blockDim.x;
+  // kU units per round as in a2a_to_heads_kernel
+  for (int i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < total; i0 += kU * stride) {
+    uint4 lo[kU], hi[kU];
+    __nv_bfloat16* dp[kU];
+    int spos[kU], part_u[kU], j_u[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * stride;
+      dp[u] = nullptr;
+      if (i >= total) continue;
+      const int t = i / per_row;
+      int rem = i - t * per_row;
+      const int part = rem / per_part;
+      rem -= part * per_part;
+      const int hg = rem / g8, j = (rem - hg * g8) * 8;  // hg = global head
+      const int q = hg / heads_l;                        // owner rank of that head
+      const int hl = hg - q * heads_l;
+      const int s = rank * T + t;                        // global position
+      const __nv_bfloat16* sp = static_cast<const __nv_bfloat16*>(src.p[q]) +
+                                (static_cast<int64_t>(s) * parts + part) * Hl + hl * d + j;
+      dp[u] = dst + (static_cast<int64_t>(t) * parts + part) * H + hg * d + j;
+      spos[u] = s; part_u[u] = part; j_u[u] = j;
+      lo[u] = ld_v4(sp);
+      hi[u] = ld_v4(sp + half);
     }
-    *reinterpret_cast<uint4*>(dp) = lo;
-    *reinterpret_cast<uint4*>(dp + half) = hi;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (!dp[u]) continue;
+      if (part_u[u] < rope_parts) {
+        const int64_t cs = static_cast<int64_t>(spos[u]) * half + j_u[u];
+        rotate8(lo[u], hi[u], cos_t + cs, sin_t + cs, -1.f);
+      }
+      *reinterpret_cast<uint4*>(dp[u]) = lo[u];
+      *reinterpret_cast<uint4*>(dp[u] + half) = hi[u];
+    }
   }
 }
 
@@ -426,12 +465,22 @@ cudaError_t reduce_scatter_pull_interleave(const PeerPtrs& part, int world, int 
   return cudaGetLastError();
 }
 
+// Units per thread per round of the all-to-all kernels (SEQPLAN_ISP_A2A_UNROLL=1 for A/B).
+int a2a_unroll() {
+  static const int u = [] {
+    const char* e = std::getenv("SEQPLAN_ISP_A2A_UNROLL");
+    return e && std::atoi(e) == 1 ? 1 : 4;
+  }();
+  return u;
+}
+
 cudaError_t a2a_tokens_to_heads(const PeerPtrs& src, int world, int rank, int T, int H, int parts,
                                 __nv_bfloat16* dst, const float* cos_t, const float* sin_t, int d,
                                 int rope_parts, cudaStream_t st, int num_ctas) {
   if ((H / world) % d || d % 16) return cudaErrorInvalidValue;
   const int64_t work = static_cast<int64_t>(T) * world * parts * (H / world / d) * (d / 16);
-  a2a_to_heads_kernel<<<ctas(work, 256, num_ctas), 256, 0, st>>>(src, world, rank, T, H, parts, d,
+  auto kern = a2a_unroll() == 1 ? a2a_to_heads_kernel<1> : a2a_to_heads_kernel<4>;
+  kern<<<ctas(work, 256, num_ctas), 256, 0, st>>>(src, world, rank, T, H, parts, d,
                                                                   dst, cos_t, sin_t, rope_parts);
   return cudaGetLastError();
 }
@@ -441,7 +490,8 @@ cudaError_t a2a_heads_to_tokens(const PeerPtrs& src, int world, int rank, int T,
                                 int rope_parts, cudaStream_t st, int num_ctas) {
   if ((H / world) % d || d % 16) return cudaErrorInvalidValue;
   const int64_t work = static_cast<int64_t>(T) * parts * (H / d) * (d / 16);
-  a2a_to_tokens_kernel<<<ctas(work, 256, num_ctas), 256, 0, st>>>(src, world, rank, T, H, parts, d,
+  auto kern = a2a_unroll() == 1 ? a2a_to_tokens_kernel<1> : a2a_to_tokens_kernel<4>;
+  kern<<<ctas(work, 256, num_ctas), 256, 0, st>>>(src, world, rank, T, H, parts, d,
                                                                    dst, cos_t, sin_t, rope_parts);
   return cudaGetLastError();
 }
