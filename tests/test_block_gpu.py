@@ -325,3 +325,27 @@ def test_stack_recompute_consolidated_pool(cuda):
             e = rel(st.layer(l).grad_shard(t), g_ref[l][t].reshape(-1))
             assert e <= TOL, (l, capi.W_NAMES[t], e)
     st.close()
+
+
+@pytest.mark.parametrize("p", [2, 4])
+def test_block_fused_swiglu_bwd_epilogue(cuda, p, monkeypatch):
+    """Opt-in SwiGLU backward inside the down-projection dgrad epilogue (SEQPLAN_ISP_FUSE_SWIGLU_BWD=1)
+    gives the same block results as the separate kernel path."""
+    monkeypatch.setenv("SEQPLAN_ISP_FUSE_SWIGLU_BWD", "1")
+    H, D, S = 1024, 8, 1024
+    sh, w, x, dy, y_ref, dx_ref, g_ref = oracle_case(H, D, S)
+    grp = capi.IspGroup(H, D, S, world=p)
+    blocks = [grp.rank(r) for r in range(p)]
+    for r, b in enumerate(blocks):
+        load_weights(b, w, p, r)
+    T = S // p
+    xs = [torch.from_numpy(x[r * T:(r + 1) * T]).bfloat16().to(cuda) for r in range(p)]
+    dys = [torch.from_numpy(dy[r * T:(r + 1) * T]).bfloat16().to(cuda) for r in range(p)]
+    ys = [torch.empty_like(v) for v in xs]
+    dxs = [torch.empty_like(v) for v in xs]
+    grp.fwd(xs, ys)
+    grp.bwd(dys, dxs)
+    torch.cuda.synchronize()
+    assert rel(torch.cat(dxs).float().cpu(), dx_ref) <= TOL
+    check_grads(blocks, g_ref, p)
+    grp.close()
