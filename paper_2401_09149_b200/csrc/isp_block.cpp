@@ -154,6 +154,10 @@ struct seqplan_isp_ctx {
   bool no_bwd_prefetch = false;  // SEQPLAN_ISP_BWD_PREFETCH=0: copy-engine re-gather at backward start
   bool ce_a2a = false;           // Ulysses all-to-all on the copy engines (SEQPLAN_ISP_A2A_CE)
   bool rs_ce = false;            // push mode: reduce-scatter staged by the copy engines (SEQPLAN_ISP_RS_CE)
+  bool early_reduce = true;      // RS reductions on their own stream as slices land (SEQPLAN_ISP_EARLY_REDUCE=0: at step end)
+  cudaStream_t red = nullptr;    // reduction stream of the early reduce-scatter
+  cudaEvent_t ev_rs_sent[SEQPLAN_W_COUNT] = {};
+  cudaEvent_t ev_red_done = nullptr;
   bool qkv_slice = true;         // QKV GEMM sliced by weight-shard source (SEQPLAN_ISP_QKV_SLICE=0 turns off; +1.1 % at 4K p = 2, neutral at p = 4)
   bool recomputing = false;      // inside the backward's forward recomputation
   bool acts_live = false;        // saved activations currently allocated
@@ -937,7 +941,8 @@ void wgrad(Ctx* c, int t, const GemmOperand& A, const GemmOperand& B, int M, int
 
 // After the G-W of tensor t: hand its partial to the comm stream for the reduce-scatter.
 // Copy-engine staging of this rank's slice of every rank's partial (rank order) on the comm
-// stream; the fp32 reduction + cast/scale runs later on the compute stream (reduce_staged).
+// stream; the fp32 reduction + cast/scale runs on the reduction stream as soon as the slices land
+// (schedule_rs, early_reduce) or at the end of the step on the compute stream (reduce_staged).
 void stage_rs(Ctx* c, int t, cudaStream_t cs) {
   const bool norm = (t == SEQPLAN_W_NORM1 || t == SEQPLAN_W_NORM2);
   const int64_t esz = norm ? 4 : 2;
@@ -996,10 +1001,16 @@ void schedule_rs(Ctx* c, int t, cudaStream_t st) {
   ISP_CUDA(cudaStreamWaitEvent(c->comm, c->ev_wgrad[t], 0));
   if (c->push_mode() && !c->rs_ce) {
     push_rs(c, t, c->comm);
-    return;
+  } else {
+    barrier(c, c->comm, true);
+    stage_rs(c, t, c->comm);
   }
-  barrier(c, c->comm, true);
-  stage_rs(c, t, c->comm);
+  if (c->early_reduce) {  // reduce this tensor as soon as its slices land, beside the compute stream
+    ISP_CUDA(cudaEventRecord(c->ev_rs_sent[t], c->comm));
+    ISP_CUDA(cudaStreamWaitEvent(c->red, c->ev_rs_sent[t], 0));
+    if (c->push_mode() && !c->rs_ce) reduce_pushed(c, t, c->red);
+    else reduce_staged(c, t, c->red);
+  }
 }
 
 void bwd_phase1(Ctx* c, const bf16* dy, cudaStream_t st) {
@@ -1309,6 +1320,7 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   if (const char* e = std::getenv("SEQPLAN_ISP_BWD_PREFETCH")) c->no_bwd_prefetch = std::atoi(e) == 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_RS_CE")) c->rs_ce = std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_QKV_SLICE")) c->qkv_slice = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SEQPLAN_ISP_EARLY_REDUCE")) c->early_reduce = std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_A2A_CE")) c->ce_a2a = c->world > 1 && !c->fused_a2a && std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_RS_CTAS")) c->rs_ctas = std::atoi(e) ? std::atoi(e) : 128;
   if (const char* e = std::getenv("SEQPLAN_ISP_AG_CTAS")) c->ag_ctas = std::max(1, std::atoi(e));
@@ -1360,6 +1372,9 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
     ISP_CUDA(cudaEventCreateWithFlags(&c->ev_staged[t], cudaEventDisableTiming));
   }
   ISP_CUDA(cudaEventCreateWithFlags(&c->ev_comm_done, cudaEventDisableTiming));
+  ISP_CUDA(cudaStreamCreateWithFlags(&c->red, cudaStreamNonBlocking));
+  ISP_CUDA(cudaEventCreateWithFlags(&c->ev_red_done, cudaEventDisableTiming));
+  for (int t = 0; t < SEQPLAN_W_COUNT; ++t) ISP_CUDA(cudaEventCreateWithFlags(&c->ev_rs_sent[t], cudaEventDisableTiming));
   ISP_CUDA(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
 
   // RoPE table, computed like oracle/block_oracle.c:ob_rope_table (double -> fp32)
@@ -1517,6 +1532,10 @@ void seqplan_isp_ctx_destroy(seqplan_isp_ctx* c) {
     if (c->ev_staged[t]) cudaEventDestroy(c->ev_staged[t]);
   }
   if (c->ev_comm_done) cudaEventDestroy(c->ev_comm_done);
+  if (c->red) cudaStreamDestroy(c->red);
+  if (c->ev_red_done) cudaEventDestroy(c->ev_red_done);
+  for (int t = 0; t < SEQPLAN_W_COUNT; ++t)
+    if (c->ev_rs_sent[t]) cudaEventDestroy(c->ev_rs_sent[t]);
   if (c->ev_start) cudaEventDestroy(c->ev_start);
   delete c;
 }
@@ -1769,6 +1788,7 @@ static void bwd_epilogue(Ctx* c, cudaStream_t st) {
   } else if (c->world > 1) {
     // reduce the staged slices (fp32 accumulate, cast/scale) and join the comm stream
     for (int t : {SEQPLAN_W_DOWN, SEQPLAN_W_GATE, SEQPLAN_W_NORM2, SEQPLAN_W_O, SEQPLAN_W_QKV, SEQPLAN_W_NORM1}) {
+      if (c->early_reduce) break;  // already reduced on c->red (schedule_rs)
       if (c->push_mode() && !c->rs_ce) {
         if (!c->skip_comm()) reduce_pushed(c, t, st);
       } else {
@@ -1777,6 +1797,10 @@ static void bwd_epilogue(Ctx* c, cudaStream_t st) {
     }
     ISP_CUDA(cudaEventRecord(c->ev_comm_done, c->comm));
     ISP_CUDA(cudaStreamWaitEvent(st, c->ev_comm_done, 0));
+    if (c->early_reduce) {
+      ISP_CUDA(cudaEventRecord(c->ev_red_done, c->red));
+      ISP_CUDA(cudaStreamWaitEvent(st, c->ev_red_done, 0));
+    }
   }
   if (c->owns_pool) c->pool->step_boundary();
   if (c->push_mode()) c->push_primed = true;

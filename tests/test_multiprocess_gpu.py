@@ -14,6 +14,18 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+def _json_rows(out):
+    """Every JSON object the ranks printed; ranks share one stdout, so two rows can end up on one
+    line — decode objects one after another instead of line by line."""
+    dec, rows, i = json.JSONDecoder(), [], out.find("{")
+    while i >= 0:
+        obj, end = dec.raw_decode(out, i)
+        if isinstance(obj, dict) and "rank" in obj:
+            rows.append(obj)
+        i = out.find("{", end)
+    return rows
+
+
 def _run(n, H, D, S, mode="selective", env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={29500 + n + (7 if mode == 'fused' else 0) + (20 if H == 1024 else 0) + (40 + 3 * int(env.get('SEQPLAN_ISP_PUSH', '0')) + 5 * int(env.get('SEQPLAN_ISP_FUSED_A2A', '0')) if env else 0)}",
@@ -21,7 +33,7 @@ def _run(n, H, D, S, mode="selective", env=None):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
                        env={**os.environ, **(env or {})})
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    rows = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    rows = _json_rows(r.stdout)
     assert len(rows) == n
     return rows
 
@@ -75,7 +87,7 @@ def test_multiprocess_stack_parity(n, push):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
                        env={**os.environ, "SEQPLAN_ISP_PUSH": push})
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    rows = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    rows = _json_rows(r.stdout)
     assert len(rows) == n
     for row in rows:
         for k, v in row.items():
@@ -97,7 +109,7 @@ def test_multiprocess_stack_recompute_parity(n, push):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
                        env={**os.environ, "SEQPLAN_ISP_PUSH": push})
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    rows = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    rows = _json_rows(r.stdout)
     assert len(rows) == n
     for row in rows:
         for k, v in row.items():
