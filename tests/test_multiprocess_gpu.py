@@ -19,7 +19,11 @@ def _json_rows(out):
     line — decode objects one after another instead of line by line."""
     dec, rows, i = json.JSONDecoder(), [], out.find("{")
     while i >= 0:
-        obj, end = dec.raw_decode(out, i)
+        try:
+            obj, end = dec.raw_decode(out, i)
+        except json.JSONDecodeError:  # a brace in a log line
+            i = out.find("{", i + 1)
+            continue
         if isinstance(obj, dict) and "rank" in obj:
             rows.append(obj)
         i = out.find("{", end)
