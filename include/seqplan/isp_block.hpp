@@ -72,6 +72,25 @@ public:
         return out;
     }
 
+    /// The reference's model of this pool: run_mempool over the device pool's own recorded trace
+    /// (mempool.hpp:285-387); peak_reserved / peak_fragmented cover the whole trace.
+    FragmentationReport pool_replay() const {
+        seqplan_step_stats s{};
+        std::int64_t n = 0;
+        raise(seqplan_isp_pool_replay(ctx_, &s, &n));
+        FragmentationReport r;
+        r.peak_reserved = s.peak_reserved;
+        r.peak_fragmented = s.peak_fragmented;
+        StepStats last;
+        last.reserved = s.reserved;
+        last.allocated = s.allocated;
+        last.free_cached = s.free_cached;
+        last.fragmented = s.fragmented;
+        r.per_step.push_back(last);
+        r.final_fragmented = s.fragmented;
+        return r;
+    }
+
     /// The last fwd+bwd as a reference Timeline (needs SEQPLAN_ISP_FLAG_TIMELINE). Module
     /// index plays the role of the layer; all-to-all events run on the compute stream.
     Timeline timeline() const {
@@ -99,6 +118,52 @@ private:
     }
 
     seqplan_isp_ctx* ctx_ = nullptr;
+};
+
+/// ModelConfig::layers ISP blocks run as one step (seqplan_isp_stack_*): every forward gather
+/// issued up front and the backward re-gathers in reverse layer order on one comm stream
+/// (overlap_sim.hpp:80-153), one device pool for all layers (checkpoints between layers are
+/// MlpOutput allocations, mempool.hpp:91-135); Strategy::recompute = 1 re-runs each layer's
+/// forward in its backward.
+class IspStack {
+public:
+    IspStack(const ModelConfig& model, const Strategy& s, int rank, int device,
+             const MempoolPolicy& policy = IspBlock::default_policy(), std::uint32_t flags = 0) {
+        if (model.layers < 1) throw std::invalid_argument("IspStack needs at least one layer");
+        seqplan_isp_shape sh{model.hidden_dim, model.heads, model.seq_len, 0, 10000.0, 1e-5};
+        seqplan_strategy st{s.micro_batch, s.micro_batch_num, s.recompute, s.pp, s.dp,
+                            s.tp, s.sp, s.ps, s.gs, s.oss};
+        seqplan_mempool_policy p{policy.pinned_comm_pool ? 1 : 0, policy.consolidate_every_k_mlp,
+                                 policy.grad_premap ? 1 : 0, policy.capacity};
+        const int status = seqplan_isp_stack_create(static_cast<int>(model.layers), static_cast<int>(s.sp), rank,
+                                                    device, &sh, &st, &p, flags, &stack_);
+        if (status == SEQPLAN_ISP_ERR_INVALID) throw std::invalid_argument("seqplan_isp_stack_create: invalid plan");
+        if (status != SEQPLAN_ISP_OK)
+            throw std::runtime_error("seqplan_isp_stack_create failed (status " + std::to_string(status) + ")");
+    }
+    IspStack(const IspStack&) = delete;
+    IspStack& operator=(const IspStack&) = delete;
+    ~IspStack() { seqplan_isp_stack_destroy(stack_); }
+
+    int layers() const { return seqplan_isp_stack_layers(stack_); }
+    /// Layer l's context (weights, gradient shards, peer bootstrap); owned by the stack.
+    seqplan_isp_ctx* layer(int l) const { return seqplan_isp_stack_layer(stack_, l); }
+
+    void forward(const void* x, void* y, void* stream = nullptr) { check(seqplan_isp_stack_fwd(stack_, x, y, stream)); }
+    void backward(const void* dy, void* dx, void* stream = nullptr) {
+        check(seqplan_isp_stack_bwd(stack_, dy, dx, stream));
+    }
+
+private:
+    void check(int status) const {
+        if (status == SEQPLAN_ISP_OK) return;
+        seqplan_isp_ctx* c = seqplan_isp_stack_layer(stack_, 0);
+        const std::string msg = c ? seqplan_isp_last_error(c) : "seqplan_isp_stack";
+        if (status == SEQPLAN_ISP_ERR_INVALID) throw std::invalid_argument(msg);
+        throw std::runtime_error(msg + " (status " + std::to_string(status) + ")");
+    }
+
+    seqplan_isp_stack* stack_ = nullptr;
 };
 
 }  // namespace seqplan

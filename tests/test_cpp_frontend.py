@@ -34,3 +34,42 @@ def test_cpp_frontend_runs_and_feeds_compare_to_analytic(tmp_path, cuda):
     d = json.loads(r.stdout.strip().splitlines()[-1])
     assert d["events"] > 0 and d["makespan_ms"] > 0 and d["compute_ms"] > 0
     assert d["pool_reserved"] >= d["pool_allocated"] > 0
+
+
+def test_cpp_frontend_stack_and_replay_compile(tmp_path):
+    """seqplan::IspStack (multi-layer stacks, a = 1) and IspBlock::pool_replay build against the
+    C-ABI library; construction on a machine without a GPU fails with the reference's
+    std::runtime_error, not a crash."""
+    from paper_2401_09149_b200 import capi
+    capi.lib()
+    src = tmp_path / "stack_demo.cpp"
+    src.write_text(r'''
+#include <cstdio>
+#include "seqplan/isp_block.hpp"
+int main() {
+    seqplan::ModelConfig m;
+    m.hidden_dim = 512; m.layers = 3; m.heads = 8; m.vocab = 1; m.seq_len = 1024; m.global_batch_tokens = 1024;
+    seqplan::Strategy s;
+    s.recompute = 1;
+    seqplan::MempoolPolicy pol = seqplan::IspBlock::default_policy();
+    pol.consolidate_every_k_mlp = 2;
+    try {
+        seqplan::IspStack st(m, s, 0, 0, pol);
+        std::printf("layers %d\n", st.layers());
+        seqplan::IspBlock b(m, s, 0, 0, pol);
+        const seqplan::FragmentationReport r = b.pool_replay();
+        std::printf("replay %lld\n", static_cast<long long>(r.peak_reserved));
+    } catch (const std::runtime_error& e) {
+        std::printf("runtime_error %s\n", e.what());
+    }
+    return 0;
+}
+''')
+    exe = tmp_path / "stack_demo"
+    cmd = ["g++", "-std=c++20", "-O1", f"-I{ROOT/'include'}", "-I/usr/local/cuda/include", str(src), "-o", str(exe),
+           f"-L{LIBDIR}", "-lseqplan_isp", "-L/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{LIBDIR}"]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120,
+                       env={**os.environ, "LD_LIBRARY_PATH": "/usr/local/cuda/lib64"})
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "layers 3" in r.stdout or "runtime_error" in r.stdout
