@@ -201,6 +201,9 @@ def main():
     import faulthandler
     import signal
     faulthandler.register(signal.SIGUSR1, all_threads=True)  # `kill -USR1` dumps where a run hangs
+    # watchdog: a run that is still going after 30 min (normal runs take 1-3 min) dumps every
+    # thread's stack to stderr and exits non-zero instead of holding the GPU until an outer timeout
+    faulthandler.dump_traceback_later(float(os.environ.get("BENCH_WATCHDOG_S", "1800")), exit=True)
     args = parse()
     if args.impl == "reference":
         run_reference(args)
