@@ -46,11 +46,10 @@ struct GemmCfg {
 };
 
 struct TileSched {
-  int num_m, num_n, num_tiles;
+  int num_m, num_n, num_tiles, kGroupM = 16;
   __device__ __forceinline__ void coords(int t, int& m_blk, int& n_blk) const {
-    // Group GROUP_M row-blocks together so the ~148 concurrently resident
-    // tiles share A rows and B columns in L2.
-    constexpr int kGroupM = 16;
+    // Group kGroupM row-blocks together so the ~148 concurrently resident
+    // tiles share A rows and B columns in L2 (GemmArgs::group_m; 16 by default).
     const int per_group = kGroupM * num_n;
     const int g = t / per_group;
     const int first_m = g * kGroupM;
@@ -310,7 +309,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
 
-  TileSched sched{args.M / BM, args.N / BN, (args.M / BM) * (args.N / BN)};
+  TileSched sched{args.M / BM, args.N / BN, (args.M / BM) * (args.N / BN), args.group_m};
   const int num_kb = args.K / BK;
 
   if (warp == 0 && lane == 0) {
@@ -462,7 +461,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   const uint32_t crank = cluster_rank();
   const bool leader = crank == 0;
   const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
-  TileSched sched{args.M / (2 * BM), args.N / BN, (args.M / (2 * BM)) * (args.N / BN)};
+  TileSched sched{args.M / (2 * BM), args.N / BN, (args.M / (2 * BM)) * (args.N / BN), args.group_m};
   const int num_kb = args.K / BK;
   // work units: split_base whole tiles, then split_L tiles x split_s K-ranges (the last wave)
   const int n_units = args.split_L > 0 ? args.split_base + args.split_L * args.split_s : sched.num_tiles;
@@ -803,6 +802,7 @@ cudaError_t gemm_launch(const GemmOperand& A, const GemmOperand& B, GemmArgs arg
                         cudaStream_t stream) {
   if (args.M % BM || args.K % BK || args.M <= 0 || args.N <= 0 || args.K <= 0)
     return cudaErrorInvalidValue;
+  if (const char* f = std::getenv("SEQPLAN_GEMM_GROUP_M")) args.group_m = std::max(1, std::atoi(f));  // development
   int bn = gemm_pick_bn(args.N);
   if (const char* f = std::getenv("SEQPLAN_GEMM_BN")) {  // development override
     const int want = std::atoi(f);

@@ -54,6 +54,8 @@ struct GemmArgs {
   // persistent-grid size limit (0 = every SM): SMs held by concurrent bulk-copy comm kernels
   // are left out so no CTA of the persistent grid waits for them
   int sm_budget = 0;
+  // tile order: groups of group_m row-blocks walk the N dimension together (L2 reuse of A and B)
+  int group_m = 16;
   // Split-K of the last partial wave (CTA-pair kernel; set by gemm_launch, not by callers): the
   // first split_base tiles run whole; each of the remaining split_L tiles is cut into split_s
   // K-ranges run concurrently in the last wave. Finishers but the last leave fp32 partials in
