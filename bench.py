@@ -164,6 +164,37 @@ def parse():
     return ap.parse_args()
 
 
+def timeline_exposure(events):
+    """Exposed communication from a measured Timeline: |(comm ∪ all-to-all) minus compute| / makespan,
+    where compute = compute-stream spans other than the all-to-alls (SURVEY.md §8d cross-check)."""
+    def union(iv):
+        out = []
+        for a, b in sorted(iv):
+            if out and a <= out[-1][1]:
+                out[-1][1] = max(out[-1][1], b)
+            else:
+                out.append([a, b])
+        return out
+    comp = union([(e["start"], e["end"]) for e in events if e["stream"] == 0 and e["kind"] != "all_to_all"])
+    comm = union([(e["start"], e["end"]) for e in events if e["stream"] == 1 or e["kind"] == "all_to_all"])
+    exposed = 0.0
+    for a, b in comm:  # subtract the compute cover from each comm interval
+        cur = a
+        for c, d in comp:
+            if d <= cur or c >= b:
+                continue
+            if c > cur:
+                exposed += c - cur
+            cur = max(cur, d)
+            if cur >= b:
+                break
+        if cur < b:
+            exposed += b - cur
+    span = max(e["end"] for e in events) - min(e["start"] for e in events) if events else 0.0
+    return {"pct": 100.0 * exposed / span if span > 0 else None, "makespan_ms": span * 1e3,
+            "events": len(events), "rank": 0}
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -404,6 +435,23 @@ def main():
     else:
         pblk.close()
 
+    # cross-check of the exposure from the measured CUDA-event Timeline of one step on rank 0
+    # (SURVEY.md §8d): time the comm stream (or an all-to-all on the compute stream) is busy
+    # while no compute span runs, over the makespan. Never allowed to sink the bench line.
+    exposed_tl = None
+    if world > 1:
+        try:
+            tblk = make_ctx(capi.FLAG_TIMELINE)
+            for _ in range(2):
+                with torch.cuda.stream(stream):
+                    tblk.fwd(x, y, stream)
+                    tblk.bwd(dy, dx, stream)
+            torch.cuda.synchronize(dev)
+            exposed_tl = timeline_exposure(tblk.timeline())
+            tblk.close()
+        except Exception as ex:  # noqa: BLE001
+            exposed_tl = {"error": str(ex)[:200]}
+
     peaks = load_peaks()
     g = by.get("gemm", {"flops": 0, "s": 1e-30, "n": 0})
     achieved = g["flops"] / g["s"] / 1e12 if g["s"] > 0 else 0.0
@@ -428,6 +476,7 @@ def main():
                        "bwd_policy": "fused" if args.fused_bwd else "selective",
                        "recompute": int(args.recompute)},
             "exposed_comm_pct": None if exposed is None else 100.0 * exposed,
+            "exposed_comm_timeline": exposed_tl,
             "block_roofline": {"t_roof_ms": t_roof * 1e3, "bound": "tensor" if t_comp >= t_nvl else "nvlink",
                                "frac": (t_roof * 1e3) / ms, "flops": block_flops(H, S),
                                "nvl_bytes_per_rank": block_nvl_bytes(H, S, world),
