@@ -14,6 +14,7 @@ int main() {
         for (int trial = 0; trial < 20; ++trial) {
             seqplan::MempoolPolicy pol;
             pol.pinned_comm_pool = pol_i & 1;
+            pol.consolidate_every_k_mlp = (pol_i & 2) ? 3 : 0;  // mixed-size MLP outputs packed 3 to a region
             pol.grad_premap = false;
             isp::DevicePool pool;
             pool.set_host_only(true);
@@ -32,6 +33,12 @@ int main() {
                     live.push_back(pool.alloc(sizes[rng() % 7], tags[rng() % 4], nullptr));
                 }
                 if (op % 50 == 49) pool.step_boundary();
+                // device accounting conserves bytes under every policy
+                const auto d = pool.stats();
+                if (d.reserved != d.allocated + d.free_cached + d.fragmented) {
+                    std::printf("policy %d trial %d op %d: device conservation broken\n", pol_i, trial, op);
+                    ++failures;
+                }
             }
             for (void* p : live) pool.free(p, nullptr);
             pool.step_boundary();
@@ -39,7 +46,7 @@ int main() {
             seqplan::MempoolPolicy base = pol;
             base.pinned_comm_pool = false;
             const auto rep = seqplan::run_mempool(pool.trace(), pol);
-            if (!pol.pinned_comm_pool) {
+            if (!pol.pinned_comm_pool && !pol.consolidate_every_k_mlp) {
                 if (rep.per_step.back().reserved != pool.general_reserved()) {
                     std::printf("policy %d trial %d: pool reserved %lld model %lld\n", pol_i, trial,
                                 (long long)pool.general_reserved(), (long long)rep.per_step.back().reserved);
