@@ -53,3 +53,17 @@ def test_peer_bootstrap_gloo_world2():
     for p in procs:
         p.join(timeout=60)
     assert res == [(0, [0, 1], [64, 64]), (1, [0, 1], [64, 64])]
+
+
+def test_bench_dominant_kernel_and_timeline_exposure():
+    """bench.py's roofline line reports the tensor-core kernel with the largest share of the step,
+    and the timeline cross-check counts comm (or all-to-all) time not covered by compute."""
+    import bench
+    by = {"gemm": {"s": 26.3, "flops": 1.0}, "attn_bwd": {"s": 30.3, "flops": 1.0}, "all_gather": {"s": 50.0, "flops": 0}}
+    assert bench.dominant_kernel(by) == "attn_bwd"
+    assert bench.dominant_kernel({"gemm": {"s": 3.3, "flops": 1.0}, "attn_bwd": {"s": 0.5, "flops": 1.0}}) == "gemm"
+    assert bench.dominant_kernel({}) == "gemm"
+    ev = [dict(stream=0, kind="forward", start=0.0, end=1.0), dict(stream=1, kind="all_gather", start=0.5, end=1.5),
+          dict(stream=0, kind="all_to_all", start=1.5, end=2.0), dict(stream=0, kind="forward", start=2.0, end=3.0)]
+    r = bench.timeline_exposure(ev)
+    assert abs(r["pct"] - 100.0 / 3.0) < 1e-9 and r["events"] == 4
