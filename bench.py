@@ -1,6 +1,8 @@
 """Benchmark of the B200-native ISP transformer block (fwd + bwd), one JSON line on rank 0.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 7b_s4k] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 7b_s32k] [--impl ours|reference]
+
+Default config: 7b_s32k, the configuration BASELINE.md §3 quotes the target on (it fits one GPU).
 
 N > 1 is launched by the driver with torchrun (one process per GPU). Each rank owns S/N
 tokens and 1/N of every weight (ISP: sp = ps = N) and runs the block through the C ABI
@@ -10,10 +12,14 @@ torch.distributed), collectives are the library's own peer-memory kernels.
 metric  block fwd+bwd tokens/s (S / max-over-ranks step time), BASELINE.json
 value   device-resident inputs, CUDA events on the compute stream, L2 flushed between
         timed steps (256 MiB write), max over ranks
-e2e     same metric through the public API with pinned-host x/dy copied in and dx copied
+e2e     same metric through the public API with pinned-host x/dy copied in and y/dx copied
         out every step
-roofline  dominant kernel = the tcgen05 GEMMs (per-launch CUDA events in a profiled pass)
-cpu_baseline  the CPU fp32 oracle (oracle/block_oracle.c, OpenMP) on a bounded sample
+roofline  dominant tensor-core kernel of the config (the attention backward at 32K, the GEMMs
+        at 4K), per-launch CUDA events in a profiled pass on the launching stream
+block_roofline  max(F / (p * bf16 peak), NVLink bytes / 900 GB/s) over the step time
+cpu_baseline  the CPU fp32 oracle (oracle/block_oracle.c, OpenMP, all threads) measured on a
+        bounded sample of the config (n of the S tokens' full block work), plus the reference's
+        own planner functions (oracle/_ref/seqplan_probe --time), single-threaded
 """
 from __future__ import annotations
 
@@ -121,32 +127,95 @@ class Clocks:
 
 
 # ----------------------------------------------------------------------------------------
-# CPU baseline (oracle port, bounded sample)
+# CPU baseline (oracle port, bounded sample — measured, never extrapolated)
 # ----------------------------------------------------------------------------------------
-def cpu_baseline(cfg, budget_s=20.0):
-    """Times the CPU fp32 block oracle at a reduced sequence and extrapolates by F(S)."""
-    from oracle import block as ob
-    H, D, S = cfg["H"], cfg["D"], cfg["S"]
-    l = ob.lib()
-    cores = os.cpu_count() or 1
-    l.ob_set_threads(cores)
-    import numpy as np
-    s_sample = 128
-    while True:
-        sh = ob.Shape(H=H, D=D, S=s_sample)
-        w = ob.make_weights(sh)
-        x = ob.make_activation(sh, ob.TID_X)
-        dy = ob.make_activation(sh, ob.TID_DY)
+class CpuSample:
+    """The CPU fp32 oracle's full block fwd + bwd restricted to n token rows spread evenly over the
+    S-token sequence (oracle/block_oracle.c ob_block_sample): per-row norms, every GEMM and its
+    gradients, RoPE and each row's causal attention against its whole prefix, forward and backward.
+    That is n/S of the block's FLOPs (ratio reported), so tokens/s = n / measured seconds is the
+    oracle's own throughput on this config. The prefix K|V (the other rows' projections) is
+    prepared outside the timed region, like the GPU arm's inputs."""
+
+    def __init__(self, cfg):
+        import numpy as np
+        from oracle import block as ob
+        self.np, self.ob = np, ob
+        self.sh = ob.Shape(H=cfg["H"], D=cfg["D"], S=cfg["S"])
+        rng = np.random.default_rng(SEED)
+        self.rng = rng
+        self.w = []
+        for shp in self.sh.weight_shapes():
+            w = rng.standard_normal(shp, dtype=np.float32) * np.float32(0.02)
+            if len(shp) == 1:
+                w += 1
+            self.w.append(w)
+        S, H = self.sh.S, self.sh.H
+        self.kv = rng.random((S, 2 * H), dtype=np.float32)
+        self.kv -= 0.5
+        self.dkv = np.zeros_like(self.kv)
+        self.cores = os.cpu_count() or 1
+        ob.lib().ob_set_threads(self.cores)
+
+    def positions(self, n):
+        S = self.sh.S
+        return (self.np.arange(n, dtype=self.np.int64) * (S // n) + (S // n) // 2)
+
+    def run(self, n):
+        np = self.np
+        pos = self.positions(n)
+        x = self.rng.standard_normal((n, self.sh.H), dtype=np.float32)
+        dy = self.rng.standard_normal((n, self.sh.H), dtype=np.float32)
         t0 = time.perf_counter()
-        ob.block(sh, w, x, dy, p=1)
-        dt = time.perf_counter() - t0
-        if dt * 2.5 > budget_s or s_sample * 2 > S:
-            break
-        s_sample *= 2
-    t_full = dt * block_flops(H, S) / block_flops(H, s_sample)
-    return {"value": S / t_full, "unit": "tokens/s", "cores": cores, "kind": "port",
-            "sample": f"oracle fwd+bwd of the {H}/{D}-head block at S'={s_sample} ({dt:.2f} s, {cores} threads), "
-                      f"extrapolated to S={S} by F(S)/F(S') (F = 3(8SH^2 + 6SHI + 2S^2H))"}
+        self.ob.block_sample(self.sh, self.w, pos, x, dy, self.kv, self.dkv)
+        return time.perf_counter() - t0
+
+    def calibrate(self, target_s):
+        self.run(8)  # first touch of the weights / K|V pages and the thread pool, untimed
+        n = 32
+        while True:
+            dt = self.run(n)
+            if dt >= target_s / 2 or 2 * n > self.sh.S // 8:
+                break
+            n *= 2
+        return n, dt
+
+    def flops_ratio(self, n):
+        pos = self.positions(n)
+        H, S = self.sh.H, self.sh.S
+        return self.ob.sample_flops(self.sh, pos) / (n / S * block_flops(H, S))
+
+    def describe(self, n, dts):
+        return (f"oracle fwd+bwd of n={n} of the S={self.sh.S} tokens (every {self.sh.S // n}th position), full "
+                f"H={self.sh.H}/{self.sh.D}-head/I={self.sh.I} block work for those rows incl. causal attention "
+                f"against their whole prefix ({self.flops_ratio(n):.5f} x n/S of the block FLOPs), "
+                f"{len(dts)} runs of {min(dts):.2f}-{max(dts):.2f} s, {self.cores} threads; measured, not extrapolated")
+
+
+def cpu_baseline(cfg, budget_s=20.0):
+    """One bounded measurement of the CPU oracle on this config (bench line's cpu_baseline)."""
+    cs = CpuSample(cfg)
+    n, _ = cs.calibrate(budget_s / 4)
+    dts = [cs.run(n) for _ in range(2)]
+    dt = sorted(dts)[len(dts) // 2]
+    return {"value": n / dt, "unit": "tokens/s", "cores": cs.cores, "kind": "port",
+            "sample": cs.describe(n, dts), "reference_cpu_path": reference_cpu_path(cfg)}
+
+
+def reference_cpu_path(cfg_name_or_cfg):
+    """The reference's own executable code on this path — its planner's estimate_step,
+    simulate_forward/backward and run_mempool, compiled from the reference headers into
+    oracle/_ref/seqplan_probe — timed single-threaded on this host (µs per call)."""
+    name = cfg_name_or_cfg if isinstance(cfg_name_or_cfg, str) else next(
+        (k for k, v in CONFIGS.items() if v == cfg_name_or_cfg), None)
+    exe = ROOT / "oracle" / "_ref" / "seqplan_probe"
+    if name is None or not exe.exists():
+        return {"error": "oracle/_ref/seqplan_probe not built"}
+    try:
+        r = subprocess.run([str(exe), "--time", name], capture_output=True, text=True, timeout=120)
+        return json.loads(r.stdout)
+    except Exception as ex:  # never sinks the bench line
+        return {"error": str(ex)[:200]}
 
 
 # ----------------------------------------------------------------------------------------
@@ -155,7 +224,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="7b_s4k", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="7b_s32k", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -218,25 +287,29 @@ def dist_env():
 
 def run_reference(args):
     """--impl reference: the reference has no executable block (its CPU path is the planner's
-    price model), so the CPU restatement of the path (oracle port) is timed on the host."""
+    price model, timed in cpu_baseline.reference_cpu_path), so the CPU restatement of the path
+    (oracle port, all host threads) is timed on the same config: every step is one bounded
+    sample of the workload (CpuSample: n of the S tokens' full block work), sized to ~2 s."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
-    steps = []
+    cs = CpuSample(cfg)
+    n, _ = cs.calibrate(2.0)
     for _ in range(max(1, args.warmup)):
-        cpu_baseline(cfg, budget_s=4.0)
-    for _ in range(max(1, args.steps)):
-        steps.append(cpu_baseline(cfg, budget_s=8.0))
-    v = sorted(s["value"] for s in steps)[len(steps) // 2]
-    cb = dict(steps[0])
-    cb["value"] = v
+        cs.run(n)
+    dts = [cs.run(n) for _ in range(max(1, args.steps))]
+    v = n * len(dts) / sum(dts)
+    cb = {"value": v, "unit": "tokens/s", "cores": cs.cores, "kind": "port", "sample": cs.describe(n, dts),
+          "reference_cpu_path": reference_cpu_path(args.config)}
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cfg["S"] / v * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum(dts) / len(dts) * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (index-keyed splitmix64 normals)",
+            "data": "synthetic",
             "config": {"workload": f"{args.config}: one ISP block fwd+bwd, H={cfg['H']}, heads={cfg['D']}, "
-                                   f"S={cfg['S']}, b=1 (CPU oracle port, reduced-S sample extrapolated)"},
+                                   f"I={mlp_dim(cfg['H'])}, S={cfg['S']}, b=1 (CPU oracle port; each step = "
+                                   f"{n} of the {cfg['S']} tokens' block work, ms_per_step is that sample's time)",
+                       "sample_tokens_per_step": n, "sample_flops_ratio": cs.flops_ratio(n)},
             "cpu_baseline": cb, "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -333,27 +406,31 @@ def main():
     clocks = clk.summary()
 
     # ---- end to end through the public API with host buffers ----
-    # Every step copies its own inputs x, dy from pinned host memory and reads its result dx back.
-    # The loop is the one a training job runs: inputs are double-buffered, step i+1's H2D copies run
-    # on a copy stream while step i computes, and step i's D2H overlaps step i+1. The timed region
-    # spans the first copy-in to the last copy-out (all copies of all steps are inside it).
+    # Every step copies its own inputs x, dy from pinned host memory and reads its results y and dx
+    # back. The loop is the one a training job runs: inputs and outputs are double-buffered, step
+    # i+1's H2D copies run on a copy stream while step i computes, and step i's D2H copies overlap
+    # step i+1. Step i+2 reuses step i's buffers only after step i's D2H has read them (copied[b]).
+    # The timed region spans the first copy-in to the last copy-out.
     e2e = None
     if not args.no_e2e:
         hx = torch.empty(T, H, dtype=torch.bfloat16).pin_memory()
         hdy = torch.empty_like(hx).pin_memory()
+        hy = [torch.empty_like(hx).pin_memory() for _ in range(2)]
         hdx = [torch.empty_like(hx).pin_memory() for _ in range(2)]
         hx.copy_(x.cpu())
         hdy.copy_(dy.cpu())
-        xb, dyb, dxb = [x, torch.empty_like(x)], [dy, torch.empty_like(dy)], [dx, torch.empty_like(dx)]
+        xb, dyb = [x, torch.empty_like(x)], [dy, torch.empty_like(dy)]
+        yb, dxb = [y, torch.empty_like(y)], [dx, torch.empty_like(dx)]
         copy_in, copy_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
         in_ready = [torch.cuda.Event() for _ in range(2)]
         step_done = [torch.cuda.Event() for _ in range(2)]
-        for ev in step_done:
+        copied = [torch.cuda.Event() for _ in range(2)]
+        for ev in step_done + copied:
             ev.record(stream)
 
         def issue_in(i):
             b = i % 2
-            copy_in.wait_event(step_done[b])  # step i-2 is done with this buffer pair
+            copy_in.wait_event(step_done[b])  # step i-2 is done reading this input pair
             with torch.cuda.stream(copy_in):
                 xb[b].copy_(hx, non_blocking=True)
                 dyb[b].copy_(hdy, non_blocking=True)
@@ -362,12 +439,15 @@ def main():
         def run(i):
             b = i % 2
             stream.wait_event(in_ready[b])
-            blk.fwd(xb[b], y, stream)
+            stream.wait_event(copied[b])  # step i-2's y / dx have been read back
+            blk.fwd(xb[b], yb[b], stream)
             blk.bwd(dyb[b], dxb[b], stream)
             step_done[b].record(stream)
             copy_out.wait_event(step_done[b])
             with torch.cuda.stream(copy_out):
+                hy[b].copy_(yb[b], non_blocking=True)
                 hdx[b].copy_(dxb[b], non_blocking=True)
+                copied[b].record(copy_out)
 
         def e2e_loop(n):
             issue_in(0)
@@ -394,8 +474,9 @@ def main():
         ms_e2e = float(t.item())
         nb = T * H * 2
         e2e = {"value": S / (ms_e2e / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": 2 * nb,
-               "d2h_bytes_per_step": nb, "ms_per_step": ms_e2e,
-               "pipelining": "double-buffered inputs: step i+1's H2D and step i's D2H overlap compute",
+               "d2h_bytes_per_step": 2 * nb, "ms_per_step": ms_e2e,
+               "copies": "per step and rank: x, dy pinned-host -> device; y, dx device -> pinned host",
+               "pipelining": "double-buffered inputs and outputs: step i+1's H2D and step i's D2H overlap compute",
                "l2": "flushed once before the loop; per-step working set (weights, activations) > L2"}
 
     # ---- profiled pass: per-kernel CUDA events (not the headline number) ----
@@ -471,7 +552,7 @@ def main():
     g = by.get(dom, {"flops": 0, "s": 1e-30, "n": 0})
     achieved = g["flops"] / g["s"] / 1e12 if g["s"] > 0 else 0.0
     t_comp = block_flops(H, S) / world / (peaks["bf16"] * 1e12)
-    t_nvl = block_nvl_bytes(H, S, world) / 770e9
+    t_nvl = block_nvl_bytes(H, S, world) / 900e9  # 900 GB/s per direction
     t_roof = max(t_comp, t_nvl)
     traffic = None
     tf = ROOT / "profiles" / f"{dom}_traffic_{args.config}.json"
@@ -494,7 +575,8 @@ def main():
             "exposed_comm_timeline": exposed_tl,
             "block_roofline": {"t_roof_ms": t_roof * 1e3, "bound": "tensor" if t_comp >= t_nvl else "nvlink",
                                "frac": (t_roof * 1e3) / ms, "flops": block_flops(H, S),
-                               "nvl_bytes_per_rank": block_nvl_bytes(H, S, world),
+                               "nvl_bytes_per_rank": block_nvl_bytes(H, S, world), "nvl_gbs": 900.0,
+                               "frac_at_measured_770_gbs": max(t_comp, block_nvl_bytes(H, S, world) / 770e9) * 1e3 / ms,
                                "peak_tflops": peaks["bf16"], "peak_src": peaks["src"]},
             "roofline": {"kernel": KERNEL_NAMES[dom], "bound": "tensor",
                          "achieved": achieved, "peak": peaks["bf16"], "unit": "TFLOP/s",

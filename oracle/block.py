@@ -42,6 +42,8 @@ def lib():
         l.ob_rope_table.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_double, fp, fp]
         pp = ctypes.POINTER(fp)
         l.ob_block_isp.argtypes = [ctypes.POINTER(ObShape), ctypes.c_int, pp, fp, fp, fp, fp, pp]
+        l.ob_block_sample.argtypes = [ctypes.POINTER(ObShape), pp, ctypes.POINTER(ctypes.c_int64), ctypes.c_int64,
+                                      fp, fp, fp, fp, fp, fp, pp]
         l.ob_set_threads.argtypes = [ctypes.c_int]
         l.ob_max_threads.restype = ctypes.c_int
         _lib = l
@@ -116,6 +118,41 @@ def block(shape: Shape, weights, x, dy, p: int = 1, threads: int = 0):
     if rc != 0:
         raise ValueError(f"oracle rejected shape {shape} p={p}")
     return y, dx, [g.reshape(s) for g, s in zip(grads, shape.weight_shapes())]
+
+
+def block_sample(shape: Shape, weights, pos, x_rows, dy_rows, kv, dkv, grads=None):
+    """The full fwd + bwd work of the token rows at positions `pos` (bench.py's bounded CPU sample;
+    block_oracle.c ob_block_sample). kv [S, 2H]: rotated K|V of every position (the sampled rows'
+    own are written in); dkv [S, 2H] accumulates their dK|dV contributions. Returns (y, dx, grads)."""
+    l = lib()
+    ws = [np.ascontiguousarray(w, dtype=np.float32).reshape(-1) for w in weights]
+    if grads is None:
+        grads = [np.zeros_like(w) for w in ws]
+    pos = np.ascontiguousarray(pos, dtype=np.int64)
+    x_rows = np.ascontiguousarray(x_rows, dtype=np.float32)
+    dy_rows = np.ascontiguousarray(dy_rows, dtype=np.float32)
+    assert kv.dtype == np.float32 and kv.flags.c_contiguous and kv.shape == (shape.S, 2 * shape.H)
+    assert dkv.dtype == np.float32 and dkv.flags.c_contiguous and dkv.shape == kv.shape
+    y = np.empty_like(x_rows)
+    dx = np.empty_like(x_rows)
+    FP = ctypes.POINTER(ctypes.c_float)
+    warr = (FP * 7)(*[_fp(w) for w in ws])
+    garr = (FP * 7)(*[_fp(g) for g in grads])
+    sh = shape.c()
+    rc = l.ob_block_sample(ctypes.byref(sh), warr, pos.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), pos.size,
+                           _fp(x_rows), _fp(dy_rows), _fp(kv), _fp(dkv), _fp(y), _fp(dx), garr)
+    if rc != 0:
+        raise ValueError(f"oracle rejected sample of {shape}")
+    return y, dx, grads
+
+
+def sample_flops(shape: Shape, pos):
+    """Algorithmic FLOPs of block_sample (same convention as the block: 3x the forward, causal
+    attention 4*d per head per (query, key<=query) pair in the forward)."""
+    H, I = shape.H, shape.I
+    per_row = 8 * H * H + 6 * H * I
+    attn = 4 * H * float(np.sum(np.asarray(pos, np.float64) + 1))
+    return 3.0 * (len(pos) * per_row + attn)
 
 
 def rope_table(S: int, d: int, base: float = 10000.0):

@@ -108,34 +108,54 @@ static void mm_nt(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, 
     }
 }
 
-/* C[M,N] (+)= A[M,K] * B[K,N] */
+/* C[M,N] (+)= A[M,K] * B[K,N]. Cache-blocked (16 rows x 512 columns of C per task, K in
+ * blocks of 128 so the B block stays in L2 across the 16 rows); every C element still sums k
+ * in ascending order, so the result is independent of the blocking. */
 static void mm_nn(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
                   int64_t ldb, float* C, int64_t ldc, int accumulate) {
-#pragma omp parallel for schedule(static)
-  for (int64_t i = 0; i < M; ++i) {
-    float* c = C + i * ldc;
-    if (!accumulate) memset(c, 0, sizeof(float) * (size_t)N);
-    for (int64_t k = 0; k < K; ++k) {
-      const float a = A[i * lda + k];
-      const float* b = B + k * ldb;
-      for (int64_t j = 0; j < N; ++j) c[j] += a * b[j];
+#pragma omp parallel for schedule(static) collapse(2)
+  for (int64_t i0 = 0; i0 < M; i0 += 16)
+    for (int64_t j0 = 0; j0 < N; j0 += 512) {
+      const int64_t i1 = i0 + 16 < M ? i0 + 16 : M;
+      const int64_t j1 = j0 + 512 < N ? j0 + 512 : N;
+      if (!accumulate)
+        for (int64_t i = i0; i < i1; ++i) memset(C + i * ldc + j0, 0, sizeof(float) * (size_t)(j1 - j0));
+      for (int64_t k0 = 0; k0 < K; k0 += 128) {
+        const int64_t k1 = k0 + 128 < K ? k0 + 128 : K;
+        for (int64_t i = i0; i < i1; ++i) {
+          float* c = C + i * ldc;
+          for (int64_t k = k0; k < k1; ++k) {
+            const float a = A[i * lda + k];
+            const float* b = B + k * ldb;
+            for (int64_t j = j0; j < j1; ++j) c[j] += a * b[j];
+          }
+        }
+      }
     }
-  }
 }
 
-/* C[M,N] (+)= A[K,M]^T * B[K,N]  (weight gradients) */
+/* C[M,N] (+)= A[K,M]^T * B[K,N]  (weight gradients); blocked like mm_nn */
 static void mm_tn(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
                   int64_t ldb, float* C, int64_t ldc, int accumulate) {
-#pragma omp parallel for schedule(static)
-  for (int64_t i = 0; i < M; ++i) {
-    float* c = C + i * ldc;
-    if (!accumulate) memset(c, 0, sizeof(float) * (size_t)N);
-    for (int64_t k = 0; k < K; ++k) {
-      const float a = A[k * lda + i];
-      const float* b = B + k * ldb;
-      for (int64_t j = 0; j < N; ++j) c[j] += a * b[j];
+#pragma omp parallel for schedule(static) collapse(2)
+  for (int64_t i0 = 0; i0 < M; i0 += 16)
+    for (int64_t j0 = 0; j0 < N; j0 += 512) {
+      const int64_t i1 = i0 + 16 < M ? i0 + 16 : M;
+      const int64_t j1 = j0 + 512 < N ? j0 + 512 : N;
+      if (!accumulate)
+        for (int64_t i = i0; i < i1; ++i) memset(C + i * ldc + j0, 0, sizeof(float) * (size_t)(j1 - j0));
+      for (int64_t k0 = 0; k0 < K; k0 += 128) {
+        const int64_t k1 = k0 + 128 < K ? k0 + 128 : K;
+        for (int64_t i = i0; i < i1; ++i) {
+          float* c = C + i * ldc;
+          for (int64_t k = k0; k < k1; ++k) {
+            const float a = A[k * lda + i];
+            const float* b = B + k * ldb;
+            for (int64_t j = j0; j < j1; ++j) c[j] += a * b[j];
+          }
+        }
+      }
     }
-  }
 }
 
 /* y = x * rstd * g ; rstd[t] saved */
@@ -520,4 +540,180 @@ int ob_max_threads(void) {
 #else
   return 1;
 #endif
+}
+
+/* dot product with 16 partial sums (vectorisable without -ffast-math); d % 16 == 0 */
+static inline float dot16(const float* a, const float* b, int64_t d) {
+  float acc[16] = {0};
+  for (int64_t k = 0; k < d; k += 16)
+    for (int l = 0; l < 16; ++l) acc[l] += a[k + l] * b[k + l];
+  float s = 0;
+  for (int l = 0; l < 16; ++l) s += acc[l];
+  return s;
+}
+
+/* ------------------------------------------------------------------------------------
+ * Bounded sample of the block's work (bench.py's CPU baseline / reference arm; never a
+ * parity path). The full fwd + bwd of n token rows at positions pos[] of an S-token sequence:
+ * per-row norms, the QKV / O / gate / up / down GEMMs and all their gradients, RoPE, and the
+ * causal attention of each row against its whole prefix, forward and backward (the row's
+ * dK / dV contributions accumulate into dkv). kv [S, 2H] holds the rotated K | V of every
+ * position (the caller prepares it outside the timed region; the sampled rows' own K, V are
+ * written in). With n rows spread evenly over the sequence this is n/S of the block's FLOPs.
+ * W: full weights (OB_* order); grad: full-size gradient accumulators.
+ * ------------------------------------------------------------------------------------ */
+int ob_block_sample(const ob_shape* sh, const float* const* W, const int64_t* pos, int64_t n,
+                    const float* x, const float* dy, float* kv, float* dkv, float* y, float* dx,
+                    float* const* grad) {
+  const int64_t H = sh->H, D = sh->D, S = sh->S, I = sh->I, d = H / D;
+  if (n < 1 || H % D || d % 16) return -1;
+  for (int64_t i = 0; i < n; ++i)
+    if (pos[i] < 0 || pos[i] >= S) return -1;
+  const float scale = (float)(1.0 / sqrt((double)d));
+  float* cos_t = zalloc(S * (d / 2));
+  float* sin_t = zalloc(S * (d / 2));
+  ob_rope_table(S, d, sh->rope_base, cos_t, sin_t);
+  float *n1 = zalloc(n * H), *r1 = zalloc(n), *qkv = zalloc(n * 3 * H), *o = zalloc(n * H);
+  float *lse = zalloc(n * D), *h = zalloc(n * H), *n2 = zalloc(n * H), *r2 = zalloc(n);
+  float *g = zalloc(n * I), *u = zalloc(n * I), *a = zalloc(n * I);
+
+  /* forward */
+  rmsnorm_fwd(n, H, x, W[OB_NORM1], sh->eps, n1, r1);
+  mm_nt(n, 3 * H, H, n1, H, W[OB_QKV], H, qkv, 3 * H, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    rope_apply(1, pos[i], sh, qkv + i * 3 * H, 3 * H, cos_t, sin_t, +1);
+    memcpy(kv + pos[i] * 2 * H, qkv + i * 3 * H + H, sizeof(float) * (size_t)(2 * H));
+  }
+  /* attention, head-parallel; keys in blocks of 64 shared by all rows (K / V read once per
+   * block instead of once per row) */
+  int64_t pmax = 0;
+  for (int64_t i = 0; i < n; ++i) pmax = pos[i] > pmax ? pos[i] : pmax;
+  const int64_t KB = 64;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t hh = 0; hh < D; ++hh) {
+    float* sc = (float*)malloc(sizeof(float) * (size_t)(n * (pmax + 1)));
+    const int64_t ld = pmax + 1;
+    for (int64_t j0 = 0; j0 <= pmax; j0 += KB)
+      for (int64_t i = 0; i < n; ++i) {
+        const float* qr = qkv + i * 3 * H + hh * d;
+        const int64_t j1 = j0 + KB - 1 < pos[i] ? j0 + KB - 1 : pos[i];
+        for (int64_t j = j0; j <= j1; ++j) {
+          const float* kr = kv + j * 2 * H + hh * d;
+          sc[i * ld + j] = dot16(qr, kr, d) * scale;
+        }
+      }
+    for (int64_t i = 0; i < n; ++i) {
+      float* p = sc + i * ld;
+      float mx = -INFINITY;
+      for (int64_t j = 0; j <= pos[i]; ++j) mx = p[j] > mx ? p[j] : mx;
+      double sum = 0;
+      for (int64_t j = 0; j <= pos[i]; ++j) { p[j] = expf(p[j] - mx); sum += p[j]; }
+      const float inv = (float)(1.0 / sum);
+      for (int64_t j = 0; j <= pos[i]; ++j) p[j] *= inv;
+      lse[i * D + hh] = mx + (float)log(sum);
+      float* orow = o + i * H + hh * d;
+      for (int64_t c = 0; c < d; ++c) orow[c] = 0;
+    }
+    for (int64_t j0 = 0; j0 <= pmax; j0 += KB)
+      for (int64_t i = 0; i < n; ++i) {
+        float* orow = o + i * H + hh * d;
+        const int64_t j1 = j0 + KB - 1 < pos[i] ? j0 + KB - 1 : pos[i];
+        for (int64_t j = j0; j <= j1; ++j) {
+          const float w = sc[i * ld + j];
+          const float* vr = kv + j * 2 * H + H + hh * d;
+          for (int64_t c = 0; c < d; ++c) orow[c] += w * vr[c];
+        }
+      }
+    free(sc);
+  }
+  mm_nt(n, H, H, o, H, W[OB_O], H, h, H, 0);
+  for (int64_t i = 0; i < n * H; ++i) h[i] += x[i];
+  rmsnorm_fwd(n, H, h, W[OB_NORM2], sh->eps, n2, r2);
+  mm_nt(n, I, H, n2, H, W[OB_GATE], H, g, I, 0);
+  mm_nt(n, I, H, n2, H, W[OB_UP], H, u, I, 0);
+  for (int64_t i = 0; i < n * I; ++i) a[i] = silu_f(g[i]) * u[i];
+  mm_nt(n, H, I, a, I, W[OB_DOWN], I, y, H, 0);
+  for (int64_t i = 0; i < n * H; ++i) y[i] += h[i];
+
+  /* backward */
+  float *da = zalloc(n * I), *dgu = zalloc(n * I), *dn2 = zalloc(n * H), *dh = zalloc(n * H);
+  float *dO = zalloc(n * H), *dqkv = zalloc(n * 3 * H), *dn1 = zalloc(n * H);
+  memcpy(dh, dy, sizeof(float) * (size_t)(n * H));
+  mm_nn(n, I, H, dy, H, W[OB_DOWN], I, da, I, 0);
+  mm_tn(H, I, n, dy, H, a, I, grad[OB_DOWN], I, 1);
+  for (int64_t i = 0; i < n * I; ++i) {
+    const float gv = g[i], sg = 1.f / (1.f + expf(-gv)), dav = da[i];
+    dgu[i] = dav * u[i] * sg * (1.f + gv * (1.f - sg));
+    da[i] = dav * gv * sg;
+  }
+  mm_nn(n, H, I, dgu, I, W[OB_GATE], H, dn2, H, 0);
+  mm_nn(n, H, I, da, I, W[OB_UP], H, dn2, H, 1);
+  mm_tn(I, H, n, dgu, I, n2, H, grad[OB_GATE], H, 1);
+  mm_tn(I, H, n, da, I, n2, H, grad[OB_UP], H, 1);
+  rmsnorm_bwd(n, H, h, W[OB_NORM2], r2, dn2, dh, grad[OB_NORM2]);
+  mm_nn(n, H, H, dh, H, W[OB_O], H, dO, H, 0);
+  mm_tn(H, H, n, dh, H, o, H, grad[OB_O], H, 1);
+  /* attention backward: head-parallel (every head's dK / dV columns have one writer), keys in
+   * blocks shared by all rows as in the forward */
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t hh = 0; hh < D; ++hh) {
+    const int64_t ld = pmax + 1;
+    float* P = (float*)malloc(sizeof(float) * (size_t)(n * ld));
+    float* dS = (float*)malloc(sizeof(float) * (size_t)(n * ld));
+    float* Dt = (float*)malloc(sizeof(float) * (size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+      const float* dor = dO + i * H + hh * d;
+      const float* orow = o + i * H + hh * d;
+      float acc = 0;
+      for (int64_t c = 0; c < d; ++c) acc += dor[c] * orow[c];
+      Dt[i] = acc;
+    }
+    for (int64_t j0 = 0; j0 <= pmax; j0 += KB)
+      for (int64_t i = 0; i < n; ++i) {
+        const float* qr = qkv + i * 3 * H + hh * d;
+        const float* dor = dO + i * H + hh * d;
+        const float Lse = lse[i * D + hh];
+        const int64_t j1 = j0 + KB - 1 < pos[i] ? j0 + KB - 1 : pos[i];
+        for (int64_t j = j0; j <= j1; ++j) {
+          const float* kr = kv + j * 2 * H + hh * d;
+          const float* vr = kr + H;
+          const float sv = dot16(qr, kr, d), dp = dot16(dor, vr, d);
+          const float pv = expf(sv * scale - Lse);
+          P[i * ld + j] = pv;
+          dS[i * ld + j] = pv * (dp - Dt[i]) * scale;
+        }
+      }
+    for (int64_t j0 = 0; j0 <= pmax; j0 += KB)
+      for (int64_t i = 0; i < n; ++i) {
+        const float* qr = qkv + i * 3 * H + hh * d;
+        const float* dor = dO + i * H + hh * d;
+        float* dqr = dqkv + i * 3 * H + hh * d;
+        const int64_t j1 = j0 + KB - 1 < pos[i] ? j0 + KB - 1 : pos[i];
+        for (int64_t j = j0; j <= j1; ++j) {
+          const float* kr = kv + j * 2 * H + hh * d;
+          float* dkr = dkv + j * 2 * H + hh * d;
+          float* dvr = dkr + H;
+          const float ds = dS[i * ld + j], pv = P[i * ld + j];
+          for (int64_t c = 0; c < d; ++c) {
+            dqr[c] += ds * kr[c];
+            dkr[c] += ds * qr[c];
+            dvr[c] += pv * dor[c];
+          }
+        }
+      }
+    free(P); free(dS); free(Dt);
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    memcpy(dqkv + i * 3 * H + H, dkv + pos[i] * 2 * H, sizeof(float) * (size_t)(2 * H));
+    rope_apply(1, pos[i], sh, dqkv + i * 3 * H, 3 * H, cos_t, sin_t, -1);
+  }
+  mm_nn(n, H, 3 * H, dqkv, 3 * H, W[OB_QKV], H, dn1, H, 0);
+  mm_tn(3 * H, H, n, dqkv, 3 * H, n1, H, grad[OB_QKV], H, 1);
+  memcpy(dx, dh, sizeof(float) * (size_t)(n * H));
+  rmsnorm_bwd(n, H, x, W[OB_NORM1], r1, dn1, dx, grad[OB_NORM1]);
+
+  free(da); free(dgu); free(dn2); free(dh); free(dO); free(dqkv); free(dn1);
+  free(n1); free(r1); free(qkv); free(o); free(lse); free(h); free(n2); free(r2);
+  free(g); free(u); free(a); free(cos_t); free(sin_t);
+  return 0;
 }

@@ -16,9 +16,12 @@
 //   simulate_forward / backward  overlap_sim.hpp:80-153
 //   compare_to_analytic          overlap_sim.hpp:165-173
 //   synthesize_trace, run_mempool mempool.hpp:91-135, 285-387
+#include <chrono>
 #include <cstdio>
+#include <cstring>
 #include <random>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "seqplan/cost.hpp"
@@ -110,9 +113,90 @@ void dump_report(const FragmentationReport& r) {
     std::printf("}}");
 }
 
+// --time <config>: the reference's own CPU path for one block of the config, timed on this host
+// (bench.py's cpu_baseline): estimate_step at p = 1, 2, 4, 8 (cost.hpp:268-297),
+// simulate_forward(InterLayerPrefetch) + simulate_backward(Selective) of a 32-layer workload built
+// from the block's own prices (overlap_sim.hpp:80-153), synthesize_trace + run_mempool (all
+// policies on) of the 32-layer a = 1 trace at p = 8 (mempool.hpp:91-135, 285-387). Microseconds
+// per call, median of 7 repetitions of a loop sized to ~20 ms.
+template <class F>
+double time_us(F&& f) {
+    using clk = std::chrono::steady_clock;
+    int iters = 1;
+    for (;;) {
+        auto t0 = clk::now();
+        for (int i = 0; i < iters; ++i) f();
+        const double dt = std::chrono::duration<double>(clk::now() - t0).count();
+        if (dt > 0.02 || iters > (1 << 24)) break;
+        iters *= 2;
+    }
+    std::vector<double> v;
+    for (int r = 0; r < 7; ++r) {
+        auto t0 = clk::now();
+        for (int i = 0; i < iters; ++i) f();
+        v.push_back(std::chrono::duration<double>(clk::now() - t0).count() * 1e6 / iters);
+    }
+    std::sort(v.begin(), v.end());
+    return v[3];
+}
+
+volatile double g_sink = 0;
+
+int time_config(const char* name) {
+    const BlockCfg* c = nullptr;
+    for (const auto& k : kConfigs)
+        if (!std::strcmp(k.name, name)) c = &k;
+    if (!c) return 2;
+    const BandwidthProfile flat = BandwidthProfile::flat(900e9);
+    ComputeModel cm;
+    cm.peak_flops_per_gpu = 1656.3e12;
+    cm.efficiency = 1.0;
+    OverlapModel om;
+    std::printf("{\"config\":\"%s\"", c->name);
+    for (long long p : {1LL, 2LL, 4LL, 8LL}) {
+        const ModelConfig m = block_model(*c);
+        ClusterConfig cl{p, p < 8 ? p : 8, 192LL << 30};
+        const Strategy s = isp(p);
+        std::printf(",\"estimate_step_p%lld_us\":", p);
+        num(time_us([&] { g_sink = g_sink + estimate_step(s, m, cl, flat, cm, om).t_step; }));
+    }
+    {  // 32 layers with this block's p = 8 prices (fwd compute, gather, bwd G-X / G-W, RS)
+        const ModelConfig m = block_model(*c);
+        ClusterConfig cl{8, 8, 192LL << 30};
+        const Strategy s = isp(8);
+        auto pl = place_groups(cl, s);
+        const auto comm = estimate_comm_layer(s, m, cl, pl, flat);
+        const double comp = estimate_comp_layer(s, m, cm);
+        const double ag = comm.ps / 3.0;
+        std::vector<LayerWorkload> layers(32, LayerWorkload{comp / 3.0, ag, comp / 3.0, comp / 3.0, ag});
+        std::printf(",\"simulate_fwd_bwd_L32_us\":");
+        num(time_us([&] {
+            g_sink = g_sink + simulate_forward(layers, ForwardPolicy::InterLayerPrefetch, 0.0).makespan +
+                     simulate_backward(layers, BackwardPolicy::Selective, 0.0).makespan;
+        }));
+    }
+    {
+        ModelConfig m = block_model(*c, 32);
+        Strategy s = isp(8, 1);
+        ClusterConfig cl{8, 8, 192LL << 30};
+        auto trace = synthesize_trace(m, s, cl);
+        MempoolPolicy pol;
+        pol.pinned_comm_pool = true;
+        pol.consolidate_every_k_mlp = 3;
+        pol.grad_premap = true;
+        pol.capacity = 192LL << 30;
+        std::printf(",\"run_mempool_L32_p8_us\":");
+        num(time_us([&] { g_sink = g_sink + (double)run_mempool(trace, pol).peak_reserved; }));
+        std::printf(",\"trace_ops\":%zu", trace.ops.size());
+    }
+    std::printf(",\"threads\":1}\n");
+    return 0;
+}
+
 }  // namespace
 
-int main() {
+int main(int argc, char** argv) {
+    if (argc == 3 && !std::strcmp(argv[1], "--time")) return time_config(argv[2]);
     Out o;
     std::printf("{");
 

@@ -1433,6 +1433,387 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
+// =====================================================================================
+// Causal flash-attention backward, 128 x 128 tiles (d = 128): the production backward.
+//
+// CTA = 128 keys x 1 head; iterates over 128-query tiles i >= the key tile (causal). Every
+// MMA is M = 128, N = 128, so the shared-memory operand traffic of the SS MMAs is 8 KB per
+// 64 tensor cycles (the 128 B/clk smem port is never the bound, unlike N = 64 tiles):
+//   S^T  = K Q_i^T          (SS)   -> TMEM S   (cols   0..127)
+//   dP^T = V dO_i^T         (SS)   -> TMEM dP  (cols 128..255)
+//   P^T  = exp2(S^T*scale*log2e - lse*log2e) (bf16, over the S columns it came from)
+//   dS^T = P^T (dP^T - delta)        (bf16, over the dP columns, and into smem as [key][q])
+//   dV  += P^T dO_i         (TS)   -> TMEM dV  (cols 384..511)
+//   dK  += dS^T Q_i         (TS)   -> TMEM dK  (cols 256..383)
+//   dQ_i = dS K             (SS, A = dS^T smem MN-major) -> TMEM dP columns (dP^T consumed)
+// MMA issue order per tile: dV(i), S(i+1), dK(i), dQ(i), dP(i+1): S(i+1) reuses the S columns
+// right after dV(i) consumed P(i) (tcgen05 ops of one thread execute in order), so softmax of
+// tile i+1 runs under dK(i)/dQ(i)/dP(i+1); dS(i+1) runs under dV(i+1)/S(i+2).
+// dQ: 4 warps drain the dQ columns (thread = query row), then stage them (fp32, SW128) in the
+// dS buffer and TMA-reduce (cp.reduce.async.bulk.tensor .add) into dq_acc, 64 columns a round.
+// Shared memory: K, V 64 KB + Q, dO 2 stages 128 KB + dS^T / dQ staging 32 KB = 224 KB.
+// Warps: 0..7 P/dS (a warp pair per TMEM lane quadrant, 64 queries each), 8..11 dQ drain +
+// reduction, 12 TMA, 13 MMA (14, 15 idle: warpgroup-aligned roles).
+// =====================================================================================
+struct Bwd2Cfg {
+  static constexpr int kTile = 128 * 128 * 2;  // [2 chunks][128 rows][64 cols] bf16, SW128
+  static constexpr int kOffK = 0;
+  static constexpr int kOffV = kTile;
+  static constexpr int kOffQ = 2 * kTile;   // stage s at kOffQ + s * kTile
+  static constexpr int kOffDO = 4 * kTile;  // stage s at kOffDO + s * kTile
+  static constexpr int kOffDS = 6 * kTile;  // dS^T [2 q chunks][128 keys][64 q]; dQ fp32 staging
+  static constexpr int kOffBar = 7 * kTile;
+  static constexpr int kBytes = kOffBar + 256 + 1024;
+  static_assert(kBytes <= 232448, "exceeds the 227 KB per-CTA shared memory");
+};
+constexpr int kBwd2Threads = 512;
+
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* smem_src, int32_t c0,
+                                                  int32_t c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kBwd2Threads, 1)
+    attn_bwd2_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
+                     const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mDO,
+                     const __grid_constant__ CUtensorMap mDQ, const float* __restrict__ lse,
+                     const float* __restrict__ delta, float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dk_out,
+                     __nv_bfloat16* __restrict__ dv_out, int64_t ld_d, int S, float scale,
+                     const __grid_constant__ AttnPush push, int dbg) {
+  using L = Bwd2Cfg;
+  constexpr int D = 128;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* q_full = bar + 1;     // [2]
+  uint64_t* q_empty = bar + 3;    // [2]
+  uint64_t* do_full = bar + 5;    // [2]
+  uint64_t* do_empty = bar + 7;   // [2]
+  uint64_t* s_full = bar + 9;
+  uint64_t* p_full = bar + 10;
+  uint64_t* dp_full = bar + 11;
+  uint64_t* ds_full = bar + 12;
+  uint64_t* dq_full = bar + 13;
+  uint64_t* dq_drained = bar + 14;
+  uint64_t* ds_free = bar + 15;
+  uint64_t* dkv_full = bar + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // longest-first: key tile 0 (the most query tiles) of every head of the group first
+  const int lin = static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x);
+  const int kt = lin / static_cast<int>(gridDim.y);
+  const int h = static_cast<int>(blockIdx.z * gridDim.y) + lin % static_cast<int>(gridDim.y);
+  const int k0 = kt * 128;
+  const int n = S / 128 - kt;  // query tiles kt .. S/128 - 1
+
+  if (warp == 12 && lane == 0) {
+    tma_prefetch(&mQ); tma_prefetch(&mK); tma_prefetch(&mV); tma_prefetch(&mDO); tma_prefetch(&mDQ);
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&q_full[s], 1); mbar_init(&q_empty[s], 1);
+      mbar_init(&do_full[s], 1); mbar_init(&do_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 8);
+    mbar_init(dp_full, 1);
+    mbar_init(ds_full, 8);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_drained, 4);
+    mbar_init(ds_free, 1);
+    mbar_init(dkv_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 13) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tP = tmem + 128, tDK = tmem + 256, tDV = tmem + 384;
+
+  if (warp == 12) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      mbar_arrive_expect_tx(kv_full, 2 * L::kTile);
+      for (int c = 0; c < 2; ++c) {
+        tma_load_2d(smem + L::kOffK + c * (L::kTile / 2), &mK, kv_full, h * D + c * 64, k0);
+        tma_load_2d(smem + L::kOffV + c * (L::kTile / 2), &mV, kv_full, h * D + c * 64, k0);
+      }
+      for (int i = 0; i < n; ++i) {
+        const int s = i & 1, q0 = (kt + i) * 128;
+        if (i >= 2) mbar_wait(&q_empty[s], ((i >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(&q_full[s], L::kTile);
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d(smem + L::kOffQ + s * L::kTile + c * (L::kTile / 2), &mQ, &q_full[s], h * D + c * 64, q0);
+        if (i >= 2) mbar_wait(&do_empty[s], ((i >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(&do_full[s], L::kTile);
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d(smem + L::kOffDO + s * L::kTile + c * (L::kTile / 2), &mDO, &do_full[s], h * D + c * 64, q0);
+      }
+    }
+  } else if (warp == 13) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      constexpr uint32_t idSS = make_idesc_bf16(128, 128, false, false);  // S^T, dP^T (both K-major)
+      constexpr uint32_t idG = make_idesc_bf16(128, 128, false, true);    // dV, dK: A in TMEM, B MN-major
+      constexpr uint32_t idQ = make_idesc_bf16(128, 128, true, true);     // dQ: A = dS^T MN-major, B = K MN-major
+      const uint32_t sK = smem_u32(smem + L::kOffK), sV = smem_u32(smem + L::kOffV);
+      const uint32_t sDS = smem_u32(smem + L::kOffDS);
+      auto sQ = [&](int s) { return smem_u32(smem + L::kOffQ + s * L::kTile); };
+      auto sDO = [&](int s) { return smem_u32(smem + L::kOffDO + s * L::kTile); };
+      auto mma_ss = [&](uint32_t d, uint32_t a, uint32_t b) {  // K = d: 8 steps of 16 head dims
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t off = (k >> 2) * (L::kTile / 2) + (k & 3) * 32;
+          tc_mma_bf16(d, make_sw128_desc(a + off, 16, 1024), make_sw128_desc(b + off, 16, 1024), idSS, k > 0);
+        }
+      };
+      auto mma_grad = [&](uint32_t d, uint32_t a_tm, uint32_t b, bool acc) {  // K = 128 queries
+#pragma unroll
+        for (int k = 0; k < 8; ++k)  // queries 16k..: half k/4 holds them at columns 64 (k/4) + 8 (k%4)
+          tc_mma_bf16_ts(d, a_tm + (k >> 2) * 64 + (k & 3) * 8, make_sw128_desc(b + k * 2048, L::kTile / 2, 1024),
+                         idG, (acc || k > 0) ? 1u : 0u);
+      };
+      mbar_wait(kv_full, 0);
+      mbar_wait(&q_full[0], 0);
+      tc_fence_after();
+      mma_ss(tS, sK, sQ(0));
+      tc_commit(s_full);
+      mbar_wait(&do_full[0], 0);
+      tc_fence_after();
+      mma_ss(tP, sV, sDO(0));
+      tc_commit(dp_full);
+      for (int i = 0; i < n; ++i) {
+        const int s = i & 1, s1 = (i + 1) & 1;
+        mbar_wait(p_full, i & 1);
+        tc_fence_after();
+        mma_grad(tDV, tS, sDO(s), i > 0);
+        tc_commit(&do_empty[s]);
+        if (i + 1 < n) {
+          mbar_wait(&q_full[s1], ((i + 1) >> 1) & 1);
+          tc_fence_after();
+          mma_ss(tS, sK, sQ(s1));
+          tc_commit(s_full);
+        }
+        mbar_wait(ds_full, i & 1);
+        tc_fence_after();
+        mma_grad(tDK, tP, sQ(s), i > 0);
+        tc_commit(&q_empty[s]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)  // K = 128 keys: 16 rows of dS^T / K per step
+          tc_mma_bf16(tP, make_sw128_desc(sDS + k * 2048, L::kTile / 2, 1024),
+                      make_sw128_desc(sK + k * 2048, L::kTile / 2, 1024), idQ, k > 0);
+        tc_commit(dq_full);
+        if (i + 1 < n) {
+          mbar_wait(dq_drained, i & 1);
+          mbar_wait(&do_full[s1], ((i + 1) >> 1) & 1);
+          tc_fence_after();
+          mma_ss(tP, sV, sDO(s1));
+          tc_commit(dp_full);
+        }
+      }
+      tc_commit(dkv_full);
+    }
+  } else if (warp >= 14) {
+    // idle warps of warpgroup 3
+  } else if (warp >= 8) {
+    // ---------------- dQ warps 8..11: drain dQ (thread = query row), TMA reduce-add ----------------
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const uint32_t lo = static_cast<uint32_t>(quad * 32) << 16;
+    const bool issuer = warp == 8 && lane == 0;
+    uint8_t* stage = smem + L::kOffDS;
+    for (int i = 0; i < n; ++i) {
+      const int q0 = (kt + i) * 128;
+      mbar_wait(dq_full, i & 1);
+      tc_fence_after();
+      uint32_t v[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(tP + lo + c * 32, v[c]);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dq_drained);
+      if (dbg & 4) {  // development: dQ rows straight from registers as 16-B vector reductions
+        float* dst = dq_acc + (static_cast<int64_t>(h) * S + q0 + r) * D;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + c * 32 + u * 4),
+                         "f"(__uint_as_float(v[c][4 * u]) * scale), "f"(__uint_as_float(v[c][4 * u + 1]) * scale),
+                         "f"(__uint_as_float(v[c][4 * u + 2]) * scale), "f"(__uint_as_float(v[c][4 * u + 3]) * scale)
+                         : "memory");
+        if (issuer) mbar_arrive(ds_free);
+        continue;
+      }
+#pragma unroll
+      for (int round = 0; round < 2; ++round) {
+        if (!(dbg & 2)) {
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {  // box b: 32 fp32 columns, [128 rows][128 B] SW128
+            uint8_t* row = stage + b * 16384 + r * 128;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const uint32_t* x = &v[round * 2 + b][4 * u];
+              *reinterpret_cast<float4*>(row + ((u ^ (r & 7)) * 16)) =
+                  make_float4(__uint_as_float(x[0]) * scale, __uint_as_float(x[1]) * scale,
+                              __uint_as_float(x[2]) * scale, __uint_as_float(x[3]) * scale);
+            }
+          }
+          fence_proxy_async();
+        }
+        named_bar(1, 128);
+        if (issuer) {
+          if (!(dbg & 2)) {
+            tma_reduce_add_2d(&mDQ, stage, round * 64, h * S + q0);
+            tma_reduce_add_2d(&mDQ, stage + 16384, round * 64 + 32, h * S + q0);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            bulk_wait_read();
+          }
+          if (round == 1) mbar_arrive(ds_free);
+        }
+        if (round == 0) named_bar(1, 128);
+      }
+    }
+    if (issuer) bulk_wait_all();
+  } else {
+    // ---------------- P^T / dS^T warps 0..7 ----------------
+    const int quad = warp & 3, half = warp >> 2;
+    const int r = quad * 32 + lane;  // key row
+    const uint32_t lo = static_cast<uint32_t>(quad * 32) << 16;
+    const int key = k0 + r;
+    const float scale_log2 = scale * kLog2e;
+    const float* lse_h = lse + static_cast<int64_t>(h) * S;
+    const float* delta_h = delta + static_cast<int64_t>(h) * S;
+    for (int i = 0; i < n; ++i) {
+      const int qb = (kt + i) * 128 + half * 64;  // this warp's 64 queries
+      const bool diag = i == 0;
+      if (dbg & 8) {  // development: MMA pipeline bound (no P / dS math, no TMEM traffic)
+        mbar_wait(s_full, i & 1);
+        if (lane == 0) mbar_arrive(p_full);
+        mbar_wait(dp_full, i & 1);
+        if (i >= 1) mbar_wait(ds_free, (i - 1) & 1);
+        if (lane == 0) mbar_arrive(ds_full);
+        continue;
+      }
+      float pf[64];
+      mbar_wait(s_full, i & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {  // 16 queries per chunk
+        uint32_t sv[16];
+        tmem_ld_x16(tS + lo + half * 64 + c * 16, sv);
+        tmem_ld_wait();
+        const float4* l4 = reinterpret_cast<const float4*>(lse_h + qb + c * 16);
+#pragma unroll
+        for (int j4 = 0; j4 < 4; ++j4) {
+          const float4 l = __ldg(l4 + j4);  // warp-uniform: broadcast
+          const float lv[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int j = j4 * 4 + e;
+            float p = (dbg & 1) ? 0.f : fast_exp2(fmaf(__uint_as_float(sv[j]), scale_log2, -lv[e] * kLog2e));
+            if (diag && key > qb + c * 16 + j) p = 0.f;
+            pf[c * 16 + j] = p;
+          }
+        }
+        uint32_t pk[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) pk[j] = pack_bf16(pf[c * 16 + 2 * j], pf[c * 16 + 2 * j + 1]);
+        // P^T over this warp's own (already read) S^T columns: the A operand of dV
+        tmem_st_x8(tS + lo + half * 64 + c * 8, pk);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+
+      mbar_wait(dp_full, i & 1);
+      if (i >= 1) mbar_wait(ds_free, (i - 1) & 1);  // dQ staging of tile i-1 read by the TMA unit
+      tc_fence_after();
+      uint8_t* drow = smem + L::kOffDS + half * (L::kTile / 2) + r * 128;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t dv[16];
+        tmem_ld_x16(tP + lo + half * 64 + c * 16, dv);
+        tmem_ld_wait();
+        const float4* d4 = reinterpret_cast<const float4*>(delta_h + qb + c * 16);
+        uint32_t dk[8];
+#pragma unroll
+        for (int j4 = 0; j4 < 4; ++j4) {
+          const float4 dl = __ldg(d4 + j4);
+          const float dlv[4] = {dl.x, dl.y, dl.z, dl.w};
+          float ds[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) ds[e] = pf[c * 16 + j4 * 4 + e] * (__uint_as_float(dv[j4 * 4 + e]) - dlv[e]);
+          dk[j4 * 2] = pack_bf16(ds[0], ds[1]);
+          dk[j4 * 2 + 1] = pack_bf16(ds[2], ds[3]);
+        }
+        // dS^T over this warp's own dP^T columns (A operand of dK) and into smem (A of dQ)
+        tmem_st_x8(tP + lo + half * 64 + c * 8, dk);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int unit = c * 2 + u;
+          *reinterpret_cast<uint4*>(drow + ((unit ^ (r & 7)) * 16)) =
+              make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+        }
+      }
+      tmem_st_wait();
+      fence_proxy_async();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_full);
+    }
+    // dK (scaled), dV -> bf16
+    mbar_wait(dkv_full, 0);
+    tc_fence_after();
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      const int col = half * 64 + c * 32;
+      uint32_t a[32], b[32];
+      tmem_ld_32x32b_x32(tDK + lo + col, a);
+      tmem_ld_32x32b_x32(tDV + lo + col, b);
+      tmem_ld_wait();
+      uint4* pk_out;
+      uint4* pv_out;
+      if (push.p[0]) {  // fused all-to-all: rows go to the owner of the key token
+        const int owner = key / push.T;
+        __nv_bfloat16* base = static_cast<__nv_bfloat16*>(push.p[owner]) +
+                              static_cast<int64_t>(key - owner * push.T) * push.ld + h * D + col;
+        pk_out = reinterpret_cast<uint4*>(base + push.col_k);
+        pv_out = reinterpret_cast<uint4*>(base + push.col_v);
+      } else {
+        pk_out = reinterpret_cast<uint4*>(dk_out + static_cast<int64_t>(key) * ld_d + h * D + col);
+        pv_out = reinterpret_cast<uint4*>(dv_out + static_cast<int64_t>(key) * ld_d + h * D + col);
+      }
+#pragma unroll
+      for (int v4 = 0; v4 < 4; ++v4) {
+        uint32_t x[4], y[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          x[e] = pack_bf16(__uint_as_float(a[v4 * 8 + 2 * e]) * scale, __uint_as_float(a[v4 * 8 + 2 * e + 1]) * scale);
+          y[e] = pack_bf16(__uint_as_float(b[v4 * 8 + 2 * e]), __uint_as_float(b[v4 * 8 + 2 * e + 1]));
+        }
+        pk_out[v4] = make_uint4(x[0], x[1], x[2], x[3]);
+        pv_out[v4] = make_uint4(y[0], y[1], y[2], y[3]);
+      }
+    }
+    if (push.p[0]) __threadfence_system();  // pushed rows visible before the next barrier flag
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 13) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 }  // namespace
 
 long long* g_attn_trace = nullptr;  // development: clock64 trace of CTA (0,0)
@@ -1486,10 +1867,48 @@ cudaError_t attention_bwd_split_tc(const AttnTensors& t, const __nv_bfloat16* do
                             ld_d, t.S, scale, t.push);
 }
 
+// [rows, 128] fp32 (dq_acc) with box {32 cols, 128 rows}, 128-B swizzle: the TMA reduce-add target.
+static bool map2d_f32(CUtensorMap* m, const void* base, int64_t rows, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {128u, static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {128u * 4u};
+  cuuint32_t box[2] = {32u, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t es[2] = {1u, 1u};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 128 x 128-tile backward (attn_bwd2_kernel). dq_acc must be zeroed and delta computed before.
+static cudaError_t attention_bwd_tc2(const AttnTensors& t, const __nv_bfloat16* dout, int64_t ld_dout,
+                                     __nv_bfloat16* dk, __nv_bfloat16* dv, int64_t ld_d, const float* delta,
+                                     float* dq_acc, cudaStream_t st) {
+  using L = Bwd2Cfg;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  CUtensorMap mq, mk, mv, mdo, mdq;
+  const int64_t cols = static_cast<int64_t>(t.heads) * 128;
+  if (!map2d(&mq, t.q, t.S, cols, t.ld_qkv, 128) || !map2d(&mk, t.k, t.S, cols, t.ld_qkv, 128) ||
+      !map2d(&mv, t.v, t.S, cols, t.ld_qkv, 128) || !map2d(&mdo, dout, t.S, cols, ld_dout, 128) ||
+      !map2d_f32(&mdq, dq_acc, static_cast<int64_t>(t.heads) * t.S, 128))
+    return cudaErrorInvalidValue;
+  const float scale = 1.0f / sqrtf(128.0f);
+  const int dbg = std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0;
+  attn_bwd2_kernel<<<lpt_grid(t.S / 128, t.heads, t.S, 128), kBwd2Threads, L::kBytes, st>>>(
+      mq, mk, mv, mdo, mdq, t.lse, delta, dq_acc, dk, dv, ld_d, t.S, scale, t.push, dbg);
+  return cudaGetLastError();
+}
+
 // dq_acc must be zeroed and delta = rowsum(dO * O) computed before this launch.
 cudaError_t attention_bwd_tc(const AttnTensors& t, const __nv_bfloat16* dout, int64_t ld_dout, __nv_bfloat16* dk,
                              __nv_bfloat16* dv, int64_t ld_d, const float* delta, float* dq_acc, cudaStream_t st) {
   if (t.d != 128 || t.S % kBwdKeys) return cudaErrorInvalidValue;
+  if (std::getenv("SEQPLAN_ISP_ATTN_BWD128")) return attention_bwd_tc2(t, dout, ld_dout, dk, dv, ld_d, delta, dq_acc, st);
   using L = BwdSmem;
   static bool attr = false;
   if (!attr) {

@@ -86,3 +86,25 @@ def test_oracle_rejects_bad_sharding():
 
 FROZEN = [-1.1993611852119628, -0.059745141150991395, 0.8620070529295685, -0.5620351665735817,
           -0.45045825860339406, 0.16131780976187002]
+
+
+def test_block_sample_is_the_block_work_of_its_rows():
+    """bench.py's bounded CPU sample (ob_block_sample): with every position sampled it is the full
+    block (y, dx, grads); with a subset and the true K|V of the prefix, the sampled rows' forward
+    outputs equal the full block's rows; its FLOPs are n/S of the block's."""
+    sh = ob.Shape(H=256, D=4, S=256)
+    w = ob.make_weights(sh)
+    x = ob.make_activation(sh, ob.TID_X)
+    dy = ob.make_activation(sh, ob.TID_DY)
+    y, dx, g = ob.block(sh, w, x, dy)
+    kv = np.zeros((sh.S, 2 * sh.H), np.float32)
+    dkv = np.zeros_like(kv)
+    y2, dx2, g2 = ob.block_sample(sh, w, np.arange(sh.S), x, dy, kv, dkv)
+    assert rel(y2, y) < 1e-5 and rel(dx2, dx) < 1e-5
+    for a, b in zip(g2, g):
+        assert rel(a.reshape(-1), b.reshape(-1)) < 1e-5
+    pos = np.arange(8) * 32 + 16
+    y3, _, _ = ob.block_sample(sh, w, pos, x[pos], dy[pos], kv.copy(), np.zeros_like(kv))
+    assert rel(y3, y[pos]) < 1e-5
+    full = 3.0 * (8 * sh.S * sh.H ** 2 + 6 * sh.S * sh.H * sh.I + 2 * sh.S ** 2 * sh.H)
+    assert abs(ob.sample_flops(sh, pos) / (len(pos) / sh.S * full) - 1) < 0.01
