@@ -133,7 +133,9 @@ enum {
 
 /* Creates the context of rank `rank` of `world` on CUDA device `device`.
  * The strategy must be the ISP plan [b=1,n=1,pp=1,dp=1,tp=1,sp=ps=world,gs=oss=1]
- * and must pass seqplan::validate (strategy.hpp:72-99). policy may be NULL. */
+ * and must pass seqplan::validate (strategy.hpp:72-99): an illegal plan, or a non-ISP one, is
+ * SEQPLAN_ISP_ERR_INVALID; a legal ISP plan with micro_batch != 1, micro_batch_num != 1, gs != 1
+ * or oss != 1 is SEQPLAN_ISP_ERR_UNSUPPORTED. policy may be NULL. */
 int seqplan_isp_ctx_create(int world, int rank, int device, const seqplan_isp_shape* shape,
                            const seqplan_strategy* strategy, const seqplan_mempool_policy* policy,
                            uint32_t flags, seqplan_isp_ctx** out);
@@ -245,6 +247,16 @@ int seqplan_isp_debug_attention(const void* q, const void* k, const void* v, int
 /* RMSNorm forward (dn == NULL) or backward: dx = dres + d(norm), dg += sum dn*xhat. */
 int seqplan_isp_debug_rmsnorm(const void* x, const void* g, void* y, float* rstd, const void* dn,
                               const void* dres, void* dx, float* dg, int T, int H, float eps, void* stream);
+/* One rank's Ulysses all-to-all (priced at cost.hpp:179-183): dir = +1
+ * token-sharded [T, parts*H] on every rank q (src[q]) -> this rank's head-sharded [S, parts*H/world];
+ * dir = -1 the reverse. RoPE (+1 / inverse -1) on parts < rope_parts when cos_t != NULL. */
+int seqplan_isp_debug_all_to_all(int world, int rank, int T, int H, int parts, int d, int dir,
+                                 const void* const* src, void* dst, const float* cos_t, const float* sin_t,
+                                 int rope_parts, void* stream);
+/* One rank's gradient reduce-scatter fused with the fp32 cast / scale (cost.hpp:184-188):
+ * out[i] (+)= scale * sum_{q=0..world-1, in order} part[q][rank*shard_elems + i]. */
+int seqplan_isp_debug_reduce_scatter(int world, int rank, int64_t shard_elems, const void* const* part,
+                                     int part_is_f32, float scale, int accumulate, float* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -218,7 +218,8 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_kernel(AttnTensors t, float s
 template <int D>
 __global__ void attn_delta_kernel(const __nv_bfloat16* __restrict__ o, int64_t ld_o,
                                   const __nv_bfloat16* __restrict__ dout, float* __restrict__ delta,
-                                  int S, int heads) {
+                                  int S, int heads, const float* __restrict__ lse = nullptr,
+                                  float* __restrict__ nlse2 = nullptr) {
   const int warps = blockDim.x / 32;
   const int64_t n = static_cast<int64_t>(S) * heads;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(warps) + threadIdx.x / 32; i < n;
@@ -234,6 +235,10 @@ __global__ void attn_delta_kernel(const __nv_bfloat16* __restrict__ o, int64_t l
     }
     acc = warp_sum(acc);
     if (lane == 0) delta[static_cast<int64_t>(h) * S + tok] = acc;
+    if (nlse2 && lane == 1) {  // -lse * log2(e): the exponent offset of the tcgen05 backward
+      const int64_t k = static_cast<int64_t>(h) * S + tok;
+      nlse2[k] = -lse[k] * kLog2e;
+    }
   }
 }
 
@@ -467,11 +472,11 @@ cudaError_t bwd_impl(const AttnTensors& t, const __nv_bfloat16* dout, __nv_bfloa
     set = true;
   }
   const float scale = 1.0f / sqrtf(static_cast<float>(D));
-  if (D == 128 && t.S % 256 == 0 && !std::getenv("SEQPLAN_ISP_ATTN_MMA_SYNC") && std::getenv("SEQPLAN_ISP_ATTN_SPLIT_BWD")) {
-    // split tcgen05 backward: dK/dV kernel + CTA-pair dQ kernel (no dq_acc, no atomics). Opt-in:
-    // measured 2.41 ms vs 1.7 ms fused at S = 16K x 8 heads (dK/dV 894 TF/s, dQ 699 TF/s)
-    attn_delta_kernel<D><<<num_sms * 8, 256, 0, st>>>(t.o, t.ld_o, dout, delta, t.S, t.heads);
-    return attention_bwd_split_tc(t, dout, t.ld_o, dq, dk, dv, ld_d, delta, st);
+  if (D == 128 && !std::getenv("SEQPLAN_ISP_ATTN_MMA_SYNC") && !std::getenv("SEQPLAN_ISP_ATTN_FUSED_BWD")) {
+    // production: atomic-free tcgen05 backward (attention_tc.cu attn_bwd_split_kernel)
+    // dq_acc (unused by this path) holds -lse*log2e [heads, S]
+    attn_delta_kernel<D><<<num_sms * 8, 256, 0, st>>>(t.o, t.ld_o, dout, delta, t.S, t.heads, t.lse, dq_acc);
+    return attention_bwd_nored_tc(t, dout, t.ld_o, dq, dk, dv, ld_d, delta, dq_acc, st);
   }
   cudaError_t e = cudaMemsetAsync(dq_acc, 0, sizeof(float) * static_cast<size_t>(t.heads) * t.S * D, st);
   if (e != cudaSuccess) return e;

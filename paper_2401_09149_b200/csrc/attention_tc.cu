@@ -14,7 +14,12 @@
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <type_traits>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -870,7 +875,7 @@ __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.w
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-// kDQ = false: the dK/dV kernel of the split backward (dQ comes from attn_bwd_dq_pair_kernel):
+// kDQ = false: a dK/dV-only variant (dQ from elsewhere):
 // no dQ^T MMA / warps / atomics, and K lives in TMEM so S^T = K Q^T is a TS MMA.
 // kKT (fused kernel): K also lives in TMEM (S^T as a TS MMA, 32 KB less shared-memory operand
 // traffic per tile); P^T / dS^T then share the dQ^T columns, so the P/dS warps also wait for the
@@ -1199,372 +1204,160 @@ __global__ void __launch_bounds__(kDQ ? kBwdThreads : 320, 1)
 }
 
 // =====================================================================================
-// Split backward, dQ part: CTA-pair kernel (d = 128), no atomics.
+// Causal flash-attention backward without atomics, one launch, two CTA roles (d = 128):
+// the production backward.
 //
-// A cluster owns 2 query tiles of 128 (CTA c: tile 2pp + c) of one head and walks 64-key tiles.
-// Q and dO rows live in TMEM (each CTA's own 128 rows, bf16 pairs) as the A operands of the
-// M = 256 pair MMAs S = Q K^T and dP = dO V^T (each CTA holds half of the tile's K and V rows);
-// S and dP are double-buffered in TMEM so the next tile's MMAs overlap this tile's
-// P = exp2(S*scale - lse), dS = P (dP - delta) (one thread per query row, no cross-thread
-// reduction); dS (bf16) overwrites its own S columns and is the A operand of dQ += dS K
-// (each CTA holds half of K's head-dim columns). dQ accumulates in TMEM; the epilogue scales,
-// converts and stores (or pushes to the owner rank) each query row once.
-// TMEM per CTA: Q 0 (64) | dO 64 (64) | S[2] 128, 192 | dP[2] 256, 320 | dQ 384 (128).
-// Warps 0..7 dS math (warp pair per lane quadrant, 32 keys each), warp 8 TMA, warp 9 MMA.
+// The fused backward (one CTA per 128 keys, dQ reduced into fp32 with L2 atomics) is capped by
+// the L2 reduction rate: (S/128)·S·d·4 B per head of fp32 reductions ran at ~2.8 TB/s whatever the
+// issuing path (scalar red.global or TMA cp.reduce), i.e. <= ~720 TF/s. Here every gradient is
+// accumulated in TMEM and written once:
+//   role KV (one CTA per 128 keys kt, walks query tiles i >= kt):   4 MMAs per tile
+//     S^T = K Q_i^T (SS), dP^T = V dO_i^T (SS)                 -> TMEM S^T 0..127, dP^T 128..255
+//     P^T = exp2(S^T*scale*log2e - lse*log2e) (registers), dS^T = P^T (dP^T - delta); both bf16
+//     into the dP^T columns (per 64-query half: P^T 32 columns | dS^T 32 columns)
+//     dV += P^T dO_i (TS), dK += dS^T Q_i (TS)                -> TMEM dK 256..383, dV 384..511
+//     issue order S(i+1), dV(i), dK(i), dP(i+1): S^T is free as soon as it is in registers, so
+//     P(i+1) is computed under dV(i)/dK(i)/dP(i+1) and only the dS store sits between dP(i) and
+//     dV(i), under S(i+1).
+//   role Q (one CTA per 128 queries qt, walks key tiles j <= qt):    3 MMAs per tile
+//     S = Q K_j^T (SS), dP = dO V_j^T (SS)                     -> TMEM S 0..127, dP 128..255
+//     P = exp2(S*scale*log2e - lse*log2e), dS = P (dP - delta)  bf16 over the dP columns
+//     dQ += dS K_j (TS)                                        -> TMEM dQ 256..383
+//     issue order S(j+1), dQ(j), dP(j+1): P(j+1) under dQ(j)/dP(j+1), dS(j) under S(j+1).
+// Every MMA is M = 128, N = 128. 7 MMAs per (key tile, query tile) instead of the fused 5, but
+// none waits on an L2 reduction; the dQ rows come out in bf16 (scaled), no fp32 accumulator.
+// Dispatch: one grid over (role, tile) entries sorted by decreasing work (host table), inside
+// L2-sized head groups (lpt_grid), so the heaviest CTAs of both roles start first.
+// Shared memory: KV role K, V 64 KB + Q, dO 2 stages 128 KB; Q role Q, dO 64 KB + K 3 stages
+// 96 KB + V 2 stages 64 KB.
+// Warps: 0..7 math (a warp pair per TMEM lane quadrant, 64 columns each), 8 TMA, 9 MMA.
 // =====================================================================================
-struct DqCfg {
-  static constexpr int D = 128, BN = 64, NS = 4;
-  static constexpr int kKr = (BN / 2) * D * 2;  // K rows half: 2 chunks [32 keys][64]
-  static constexpr int kVr = (BN / 2) * D * 2;  // V rows half
-  static constexpr int kKc = BN * 64 * 2;       // K head-dim half: 1 chunk [64 keys][64 d]
-  static constexpr int kStage = kKr + kVr + kKc;
-  static constexpr int kOffBar = NS * kStage;
-  static constexpr int kBytes = kOffBar + 256 + 1024;
-  static_assert(kBytes <= 232448, "exceeds the 227 KB per-CTA shared memory");
-};
-
-__global__ void __launch_bounds__(320, 1)
-    attn_bwd_dq_pair_kernel(const __grid_constant__ CUtensorMap mKr, const __grid_constant__ CUtensorMap mVr,
-                            const __grid_constant__ CUtensorMap mKc, const __nv_bfloat16* __restrict__ qg,
-                            int64_t ld_q, const __nv_bfloat16* __restrict__ dog, int64_t ld_do,
-                            const float* __restrict__ lse, const float* __restrict__ delta,
-                            __nv_bfloat16* __restrict__ dq_out, int64_t ld_dq, int S, float scale,
-                            const __grid_constant__ AttnPush push) {
-  using L = DqCfg;
-  constexpr int D = L::D, BN = L::BN, NS = L::NS;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
-  uint64_t* qo_full = bar + 0;         // leader's: Q / dO rows of both CTAs in TMEM (8 warps x 2)
-  uint64_t* s_full = bar + 1;          // [2] local (multicast commit)
-  uint64_t* p_full = bar + 3;          // [2] leader's: dS of the buffer written (8 warps x 2)
-  uint64_t* o_full = bar + 5;          // local (multicast commit): last dQ MMA done
-  uint64_t* kv_full = bar + 6;         // [NS] leader's
-  uint64_t* kv_empty = kv_full + NS;   // [NS] local (multicast commit)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_empty + NS);
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t crank = cluster_rank();
-  const bool leader = crank == 0;
-  const int lp = static_cast<int>((blockIdx.y * gridDim.x + blockIdx.x) / 2);  // longest-first, all heads
-  const int pp = static_cast<int>(gridDim.x / 2) - 1 - lp / static_cast<int>(gridDim.y);
-  const int h = static_cast<int>(blockIdx.z * gridDim.y) + lp % static_cast<int>(gridDim.y);
-  const int q0 = (2 * pp + static_cast<int>(crank)) * kBM;
-  const int n = (2 * pp + 2) * kBM / BN;  // key tiles of the upper query tile (both CTAs)
-
-  if (warp == 8 && lane == 0) {
-    tma_prefetch(&mKr);
-    tma_prefetch(&mVr);
-    tma_prefetch(&mKc);
-    mbar_init(qo_full, 16);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 16);
-    }
-    mbar_init(o_full, 1);
-    for (int i = 0; i < NS; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 9) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-  }
-  tc_fence_before();
-  cluster_sync_all();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t tQ = tmem, tDO = tmem + 64, tSb = tmem + 128, tDPb = tmem + 256, tDQ = tmem + 384;
-
-  if (warp == 8) {
-    if (lane == 0) {
-      // ---------------- TMA producer (both CTAs; completion on the leader's barriers) ----------------
-      const int ch = static_cast<int>(crank);
-      for (int j = 0; j < n; ++j) {
-        const int s = j % NS;
-        if (j >= NS) mbar_wait(&kv_empty[s], ((j / NS) - 1) & 1);
-        if (leader) mbar_arrive_expect_tx(&kv_full[s], 2 * L::kStage);
-        uint8_t* st = smem + s * L::kStage;
-        for (int c = 0; c < 2; ++c) {
-          tma_load_2d_pair(st + c * (BN / 2) * 128, &mKr, &kv_full[s], h * D + c * 64, j * BN + ch * (BN / 2));
-          tma_load_2d_pair(st + L::kKr + c * (BN / 2) * 128, &mVr, &kv_full[s], h * D + c * 64, j * BN + ch * (BN / 2));
-        }
-        tma_load_2d_pair(st + L::kKr + L::kVr, &mKc, &kv_full[s], h * D + ch * 64, j * BN);
-      }
-    }
-  } else if (warp == 9) {
-    if (leader && lane == 0) {
-      // ---------------- MMA issuer (leader only) ----------------
-      constexpr uint32_t idS = make_idesc_bf16(2 * kBM, BN, false, false);  // S, dP: N = keys
-      constexpr uint32_t idQ = make_idesc_bf16(2 * kBM, D, false, true);    // dQ: N = head dim, B MN-major
-      auto issue_dq = [&](int i) {
-        const int b = i & 1;
-        mbar_wait(&p_full[b], (i >> 1) & 1);
-        tc_fence_after();
-        const uint32_t sKc = smem_u32(smem + (i % NS) * L::kStage + L::kKr + L::kVr);
-#pragma unroll
-        for (int k = 0; k < BN / 16; ++k)  // dS packed: keys 0..31 in columns 0..15, keys 32..63 in 32..47
-          tc_mma_bf16_ts_pair(tDQ, tSb + b * 64 + (k >> 1) * 32 + (k & 1) * 8,
-                              make_sw128_desc(sKc + k * 2048, BN * 128, 1024), idQ, (i > 0 || k > 0) ? 1u : 0u);
-        tc_commit_pair(&kv_empty[i % NS]);
-      };
-      mbar_wait(qo_full, 0);
-      for (int j = 0; j < n; ++j) {
-        const int b = j & 1;
-        mbar_wait(&kv_full[j % NS], (j / NS) & 1);
-        tc_fence_after();
-        const uint32_t sKr = smem_u32(smem + (j % NS) * L::kStage), sVr = sKr + L::kKr;
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const int c = k / 4, kk = k % 4;
-          tc_mma_bf16_ts_pair(tSb + b * 64, tQ + k * 8, make_sw128_desc(sKr + c * (BN / 2) * 128 + kk * 32, 16, 1024),
-                              idS, k > 0 ? 1u : 0u);
-        }
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const int c = k / 4, kk = k % 4;
-          tc_mma_bf16_ts_pair(tDPb + b * 64, tDO + k * 8,
-                              make_sw128_desc(sVr + c * (BN / 2) * 128 + kk * 32, 16, 1024), idS, k > 0 ? 1u : 0u);
-        }
-        tc_commit_pair(&s_full[b]);
-        if (j >= 1) issue_dq(j - 1);
-      }
-      issue_dq(n - 1);
-      tc_commit_pair(o_full);
-    }
-  } else {
-    // ---------------- dS warps 0..7 ----------------
-    const int quad = warp & 3, half = warp >> 2;
-    const int r = quad * 32 + lane;
-    const int q = q0 + r;
-    const uint32_t lo = static_cast<uint32_t>(quad * 32) << 16;
-    auto arrive_leader = [&](uint64_t* bar_) {
-      __syncwarp();
-      if (lane == 0) {
-        if (leader) mbar_arrive(bar_);
-        else mbar_arrive_leader(bar_);
-      }
-    };
-    {  // Q and dO rows of this query (this warp's 64 head dims) into TMEM
-      uint32_t v[32];
-      const uint4* sq = reinterpret_cast<const uint4*>(qg + static_cast<int64_t>(q) * ld_q + h * D + half * 64);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint4 u = sq[i];
-        v[4 * i] = u.x; v[4 * i + 1] = u.y; v[4 * i + 2] = u.z; v[4 * i + 3] = u.w;
-      }
-      tmem_st_32x32b_x32(tQ + lo + half * 32, v);
-      const uint4* sd = reinterpret_cast<const uint4*>(dog + static_cast<int64_t>(q) * ld_do + h * D + half * 64);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint4 u = sd[i];
-        v[4 * i] = u.x; v[4 * i + 1] = u.y; v[4 * i + 2] = u.z; v[4 * i + 3] = u.w;
-      }
-      tmem_st_32x32b_x32(tDO + lo + half * 32, v);
-      tmem_st_wait();
-      tc_fence_before();
-      arrive_leader(qo_full);
-    }
-    const float scale_log2 = scale * kLog2e;
-    const float lse2 = lse[static_cast<int64_t>(h) * S + q] * kLog2e;
-    const float dl = delta[static_cast<int64_t>(h) * S + q];
-    for (int j = 0; j < n; ++j) {
-      const int b = j & 1;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t sv[32], pv[32];
-      tmem_ld_32x32b_x32(tSb + b * 64 + lo + half * 32, sv);
-      tmem_ld_32x32b_x32(tDPb + b * 64 + lo + half * 32, pv);
-      tmem_ld_wait();
-      const int key0 = j * BN + half * 32;
-      const bool diag = key0 + 31 > q0;  // some key of this chunk may lie past some query of the tile
-      uint32_t dk[16];
-#pragma unroll
-      for (int c = 0; c < 32; c += 2) {
-        float d2[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          float p = fast_exp2(fmaf(__uint_as_float(sv[c + e]), scale_log2, -lse2));
-          if (diag && key0 + c + e > q) p = 0.f;
-          d2[e] = p * (__uint_as_float(pv[c + e]) - dl);
-        }
-        dk[c / 2] = pack_bf16(d2[0], d2[1]);
-      }
-      // dS over this warp's own (already read) S columns: the A operand of dQ += dS K
-      tmem_st_cols<16>(tSb + b * 64 + lo + half * 32, dk);
-      tmem_st_wait();
-      tc_fence_before();
-      arrive_leader(&p_full[b]);
-    }
-    // epilogue: dQ * scale -> bf16 row (or pushed to the owner rank of token q)
-    mbar_wait(o_full, 0);
-    tc_fence_after();
-    __nv_bfloat16* row = dq_out + static_cast<int64_t>(q) * ld_dq + h * D + half * 64;
-    if (push.p[0]) {
-      const int owner = q / push.T;
-      row = static_cast<__nv_bfloat16*>(push.p[owner]) + static_cast<int64_t>(q - owner * push.T) * push.ld +
-            push.col_q + h * D + half * 64;
-    }
-#pragma unroll 1
-    for (int c = 0; c < 2; ++c) {
-      uint32_t o[32];
-      tmem_ld_32x32b_x32(tDQ + lo + half * 64 + c * 32, o);
-      tmem_ld_wait();
-      uint4* dst = reinterpret_cast<uint4*>(row + c * 32);
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        uint32_t pk2[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          pk2[e] = pack_bf16(__uint_as_float(o[v * 8 + 2 * e]) * scale, __uint_as_float(o[v * 8 + 2 * e + 1]) * scale);
-        dst[v] = make_uint4(pk2[0], pk2[1], pk2[2], pk2[3]);
-      }
-    }
-    if (push.p[0]) __threadfence_system();  // pushed rows visible before the next barrier flag
-  }
-
-  tc_fence_before();
-  cluster_sync_all();
-  if (warp == 9) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-  }
-}
-
-// =====================================================================================
-// Causal flash-attention backward, 128 x 128 tiles (d = 128): the production backward.
-//
-// CTA = 128 keys x 1 head; iterates over 128-query tiles i >= the key tile (causal). Every
-// MMA is M = 128, N = 128, so the shared-memory operand traffic of the SS MMAs is 8 KB per
-// 64 tensor cycles (the 128 B/clk smem port is never the bound, unlike N = 64 tiles):
-//   S^T  = K Q_i^T          (SS)   -> TMEM S   (cols   0..127)
-//   dP^T = V dO_i^T         (SS)   -> TMEM dP  (cols 128..255)
-//   P^T  = exp2(S^T*scale*log2e - lse*log2e) (bf16, over the S columns it came from)
-//   dS^T = P^T (dP^T - delta)        (bf16, over the dP columns, and into smem as [key][q])
-//   dV  += P^T dO_i         (TS)   -> TMEM dV  (cols 384..511)
-//   dK  += dS^T Q_i         (TS)   -> TMEM dK  (cols 256..383)
-//   dQ_i = dS K             (SS, A = dS^T smem MN-major) -> TMEM dP columns (dP^T consumed)
-// MMA issue order per tile: dV(i), S(i+1), dK(i), dQ(i), dP(i+1): S(i+1) reuses the S columns
-// right after dV(i) consumed P(i) (tcgen05 ops of one thread execute in order), so softmax of
-// tile i+1 runs under dK(i)/dQ(i)/dP(i+1); dS(i+1) runs under dV(i+1)/S(i+2).
-// dQ: 4 warps drain the dQ columns (thread = query row), then stage them (fp32, SW128) in the
-// dS buffer and TMA-reduce (cp.reduce.async.bulk.tensor .add) into dq_acc, 64 columns a round.
-// Shared memory: K, V 64 KB + Q, dO 2 stages 128 KB + dS^T / dQ staging 32 KB = 224 KB.
-// Warps: 0..7 P/dS (a warp pair per TMEM lane quadrant, 64 queries each), 8..11 dQ drain +
-// reduction, 12 TMA, 13 MMA (14, 15 idle: warpgroup-aligned roles).
-// =====================================================================================
-struct Bwd2Cfg {
+struct BwdSCfg {
   static constexpr int kTile = 128 * 128 * 2;  // [2 chunks][128 rows][64 cols] bf16, SW128
-  static constexpr int kOffK = 0;
-  static constexpr int kOffV = kTile;
-  static constexpr int kOffQ = 2 * kTile;   // stage s at kOffQ + s * kTile
-  static constexpr int kOffDO = 4 * kTile;  // stage s at kOffDO + s * kTile
-  static constexpr int kOffDS = 6 * kTile;  // dS^T [2 q chunks][128 keys][64 q]; dQ fp32 staging
+  // role KV
+  static constexpr int kOffK = 0, kOffV = kTile, kOffQ = 2 * kTile, kOffDO = 4 * kTile;  // Q, dO: 2 stages
+  static constexpr int kOffLD = 6 * kTile;  // per stage lse[128] | delta[128] fp32 (bulk-loaded with Q / dO)
+  // role Q
+  static constexpr int kOffQq = 0, kOffDOq = kTile, kOffKq = 2 * kTile, kOffVq = 5 * kTile;  // K 3, V 2 stages
   static constexpr int kOffBar = 7 * kTile;
   static constexpr int kBytes = kOffBar + 256 + 1024;
   static_assert(kBytes <= 232448, "exceeds the 227 KB per-CTA shared memory");
 };
-constexpr int kBwd2Threads = 512;
+constexpr int kBwdSThreads = 320;
 
-__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* smem_src, int32_t c0,
-                                                  int32_t c1) {
-  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
-               : "memory");
+__device__ __forceinline__ float4 lds_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+// exp2 of a packed pair: MUFU for most columns, the FMA-pipe polynomial for every 4th pair
+template <bool kPoly>
+__device__ __forceinline__ float2 exp2_pair(float2 x) {
+  if constexpr (kPoly) return exp2_poly2(x);
+  return make_float2(fast_exp2(x.x), fast_exp2(x.y));
 }
 
-__global__ void __launch_bounds__(kBwd2Threads, 1)
-    attn_bwd2_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
-                     const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mDO,
-                     const __grid_constant__ CUtensorMap mDQ, const float* __restrict__ lse,
-                     const float* __restrict__ delta, float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dk_out,
-                     __nv_bfloat16* __restrict__ dv_out, int64_t ld_d, int S, float scale,
-                     const __grid_constant__ AttnPush push, int dbg) {
-  using L = Bwd2Cfg;
+template <int kPolyKV, int kPolyQ>
+__global__ void __launch_bounds__(kBwdSThreads, 1)
+    attn_bwd_split_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
+                          const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mDO,
+                          const int* __restrict__ table, const float* __restrict__ nlse2,
+                          const float* __restrict__ delta, __nv_bfloat16* __restrict__ dq_out,
+                          __nv_bfloat16* __restrict__ dk_out, __nv_bfloat16* __restrict__ dv_out, int64_t ld_d, int S,
+                          float scale, const __grid_constant__ AttnPush push, int dbg, long long* trace) {
+  using L = BwdSCfg;
   constexpr int D = 128;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
-  uint64_t* kv_full = bar + 0;
-  uint64_t* q_full = bar + 1;     // [2]
-  uint64_t* q_empty = bar + 3;    // [2]
-  uint64_t* do_full = bar + 5;    // [2]
-  uint64_t* do_empty = bar + 7;   // [2]
-  uint64_t* s_full = bar + 9;
-  uint64_t* p_full = bar + 10;
-  uint64_t* dp_full = bar + 11;
-  uint64_t* ds_full = bar + 12;
-  uint64_t* dq_full = bar + 13;
-  uint64_t* dq_drained = bar + 14;
-  uint64_t* ds_free = bar + 15;
-  uint64_t* dkv_full = bar + 16;
+  uint64_t* fixed_full = bar + 0;  // KV: K, V   Q: Q, dO
+  uint64_t* a_full = bar + 1;      // [3] KV: Q stages   Q: K stages
+  uint64_t* a_empty = bar + 4;     // [3]
+  uint64_t* b_full = bar + 7;      // [2] KV: dO stages  Q: V stages
+  uint64_t* b_empty = bar + 9;     // [2]
+  uint64_t* s_full = bar + 11;
+  uint64_t* s_free = bar + 12;     // Q role: S read into registers
+  uint64_t* p_full = bar + 13;     // KV role: P^T in TMEM
+  uint64_t* dp_full = bar + 14;
+  uint64_t* ds_full = bar + 15;
+  uint64_t* acc_full = bar + 16;   // last gradient MMA done
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // longest-first: key tile 0 (the most query tiles) of every head of the group first
   const int lin = static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x);
-  const int kt = lin / static_cast<int>(gridDim.y);
+  const int entry = table[lin / static_cast<int>(gridDim.y)];
   const int h = static_cast<int>(blockIdx.z * gridDim.y) + lin % static_cast<int>(gridDim.y);
-  const int k0 = kt * 128;
-  const int n = S / 128 - kt;  // query tiles kt .. S/128 - 1
+  const bool role_q = entry < 0;
+  const int tile = role_q ? -entry - 1 : entry;  // KV: key tile kt; Q: query tile qt
+  const int T = S / 128;
+  const int n = role_q ? tile + 1 : T - tile;    // KV: query tiles kt..T-1; Q: key tiles 0..qt
+  const int t0 = role_q ? 0 : tile;              // first streamed tile index
+  if (((dbg & 16) && role_q) || ((dbg & 32) && !role_q)) return;  // development: one role alone
 
-  if (warp == 12 && lane == 0) {
-    tma_prefetch(&mQ); tma_prefetch(&mK); tma_prefetch(&mV); tma_prefetch(&mDO); tma_prefetch(&mDQ);
-    mbar_init(kv_full, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&q_full[s], 1); mbar_init(&q_empty[s], 1);
-      mbar_init(&do_full[s], 1); mbar_init(&do_empty[s], 1);
-    }
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&mQ); tma_prefetch(&mK); tma_prefetch(&mV); tma_prefetch(&mDO);
+    mbar_init(fixed_full, 1);
+    for (int s = 0; s < 3; ++s) { mbar_init(&a_full[s], 1); mbar_init(&a_empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1); }
     mbar_init(s_full, 1);
+    mbar_init(s_free, 8);
     mbar_init(p_full, 8);
     mbar_init(dp_full, 1);
     mbar_init(ds_full, 8);
-    mbar_init(dq_full, 1);
-    mbar_init(dq_drained, 4);
-    mbar_init(ds_free, 1);
-    mbar_init(dkv_full, 1);
+    mbar_init(acc_full, 1);
     fence_barrier_init();
   }
-  if (warp == 13) tmem_alloc<512>(tmem_slot);
+  if (warp == 9) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem, tP = tmem + 128, tDK = tmem + 256, tDV = tmem + 384;
+  const uint32_t tS = tmem, tP = tmem + 128, tG0 = tmem + 256, tG1 = tmem + 384;  // KV: dK, dV; Q: dQ
+  const int NA = role_q ? 3 : 2;  // stages of the A stream (KV: Q; Q: K)
 
-  if (warp == 12) {
+  if (warp == 8) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
-      mbar_arrive_expect_tx(kv_full, 2 * L::kTile);
+      const int own = tile * 128;
+      mbar_arrive_expect_tx(fixed_full, 2 * L::kTile);
       for (int c = 0; c < 2; ++c) {
-        tma_load_2d(smem + L::kOffK + c * (L::kTile / 2), &mK, kv_full, h * D + c * 64, k0);
-        tma_load_2d(smem + L::kOffV + c * (L::kTile / 2), &mV, kv_full, h * D + c * 64, k0);
+        if (role_q) {
+          tma_load_2d(smem + L::kOffQq + c * (L::kTile / 2), &mQ, fixed_full, h * D + c * 64, own);
+          tma_load_2d(smem + L::kOffDOq + c * (L::kTile / 2), &mDO, fixed_full, h * D + c * 64, own);
+        } else {
+          tma_load_2d(smem + L::kOffK + c * (L::kTile / 2), &mK, fixed_full, h * D + c * 64, own);
+          tma_load_2d(smem + L::kOffV + c * (L::kTile / 2), &mV, fixed_full, h * D + c * 64, own);
+        }
       }
       for (int i = 0; i < n; ++i) {
-        const int s = i & 1, q0 = (kt + i) * 128;
-        if (i >= 2) mbar_wait(&q_empty[s], ((i >> 1) - 1) & 1);
-        mbar_arrive_expect_tx(&q_full[s], L::kTile);
-        for (int c = 0; c < 2; ++c)
-          tma_load_2d(smem + L::kOffQ + s * L::kTile + c * (L::kTile / 2), &mQ, &q_full[s], h * D + c * 64, q0);
-        if (i >= 2) mbar_wait(&do_empty[s], ((i >> 1) - 1) & 1);
-        mbar_arrive_expect_tx(&do_full[s], L::kTile);
-        for (int c = 0; c < 2; ++c)
-          tma_load_2d(smem + L::kOffDO + s * L::kTile + c * (L::kTile / 2), &mDO, &do_full[s], h * D + c * 64, q0);
+        const int row = (t0 + i) * 128;
+        const int sa = i % NA, sb = i & 1;
+        if (i >= NA) mbar_wait(&a_empty[sa], ((i / NA) - 1) & 1);
+        mbar_arrive_expect_tx(&a_full[sa], L::kTile + (role_q ? 0 : 512));
+        if (!role_q) bulk_load(smem + L::kOffLD + sa * 1024, nlse2 + static_cast<int64_t>(h) * S + row, 512, &a_full[sa]);
+        for (int c = 0; c < 2; ++c) {
+          if (role_q)
+            tma_load_2d(smem + L::kOffKq + sa * L::kTile + c * (L::kTile / 2), &mK, &a_full[sa], h * D + c * 64, row);
+          else
+            tma_load_2d(smem + L::kOffQ + sa * L::kTile + c * (L::kTile / 2), &mQ, &a_full[sa], h * D + c * 64, row);
+        }
+        if (i >= 2) mbar_wait(&b_empty[sb], ((i >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(&b_full[sb], L::kTile + (role_q ? 0 : 512));
+        if (!role_q)
+          bulk_load(smem + L::kOffLD + sb * 1024 + 512, delta + static_cast<int64_t>(h) * S + row, 512, &b_full[sb]);
+        for (int c = 0; c < 2; ++c) {
+          if (role_q)
+            tma_load_2d(smem + L::kOffVq + sb * L::kTile + c * (L::kTile / 2), &mV, &b_full[sb], h * D + c * 64, row);
+          else
+            tma_load_2d(smem + L::kOffDO + sb * L::kTile + c * (L::kTile / 2), &mDO, &b_full[sb], h * D + c * 64, row);
+        }
       }
     }
-  } else if (warp == 13) {
+  } else if (warp == 9) {
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
-      constexpr uint32_t idSS = make_idesc_bf16(128, 128, false, false);  // S^T, dP^T (both K-major)
-      constexpr uint32_t idG = make_idesc_bf16(128, 128, false, true);    // dV, dK: A in TMEM, B MN-major
-      constexpr uint32_t idQ = make_idesc_bf16(128, 128, true, true);     // dQ: A = dS^T MN-major, B = K MN-major
-      const uint32_t sK = smem_u32(smem + L::kOffK), sV = smem_u32(smem + L::kOffV);
-      const uint32_t sDS = smem_u32(smem + L::kOffDS);
-      auto sQ = [&](int s) { return smem_u32(smem + L::kOffQ + s * L::kTile); };
-      auto sDO = [&](int s) { return smem_u32(smem + L::kOffDO + s * L::kTile); };
+      constexpr uint32_t idSS = make_idesc_bf16(128, 128, false, false);  // S / S^T, dP / dP^T: K-major
+      constexpr uint32_t idG = make_idesc_bf16(128, 128, false, true);    // A in TMEM, B MN-major
       auto mma_ss = [&](uint32_t d, uint32_t a, uint32_t b) {  // K = d: 8 steps of 16 head dims
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -1572,235 +1365,287 @@ __global__ void __launch_bounds__(kBwd2Threads, 1)
           tc_mma_bf16(d, make_sw128_desc(a + off, 16, 1024), make_sw128_desc(b + off, 16, 1024), idSS, k > 0);
         }
       };
-      auto mma_grad = [&](uint32_t d, uint32_t a_tm, uint32_t b, bool acc) {  // K = 128 queries
+      // A from TMEM (packed bf16 pairs, 64 columns per 128-wide half at +64), B [128 x 128] MN-major
+      auto mma_ts = [&](uint32_t d, uint32_t a_tm, uint32_t b, bool acc) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k)  // queries 16k..: half k/4 holds them at columns 64 (k/4) + 8 (k%4)
+        for (int k = 0; k < 8; ++k)
           tc_mma_bf16_ts(d, a_tm + (k >> 2) * 64 + (k & 3) * 8, make_sw128_desc(b + k * 2048, L::kTile / 2, 1024),
                          idG, (acc || k > 0) ? 1u : 0u);
       };
-      mbar_wait(kv_full, 0);
-      mbar_wait(&q_full[0], 0);
-      tc_fence_after();
-      mma_ss(tS, sK, sQ(0));
-      tc_commit(s_full);
-      mbar_wait(&do_full[0], 0);
-      tc_fence_after();
-      mma_ss(tP, sV, sDO(0));
-      tc_commit(dp_full);
-      for (int i = 0; i < n; ++i) {
-        const int s = i & 1, s1 = (i + 1) & 1;
-        mbar_wait(p_full, i & 1);
+      mbar_wait(fixed_full, 0);
+      if (!role_q) {
+        const uint32_t sK = smem_u32(smem + L::kOffK), sV = smem_u32(smem + L::kOffV);
+        auto sQ = [&](int s) { return smem_u32(smem + L::kOffQ + s * L::kTile); };
+        auto sDO = [&](int s) { return smem_u32(smem + L::kOffDO + s * L::kTile); };
+        mbar_wait(&a_full[0], 0);
         tc_fence_after();
-        mma_grad(tDV, tS, sDO(s), i > 0);
-        tc_commit(&do_empty[s]);
-        if (i + 1 < n) {
-          mbar_wait(&q_full[s1], ((i + 1) >> 1) & 1);
-          tc_fence_after();
-          mma_ss(tS, sK, sQ(s1));
-          tc_commit(s_full);
-        }
-        mbar_wait(ds_full, i & 1);
+        mma_ss(tS, sK, sQ(0));
+        tc_commit(s_full);
+        mbar_wait(&b_full[0], 0);
         tc_fence_after();
-        mma_grad(tDK, tP, sQ(s), i > 0);
-        tc_commit(&q_empty[s]);
-#pragma unroll
-        for (int k = 0; k < 8; ++k)  // K = 128 keys: 16 rows of dS^T / K per step
-          tc_mma_bf16(tP, make_sw128_desc(sDS + k * 2048, L::kTile / 2, 1024),
-                      make_sw128_desc(sK + k * 2048, L::kTile / 2, 1024), idQ, k > 0);
-        tc_commit(dq_full);
-        if (i + 1 < n) {
-          mbar_wait(dq_drained, i & 1);
-          mbar_wait(&do_full[s1], ((i + 1) >> 1) & 1);
+        mma_ss(tP, sV, sDO(0));
+        tc_commit(dp_full);
+        const bool tr = trace && lin == 0;
+        for (int i = 0; i < n; ++i) {
+          const int s = i & 1, s1 = (i + 1) & 1;
+          if (tr && i < 64) trace[i * 8 + 0] = clock64();
+          if (i + 1 < n) {
+            mbar_wait(s_free, i & 1);  // S^T(i) is in registers
+            mbar_wait(&a_full[s1], ((i + 1) >> 1) & 1);
+            tc_fence_after();
+            mma_ss(tS, sK, sQ(s1));
+            tc_commit(s_full);
+          }
+          if (tr && i < 64) trace[i * 8 + 1] = clock64();
+          mbar_wait(ds_full, i & 1);  // P^T(i), dS^T(i) in the dP^T columns
+          if (tr && i < 64) trace[i * 8 + 2] = clock64();
           tc_fence_after();
-          mma_ss(tP, sV, sDO(s1));
-          tc_commit(dp_full);
-        }
-      }
-      tc_commit(dkv_full);
-    }
-  } else if (warp >= 14) {
-    // idle warps of warpgroup 3
-  } else if (warp >= 8) {
-    // ---------------- dQ warps 8..11: drain dQ (thread = query row), TMA reduce-add ----------------
-    const int quad = warp & 3;
-    const int r = quad * 32 + lane;
-    const uint32_t lo = static_cast<uint32_t>(quad * 32) << 16;
-    const bool issuer = warp == 8 && lane == 0;
-    uint8_t* stage = smem + L::kOffDS;
-    for (int i = 0; i < n; ++i) {
-      const int q0 = (kt + i) * 128;
-      mbar_wait(dq_full, i & 1);
-      tc_fence_after();
-      uint32_t v[4][32];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(tP + lo + c * 32, v[c]);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(dq_drained);
-      if (dbg & 4) {  // development: dQ rows straight from registers as 16-B vector reductions
-        float* dst = dq_acc + (static_cast<int64_t>(h) * S + q0 + r) * D;
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + c * 32 + u * 4),
-                         "f"(__uint_as_float(v[c][4 * u]) * scale), "f"(__uint_as_float(v[c][4 * u + 1]) * scale),
-                         "f"(__uint_as_float(v[c][4 * u + 2]) * scale), "f"(__uint_as_float(v[c][4 * u + 3]) * scale)
-                         : "memory");
-        if (issuer) mbar_arrive(ds_free);
-        continue;
-      }
-#pragma unroll
-      for (int round = 0; round < 2; ++round) {
-        if (!(dbg & 2)) {
-#pragma unroll
-          for (int b = 0; b < 2; ++b) {  // box b: 32 fp32 columns, [128 rows][128 B] SW128
-            uint8_t* row = stage + b * 16384 + r * 128;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const uint32_t* x = &v[round * 2 + b][4 * u];
-              *reinterpret_cast<float4*>(row + ((u ^ (r & 7)) * 16)) =
-                  make_float4(__uint_as_float(x[0]) * scale, __uint_as_float(x[1]) * scale,
-                              __uint_as_float(x[2]) * scale, __uint_as_float(x[3]) * scale);
-            }
+          mma_ts(tG1, tP, sDO(s), i > 0);       // dV += P^T dO(i)
+          tc_commit(&b_empty[s]);
+          mma_ts(tG0, tP + 32, sQ(s), i > 0);  // dK += dS^T Q(i)
+          tc_commit(&a_empty[s]);
+          if (i + 1 < n) {
+            mbar_wait(&b_full[s1], ((i + 1) >> 1) & 1);
+            tc_fence_after();
+            mma_ss(tP, sV, sDO(s1));  // dP^T(i+1) over P^T / dS^T(i), consumed by dV(i) / dK(i) before it
+            tc_commit(dp_full);
           }
-          fence_proxy_async();
+          if (tr && i < 64) trace[i * 8 + 3] = clock64();
         }
-        named_bar(1, 128);
-        if (issuer) {
-          if (!(dbg & 2)) {
-            tma_reduce_add_2d(&mDQ, stage, round * 64, h * S + q0);
-            tma_reduce_add_2d(&mDQ, stage + 16384, round * 64 + 32, h * S + q0);
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            bulk_wait_read();
+      } else {
+        const uint32_t sQ = smem_u32(smem + L::kOffQq), sDO = smem_u32(smem + L::kOffDOq);
+        auto sK = [&](int s) { return smem_u32(smem + L::kOffKq + s * L::kTile); };
+        auto sV = [&](int s) { return smem_u32(smem + L::kOffVq + s * L::kTile); };
+        mbar_wait(&a_full[0], 0);
+        tc_fence_after();
+        mma_ss(tS, sQ, sK(0));
+        tc_commit(s_full);
+        mbar_wait(&b_full[0], 0);
+        tc_fence_after();
+        mma_ss(tP, sDO, sV(0));
+        tc_commit(&b_empty[0]);
+        tc_commit(dp_full);
+        for (int j = 0; j < n; ++j) {
+          if (j + 1 < n) {
+            const int sa = (j + 1) % 3;
+            mbar_wait(s_free, j & 1);  // S(j) is in registers
+            mbar_wait(&a_full[sa], ((j + 1) / 3) & 1);
+            tc_fence_after();
+            mma_ss(tS, sQ, sK(sa));
+            tc_commit(s_full);
           }
-          if (round == 1) mbar_arrive(ds_free);
+          mbar_wait(ds_full, j & 1);
+          tc_fence_after();
+          mma_ts(tG0, tP, sK(j % 3), j > 0);  // dQ += dS K(j)
+          tc_commit(&a_empty[j % 3]);
+          if (j + 1 < n) {
+            const int sb = (j + 1) & 1;
+            mbar_wait(&b_full[sb], ((j + 1) >> 1) & 1);
+            tc_fence_after();
+            mma_ss(tP, sDO, sV(sb));  // dP(j+1) over dS(j), consumed by dQ(j) before it
+            tc_commit(&b_empty[sb]);
+            tc_commit(dp_full);
+          }
         }
-        if (round == 0) named_bar(1, 128);
       }
+      tc_commit(acc_full);
     }
-    if (issuer) bulk_wait_all();
   } else {
-    // ---------------- P^T / dS^T warps 0..7 ----------------
+    // ---------------- math warps 0..7 ----------------
     const int quad = warp & 3, half = warp >> 2;
-    const int r = quad * 32 + lane;  // key row
+    const int r = quad * 32 + lane;  // TMEM lane: KV key row / Q query row
     const uint32_t lo = static_cast<uint32_t>(quad * 32) << 16;
-    const int key = k0 + r;
     const float scale_log2 = scale * kLog2e;
-    const float* lse_h = lse + static_cast<int64_t>(h) * S;
-    const float* delta_h = delta + static_cast<int64_t>(h) * S;
-    for (int i = 0; i < n; ++i) {
-      const int qb = (kt + i) * 128 + half * 64;  // this warp's 64 queries
-      const bool diag = i == 0;
-      if (dbg & 8) {  // development: MMA pipeline bound (no P / dS math, no TMEM traffic)
+    // exponentials: MUFU.EX2 for all but kPoly of every 8 pairs (the math warps are issue-bound,
+    // and the polynomial costs ~5 issue slots per element against 1 for MUFU)
+    auto exp_pair = [&](int j4, int e2, float2 x, int kPoly) {
+      return (2 * (j4 & 3) + e2 < kPoly) ? exp2_pair<true>(x) : exp2_pair<false>(x);
+    };
+    if (!role_q) {
+      const int key = tile * 128 + r;
+      // one query tile; kDiag (the first tile only) masks key > query
+      auto kv_tile = [&](int i, auto diag_c) {
+        constexpr bool kDiag = decltype(diag_c)::value;
+        const int qb = (tile + i) * 128 + half * 64;  // this warp's 64 queries
+        const bool tr = trace && lin == 0 && warp == 0 && lane == 0 && i < 64;
+        float pf[64];
+        uint32_t sv[64];
         mbar_wait(s_full, i & 1);
-        if (lane == 0) mbar_arrive(p_full);
+        if (tr) trace[i * 8 + 4] = clock64();
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld_x16(tS + lo + half * 64 + c * 16, *reinterpret_cast<uint32_t(*)[16]>(&sv[c * 16]));
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_free);  // S^T(i+1) may overwrite the S^T columns
+        mbar_wait(&a_full[i & 1], (i >> 1) & 1);  // this tile's -lse*log2e (with Q(i)) is in shared memory
+        const uint32_t l4 = smem_u32(smem + L::kOffLD + (i & 1) * 1024 + half * 256);
+#pragma unroll
+        for (int j4 = 0; j4 < 16; ++j4) {
+          const float4 l = lds_f4(l4 + j4 * 16);  // warp-uniform: shared-memory broadcast
+          const float2 x01 = __ffma2_rn(make_float2(__uint_as_float(sv[j4 * 4]), __uint_as_float(sv[j4 * 4 + 1])),
+                                        make_float2(scale_log2, scale_log2), make_float2(l.x, l.y));
+          const float2 x23 = __ffma2_rn(make_float2(__uint_as_float(sv[j4 * 4 + 2]), __uint_as_float(sv[j4 * 4 + 3])),
+                                        make_float2(scale_log2, scale_log2), make_float2(l.z, l.w));
+          const float2 p01 = exp_pair(j4, 0, x01, kPolyKV), p23 = exp_pair(j4, 1, x23, kPolyKV);
+          pf[j4 * 4 + 0] = p01.x; pf[j4 * 4 + 1] = p01.y;
+          pf[j4 * 4 + 2] = p23.x; pf[j4 * 4 + 3] = p23.y;
+        }
+        if constexpr (kDiag) {
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (key > qb + j) pf[j] = 0.f;
+        }
+        if (tr) trace[i * 8 + 5] = clock64();
         mbar_wait(dp_full, i & 1);
-        if (i >= 1) mbar_wait(ds_free, (i - 1) & 1);
+        if (tr) trace[i * 8 + 6] = clock64();
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld_x16(tP + lo + half * 64 + c * 16, *reinterpret_cast<uint32_t(*)[16]>(&sv[c * 16]));
+        tmem_ld_wait();
+        mbar_wait(&b_full[i & 1], (i >> 1) & 1);  // this tile's delta (with dO(i)) is in shared memory
+        const uint32_t d4 = smem_u32(smem + L::kOffLD + (i & 1) * 1024 + 512 + half * 256);
+        uint32_t pk[32], dk[32];
+#pragma unroll
+        for (int j4 = 0; j4 < 16; ++j4) {
+          const float4 dl = lds_f4(d4 + j4 * 16);
+          const float2 a01 = __fadd2_rn(make_float2(__uint_as_float(sv[j4 * 4]), __uint_as_float(sv[j4 * 4 + 1])),
+                                        make_float2(-dl.x, -dl.y));
+          const float2 a23 = __fadd2_rn(make_float2(__uint_as_float(sv[j4 * 4 + 2]), __uint_as_float(sv[j4 * 4 + 3])),
+                                        make_float2(-dl.z, -dl.w));
+          const float2 d01 = __fmul2_rn(make_float2(pf[j4 * 4], pf[j4 * 4 + 1]), a01);
+          const float2 d23 = __fmul2_rn(make_float2(pf[j4 * 4 + 2], pf[j4 * 4 + 3]), a23);
+          dk[j4 * 2] = pack_bf16(d01.x, d01.y);
+          dk[j4 * 2 + 1] = pack_bf16(d23.x, d23.y);
+          pk[j4 * 2] = pack_bf16(pf[j4 * 4], pf[j4 * 4 + 1]);
+          pk[j4 * 2 + 1] = pack_bf16(pf[j4 * 4 + 2], pf[j4 * 4 + 3]);
+        }
+        // P^T | dS^T over this warp's own 64 dP^T columns (all read above): A operands of dV / dK
+        tmem_st_32x32b_x32(tP + lo + half * 64, pk);
+        tmem_st_32x32b_x32(tP + lo + half * 64 + 32, dk);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
         if (lane == 0) mbar_arrive(ds_full);
-        continue;
+        if (tr) trace[i * 8 + 7] = clock64();
+      };
+      for (int i = 0; i < n; ++i) {
+        if (dbg & 8) {  // development: MMA pipeline bound (no P / dS math)
+          mbar_wait(s_full, i & 1);
+          if (lane == 0) mbar_arrive(s_free);
+          mbar_wait(dp_full, i & 1);
+          if (lane == 0) mbar_arrive(ds_full);
+          continue;
+        }
+        if (i == 0) kv_tile(i, std::true_type{});
+        else kv_tile(i, std::false_type{});
       }
-      float pf[64];
-      mbar_wait(s_full, i & 1);
-      tc_fence_after();
+    } else {
+      const int q = tile * 128 + r;
+      const float nl2 = nlse2[static_cast<int64_t>(h) * S + q];
+      const float dl = delta[static_cast<int64_t>(h) * S + q];
+      // one key tile; kDiag (the last tile only) masks key > query
+      auto q_tile = [&](int j, auto diag_c) {
+        constexpr bool kDiag = decltype(diag_c)::value;
+        const int kb = j * 128 + half * 64;  // this warp's 64 keys
+        float pf[64];
+        uint32_t sv[64];
+        mbar_wait(s_full, j & 1);
+        tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {  // 16 queries per chunk
-        uint32_t sv[16];
-        tmem_ld_x16(tS + lo + half * 64 + c * 16, sv);
+        for (int c = 0; c < 4; ++c) tmem_ld_x16(tS + lo + half * 64 + c * 16, *reinterpret_cast<uint32_t(*)[16]>(&sv[c * 16]));
         tmem_ld_wait();
-        const float4* l4 = reinterpret_cast<const float4*>(lse_h + qb + c * 16);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_free);  // S(j+1) may overwrite the S columns
 #pragma unroll
-        for (int j4 = 0; j4 < 4; ++j4) {
-          const float4 l = __ldg(l4 + j4);  // warp-uniform: broadcast
-          const float lv[4] = {l.x, l.y, l.z, l.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int j = j4 * 4 + e;
-            float p = (dbg & 1) ? 0.f : fast_exp2(fmaf(__uint_as_float(sv[j]), scale_log2, -lv[e] * kLog2e));
-            if (diag && key > qb + c * 16 + j) p = 0.f;
-            pf[c * 16 + j] = p;
-          }
+        for (int j4 = 0; j4 < 16; ++j4) {
+          const float2 x01 = __ffma2_rn(make_float2(__uint_as_float(sv[j4 * 4]), __uint_as_float(sv[j4 * 4 + 1])),
+                                        make_float2(scale_log2, scale_log2), make_float2(nl2, nl2));
+          const float2 x23 = __ffma2_rn(make_float2(__uint_as_float(sv[j4 * 4 + 2]), __uint_as_float(sv[j4 * 4 + 3])),
+                                        make_float2(scale_log2, scale_log2), make_float2(nl2, nl2));
+          const float2 p01 = exp_pair(j4, 0, x01, kPolyQ), p23 = exp_pair(j4, 1, x23, kPolyQ);
+          pf[j4 * 4 + 0] = p01.x; pf[j4 * 4 + 1] = p01.y;
+          pf[j4 * 4 + 2] = p23.x; pf[j4 * 4 + 3] = p23.y;
         }
-        uint32_t pk[8];
+        if constexpr (kDiag) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) pk[j] = pack_bf16(pf[c * 16 + 2 * j], pf[c * 16 + 2 * j + 1]);
-        // P^T over this warp's own (already read) S^T columns: the A operand of dV
-        tmem_st_x8(tS + lo + half * 64 + c * 8, pk);
-      }
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
-
-      mbar_wait(dp_full, i & 1);
-      if (i >= 1) mbar_wait(ds_free, (i - 1) & 1);  // dQ staging of tile i-1 read by the TMA unit
-      tc_fence_after();
-      uint8_t* drow = smem + L::kOffDS + half * (L::kTile / 2) + r * 128;
+          for (int e = 0; e < 64; ++e)
+            if (kb + e > q) pf[e] = 0.f;
+        }
+        mbar_wait(dp_full, j & 1);
+        tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t dv[16];
-        tmem_ld_x16(tP + lo + half * 64 + c * 16, dv);
+        for (int c = 0; c < 4; ++c) tmem_ld_x16(tP + lo + half * 64 + c * 16, *reinterpret_cast<uint32_t(*)[16]>(&sv[c * 16]));
         tmem_ld_wait();
-        const float4* d4 = reinterpret_cast<const float4*>(delta_h + qb + c * 16);
-        uint32_t dk[8];
+        uint32_t dk[32];
 #pragma unroll
-        for (int j4 = 0; j4 < 4; ++j4) {
-          const float4 dl = __ldg(d4 + j4);
-          const float dlv[4] = {dl.x, dl.y, dl.z, dl.w};
-          float ds[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) ds[e] = pf[c * 16 + j4 * 4 + e] * (__uint_as_float(dv[j4 * 4 + e]) - dlv[e]);
-          dk[j4 * 2] = pack_bf16(ds[0], ds[1]);
-          dk[j4 * 2 + 1] = pack_bf16(ds[2], ds[3]);
+        for (int j2 = 0; j2 < 32; ++j2) {
+          const float2 a2 = __fadd2_rn(make_float2(__uint_as_float(sv[2 * j2]), __uint_as_float(sv[2 * j2 + 1])),
+                                       make_float2(-dl, -dl));
+          const float2 d2 = __fmul2_rn(make_float2(pf[2 * j2], pf[2 * j2 + 1]), a2);
+          dk[j2] = pack_bf16(d2.x, d2.y);
         }
-        // dS^T over this warp's own dP^T columns (A operand of dK) and into smem (A of dQ)
-        tmem_st_x8(tP + lo + half * 64 + c * 8, dk);
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int unit = c * 2 + u;
-          *reinterpret_cast<uint4*>(drow + ((unit ^ (r & 7)) * 16)) =
-              make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+        tmem_st_32x32b_x32(tP + lo + half * 64, dk);  // dS over this warp's own, already read dP columns
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(ds_full);
+      };
+      for (int j = 0; j < n; ++j) {
+        if (dbg & 8) {  // development: MMA pipeline bound (no P / dS math)
+          mbar_wait(s_full, j & 1);
+          if (lane == 0) mbar_arrive(s_free);
+          mbar_wait(dp_full, j & 1);
+          if (lane == 0) mbar_arrive(ds_full);
+          continue;
         }
+        if (j == n - 1) q_tile(j, std::true_type{});
+        else q_tile(j, std::false_type{});
       }
-      tmem_st_wait();
-      fence_proxy_async();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(ds_full);
     }
-    // dK (scaled), dV -> bf16
-    mbar_wait(dkv_full, 0);
+    // epilogue: KV role dK (scaled) | dV; Q role dQ (scaled) -> bf16 rows (or pushed to the owner rank)
+    mbar_wait(acc_full, 0);
     tc_fence_after();
+    const int tok = tile * 128 + r;
+    int64_t off = static_cast<int64_t>(tok) * ld_d + h * D;
+    __nv_bfloat16* base0 = role_q ? dq_out : dk_out;
+    __nv_bfloat16* base1 = dv_out;
+    if (push.p[0]) {  // fused all-to-all: rows go to the owner rank of the token
+      const int owner = tok / push.T;
+      __nv_bfloat16* pb = static_cast<__nv_bfloat16*>(push.p[owner]);
+      off = static_cast<int64_t>(tok - owner * push.T) * push.ld + h * D;
+      base0 = pb + (role_q ? push.col_q : push.col_k);
+      base1 = pb + push.col_v;
+    }
 #pragma unroll 1
     for (int c = 0; c < 2; ++c) {
       const int col = half * 64 + c * 32;
-      uint32_t a[32], b[32];
-      tmem_ld_32x32b_x32(tDK + lo + col, a);
-      tmem_ld_32x32b_x32(tDV + lo + col, b);
+      uint32_t a[32];
+      tmem_ld_32x32b_x32(tG0 + lo + col, a);
       tmem_ld_wait();
-      uint4* pk_out;
-      uint4* pv_out;
-      if (push.p[0]) {  // fused all-to-all: rows go to the owner of the key token
-        const int owner = key / push.T;
-        __nv_bfloat16* base = static_cast<__nv_bfloat16*>(push.p[owner]) +
-                              static_cast<int64_t>(key - owner * push.T) * push.ld + h * D + col;
-        pk_out = reinterpret_cast<uint4*>(base + push.col_k);
-        pv_out = reinterpret_cast<uint4*>(base + push.col_v);
-      } else {
-        pk_out = reinterpret_cast<uint4*>(dk_out + static_cast<int64_t>(key) * ld_d + h * D + col);
-        pv_out = reinterpret_cast<uint4*>(dv_out + static_cast<int64_t>(key) * ld_d + h * D + col);
-      }
+      uint4* o0 = reinterpret_cast<uint4*>(base0 + off + col);
 #pragma unroll
       for (int v4 = 0; v4 < 4; ++v4) {
-        uint32_t x[4], y[4];
+        uint32_t x[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
+        for (int e = 0; e < 4; ++e)
           x[e] = pack_bf16(__uint_as_float(a[v4 * 8 + 2 * e]) * scale, __uint_as_float(a[v4 * 8 + 2 * e + 1]) * scale);
-          y[e] = pack_bf16(__uint_as_float(b[v4 * 8 + 2 * e]), __uint_as_float(b[v4 * 8 + 2 * e + 1]));
+        o0[v4] = make_uint4(x[0], x[1], x[2], x[3]);
+      }
+      if (!role_q) {
+        tmem_ld_32x32b_x32(tG1 + lo + col, a);
+        tmem_ld_wait();
+        uint4* o1 = reinterpret_cast<uint4*>(base1 + off + col);
+#pragma unroll
+        for (int v4 = 0; v4 < 4; ++v4) {
+          uint32_t x[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            x[e] = pack_bf16(__uint_as_float(a[v4 * 8 + 2 * e]), __uint_as_float(a[v4 * 8 + 2 * e + 1]));
+          o1[v4] = make_uint4(x[0], x[1], x[2], x[3]);
         }
-        pk_out[v4] = make_uint4(x[0], x[1], x[2], x[3]);
-        pv_out[v4] = make_uint4(y[0], y[1], y[2], y[3]);
       }
     }
     if (push.p[0]) __threadfence_system();  // pushed rows visible before the next barrier flag
@@ -1808,7 +1653,7 @@ __global__ void __launch_bounds__(kBwd2Threads, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 13) {
+  if (warp == 9) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
@@ -1821,86 +1666,57 @@ long long* g_attn_trace_fwd = nullptr;
 extern "C" void seqplan_isp_debug_set_trace(long long* dev_buf) { g_attn_trace = dev_buf; }
 extern "C" void seqplan_isp_debug_set_trace_fwd(long long* dev_buf) { g_attn_trace_fwd = dev_buf; }
 
-// Split backward (d = 128, S / 256 integral): dK/dV kernel (K in TMEM, no dQ) + CTA-pair dQ kernel.
-// delta = rowsum(dO * O) must be computed before; dq is written (or pushed) in bf16, no dq_acc.
-cudaError_t attention_bwd_split_tc(const AttnTensors& t, const __nv_bfloat16* dout, int64_t ld_dout, __nv_bfloat16* dq,
+// Atomic-free backward (attn_bwd_split_kernel): (role, tile) entries sorted by decreasing work
+// (KV: 4 (T - kt) MMAs, Q: 3 (qt + 1)); delta = rowsum(dO * O) computed before; dq/dk/dv bf16.
+static const int* split_table(int T) {
+  static std::map<int, int*> cache;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(T);
+  if (it != cache.end()) return it->second;
+  std::vector<std::pair<int, int>> e;  // (work, entry)
+  for (int k = 0; k < T; ++k) e.push_back({4 * (T - k), k});
+  for (int q = 0; q < T; ++q) e.push_back({3 * (q + 1), -q - 1});
+  std::stable_sort(e.begin(), e.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+  std::vector<int> host(e.size());
+  for (size_t i = 0; i < e.size(); ++i) host[i] = e[i].second;
+  int* dev = nullptr;
+  if (cudaMalloc(&dev, host.size() * sizeof(int)) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(dev, host.data(), host.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  cache[T] = dev;
+  return dev;
+}
+
+cudaError_t attention_bwd_nored_tc(const AttnTensors& t, const __nv_bfloat16* dout, int64_t ld_dout, __nv_bfloat16* dq,
                                    __nv_bfloat16* dk, __nv_bfloat16* dv, int64_t ld_d, const float* delta,
-                                   cudaStream_t st) {
-  if (t.d != 128 || t.S % 256) return cudaErrorInvalidValue;
-  using L = BwdSmem;
-  using Q = DqCfg;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_bwd_tc_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(attn_bwd_dq_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::kBytes);
-    if (e != cudaSuccess) return e;
-    attr = true;
+                                   const float* nlse2, cudaStream_t st) {
+  if (t.d != 128 || t.S % 128) return cudaErrorInvalidValue;
+  using L = BwdSCfg;
+  const char* pe = std::getenv("SEQPLAN_ISP_BWD_POLY");  // development: exponential split (kv*10+q)
+  const int poly = pe ? std::atoi(pe) : 0;
+  auto kern = attn_bwd_split_kernel<0, 0>;
+  switch (poly) {
+    case 33: kern = attn_bwd_split_kernel<3, 3>; break;
+    case 22: kern = attn_bwd_split_kernel<2, 2>; break;
+    case 43: kern = attn_bwd_split_kernel<4, 3>; break;
+    case 42: kern = attn_bwd_split_kernel<4, 2>; break;
+    case 53: kern = attn_bwd_split_kernel<5, 3>; break;
+    default: break;
   }
-  CUtensorMap mq, mk, mv, mdo, mkr, mvr, mkc;
-  const int64_t cols = static_cast<int64_t>(t.heads) * 128;
-  if (!map2d(&mq, t.q, t.S, cols, t.ld_qkv, kBwdQ) || !map2d(&mk, t.k, t.S, cols, t.ld_qkv, kBwdKeys) ||
-      !map2d(&mv, t.v, t.S, cols, t.ld_qkv, kBwdKeys) || !map2d(&mdo, dout, t.S, cols, ld_dout, kBwdQ) ||
-      !map2d(&mkr, t.k, t.S, cols, t.ld_qkv, Q::BN / 2) || !map2d(&mvr, t.v, t.S, cols, t.ld_qkv, Q::BN / 2) ||
-      !map2d(&mkc, t.k, t.S, cols, t.ld_qkv, Q::BN))
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes) != cudaSuccess)
     return cudaErrorInvalidValue;
-  const float scale = 1.0f / sqrtf(128.0f);
-  const int dbg = std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0;
-  AttnPush kv_push = t.push;  // dK / dV rows
-  attn_bwd_tc_kernel<false, true><<<lpt_grid(t.S / kBwdKeys, t.heads, t.S, 128), 320, L::kBytes, st>>>(
-      mq, mk, mv, mdo, t.lse, delta, nullptr, dk, dv, ld_d, t.S, scale, dbg, g_attn_trace, kv_push, t.k, t.ld_qkv);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = lpt_grid(t.S / kBM, t.heads, t.S, 128);
-  cfg.blockDim = dim3(320);
-  cfg.dynamicSmemBytes = Q::kBytes;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, attn_bwd_dq_pair_kernel, mkr, mvr, mkc, t.q, t.ld_qkv, dout, ld_dout, t.lse, delta, dq,
-                            ld_d, t.S, scale, t.push);
-}
-
-// [rows, 128] fp32 (dq_acc) with box {32 cols, 128 rows}, 128-B swizzle: the TMA reduce-add target.
-static bool map2d_f32(CUtensorMap* m, const void* base, int64_t rows, int box_rows) {
-  auto fn = encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[2] = {128u, static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {128u * 4u};
-  cuuint32_t box[2] = {32u, static_cast<cuuint32_t>(box_rows)};
-  cuuint32_t es[2] = {1u, 1u};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-// 128 x 128-tile backward (attn_bwd2_kernel). dq_acc must be zeroed and delta computed before.
-static cudaError_t attention_bwd_tc2(const AttnTensors& t, const __nv_bfloat16* dout, int64_t ld_dout,
-                                     __nv_bfloat16* dk, __nv_bfloat16* dv, int64_t ld_d, const float* delta,
-                                     float* dq_acc, cudaStream_t st) {
-  using L = Bwd2Cfg;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_bwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  CUtensorMap mq, mk, mv, mdo, mdq;
+  const int T = t.S / 128;
+  const int* table = split_table(T);
+  if (!table) return cudaErrorMemoryAllocation;
+  CUtensorMap mq, mk, mv, mdo;
   const int64_t cols = static_cast<int64_t>(t.heads) * 128;
   if (!map2d(&mq, t.q, t.S, cols, t.ld_qkv, 128) || !map2d(&mk, t.k, t.S, cols, t.ld_qkv, 128) ||
-      !map2d(&mv, t.v, t.S, cols, t.ld_qkv, 128) || !map2d(&mdo, dout, t.S, cols, ld_dout, 128) ||
-      !map2d_f32(&mdq, dq_acc, static_cast<int64_t>(t.heads) * t.S, 128))
+      !map2d(&mv, t.v, t.S, cols, t.ld_qkv, 128) || !map2d(&mdo, dout, t.S, cols, ld_dout, 128))
     return cudaErrorInvalidValue;
   const float scale = 1.0f / sqrtf(128.0f);
   const int dbg = std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0;
-  attn_bwd2_kernel<<<lpt_grid(t.S / 128, t.heads, t.S, 128), kBwd2Threads, L::kBytes, st>>>(
-      mq, mk, mv, mdo, mdq, t.lse, delta, dq_acc, dk, dv, ld_d, t.S, scale, t.push, dbg);
+  kern<<<lpt_grid(2 * T, t.heads, t.S, 128), kBwdSThreads, L::kBytes, st>>>(
+      mq, mk, mv, mdo, table, nlse2, delta, dq, dk, dv, ld_d, t.S, scale, t.push, dbg, g_attn_trace);
   return cudaGetLastError();
 }
 
@@ -1908,7 +1724,6 @@ static cudaError_t attention_bwd_tc2(const AttnTensors& t, const __nv_bfloat16* 
 cudaError_t attention_bwd_tc(const AttnTensors& t, const __nv_bfloat16* dout, int64_t ld_dout, __nv_bfloat16* dk,
                              __nv_bfloat16* dv, int64_t ld_d, const float* delta, float* dq_acc, cudaStream_t st) {
   if (t.d != 128 || t.S % kBwdKeys) return cudaErrorInvalidValue;
-  if (std::getenv("SEQPLAN_ISP_ATTN_BWD128")) return attention_bwd_tc2(t, dout, ld_dout, dk, dv, ld_d, delta, dq_acc, st);
   using L = BwdSmem;
   static bool attr = false;
   if (!attr) {

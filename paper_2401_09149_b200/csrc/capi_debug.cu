@@ -81,3 +81,38 @@ extern "C" int seqplan_isp_debug_rmsnorm(const void* x, const void* g, void* y, 
                          static_cast<__nv_bfloat16*>(dx), dg, T, H, st, 148);
   return e == cudaSuccess ? SEQPLAN_ISP_OK : SEQPLAN_ISP_ERR_RUNTIME;
 }
+
+// Ulysses all-to-all of one rank (dir = +1: token-sharded [T, parts*H] on every rank -> this
+// rank's head-sharded [S, parts*Hl]; dir = -1: the reverse), src[q] = rank q's buffer; no RoPE
+// when cos_t == NULL. The kernels the block runs after the QKV GEMM / before the O projection.
+extern "C" int seqplan_isp_debug_all_to_all(int world, int rank, int T, int H, int parts, int d, int dir,
+                                            const void* const* src, void* dst, const float* cos_t,
+                                            const float* sin_t, int rope_parts, void* stream) {
+  if (world < 1 || world > isp::kMaxRanks || rank < 0 || rank >= world || !src || !dst)
+    return SEQPLAN_ISP_ERR_INVALID;
+  isp::PeerPtrs p{};
+  for (int q = 0; q < world; ++q) p.p[q] = const_cast<void*>(src[q]);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int rp = cos_t ? rope_parts : 0;
+  cudaError_t e = dir > 0 ? isp::a2a_tokens_to_heads(p, world, rank, T, H, parts, static_cast<__nv_bfloat16*>(dst),
+                                                      cos_t, sin_t, d, rp, st, 592)
+                          : isp::a2a_heads_to_tokens(p, world, rank, T, H, parts, static_cast<__nv_bfloat16*>(dst),
+                                                     cos_t, sin_t, d, rp, st, 592);
+  if (e == cudaErrorInvalidValue) return SEQPLAN_ISP_ERR_INVALID;
+  return e == cudaSuccess ? SEQPLAN_ISP_OK : SEQPLAN_ISP_ERR_RUNTIME;
+}
+
+// Gradient reduce-scatter of one rank fused with the cast / scale: out[i] (+)= scale * sum over
+// q = 0..world-1 (in that order, fp32) of part[q][rank * shard + i]; part bf16 or fp32.
+extern "C" int seqplan_isp_debug_reduce_scatter(int world, int rank, int64_t shard_elems, const void* const* part,
+                                                int part_is_f32, float scale, int accumulate, float* out,
+                                                void* stream) {
+  if (world < 1 || world > isp::kMaxRanks || rank < 0 || rank >= world || !part || !out)
+    return SEQPLAN_ISP_ERR_INVALID;
+  isp::PeerPtrs p{};
+  for (int q = 0; q < world; ++q) p.p[q] = const_cast<void*>(part[q]);
+  cudaError_t e = isp::reduce_scatter_pull(p, world, rank, shard_elems, part_is_f32 != 0, scale, accumulate, out,
+                                           static_cast<cudaStream_t>(stream), 592);
+  if (e == cudaErrorInvalidValue) return SEQPLAN_ISP_ERR_INVALID;
+  return e == cudaSuccess ? SEQPLAN_ISP_OK : SEQPLAN_ISP_ERR_RUNTIME;
+}

@@ -1486,6 +1486,10 @@ static int create_ctx(int world, int rank, int device, const seqplan_isp_shape* 
     if (!seqplan::validate(s, m, cl).ok() || s.sp != world || s.ps != world || s.tp != 1 || s.pp != 1 ||
         s.dp != 1 || (s.recompute != 0 && s.recompute != 1))
       return SEQPLAN_ISP_ERR_INVALID;
+    // Legal plans this executor does not run: it processes one micro-batch (b = 1, n = 1) per
+    // fwd/bwd call, with no gradient-sync (gs) or optimizer-state-sharding (oss) groups.
+    if (s.micro_batch != 1 || s.micro_batch_num != 1 || s.gs != 1 || s.oss != 1)
+      return SEQPLAN_ISP_ERR_UNSUPPORTED;
   }
   Ctx* c = new Ctx();
   c->world = world;

@@ -67,11 +67,12 @@ cudaError_t attention_fwd_tc(const AttnTensors& t, cudaStream_t st);
 // tcgen05/TMEM backward for d = 128 (dK, dV written; dq_acc += scale * dS K, fp32).
 cudaError_t attention_bwd_tc(const AttnTensors& t, const __nv_bfloat16* dout, int64_t ld_dout, __nv_bfloat16* dk,
                              __nv_bfloat16* dv, int64_t ld_d, const float* delta, float* dq_acc, cudaStream_t st);
-// Split tcgen05 backward (d = 128, S % 256 == 0): dK/dV kernel + CTA-pair dQ kernel, dq in bf16
-// directly (no fp32 accumulator, no atomics); t.push routes dq/dk/dv rows to their owner ranks.
-cudaError_t attention_bwd_split_tc(const AttnTensors& t, const __nv_bfloat16* dout, int64_t ld_dout, __nv_bfloat16* dq,
+// Atomic-free tcgen05 backward (d = 128, S % 128 == 0): one launch of key-tile (dK/dV) and
+// query-tile (dQ) CTAs, every gradient accumulated in TMEM and written once in bf16; delta must be
+// computed before, with nlse2 = -lse*log2(e) [heads, S]; t.push routes dq/dk/dv rows to their owner ranks.
+cudaError_t attention_bwd_nored_tc(const AttnTensors& t, const __nv_bfloat16* dout, int64_t ld_dout, __nv_bfloat16* dq,
                                    __nv_bfloat16* dk, __nv_bfloat16* dv, int64_t ld_d, const float* delta,
-                                   cudaStream_t st);
+                                   const float* nlse2, cudaStream_t st);
 // dq/dk/dv written (bf16) with row stride ld_dqkv; scratch: fp32 [heads*S] (delta) and
 // fp32 [heads*S*d] (dq accumulator).
 cudaError_t attention_bwd(const AttnTensors& t, const __nv_bfloat16* dout, __nv_bfloat16* dq,

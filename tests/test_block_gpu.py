@@ -138,6 +138,10 @@ def test_pool_trace_replays_through_run_mempool_model(cuda):
     st = blk.pool_stats()
     assert st["peak_reserved"] >= st["reserved"] > 0
     assert st["reserved"] == st["allocated"] + st["free_cached"] + st["fragmented"]
+    # the reference's run_mempool (mempool.hpp:285-387) replaying the pool's own recorded
+    # alloc/free trace reserves exactly the bytes the device pool reserved
+    rep = blk.pool_replay()
+    assert rep["peak_reserved"] == st["peak_reserved"], (rep, st)
     blk.close()
 
 

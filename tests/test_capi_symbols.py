@@ -48,3 +48,21 @@ def test_invalid_arguments_are_rejected_without_gpu():
     sh = capi.make_shape(512, 7, 1024)  # 512 % 7 != 0 -> invalid model config
     st = l.seqplan_isp_ctx_create(1, 3, 0, ctypes.byref(sh), None, None, 0, ctypes.byref(h))
     assert st == 1 and not h.value  # rank >= world
+
+
+def test_unsupported_micro_batching_is_refused_without_gpu():
+    """A legal ISP plan the executor does not run (b != 1 or n != 1, gs / oss groups) is refused
+    with SEQPLAN_ISP_ERR_UNSUPPORTED instead of silently running b = n = 1 (isp_block.cpp create_ctx)."""
+    from paper_2401_09149_b200 import capi
+    l = capi.lib()
+    sh = capi.make_shape(512, 8, 1024)
+    for field, val in (("micro_batch", 2), ("micro_batch_num", 3)):
+        st = capi.StrategyC(micro_batch=1, micro_batch_num=1, recompute=0, pp=1, dp=1, tp=1, sp=2, ps=2, gs=1, oss=1)
+        setattr(st, field, val)
+        h = capi.c_vp()
+        rc = l.seqplan_isp_ctx_create(2, 0, 0, ctypes.byref(sh), ctypes.byref(st), None, 0, ctypes.byref(h))
+        assert rc == 4 and not h.value, (field, rc)
+    # an illegal plan stays "invalid" (sp must equal the world size)
+    st = capi.StrategyC(micro_batch=1, micro_batch_num=1, recompute=0, pp=1, dp=1, tp=1, sp=1, ps=2, gs=1, oss=1)
+    h = capi.c_vp()
+    assert l.seqplan_isp_ctx_create(2, 0, 0, ctypes.byref(sh), ctypes.byref(st), None, 0, ctypes.byref(h)) == 1

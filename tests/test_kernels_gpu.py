@@ -24,14 +24,15 @@ def torch_attention(q, k, v):  # [S, h, d] fp32, causal
     return torch.einsum("hqk,khd->qhd", p, v), lse
 
 
-@pytest.mark.parametrize("split", [False, True])
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("S,heads,d", [(256, 2, 64), (512, 3, 128), (1024, 1, 128), (384, 2, 64)])
-def test_attention_fwd_bwd(cuda, S, heads, d, split, monkeypatch):
-    # split: the opt-in two-kernel backward (dK/dV kernel + CTA-pair dQ kernel), d = 128 only
-    if split and d != 128:
-        pytest.skip("split backward is d = 128")
-    if split:
-        monkeypatch.setenv("SEQPLAN_ISP_ATTN_SPLIT_BWD", "1")
+def test_attention_fwd_bwd(cuda, S, heads, d, fused, monkeypatch):
+    # fused: the opt-in fused backward (dQ reduced with fp32 L2 atomics), d = 128 only; default is
+    # the atomic-free two-role backward
+    if fused and d != 128:
+        pytest.skip("the fused tcgen05 backward is d = 128")
+    if fused:
+        monkeypatch.setenv("SEQPLAN_ISP_ATTN_FUSED_BWD", "1")
     torch.manual_seed(S + d)
     Hl = heads * d
     qkv = torch.randn(S, 3 * Hl, device=cuda).bfloat16()
@@ -89,3 +90,70 @@ def test_rmsnorm_fwd_bwd(cuda, T, H):
     torch.cuda.synchronize()
     assert rel(dx.float() - dres.float(), xf.grad) < 1e-2
     assert rel(dg, gf.grad) < 5e-3
+
+
+def chunked_reference(q, k, v, do, chunk=2048):
+    """fp32 causal attention fwd + bwd, query chunk by query chunk (no S x S matrix): o, lse, dq, dk, dv.
+    q, k, v, do: [S, d] fp32 of one head."""
+    S, d = q.shape
+    scale = 1.0 / math.sqrt(d)
+    o = torch.empty_like(q); lse = torch.empty(S, device=q.device)
+    dq = torch.empty_like(q); dk = torch.zeros_like(k); dv = torch.zeros_like(v)
+    for a in range(0, S, chunk):
+        b = min(S, a + chunk)
+        s = (q[a:b] @ k[:b].t()) * scale
+        mask = torch.arange(b, device=q.device)[None, :] > torch.arange(a, b, device=q.device)[:, None]
+        s.masked_fill_(mask, float("-inf"))
+        l = torch.logsumexp(s, dim=-1)
+        p = torch.exp(s - l[:, None])
+        o[a:b] = p @ v[:b]
+        lse[a:b] = l
+        delta = (do[a:b] * o[a:b]).sum(-1)
+        dp = do[a:b] @ v[:b].t()
+        ds = p * (dp - delta[:, None]) * scale
+        dq[a:b] = ds @ k[:b]
+        dk[:b] += ds.t() @ q[a:b]
+        dv[:b] += p.t() @ do[a:b]
+    return o, lse, dq, dk, dv
+
+
+@pytest.mark.parametrize("S,heads,check_heads", [
+    (16384, 8, (0, 5)),    # L2-sized head groups: lpt_grid puts 4 heads in a group, gridDim.z = 2
+    (32768, 2, (0, 1)),    # the 7B-32K sequence length
+    (131072, 1, (0,)),     # the 20B-128K sequence length: S/128 = 1024 tiles per head
+])
+def test_attention_long_sequence(cuda, S, heads, check_heads):
+    """The production tcgen05 attention (d = 128) at the BASELINE sequence lengths against a chunked
+    fp32 reference: rel-L2 <= 1e-2 on o, dq, dk, dv for the checked heads, |lse| abs error small.
+    At S = 128K the backward accumulates dK/dV over 1024 query tiles (SURVEY hard part vi)."""
+    torch.manual_seed(S + heads)
+    d = 128
+    Hl = heads * d
+    qkv = (torch.randn(S, 3 * Hl, device=cuda) * 0.5).bfloat16()
+    o = torch.empty(S, Hl, device=cuda, dtype=torch.bfloat16)
+    lse = torch.empty(heads, S, device=cuda)
+    do = torch.randn(S, Hl, device=cuda).bfloat16()
+    dqkv = torch.empty(S, 3 * Hl, device=cuda, dtype=torch.bfloat16)
+    delta = torch.empty(heads, S, device=cuda)
+    dq_acc = torch.empty(heads * S * d, device=cuda)
+    q, k, v = qkv[:, :Hl], qkv[:, Hl:2 * Hl], qkv[:, 2 * Hl:]
+    l = capi.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    capi.check(l.seqplan_isp_debug_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), 3 * Hl, o.data_ptr(), Hl,
+                                             lse.data_ptr(), S, heads, d, None, None, None, None, 0, None, None, st))
+    capi.check(l.seqplan_isp_debug_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), 3 * Hl, o.data_ptr(), Hl,
+                                             lse.data_ptr(), S, heads, d, do.data_ptr(), dqkv.data_ptr(),
+                                             dqkv[:, Hl:].data_ptr(), dqkv[:, 2 * Hl:].data_ptr(), 3 * Hl,
+                                             delta.data_ptr(), dq_acc.data_ptr(), st))
+    torch.cuda.synchronize()
+    for h in check_heads:
+        cs = slice(h * d, (h + 1) * d)
+        qf, kf, vf, dof = (t[:, cs].float() for t in (q, k, v, do))
+        ro, rl, rdq, rdk, rdv = chunked_reference(qf, kf, vf, dof)
+        assert rel(o[:, cs].float(), ro) < 1e-2, (h, "o")
+        assert (lse[h] - rl).abs().max().item() < 2e-2, (h, "lse")
+        for i, ref in enumerate((rdq, rdk, rdv)):
+            got = dqkv[:, i * Hl:(i + 1) * Hl][:, cs].float()
+            e = rel(got, ref)
+            assert e < 1e-2, (h, "dq dk dv"[i * 3:i * 3 + 2], e)
+        torch.cuda.empty_cache()
