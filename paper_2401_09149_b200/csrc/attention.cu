@@ -459,6 +459,17 @@ cudaError_t fwd_impl(const AttnTensors& t, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Inverse RoPE of dq / dk for the backward variants that do not fuse it (the opt-in fused tcgen05
+// kernel, the head-dim-64 mma.sync kernel): a separate pass over the head-sharded rows.
+cudaError_t unrope_after(const AttnTensors& t, __nv_bfloat16* dq, __nv_bfloat16* dk, int64_t ld_d, cudaStream_t st,
+                         int num_sms) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || !t.rope_cos) return e;
+  if (t.push.p[0]) return cudaErrorInvalidValue;  // rows already pushed: only the fused-RoPE kernel may push
+  return rope_inplace(dq, ld_d, t.S, 0, t.heads, t.d, t.rope_cos, t.rope_sin, static_cast<int>(dk - dq), -1, st,
+                      num_sms);
+}
+
 template <int D>
 cudaError_t bwd_impl(const AttnTensors& t, const __nv_bfloat16* dout, __nv_bfloat16* dq,
                      __nv_bfloat16* dk, __nv_bfloat16* dv, int64_t ld_d, float* delta,
@@ -486,12 +497,12 @@ cudaError_t bwd_impl(const AttnTensors& t, const __nv_bfloat16* dout, __nv_bfloa
     e = attention_bwd_tc(t, dout, t.ld_o, dk, dv, ld_d, delta, dq_acc, st);
     if (e != cudaSuccess) return e;
     attn_dq_convert_kernel<D><<<num_sms * 8, 256, 0, st>>>(dq_acc, dq, ld_d, t.S, t.heads, 1.0f, t.push);
-    return cudaGetLastError();
+    return unrope_after(t, dq, dk, ld_d, st, num_sms);
   }
   attn_bwd_kernel<D><<<dim3(t.S / BN, t.heads), 256, smem, st>>>(t, dout, dk, dv, ld_d, delta, dq_acc, scale);
   if (t.push.p[0]) return cudaErrorInvalidValue;  // fused all-to-all needs the tcgen05 kernels
   attn_dq_convert_kernel<D><<<num_sms * 8, 256, 0, st>>>(dq_acc, dq, ld_d, t.S, t.heads, scale, t.push);
-  return cudaGetLastError();
+  return unrope_after(t, dq, dk, ld_d, st, num_sms);
 }
 
 }  // namespace

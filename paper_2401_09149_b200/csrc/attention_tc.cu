@@ -1264,7 +1264,8 @@ __global__ void __launch_bounds__(kBwdSThreads, 1)
                           const int* __restrict__ table, const float* __restrict__ nlse2,
                           const float* __restrict__ delta, __nv_bfloat16* __restrict__ dq_out,
                           __nv_bfloat16* __restrict__ dk_out, __nv_bfloat16* __restrict__ dv_out, int64_t ld_d, int S,
-                          float scale, const __grid_constant__ AttnPush push, int dbg, long long* trace) {
+                          float scale, const __grid_constant__ AttnPush push, const float* __restrict__ rope_cos,
+                          const float* __restrict__ rope_sin, int dbg, long long* trace) {
   using L = BwdSCfg;
   constexpr int D = 128;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1605,7 +1606,9 @@ __global__ void __launch_bounds__(kBwdSThreads, 1)
         else q_tile(j, std::false_type{});
       }
     }
-    // epilogue: KV role dK (scaled) | dV; Q role dQ (scaled) -> bf16 rows (or pushed to the owner rank)
+    // epilogue: KV role dK (scaled) | dV; Q role dQ (scaled) -> bf16 rows (or pushed to the owner rank).
+    // With rope_cos, dK / dQ leave through the inverse rotary embedding (d/dx of RoPE(x) is R^T)
+    // from fp32, so the rotated q / k gradients are rounded to bf16 once.
     mbar_wait(acc_full, 0);
     tc_fence_after();
     const int tok = tile * 128 + r;
@@ -1619,33 +1622,58 @@ __global__ void __launch_bounds__(kBwdSThreads, 1)
       base0 = pb + (role_q ? push.col_q : push.col_k);
       base1 = pb + push.col_v;
     }
-#pragma unroll 1
-    for (int c = 0; c < 2; ++c) {
-      const int col = half * 64 + c * 32;
-      uint32_t a[32];
-      tmem_ld_32x32b_x32(tG0 + lo + col, a);
+    auto store32 = [&](__nv_bfloat16* dst, const float (&v)[32]) {
+      uint4* o4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+      for (int v4 = 0; v4 < 4; ++v4)
+        o4[v4] = make_uint4(pack_bf16(v[v4 * 8], v[v4 * 8 + 1]), pack_bf16(v[v4 * 8 + 2], v[v4 * 8 + 3]),
+                            pack_bf16(v[v4 * 8 + 4], v[v4 * 8 + 5]), pack_bf16(v[v4 * 8 + 6], v[v4 * 8 + 7]));
+    };
+    if (rope_cos) {  // this thread: rotation pairs (i, i + 64), i in [32 half, 32 half + 32)
+      uint32_t a[32], b[32];
+      tmem_ld_32x32b_x32(tG0 + lo + half * 32, a);
+      tmem_ld_32x32b_x32(tG0 + lo + 64 + half * 32, b);
       tmem_ld_wait();
-      uint4* o0 = reinterpret_cast<uint4*>(base0 + off + col);
+      const float* cs = rope_cos + static_cast<int64_t>(tok) * (D / 2) + half * 32;
+      const float* sn = rope_sin + static_cast<int64_t>(tok) * (D / 2) + half * 32;
+      float fl[32], fh[32];
 #pragma unroll
-      for (int v4 = 0; v4 < 4; ++v4) {
-        uint32_t x[4];
+      for (int i = 0; i < 32; i += 4) {
+        const float4 c4 = *reinterpret_cast<const float4*>(cs + i), s4 = *reinterpret_cast<const float4*>(sn + i);
+        const float cv[4] = {c4.x, c4.y, c4.z, c4.w}, sv4[4] = {s4.x, s4.y, s4.z, s4.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          x[e] = pack_bf16(__uint_as_float(a[v4 * 8 + 2 * e]) * scale, __uint_as_float(a[v4 * 8 + 2 * e + 1]) * scale);
-        o0[v4] = make_uint4(x[0], x[1], x[2], x[3]);
+        for (int e = 0; e < 4; ++e) {
+          const float x = __uint_as_float(a[i + e]) * scale, y = __uint_as_float(b[i + e]) * scale;
+          fl[i + e] = x * cv[e] + y * sv4[e];
+          fh[i + e] = y * cv[e] - x * sv4[e];
+        }
       }
-      if (!role_q) {
+      store32(base0 + off + half * 32, fl);
+      store32(base0 + off + 64 + half * 32, fh);
+    } else {
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        const int col = half * 64 + c * 32;
+        uint32_t a[32];
+        tmem_ld_32x32b_x32(tG0 + lo + col, a);
+        tmem_ld_wait();
+        float f[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) f[e] = __uint_as_float(a[e]) * scale;
+        store32(base0 + off + col, f);
+      }
+    }
+    if (!role_q) {
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        const int col = half * 64 + c * 32;
+        uint32_t a[32];
         tmem_ld_32x32b_x32(tG1 + lo + col, a);
         tmem_ld_wait();
-        uint4* o1 = reinterpret_cast<uint4*>(base1 + off + col);
+        float f[32];
 #pragma unroll
-        for (int v4 = 0; v4 < 4; ++v4) {
-          uint32_t x[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            x[e] = pack_bf16(__uint_as_float(a[v4 * 8 + 2 * e]), __uint_as_float(a[v4 * 8 + 2 * e + 1]));
-          o1[v4] = make_uint4(x[0], x[1], x[2], x[3]);
-        }
+        for (int e = 0; e < 32; ++e) f[e] = __uint_as_float(a[e]);
+        store32(base1 + off + col, f);
       }
     }
     if (push.p[0]) __threadfence_system();  // pushed rows visible before the next barrier flag
@@ -1716,7 +1744,8 @@ cudaError_t attention_bwd_nored_tc(const AttnTensors& t, const __nv_bfloat16* do
   const float scale = 1.0f / sqrtf(128.0f);
   const int dbg = std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0;
   kern<<<lpt_grid(2 * T, t.heads, t.S, 128), kBwdSThreads, L::kBytes, st>>>(
-      mq, mk, mv, mdo, table, nlse2, delta, dq, dk, dv, ld_d, t.S, scale, t.push, dbg, g_attn_trace);
+      mq, mk, mv, mdo, table, nlse2, delta, dq, dk, dv, ld_d, t.S, scale, t.push, t.rope_cos, t.rope_sin, dbg,
+      g_attn_trace);
   return cudaGetLastError();
 }
 

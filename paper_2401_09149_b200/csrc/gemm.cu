@@ -180,8 +180,9 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t t_b
         uint32_t lo[32], hi[32];
         ld_acc(t_base + hb + c, lo, part + hb + c, pstride, np);
         ld_acc(t_base + hb + c + hd, hi, part + hb + c + hd, pstride, np);
-        const int col = n0 + hb + c;  // global output column of the low half
-        const int part = col / args.push_H, hcol = col - part * args.push_H;
+        const int col = n0 + hb + c;  // output column of the low half (storage)
+        const int lcol = args.rope_col0 + col;  // logical column in the [parts*H] row
+        const int part = lcol / args.push_H, hcol = lcol - part * args.push_H;
         const int q = hcol / args.push_Hl, lc = hcol - q * args.push_Hl;
         float fl[32], fh[32];
 #pragma unroll

@@ -51,6 +51,9 @@ struct GemmArgs {
   const float* rope_cos = nullptr;
   const float* rope_sin = nullptr;
   int rope_parts = 0;
+  // logical column of this GEMM's column 0 in the [parts*H] row (a GEMM over a column slice of
+  // the QKV projection): selects the part / head for RoPE and the push target
+  int rope_col0 = 0;
   // persistent-grid size limit (0 = every SM): SMs held by concurrent bulk-copy comm kernels
   // are left out so no CTA of the persistent grid waits for them
   int sm_budget = 0;

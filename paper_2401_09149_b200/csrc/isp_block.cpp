@@ -3,8 +3,8 @@
 // One context per rank. The block's forward and backward are written as a short
 // list of phases separated by the exchange points of the ISP plan:
 //
-//   fwd  F1  norm1 -> QKV GEMM (-> RoPE at p = 1)               | AG(W) on the comm stream
-//        --- barrier ---  A2A qkv tokens->heads (+RoPE)
+//   fwd  F1  norm1 -> QKV GEMM (+RoPE in the epilogue)          | AG(W) on the comm stream
+//        --- barrier ---  A2A qkv tokens->heads
 //        F2  causal attention on D/p heads
 //        --- barrier ---  A2A o heads->tokens
 //        F3  O GEMM(+x) -> norm2 -> gate|up GEMM(+SwiGLU) -> down GEMM(+h)
@@ -12,7 +12,7 @@
 //            -> O dgrad/wgrad                                  | re-AG(W), RS(dW) on comm
 //        --- barrier ---  A2A dO tokens->heads
 //        B2  attention backward
-//        --- barrier ---  A2A dq|dk|dv heads->tokens (+inverse RoPE)
+//        --- barrier ---  A2A dq|dk|dv heads->tokens (inverse RoPE in the attention-bwd epilogue)
 //        B3  QKV dgrad/wgrad -> norm1 bwd
 //        --- barrier ---  RS of every weight gradient (fused bf16->fp32 cast/scale)
 //
@@ -745,6 +745,20 @@ void wait_gathered(Ctx* c, int t, cudaStream_t st) {
   for (int q = 0; q < c->world; ++q) ISP_CUDA(cudaStreamWaitEvent(st, c->ev_tq[c->evset][t][q], 0));
 }
 
+// QKV GEMM epilogue applies RoPE (rotate-half, position rank*T + row) to q and k before the bf16
+// store, on the token layout [T, 3H] kept locally.
+void set_rope_epilogue(Ctx* c, GemmArgs& g) {
+  g.push_T = static_cast<int>(c->T);
+  g.push_rank = c->rank;
+  g.push_parts = 3;
+  g.push_H = static_cast<int>(c->H);
+  g.push_Hl = static_cast<int>(c->Hl);
+  g.push_d = static_cast<int>(c->d);
+  g.rope_cos = c->cos_t;
+  g.rope_sin = c->sin_t;
+  g.rope_parts = 2;
+}
+
 void fwd_phase1(Ctx* c, const bf16* x, cudaStream_t st) {
   Span sp(c, st, 0, SEQPLAN_EV_FORWARD, 0);
   const int T = static_cast<int>(c->T), H = static_cast<int>(c->H);
@@ -763,6 +777,8 @@ void fwd_phase1(Ctx* c, const bf16* x, cudaStream_t st) {
       GemmArgs g;
       g.M = T; g.N = static_cast<int>(ncols); g.K = H;
       g.out = out + col0; g.ldo = 3 * H;
+      set_rope_epilogue(c, g);  // RoPE on q, k from the fp32 accumulator (one bf16 rounding)
+      g.rope_col0 = static_cast<int>(col0);
       gemm(c, {c->n1, H, false}, {w, H, false}, g, EPI_BF16, st);
     };
     slice(c->wshard(SEQPLAN_W_QKV), r0, n_own);
@@ -782,16 +798,8 @@ void fwd_phase1(Ctx* c, const bf16* x, cudaStream_t st) {
     g.rope_cos = c->cos_t;
     g.rope_sin = c->sin_t;
     g.rope_parts = 2;
-  } else if (c->world == 1 || c->ce_a2a) {  // RoPE in the epilogue, token layout kept locally
-    g.push_T = T;
-    g.push_rank = c->rank;
-    g.push_parts = 3;
-    g.push_H = H;
-    g.push_Hl = static_cast<int>(c->Hl);
-    g.push_d = static_cast<int>(c->d);
-    g.rope_cos = c->cos_t;
-    g.rope_sin = c->sin_t;
-    g.rope_parts = 2;
+  } else {  // RoPE in the epilogue, token layout kept locally (the all-to-all is a pure permutation)
+    set_rope_epilogue(c, g);
   }
   gemm(c, {c->n1, H, false}, {c->gathered[SEQPLAN_W_QKV], H, false}, g, EPI_BF16, st);
 }
@@ -822,7 +830,7 @@ void fwd_phase2(Ctx* c, cudaStream_t st) {
     KTimer kt(c, st, SEQPLAN_K_ALL_TO_ALL, 0, double(c->world - 1) / double(c->world) * double(c->T) * 3 * double(c->H) * 2);
     ISP_LAUNCH(1, a2a_tokens_to_heads(c->peers_at(c->off_qkv_tok), c->world, c->rank, static_cast<int>(c->T),
                                  static_cast<int>(c->H), 3, c->qkv_heads, c->cos_t, c->sin_t,
-                                 static_cast<int>(c->d), 2, st, kA2ACtas));
+                                 static_cast<int>(c->d), 0, st, kA2ACtas));
   }
   Span sp(c, st, 0, SEQPLAN_EV_FORWARD, 1);
   KTimer kt(c, st, SEQPLAN_K_ATTN_FWD, 2.0 * double(c->S) * double(c->S) * double(c->Hl), 0);
@@ -1113,40 +1121,27 @@ void bwd_phase2(Ctx* c, cudaStream_t st) {
                        2 * c->H + int64_t(c->rank) * c->Hl);
   bf16* dqkv = c->world == 1 ? c->dqkv_tok : c->hp<bf16>(c->off_dqkv_heads);
   const int64_t ld = 3 * c->Hl;
+  // the inverse RoPE of dq / dk is applied in the backward's epilogue, from fp32 (the all-to-all
+  // back to tokens is then a pure permutation)
+  t.rope_cos = c->cos_t;
+  t.rope_sin = c->sin_t;
   KTimer kt(c, st, SEQPLAN_K_ATTN_BWD, 4.0 * double(c->S) * double(c->S) * double(c->Hl), 0);
   ISP_LAUNCH(3, attention_bwd(t, c->dO_heads, dqkv, dqkv + c->Hl, dqkv + 2 * c->Hl, ld, c->delta, c->dq_acc, st,
                          c->num_sms));
-  if (c->world == 1)
-    ISP_EW(1, 8.0 * T * H, rope_inplace(c->dqkv_tok, 3 * H, T, 0, static_cast<int>(c->D), static_cast<int>(c->d), c->cos_t,
-                          c->sin_t, H, -1, st, c->num_sms));
-}
-
-// Fused all-to-all mode: the inverse RoPE of dq / dk runs on the owner after the exchange.
-void bwd_unrope_local(Ctx* c, cudaStream_t st) {
-  if (!c->fused_a2a) return;
-  ISP_LAUNCH(1, rope_inplace(c->dqkv_tok, 3 * c->H, static_cast<int>(c->T), static_cast<int>(c->rank * c->T),
-                             static_cast<int>(c->D), static_cast<int>(c->d), c->cos_t, c->sin_t, static_cast<int>(c->H),
-                             -1, st, c->num_sms));
 }
 
 void bwd_phase3(Ctx* c, const bf16* x, bf16* dx, cudaStream_t st) {
   const int T = static_cast<int>(c->T), H = static_cast<int>(c->H);
   const bool selective = !(c->flags & SEQPLAN_ISP_FLAG_FUSED_BWD);
-  bwd_unrope_local(c, st);
   if (c->world > 1 && !c->skip_comm() && c->ce_a2a) {
-    {
-      Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 3);
-      KTimer kt(c, st, SEQPLAN_K_ALL_TO_ALL, 0, double(c->world - 1) / double(c->world) * double(c->T) * 3 * double(c->H) * 2);
-      a2a_ce_to_tokens(c, c->off_dqkv_heads, 3, c->dqkv_tok, st);
-    }
-    ISP_EW(1, 8.0 * T * H, rope_inplace(c->dqkv_tok, 3 * c->H, T, static_cast<int>(c->rank * c->T),
-                                         static_cast<int>(c->D), static_cast<int>(c->d), c->cos_t, c->sin_t, H, -1,
-                                         st, c->num_sms));
+    Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 3);
+    KTimer kt(c, st, SEQPLAN_K_ALL_TO_ALL, 0, double(c->world - 1) / double(c->world) * double(c->T) * 3 * double(c->H) * 2);
+    a2a_ce_to_tokens(c, c->off_dqkv_heads, 3, c->dqkv_tok, st);
   } else if (c->world > 1 && !c->skip_comm() && !c->fused_a2a) {
     Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 3);
     KTimer kt(c, st, SEQPLAN_K_ALL_TO_ALL, 0, double(c->world - 1) / double(c->world) * double(c->T) * 3 * double(c->H) * 2);
     ISP_LAUNCH(1, a2a_heads_to_tokens(c->peers_at(c->off_dqkv_heads), c->world, c->rank, T, H, 3, c->dqkv_tok,
-                                 c->cos_t, c->sin_t, static_cast<int>(c->d), 2, st, kA2ACtas));
+                                 c->cos_t, c->sin_t, static_cast<int>(c->d), 0, st, kA2ACtas));
   }
   wait_gathered(c, SEQPLAN_W_QKV, st);
   {

@@ -60,6 +60,10 @@ struct AttnTensors {
   float* lse;
   int S, heads, d;
   AttnPush push;  // push.p[0] == nullptr: outputs stay local
+  // backward only: inverse rotary embedding of dq / dk (rotate-half, position = token row) applied
+  // before they are rounded to bf16; [S, d/2] fp32 tables, nullptr = none
+  const float* rope_cos = nullptr;
+  const float* rope_sin = nullptr;
 };
 cudaError_t attention_fwd(const AttnTensors& t, cudaStream_t st, int num_sms);
 // tcgen05/TMEM/TMA forward (attention_tc.cu); attention_fwd dispatches here.
