@@ -147,6 +147,15 @@ const char* seqplan_isp_last_error(const seqplan_isp_ctx* ctx);
  * opens all of them. handles = world blobs of seqplan_isp_ipc_handle_size() bytes
  * in rank order. */
 size_t seqplan_isp_ipc_handle_size(void);
+/* The same without IPC for world ranks created in ONE process on ONE device (ranks 0..world-1 in
+ * order): each rank runs the multi-process code path (its own streams, the production weight /
+ * gradient transports, stream-memop barriers) with the peers' heaps on the same GPU. The caller
+ * issues every rank's block_fwd before any rank's block_bwd (the calls only enqueue work; ranks
+ * wait for each other on the device); TIMELINE / PROFILE records are collected when queried.
+ * The process must run with CUDA_MODULE_LOADING=EAGER (a lazily loaded kernel's first launch
+ * waits for an idle device) and CUDA_DEVICE_MAX_CONNECTIONS >= the total stream count of all
+ * ranks (a memop wait at the head of a shared hardware queue would block other ranks' streams). */
+int seqplan_isp_link_local_peers(seqplan_isp_ctx** ctxs, int world);
 int seqplan_isp_ipc_handle(seqplan_isp_ctx* ctx, void* out);
 int seqplan_isp_open_peers(seqplan_isp_ctx* ctx, const void* handles);
 

@@ -128,10 +128,18 @@ _EXTRA_SIGS = [
                                             c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     ("seqplan_isp_debug_rmsnorm", c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_f,
                                           c_vp]),
+    ("seqplan_isp_link_local_peers", c_int, [P(c_vp), c_int]),
     ("seqplan_isp_debug_all_to_all", c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, P(c_vp), c_vp, c_vp,
                                              c_vp, c_int, c_vp]),
     ("seqplan_isp_debug_reduce_scatter", c_int, [c_int, c_int, c_i64, P(c_vp), c_int, c_f, c_int, c_vp, c_vp]),
 ]
+
+
+def link_local_peers(blocks):
+    """Links IspBlock ranks 0..p-1 created in this process on one device (no IPC): each runs the
+    multi-process code path with its peers' heaps on the same GPU (include/seqplan_isp.h)."""
+    arr = (c_vp * len(blocks))(*[b.h for b in blocks])
+    check(lib().seqplan_isp_link_local_peers(arr, len(blocks)), None, "link_local_peers")
 
 
 def check(status, ctx=None, what=""):

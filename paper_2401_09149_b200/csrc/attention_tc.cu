@@ -1226,7 +1226,7 @@ __global__ void __launch_bounds__(kDQ ? kBwdThreads : 320, 1)
 //     issue order S(j+1), dQ(j), dP(j+1): P(j+1) under dQ(j)/dP(j+1), dS(j) under S(j+1).
 // Every MMA is M = 128, N = 128. 7 MMAs per (key tile, query tile) instead of the fused 5, but
 // none waits on an L2 reduction; the dQ rows come out in bf16 (scaled), no fp32 accumulator.
-// Dispatch: one grid over (role, tile) entries sorted by decreasing work (host table), inside
+// Dispatch: one grid over (role, tile) entries sorted by decreasing work (split_entry), inside
 // L2-sized head groups (lpt_grid), so the heaviest CTAs of both roles start first.
 // Shared memory: KV role K, V 64 KB + Q, dO 2 stages 128 KB; Q role Q, dO 64 KB + K 3 stages
 // 96 KB + V 2 stages 64 KB.
@@ -1257,11 +1257,34 @@ __device__ __forceinline__ float2 exp2_pair(float2 x) {
   return make_float2(fast_exp2(x.x), fast_exp2(x.y));
 }
 
+// Entry e of the (role, tile) list sorted by decreasing work — KV key tile k: 4 (T - k) MMAs,
+// Q query tile q: 3 (q + 1); ties put the KV tile first — without a table (no host copy, so the
+// launch never synchronises the host): the work W at position e is the largest W with
+// #{items of work >= W} > e (binary search), then the place inside the tie group picks the role.
+// Returns k >= 0 for a KV tile, -(q + 1) for a Q tile.
+__device__ __forceinline__ int split_entry(int e, int T) {
+  auto count_ge = [&](int W) {  // items with work >= W
+    const int a = T - (W + 3) / 4 + 1, b = T - (W + 2) / 3 + 1;
+    return max(0, min(T, a)) + max(0, min(T, b));
+  };
+  int lo = 1, hi = 4 * T;  // count_ge(lo) = 2T > e; find the largest W with count_ge(W) > e
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) / 2;
+    if (count_ge(mid) > e) lo = mid;
+    else hi = mid - 1;
+  }
+  const int W = lo;
+  const int off = e - count_ge(W + 1);
+  const bool has_kv = W % 4 == 0 && W / 4 <= T;
+  if (off == 0 && has_kv) return T - W / 4;
+  return -(W / 3 - 1) - 1;
+}
+
 template <int kPolyKV, int kPolyQ>
 __global__ void __launch_bounds__(kBwdSThreads, 1)
     attn_bwd_split_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                           const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mDO,
-                          const int* __restrict__ table, const float* __restrict__ nlse2,
+                          const float* __restrict__ nlse2,
                           const float* __restrict__ delta, __nv_bfloat16* __restrict__ dq_out,
                           __nv_bfloat16* __restrict__ dk_out, __nv_bfloat16* __restrict__ dv_out, int64_t ld_d, int S,
                           float scale, const __grid_constant__ AttnPush push, const float* __restrict__ rope_cos,
@@ -1286,7 +1309,7 @@ __global__ void __launch_bounds__(kBwdSThreads, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int lin = static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x);
-  const int entry = table[lin / static_cast<int>(gridDim.y)];
+  const int entry = split_entry(lin / static_cast<int>(gridDim.y), S / 128);
   const int h = static_cast<int>(blockIdx.z * gridDim.y) + lin % static_cast<int>(gridDim.y);
   const bool role_q = entry < 0;
   const int tile = role_q ? -entry - 1 : entry;  // KV: key tile kt; Q: query tile qt
@@ -1694,27 +1717,8 @@ long long* g_attn_trace_fwd = nullptr;
 extern "C" void seqplan_isp_debug_set_trace(long long* dev_buf) { g_attn_trace = dev_buf; }
 extern "C" void seqplan_isp_debug_set_trace_fwd(long long* dev_buf) { g_attn_trace_fwd = dev_buf; }
 
-// Atomic-free backward (attn_bwd_split_kernel): (role, tile) entries sorted by decreasing work
-// (KV: 4 (T - kt) MMAs, Q: 3 (qt + 1)); delta = rowsum(dO * O) computed before; dq/dk/dv bf16.
-static const int* split_table(int T) {
-  static std::map<int, int*> cache;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lk(mu);
-  auto it = cache.find(T);
-  if (it != cache.end()) return it->second;
-  std::vector<std::pair<int, int>> e;  // (work, entry)
-  for (int k = 0; k < T; ++k) e.push_back({4 * (T - k), k});
-  for (int q = 0; q < T; ++q) e.push_back({3 * (q + 1), -q - 1});
-  std::stable_sort(e.begin(), e.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
-  std::vector<int> host(e.size());
-  for (size_t i = 0; i < e.size(); ++i) host[i] = e[i].second;
-  int* dev = nullptr;
-  if (cudaMalloc(&dev, host.size() * sizeof(int)) != cudaSuccess) return nullptr;
-  if (cudaMemcpy(dev, host.data(), host.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
-  cache[T] = dev;
-  return dev;
-}
-
+// Atomic-free backward (attn_bwd_split_kernel): (role, tile) entries in decreasing work
+// (split_entry); delta and nlse2 = -lse*log2e computed before; dq/dk/dv bf16.
 cudaError_t attention_bwd_nored_tc(const AttnTensors& t, const __nv_bfloat16* dout, int64_t ld_dout, __nv_bfloat16* dq,
                                    __nv_bfloat16* dk, __nv_bfloat16* dv, int64_t ld_d, const float* delta,
                                    const float* nlse2, cudaStream_t st) {
@@ -1734,8 +1738,6 @@ cudaError_t attention_bwd_nored_tc(const AttnTensors& t, const __nv_bfloat16* do
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes) != cudaSuccess)
     return cudaErrorInvalidValue;
   const int T = t.S / 128;
-  const int* table = split_table(T);
-  if (!table) return cudaErrorMemoryAllocation;
   CUtensorMap mq, mk, mv, mdo;
   const int64_t cols = static_cast<int64_t>(t.heads) * 128;
   if (!map2d(&mq, t.q, t.S, cols, t.ld_qkv, 128) || !map2d(&mk, t.k, t.S, cols, t.ld_qkv, 128) ||
@@ -1744,7 +1746,7 @@ cudaError_t attention_bwd_nored_tc(const AttnTensors& t, const __nv_bfloat16* do
   const float scale = 1.0f / sqrtf(128.0f);
   const int dbg = std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0;
   kern<<<lpt_grid(2 * T, t.heads, t.S, 128), kBwdSThreads, L::kBytes, st>>>(
-      mq, mk, mv, mdo, table, nlse2, delta, dq, dk, dv, ld_d, t.S, scale, t.push, t.rope_cos, t.rope_sin, dbg,
+      mq, mk, mv, mdo, nlse2, delta, dq, dk, dv, ld_d, t.S, scale, t.push, t.rope_cos, t.rope_sin, dbg,
       g_attn_trace);
   return cudaGetLastError();
 }

@@ -270,9 +270,10 @@ __global__ void peer_barrier_kernel(PeerPtrs flags, int world, int rank, uint32_
   const long long start = clock64();
   const long long limit = 40000000000LL;  // ~20 s at 2 GHz
   while (static_cast<int32_t>(ld_acquire_sys(mine) - epoch) < 0) {
-    if (clock64() - start > limit) {
+    if (clock64() - start > limit) {  // a dead or hung peer: fail loudly instead of reading stale data
       atomicExch(error_flag, 1u);
-      break;
+      __threadfence_system();
+      __trap();
     }
     __nanosleep(64);
   }

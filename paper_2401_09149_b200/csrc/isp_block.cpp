@@ -121,6 +121,10 @@ struct seqplan_isp_ctx {
   size_t heap_bytes = 0;
   void* peer_heap[kMaxRanks] = {};
   bool peer_opened[kMaxRanks] = {};
+  // ranks of one process on one device linked by seqplan_isp_link_local_peers: the multi-process
+  // code path (own streams, production transports, memop barriers) with the peers' heaps on the
+  // same GPU; TIMELINE / PROFILE collection is deferred to the query (no host sync in block_bwd)
+  bool co_resident = false;
   size_t off_flags = 0, off_wshard[SEQPLAN_W_COUNT] = {}, off_qkv_tok = 0, off_o_heads = 0,
          off_do_tok = 0, off_dqkv_heads = 0, off_part[SEQPLAN_W_COUNT] = {};
   // fused all-to-all (p > 1, d = 128): producers' epilogues push into these peer-writable buffers
@@ -1574,6 +1578,21 @@ int seqplan_isp_open_peers(seqplan_isp_ctx* c, const void* handles) {
   return SEQPLAN_ISP_OK;
 }
 
+int seqplan_isp_link_local_peers(seqplan_isp_ctx** cs, int world) {
+  if (!cs || world < 2 || world > kMaxRanks) return SEQPLAN_ISP_ERR_INVALID;
+  for (int r = 0; r < world; ++r) {
+    if (!cs[r] || cs[r]->world != world || cs[r]->rank != r || cs[r]->device != cs[0]->device || cs[r]->group_mode)
+      return SEQPLAN_ISP_ERR_INVALID;
+    for (int q = 0; q < world; ++q)
+      if (cs[r]->peer_opened[q]) return SEQPLAN_ISP_ERR_INVALID;
+  }
+  for (int r = 0; r < world; ++r) {
+    for (int q = 0; q < world; ++q) cs[r]->peer_heap[q] = cs[q]->heap;
+    cs[r]->co_resident = true;
+  }
+  return SEQPLAN_ISP_OK;
+}
+
 int seqplan_isp_group_create(int world, int device, const seqplan_isp_shape* shape,
                              const seqplan_mempool_policy* policy, uint32_t flags, seqplan_isp_ctx** out_ctxs) {
   if (!out_ctxs || world < 1 || world > kMaxRanks) return SEQPLAN_ISP_ERR_INVALID;
@@ -1833,7 +1852,7 @@ int seqplan_isp_block_bwd(seqplan_isp_ctx* c, const void* dy, void* dx, void* st
     run_bwd(c, static_cast<const bf16*>(c->last_x), static_cast<const bf16*>(dy), static_cast<bf16*>(dx),
             static_cast<cudaStream_t>(stream));
     c->fwd_done = false;
-    if (c->flags & (SEQPLAN_ISP_FLAG_TIMELINE | SEQPLAN_ISP_FLAG_PROFILE)) {
+    if ((c->flags & (SEQPLAN_ISP_FLAG_TIMELINE | SEQPLAN_ISP_FLAG_PROFILE)) && !c->co_resident) {
       ISP_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
       check_device_error(c);
       collect_timeline(c);
@@ -1919,6 +1938,7 @@ int seqplan_isp_group_bwd(seqplan_isp_ctx** cs, int world, const void* const* dy
 
 int seqplan_isp_kernel_profile(seqplan_isp_ctx* c, seqplan_kernel_record* out, int64_t* n, int clear) {
   if (!c || !n) return SEQPLAN_ISP_ERR_INVALID;
+  collect_kprof(c);  // deferred records (co-resident ranks); waits on their events
   const int64_t have = static_cast<int64_t>(c->kprof.size());
   if (out) {
     const int64_t k = std::min(*n, have);
@@ -2144,6 +2164,15 @@ int seqplan_isp_pool_replay(seqplan_isp_ctx* c, seqplan_step_stats* out, int64_t
 
 int seqplan_isp_timeline(seqplan_isp_ctx* c, seqplan_timeline_event* events, int64_t* n) {
   if (!c || !n) return SEQPLAN_ISP_ERR_INVALID;
+  try {
+    if (!c->tl_pending.empty()) {  // deferred (co-resident ranks): waits on the step's events
+      ISP_CUDA(cudaSetDevice(c->device));
+      collect_timeline(c);
+      check_device_error(c);
+    }
+  } catch (const IspError& e) {
+    return fail(c, e);
+  }
   const int64_t have = static_cast<int64_t>(c->timeline.size());
   if (events) {
     const int64_t k = std::min(*n, have);

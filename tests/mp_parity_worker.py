@@ -19,8 +19,75 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
+def steps_mode(H, D, S, adamw):
+    """Production-path check (no flags, no host synchronisation inside): 3 back-to-back fwd/bwd
+    steps on one stream, optionally with an AdamW update of the shards after each, as a training
+    loop issues them; cross-step reuse of the peer exchange buffers then rests on the in-step
+    barriers alone. Step 3's y / dx / gradient shards and the final weight shards vs the oracle
+    running the same sequence."""
+    world, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    sh = ob.Shape(H=H, D=D, S=S)
+    w = ob.make_weights(sh)
+    x = torch.from_numpy(ob.make_activation(sh, ob.TID_X)).bfloat16()
+    dy = torch.from_numpy(ob.make_activation(sh, ob.TID_DY)).bfloat16()
+    T = S // world
+    blk = capi.IspBlock(H, D, S, world=world, rank=rank, device=local, flags=0)
+    bootstrap_peers(blk, world)
+    for t in range(7):
+        flat = w[t].reshape(-1)
+        per = flat.size // world
+        blk.set_weight_shard(t, flat[rank * per:(rank + 1) * per])
+    dist.barrier()
+    xd = x[rank * T:(rank + 1) * T].to(dev)
+    dyd = dy[rank * T:(rank + 1) * T].to(dev)
+    y, dx = torch.empty_like(xd), torch.empty_like(xd)
+    lr = 1e-3
+    w0 = [blk.weight_shard(t) for t in range(7)]
+    for k in range(3):  # AdamW after steps 1 and 2: step 3 runs on twice-updated weights
+        blk.fwd(xd, y)
+        blk.bwd(dyd, dx)
+        if adamw and k < 2:
+            blk.adamw_step(lr, k + 1)
+    torch.cuda.synchronize()
+    res = {"rank": rank}
+    # step 3 vs the oracle at the weights the device used in step 3 (its fp32 masters); the
+    # update rule itself is checked element-wise in test_adamw_step_matches_oracle
+    shards = [blk.weight_shard(t) for t in range(7)]
+    moved = [float(np.abs(a - b).max()) for a, b in zip(shards, w0)]
+    allw = [None] * world
+    dist.all_gather_object(allw, shards)
+    if rank == 0:
+        ws = [np.concatenate([allw[q][t] for q in range(world)]).reshape(s) for t, s in
+              enumerate(sh.weight_shapes())]
+        y_ref, dx_ref, g_ref = ob.block(sh, ws, x.float().numpy(), dy.float().numpy(), p=1)
+        ref = (y_ref, dx_ref, [g.reshape(-1) for g in g_ref])
+    else:
+        ref = None
+    obj = [ref]
+    dist.broadcast_object_list(obj, src=0)
+    y_ref, dx_ref, g_ref = obj[0]
+    res["y"] = rel(y.float().cpu(), y_ref[rank * T:(rank + 1) * T])
+    res["dx"] = rel(dx.float().cpu(), dx_ref[rank * T:(rank + 1) * T])
+    for t in range(7):
+        per = g_ref[t].size // world
+        res[capi.W_NAMES[t]] = rel(blk.grad_shard(t), g_ref[t][rank * per:(rank + 1) * per])
+        if adamw:  # the updates happened (0 = moved)
+            res["w_" + capi.W_NAMES[t] + "_static"] = float(moved[t] == 0.0)
+    print(json.dumps(res), flush=True)
+    blk.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     H, D, S = (int(v) for v in sys.argv[1:4])
+    if len(sys.argv) > 4 and sys.argv[4] in ("steps", "steps_adamw"):
+        steps_mode(H, D, S, sys.argv[4] == "steps_adamw")
+        return
     fused = len(sys.argv) > 4 and sys.argv[4] == "fused"
     world, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
     local = int(os.environ.get("LOCAL_RANK", rank))

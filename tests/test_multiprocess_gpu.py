@@ -133,3 +133,25 @@ def test_multiprocess_parity_ce_a2a(n, H):
         for k, v in row.items():
             if k not in ("rank", "timeline_events"):
                 assert v <= 1e-2, (row["rank"], k, v)
+
+
+@pytest.mark.parametrize("mode", ["steps", "steps_adamw"])
+@pytest.mark.parametrize("n,push", [(2, "0"), (4, "1")])
+def test_multiprocess_back_to_back_steps(n, push, mode):
+    """The path bench.py times: no flags, 3 fwd/bwd steps back to back without host sync, with
+    and without an AdamW update after steps 1 and 2, copy-engine pull at p = 2 and push at p = 4;
+    step 3's outputs and gradients (rel-L2 <= 1e-2) vs the oracle at the weights step 3 used."""
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={29620 + n + 10 * (mode == 'steps_adamw')}",
+           os.path.join(ROOT, "tests", "mp_parity_worker.py"), "1024", "8", "1024", mode]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT,
+                       env={**os.environ, "SEQPLAN_ISP_PUSH": push})
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    rows = _json_rows(r.stdout)
+    assert len(rows) == n
+    for row in rows:
+        for k, v in row.items():
+            if k != "rank":
+                assert v <= 1e-2, (row["rank"], k, v)
