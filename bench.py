@@ -235,7 +235,8 @@ def parse():
 
 KERNEL_NAMES = {
     "gemm": "tcgen05 GEMM (all linear-layer GEMMs of the step)",
-    "attn_bwd": "tcgen05 causal attention backward (attn_bwd_tc_kernel; FLOPs 4*S^2*Hl, recompute not counted)",
+    "attn_bwd": "tcgen05 causal attention backward (attn_bwd_split_kernel: key-tile dK/dV CTAs + query-tile dQ "
+                "CTAs, no atomics; algorithmic FLOPs 4*S^2*Hl, the recomputed S/dP products not counted)",
     "attn_fwd": "tcgen05 causal attention forward (attn_fwd_fa4_kernel; FLOPs 2*S^2*Hl)",
 }
 

@@ -266,6 +266,10 @@ int seqplan_isp_debug_all_to_all(int world, int rank, int T, int H, int parts, i
  * out[i] (+)= scale * sum_{q=0..world-1, in order} part[q][rank*shard_elems + i]. */
 int seqplan_isp_debug_reduce_scatter(int world, int rank, int64_t shard_elems, const void* const* part,
                                      int part_is_f32, float scale, int accumulate, float* out, void* stream);
+/* One rank's push all-gather (the p >= 4 weight transport, cost.hpp:184-188): `bytes` at src go to
+ * offset rank*bytes of every dst[q]; kind 0 = vector stores, 1 = cp.async.bulk driven. */
+int seqplan_isp_debug_push_allgather(int world, int rank, void* const* dst, const void* src, int64_t bytes, int kind,
+                                     int num_ctas, void* stream);
 
 #ifdef __cplusplus
 }

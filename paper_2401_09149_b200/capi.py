@@ -132,6 +132,7 @@ _EXTRA_SIGS = [
     ("seqplan_isp_debug_all_to_all", c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, P(c_vp), c_vp, c_vp,
                                              c_vp, c_int, c_vp]),
     ("seqplan_isp_debug_reduce_scatter", c_int, [c_int, c_int, c_i64, P(c_vp), c_int, c_f, c_int, c_vp, c_vp]),
+    ("seqplan_isp_debug_push_allgather", c_int, [c_int, c_int, P(c_vp), c_vp, c_i64, c_int, c_int, c_vp]),
 ]
 
 

@@ -116,3 +116,23 @@ extern "C" int seqplan_isp_debug_reduce_scatter(int world, int rank, int64_t sha
   if (e == cudaErrorInvalidValue) return SEQPLAN_ISP_ERR_INVALID;
   return e == cudaSuccess ? SEQPLAN_ISP_OK : SEQPLAN_ISP_ERR_RUNTIME;
 }
+
+// One rank's push all-gather of a contiguous shard (the weight all-gather transport of p >= 4):
+// this rank's `bytes` at src are stored into slot `rank` (offset rank*bytes) of every rank's
+// buffer dst[q] (own slot: a local copy). kind: 0 = 16-B vector stores (push_copy_kernel),
+// 1 = one thread per CTA driving cp.async.bulk through 2 x 16 KB slots (push_bulk_kernel).
+extern "C" int seqplan_isp_debug_push_allgather(int world, int rank, void* const* dst, const void* src, int64_t bytes,
+                                                int kind, int num_ctas, void* stream) {
+  if (world < 1 || world > isp::kMaxRanks || rank < 0 || rank >= world || !dst || !src || bytes % 16 ||
+      (kind != 0 && kind != 1) || num_ctas < 1)
+    return SEQPLAN_ISP_ERR_INVALID;
+  isp::PeerPtrs p{};
+  for (int q = 0; q < world; ++q) p.p[q] = dst[q];
+  isp::PushJobs J{};
+  J.j[0] = isp::PushJob{static_cast<const char*>(src), 0, rank * bytes, bytes, 0, 0, 1};
+  J.n = 1;
+  cudaError_t e = isp::push_copy(J, p, world, rank, static_cast<cudaStream_t>(stream), num_ctas,
+                                 kind == 1 ? isp::kPushBulk : isp::kPushLsu);
+  if (e == cudaErrorInvalidValue) return SEQPLAN_ISP_ERR_INVALID;
+  return e == cudaSuccess ? SEQPLAN_ISP_OK : SEQPLAN_ISP_ERR_RUNTIME;
+}

@@ -162,6 +162,9 @@ struct seqplan_isp_ctx {
   cudaStream_t red = nullptr;    // reduction stream of the early reduce-scatter
   cudaEvent_t ev_rs_sent[SEQPLAN_W_COUNT] = {};
   cudaEvent_t ev_red_done = nullptr;
+  // QKV GEMM reads the peers' working shards over NVLink with its own TMA loads (the weight
+  // all-gather fused into its first consumer, no gather buffer); SEQPLAN_ISP_AG_GEMM=1
+  bool ag_gemm = false;
   bool qkv_slice = true;         // QKV GEMM sliced by weight-shard source (SEQPLAN_ISP_QKV_SLICE=0 turns off; +1.1 % at 4K p = 2, neutral at p = 4)
   bool recomputing = false;      // inside the backward's forward recomputation
   bool acts_live = false;        // saved activations currently allocated
@@ -705,6 +708,15 @@ void prefetch_bwd_set(Ctx* c) {
   c->bwd_prefetched = true;
 }
 
+// The QKV GEMM sliced by weight-shard source (fwd_phase1): own rows from the working shard first.
+bool qkv_sliced(const Ctx* c) {
+  return c->world > 1 && !c->group_mode && !c->fused_a2a && !c->ce_a2a && !c->skip_comm() && c->qkv_slice &&
+         (3 * c->H / c->world) % 128 == 0;
+}
+// ... and its peer slices' B operands TMA-loaded from the peers' working shards over NVLink: the
+// forward all-gather of Wqkv is fused into the GEMM (nothing is gathered for it).
+bool qkv_ag_in_gemm(const Ctx* c) { return c->ag_gemm && qkv_sliced(c); }
+
 void fwd_issue_gathers(Ctx* c, cudaStream_t st) {
   if (c->world == 1) {
     for (int t : {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN})
@@ -720,18 +732,22 @@ void fwd_issue_gathers(Ctx* c, cudaStream_t st) {
     // forward set, then the backward re-gather into the second set (its buffers are free since
     // the step-start barrier), so the backward never waits for weights
     const int fo[] = {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN};
+    const int fo_ag[] = {SEQPLAN_W_NORM1, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN};
     const int bo[] = {SEQPLAN_W_DOWN, SEQPLAN_W_GATE, SEQPLAN_W_NORM2, SEQPLAN_W_O, SEQPLAN_W_QKV, SEQPLAN_W_NORM1};
     c->gather_set = 0;
     push_gather_set(c, 1, bo, 6, false);
-    push_gather_set(c, 0, fo, 6, !c->push_skip());
+    if (qkv_ag_in_gemm(c)) push_gather_set(c, 0, fo_ag, 5, !c->push_skip());
+    else push_gather_set(c, 0, fo, 6, !c->push_skip());
     if (!c->push_skip() && !c->defer_bwd_set) push_gather_set(c, 1, bo, 6, true);
     for (int t : fo) c->gathered[t] = c->hp<bf16>(c->off_gath[0][t]);
     return;
   }
   if (!c->group_mode) {
     const int order[] = {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN};
+    const int order_ag[] = {SEQPLAN_W_NORM1, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN};
     c->evset = 0;
-    gather_pipelined(c, order, 6, cs);
+    if (qkv_ag_in_gemm(c)) gather_pipelined(c, order_ag, 5, cs);
+    else gather_pipelined(c, order, 6, cs);
     if (!c->defer_bwd_set) prefetch_bwd_set(c);
     return;
   }
@@ -769,8 +785,7 @@ void fwd_phase1(Ctx* c, const bf16* x, cudaStream_t st) {
   wait_gathered(c, SEQPLAN_W_NORM1, st);
   ISP_EW(1, 4.0 * T * H, rmsnorm_fwd(x, c->gathered[SEQPLAN_W_NORM1], c->n1, c->rstd1, T, H, c->eps, st, c->num_sms));
   const int64_t n_own = 3 * c->H / c->world;  // rows of Wqkv in each rank's shard
-  if (c->world > 1 && !c->group_mode && !c->fused_a2a && !c->ce_a2a && !c->skip_comm() && c->qkv_slice &&
-      n_own % 128 == 0) {
+  if (qkv_sliced(c)) {
     // The step's first gather consumer, sliced by weight-shard source: this rank's own rows of
     // Wqkv are multiplied straight from its working shard while the peers' rows are in flight,
     // the rest once they have landed (unsliced, the GEMM waits for every shard).
@@ -786,6 +801,13 @@ void fwd_phase1(Ctx* c, const bf16* x, cudaStream_t st) {
       gemm(c, {c->n1, H, false}, {w, H, false}, g, EPI_BF16, st);
     };
     slice(c->wshard(SEQPLAN_W_QKV), r0, n_own);
+    if (qkv_ag_in_gemm(c)) {  // peers' rows straight from their working shards (TMA over NVLink)
+      for (int k = 1; k < c->world; ++k) {
+        const int q = (c->rank + k) % c->world;
+        slice(c->peer<bf16>(q, c->off_wshard[SEQPLAN_W_QKV]), q * n_own, n_own);
+      }
+      return;
+    }
     wait_gathered(c, SEQPLAN_W_QKV, st);
     const bf16* wq = c->gathered[SEQPLAN_W_QKV];
     slice(wq, 0, r0);
@@ -1319,6 +1341,7 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   if (const char* e = std::getenv("SEQPLAN_ISP_BWD_PREFETCH")) c->no_bwd_prefetch = std::atoi(e) == 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_RS_CE")) c->rs_ce = std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_QKV_SLICE")) c->qkv_slice = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SEQPLAN_ISP_AG_GEMM")) c->ag_gemm = std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_EARLY_REDUCE")) c->early_reduce = std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_A2A_CE")) c->ce_a2a = c->world > 1 && !c->fused_a2a && std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_RS_CTAS")) c->rs_ctas = std::atoi(e) ? std::atoi(e) : 128;

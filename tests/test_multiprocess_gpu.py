@@ -155,3 +155,23 @@ def test_multiprocess_back_to_back_steps(n, push, mode):
         for k, v in row.items():
             if k != "rank":
                 assert v <= 1e-2, (row["rank"], k, v)
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_multiprocess_parity_ag_into_gemm(n):
+    """The forward all-gather of Wqkv fused into the QKV GEMM (SEQPLAN_ISP_AG_GEMM=1): the peer
+    slices' B operands are TMA-loaded straight from the peers' working shards over NVLink."""
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={29660 + n}",
+           os.path.join(ROOT, "tests", "mp_parity_worker.py"), "1024", "8", "1024", "steps"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT,
+                       env={**os.environ, "SEQPLAN_ISP_AG_GEMM": "1"})
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    rows = _json_rows(r.stdout)
+    assert len(rows) == n
+    for row in rows:
+        for k, v in row.items():
+            if k != "rank":
+                assert v <= 1e-2, (row["rank"], k, v)
