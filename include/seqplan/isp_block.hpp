@@ -113,7 +113,7 @@ private:
     void raise(int status) const {
         if (status == SEQPLAN_ISP_OK) return;
         const std::string msg = ctx_ ? seqplan_isp_last_error(ctx_) : "seqplan_isp_ctx_create failed";
-        if (status == SEQPLAN_ISP_ERR_INVALID) throw std::invalid_argument(msg);
+        if (status == SEQPLAN_ISP_ERR_INVALID || status == SEQPLAN_ISP_ERR_UNSUPPORTED) throw std::invalid_argument(msg);
         throw std::runtime_error(msg + " (status " + std::to_string(status) + ")");
     }
 
@@ -159,7 +159,7 @@ private:
         if (status == SEQPLAN_ISP_OK) return;
         seqplan_isp_ctx* c = seqplan_isp_stack_layer(stack_, 0);
         const std::string msg = c ? seqplan_isp_last_error(c) : "seqplan_isp_stack";
-        if (status == SEQPLAN_ISP_ERR_INVALID) throw std::invalid_argument(msg);
+        if (status == SEQPLAN_ISP_ERR_INVALID || status == SEQPLAN_ISP_ERR_UNSUPPORTED) throw std::invalid_argument(msg);
         throw std::runtime_error(msg + " (status " + std::to_string(status) + ")");
     }
 
