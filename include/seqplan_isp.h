@@ -132,10 +132,12 @@ enum {
 /* ---- lifecycle ---------------------------------------------------------- */
 
 /* Creates the context of rank `rank` of `world` on CUDA device `device`.
- * The strategy must be the ISP plan [b=1,n=1,pp=1,dp=1,tp=1,sp=ps=world,gs=oss=1]
+ * The strategy must be the ISP plan [b=1,n>=1,pp=1,dp=1,tp=1,sp=ps=world,gs=oss=1]
  * and must pass seqplan::validate (strategy.hpp:72-99): an illegal plan, or a non-ISP one, is
- * SEQPLAN_ISP_ERR_INVALID; a legal ISP plan with micro_batch != 1, micro_batch_num != 1, gs != 1
- * or oss != 1 is SEQPLAN_ISP_ERR_UNSUPPORTED. policy may be NULL. */
+ * SEQPLAN_ISP_ERR_INVALID; a legal ISP plan with micro_batch != 1, gs != 1 or oss != 1 is
+ * SEQPLAN_ISP_ERR_UNSUPPORTED. micro_batch_num = n > 1: the caller runs n block_fwd/block_bwd per
+ * step and the weight gradients of calls 2..n accumulate into the fp32 shards (cost.hpp:202-204).
+ * policy may be NULL. */
 int seqplan_isp_ctx_create(int world, int rank, int device, const seqplan_isp_shape* shape,
                            const seqplan_strategy* strategy, const seqplan_mempool_policy* policy,
                            uint32_t flags, seqplan_isp_ctx** out);

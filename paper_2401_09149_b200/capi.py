@@ -190,11 +190,13 @@ class IspBlock:
     Thin ctypes wrapper; every call goes through the C ABI of include/seqplan_isp.h.
     """
 
-    def __init__(self, H, D, S, world=1, rank=0, device=0, policy=None, flags=0, I=0, recompute=False):
+    def __init__(self, H, D, S, world=1, rank=0, device=0, policy=None, flags=0, I=0, recompute=False,
+                 micro_batches=1):
         l = lib()
         self.world, self.rank = world, rank
         self.shape = make_shape(H, D, S, I)
-        strat = StrategyC(1, 1, int(recompute), 1, 1, 1, world, world, 1, 1)
+        # micro_batches = n (Strategy::micro_batch_num): n fwd/bwd calls per step, gradients accumulate
+        strat = StrategyC(1, int(micro_batches), int(recompute), 1, 1, 1, world, world, 1, 1)
         pol = policy if policy is not None else make_policy()
         h = c_vp()
         st = l.seqplan_isp_ctx_create(world, rank, device, ctypes.byref(self.shape), ctypes.byref(strat),

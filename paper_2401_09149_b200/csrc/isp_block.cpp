@@ -125,6 +125,10 @@ struct seqplan_isp_ctx {
   // code path (own streams, production transports, memop barriers) with the peers' heaps on the
   // same GPU; TIMELINE / PROFILE collection is deferred to the query (no host sync in block_bwd)
   bool co_resident = false;
+  // micro-batches per step (Strategy::micro_batch_num, cost.hpp:202-204): block_bwd calls
+  // 2..n of a step add their weight gradients into the fp32 shards instead of overwriting
+  int micro_batches = 1, mb_index = 0;
+  bool accum = false;
   size_t off_flags = 0, off_wshard[SEQPLAN_W_COUNT] = {}, off_qkv_tok = 0, off_o_heads = 0,
          off_do_tok = 0, off_dqkv_heads = 0, off_part[SEQPLAN_W_COUNT] = {};
   // fused all-to-all (p > 1, d = 128): producers' epilogues push into these peer-writable buffers
@@ -453,12 +457,12 @@ void reduce_scatter_grad(Ctx* c, int t, cudaStream_t st) {
   KTimer kt(c, st, SEQPLAN_K_REDUCE_SCATTER, 0, frac * part_bytes);
   if (t == SEQPLAN_W_GATE) {
     ISP_LAUNCH(1, reduce_scatter_pull_interleave(c->peers_at(c->off_part[SEQPLAN_W_GATE]), c->world, c->rank,
-                                            c->I, c->H, 1.0f, 0, c->grad[SEQPLAN_W_GATE],
+                                            c->I, c->H, 1.0f, c->accum ? 1 : 0, c->grad[SEQPLAN_W_GATE],
                                             c->grad[SEQPLAN_W_UP], st, kCommCtas));
   } else {
     const bool f32 = (t == SEQPLAN_W_NORM1 || t == SEQPLAN_W_NORM2);
     ISP_LAUNCH(1, reduce_scatter_pull(c->peers_at(c->off_part[t]), c->world, c->rank, c->shard(t), f32, 1.0f,
-                                 0, c->grad[t], st, kCommCtas));
+                                 c->accum ? 1 : 0, c->grad[t], st, kCommCtas));
   }
 }
 
@@ -680,14 +684,14 @@ void reduce_pushed(Ctx* c, int t, cudaStream_t st) {
     const int64_t half = (c->I / c->world) * c->H, slot = 2 * half;
     bf16* stg = c->hp<bf16>(c->off_stage[t]);
     for (int q = 0; q < c->world; ++q) src.p[q] = stg + q * slot;
-    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, half, false, 1.0f, 0, c->grad[SEQPLAN_W_GATE], st, c->num_sms * 4));
+    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, half, false, 1.0f, c->accum ? 1 : 0, c->grad[SEQPLAN_W_GATE], st, c->num_sms * 4));
     for (int q = 0; q < c->world; ++q) src.p[q] = stg + q * slot + half;
-    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, half, false, 1.0f, 0, c->grad[SEQPLAN_W_UP], st, c->num_sms * 4));
+    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, half, false, 1.0f, c->accum ? 1 : 0, c->grad[SEQPLAN_W_UP], st, c->num_sms * 4));
   } else {
     const int64_t sh = c->shard(t), esz = norm ? 4 : 2;
     char* stg = c->hp<char>(c->off_stage[t]);
     for (int q = 0; q < c->world; ++q) src.p[q] = stg + q * sh * esz;
-    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, sh, norm, 1.0f, 0, c->grad[t], st, c->num_sms * 4));
+    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, sh, norm, 1.0f, c->accum ? 1 : 0, c->grad[t], st, c->num_sms * 4));
   }
 }
 
@@ -961,6 +965,7 @@ void wgrad(Ctx* c, int t, const GemmOperand& A, const GemmOperand& B, int M, int
   if (c->world == 1) {
     g.out = c->grad[t];
     g.ldo = N;
+    g.accumulate = c->accum ? 1 : 0;
     if (t == SEQPLAN_W_GATE) {
       g.interleave64 = 1;
       g.out_b = c->grad[SEQPLAN_W_UP];
@@ -1016,14 +1021,14 @@ void reduce_staged(Ctx* c, int t, cudaStream_t st) {
     const int64_t slot = 2 * (c->I / c->world) * c->H, half = slot / 2;
     bf16* stg = static_cast<bf16*>(c->stage[t]);
     for (int q = 0; q < c->world; ++q) src.p[q] = stg + q * slot;
-    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, half, false, 1.0f, 0, c->grad[SEQPLAN_W_GATE], st, c->num_sms * 4));
+    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, half, false, 1.0f, c->accum ? 1 : 0, c->grad[SEQPLAN_W_GATE], st, c->num_sms * 4));
     for (int q = 0; q < c->world; ++q) src.p[q] = stg + q * slot + half;
-    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, half, false, 1.0f, 0, c->grad[SEQPLAN_W_UP], st, c->num_sms * 4));
+    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, half, false, 1.0f, c->accum ? 1 : 0, c->grad[SEQPLAN_W_UP], st, c->num_sms * 4));
   } else {
     const int64_t sh = c->shard(t), esz = norm ? 4 : 2;
     char* stg = static_cast<char*>(c->stage[t]);
     for (int q = 0; q < c->world; ++q) src.p[q] = stg + q * sh * esz;
-    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, sh, norm, 1.0f, 0, c->grad[t], st, c->num_sms * 4));
+    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, sh, norm, 1.0f, c->accum ? 1 : 0, c->grad[t], st, c->num_sms * 4));
   }
   c->pool->free(c->stage[t], st);
   c->stage[t] = nullptr;
@@ -1105,7 +1110,7 @@ void bwd_phase1(Ctx* c, const bf16* dy, cudaStream_t st) {
   // ---- norm2 backward: dh = dy + d(norm2) ----
   wait_gathered(c, SEQPLAN_W_NORM2, st);
   float* dg2 = c->world == 1 ? c->grad[SEQPLAN_W_NORM2] : c->hp<float>(c->off_part[SEQPLAN_W_NORM2]);
-  ISP_CUDA(cudaMemsetAsync(dg2, 0, sizeof(float) * H, st));
+  if (c->world > 1 || !c->accum) ISP_CUDA(cudaMemsetAsync(dg2, 0, sizeof(float) * H, st));
   ISP_EW(2, 8.0 * T * H, rmsnorm_bwd(c->h, c->gathered[SEQPLAN_W_NORM2], c->rstd2, c->dn, dy, c->dh, dg2, T, H, st, c->num_sms, c->dg_scratch));
   release_weight(c, SEQPLAN_W_NORM2, st);
   if (selective) schedule_rs(c, SEQPLAN_W_NORM2, st);
@@ -1185,7 +1190,7 @@ void bwd_phase3(Ctx* c, const bf16* x, bf16* dx, cudaStream_t st) {
   release_weight(c, SEQPLAN_W_QKV, st);
   wait_gathered(c, SEQPLAN_W_NORM1, st);
   float* dg1 = c->world == 1 ? c->grad[SEQPLAN_W_NORM1] : c->hp<float>(c->off_part[SEQPLAN_W_NORM1]);
-  ISP_CUDA(cudaMemsetAsync(dg1, 0, sizeof(float) * H, st));
+  if (c->world > 1 || !c->accum) ISP_CUDA(cudaMemsetAsync(dg1, 0, sizeof(float) * H, st));
   ISP_EW(2, 8.0 * T * H, rmsnorm_bwd(x, c->gathered[SEQPLAN_W_NORM1], c->rstd1, c->dn, c->dh, dx, dg1, T, H, st, c->num_sms, c->dg_scratch));
   release_weight(c, SEQPLAN_W_NORM1, st);
   if (selective) schedule_rs(c, SEQPLAN_W_NORM1, st);
@@ -1508,10 +1513,10 @@ static int create_ctx(int world, int rank, int device, const seqplan_isp_shape* 
     if (!seqplan::validate(s, m, cl).ok() || s.sp != world || s.ps != world || s.tp != 1 || s.pp != 1 ||
         s.dp != 1 || (s.recompute != 0 && s.recompute != 1))
       return SEQPLAN_ISP_ERR_INVALID;
-    // Legal plans this executor does not run: it processes one micro-batch (b = 1, n = 1) per
-    // fwd/bwd call, with no gradient-sync (gs) or optimizer-state-sharding (oss) groups.
-    if (s.micro_batch != 1 || s.micro_batch_num != 1 || s.gs != 1 || s.oss != 1)
-      return SEQPLAN_ISP_ERR_UNSUPPORTED;
+    // Legal plans this executor does not run: b > 1 sequences per micro-batch, gradient-sync (gs)
+    // or optimizer-state-sharding (oss) groups. n > 1 micro-batches run as n fwd/bwd calls per
+    // step whose weight gradients accumulate into the fp32 shards (reset by the first).
+    if (s.micro_batch != 1 || s.gs != 1 || s.oss != 1) return SEQPLAN_ISP_ERR_UNSUPPORTED;
   }
   Ctx* c = new Ctx();
   c->world = world;
@@ -1519,6 +1524,7 @@ static int create_ctx(int world, int rank, int device, const seqplan_isp_shape* 
   c->device = device;
   c->flags = flags;
   c->recompute = (strategy && strategy->recompute == 1) || (flags & SEQPLAN_ISP_FLAG_RECOMPUTE);
+  c->micro_batches = strategy ? static_cast<int>(strategy->micro_batch_num) : 1;
   if (shared_pool) {
     c->pool = shared_pool;
     c->owns_pool = false;
@@ -1848,8 +1854,10 @@ static void bwd_epilogue(Ctx* c, cudaStream_t st) {
 }
 
 static void run_bwd(Ctx* c, const bf16* x, const bf16* dy, bf16* dx, cudaStream_t st) {
+  c->accum = c->mb_index > 0;  // micro-batch 2..n of the step: accumulate the weight gradients
   bwd_body(c, x, dy, dx, st);
   bwd_epilogue(c, st);
+  c->mb_index = (c->mb_index + 1) % std::max(1, c->micro_batches);
 }
 
 int seqplan_isp_block_fwd(seqplan_isp_ctx* c, const void* x, void* y, void* stream) {
@@ -2092,6 +2100,7 @@ int seqplan_isp_stack_bwd(seqplan_isp_stack* s, const void* dy, void* dx, void* 
       const bf16* g_in = l == L - 1 ? static_cast<const bf16*>(dy) : s->grad[size_t(l + 1)];
       if (l > 0) s->grad[size_t(l)] = static_cast<bf16*>(pool_alloc(cur, bytes, seqplan::AllocTag::Other, st));
       bf16* g_out = l == 0 ? static_cast<bf16*>(dx) : s->grad[size_t(l)];
+      cur->accum = cur->mb_index > 0;  // micro-batch 2..n of the step: accumulate
       bwd_body(cur, static_cast<const bf16*>(cur->last_x), g_in, g_out, st);
       cur->fwd_done = false;
       if (l > 0) {  // the checkpoint of layer l is consumed
@@ -2106,6 +2115,7 @@ int seqplan_isp_stack_bwd(seqplan_isp_stack* s, const void* dy, void* dx, void* 
     for (int l = L; l-- > 0;) {
       cur = s->layers[size_t(l)];
       bwd_epilogue(cur, st);
+      cur->mb_index = (cur->mb_index + 1) % std::max(1, cur->micro_batches);
       if (cur->flags & (SEQPLAN_ISP_FLAG_TIMELINE | SEQPLAN_ISP_FLAG_PROFILE)) {
         ISP_CUDA(cudaStreamSynchronize(st));
         check_device_error(cur);

@@ -353,3 +353,35 @@ def test_block_fused_swiglu_bwd_epilogue(cuda, p, monkeypatch):
     assert rel(torch.cat(dxs).float().cpu(), dx_ref) <= TOL
     check_grads(blocks, g_ref, p)
     grp.close()
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_micro_batches_accumulate_gradients(cuda, n):
+    """Strategy::micro_batch_num = n (GS accumulation, cost.hpp:202-204): the n fwd/bwd calls of a
+    step add their weight gradients into the fp32 shards (the first overwrites), so a step's
+    gradients equal the oracle's summed over its micro-batches; the next step starts afresh."""
+    H, D, S = 1024, 8, 512
+    sh = ob.Shape(H=H, D=D, S=S)
+    w = ob.make_weights(sh)
+    mbs = []
+    for k in range(n):  # independent micro-batches (keyed with seeds derived from the step seed)
+        x = torch.from_numpy(ob.make_activation(sh, ob.TID_X, seed=ob.SEED + 17 * k)).bfloat16()
+        dy = torch.from_numpy(ob.make_activation(sh, ob.TID_DY, seed=ob.SEED + 17 * k)).bfloat16()
+        mbs.append((x, dy))
+    g_sum = None
+    for x, dy in mbs:
+        _, _, g = ob.block(sh, w, x.float().numpy(), dy.float().numpy(), p=1)
+        g_sum = [t.reshape(-1).copy() for t in g] if g_sum is None else [a + t.reshape(-1) for a, t in zip(g_sum, g)]
+    blk = capi.IspBlock(H, D, S, world=1, micro_batches=n)
+    load_weights(blk, w, 1, 0)
+    for step in range(2):  # the second step must not keep the first step's gradients
+        for x, dy in mbs:
+            xd, dyd = x.to(cuda), dy.to(cuda)
+            y, dx = torch.empty_like(xd), torch.empty_like(xd)
+            blk.fwd(xd, y)
+            blk.bwd(dyd, dx)
+        torch.cuda.synchronize()
+        for t in range(7):
+            e = rel(blk.grad_shard(t), g_sum[t])
+            assert e <= TOL, (step, capi.W_NAMES[t], e)
+    blk.close()

@@ -51,12 +51,13 @@ def test_invalid_arguments_are_rejected_without_gpu():
 
 
 def test_unsupported_micro_batching_is_refused_without_gpu():
-    """A legal ISP plan the executor does not run (b != 1 or n != 1, gs / oss groups) is refused
-    with SEQPLAN_ISP_ERR_UNSUPPORTED instead of silently running b = n = 1 (isp_block.cpp create_ctx)."""
+    """A legal ISP plan the executor does not run (b != 1 sequences per micro-batch, gs / oss groups)
+    is refused with SEQPLAN_ISP_ERR_UNSUPPORTED instead of silently running b = 1 (isp_block.cpp
+    create_ctx); n > 1 micro-batches are run (gradient accumulation, test_block_gpu.py)."""
     from paper_2401_09149_b200 import capi
     l = capi.lib()
     sh = capi.make_shape(512, 8, 1024)
-    for field, val in (("micro_batch", 2), ("micro_batch_num", 3)):
+    for field, val in (("micro_batch", 2), ("micro_batch", 4)):
         st = capi.StrategyC(micro_batch=1, micro_batch_num=1, recompute=0, pp=1, dp=1, tp=1, sp=2, ps=2, gs=1, oss=1)
         setattr(st, field, val)
         h = capi.c_vp()

@@ -11,6 +11,7 @@ the bytes that cross NVLink into or out of GPU 0 ((p-1)/p of the exchanged data)
 same run gives the counted link bytes per kernel.
 
     python tools/nvlink_kernels.py [iters]
+    python tools/nvlink_kernels.py --vpro profiles/r2/vpro_kernels_p<N>.csv   # message-size sweep
 """
 import ctypes
 import json
@@ -101,5 +102,53 @@ def main():
     print(json.dumps({"summary": rows}), flush=True)
 
 
+def vpro(out_csv, iters=5):
+    """Measured VPro curves in the reference's CSV schema (bandwidth.hpp:214-253): the library's
+    all-gather (push, bulk-copy), reduce-scatter (pull, fp32 sum + cast) and all-to-all (pull)
+    kernels of rank 0 at full-tensor message sizes 4..256 MiB in the tau convention of cost.hpp:177-188
+    (bandwidth = message bytes / time). Rows for both axes ("intra", "inter": one NVSwitch box, the
+    placement's inter label for sp = ps = p)."""
+    p = min(torch.cuda.device_count(), 4)
+    enable_peers(p)
+    l = capi.lib()
+    torch.cuda.set_device(0)
+    st = torch.cuda.current_stream(0).cuda_stream
+    rows = []
+    for mib in (4, 16, 64, 256):
+        v = mib << 20
+        # all-gather: each rank contributes v / p bytes of a v-byte tensor
+        shard = torch.empty(v // p // 2, device="cuda:0", dtype=torch.bfloat16)
+        gath = [torch.empty(v // 2, device=f"cuda:{q}", dtype=torch.bfloat16) for q in range(p)]
+        t = timed(lambda: capi.check(l.seqplan_isp_debug_push_allgather(p, 0, ptrs(gath), shard.data_ptr(), v // p,
+                                                                        1, 96, st)), iters)
+        rows.append(("all-gather", p, v, v / t))
+        del shard, gath
+        # reduce-scatter of a v-byte bf16 partial
+        part = [torch.empty(v // 2, device=f"cuda:{q}", dtype=torch.bfloat16).normal_() for q in range(p)]
+        out = torch.empty(v // 2 // p, device="cuda:0")
+        t = timed(lambda: capi.check(l.seqplan_isp_debug_reduce_scatter(p, 0, v // 2 // p, ptrs(part), 0, 1.0, 0,
+                                                                        out.data_ptr(), st)), iters)
+        rows.append(("reduce-scatter", p, v, v / t))
+        del part, out
+        # all-to-all of a v-byte [S, 3H] activation (H = 4096): T = v / (p * 3H * 2) rows per rank
+        Tq = max(8, v // (p * 3 * H * 2))
+        tok = [torch.empty(Tq, 3 * H, device=f"cuda:{q}", dtype=torch.bfloat16) for q in range(p)]
+        dst = torch.empty(p * Tq, 3 * (H // p), device="cuda:0", dtype=torch.bfloat16)
+        t = timed(lambda: capi.check(l.seqplan_isp_debug_all_to_all(p, 0, Tq, H, 3, 128, +1, ptrs(tok), dst.data_ptr(),
+                                                                    None, None, 0, st)), iters)
+        rows.append(("all-to-all", p, p * Tq * 3 * H * 2, p * Tq * 3 * H * 2 / t))
+        del tok, dst
+    with open(out_csv, "w") as f:
+        f.write("# measured on B200 by tools/nvlink_kernels.py --vpro (rank-0 kernel, CUDA events, isolated)\n")
+        f.write("op,participants,axis,message_bytes,bandwidth_bytes_per_sec\n")
+        for op, n, v, bw in rows:
+            for axis in ("intra", "inter"):
+                f.write(f"{op},{n},{axis},{v},{bw:.6e}\n")
+    print(json.dumps({"vpro": out_csv, "rows": len(rows)}), flush=True)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 2 and sys.argv[1] == "--vpro":
+        vpro(sys.argv[2])
+    else:
+        main()
