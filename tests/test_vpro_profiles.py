@@ -28,7 +28,7 @@ def test_measured_vpro_loads_and_interpolates(tool, csv):
     by = {}
     for r in rows:
         assert r["bw"] > 0 and math.isclose(r["lookup"], r["bw"], rel_tol=1e-9)
-        assert math.isclose(r["tau"], r["v"] / r["bw"], rel_tol=1e-9)
+        assert math.isclose(r["tau"], r["v"] / r["bw"], rel_tol=1e-7)  # %.9g print
         by.setdefault((r["op"], r["p"]), []).append(r)
     for pts in by.values():
         pts.sort(key=lambda r: r["v"])
