@@ -144,6 +144,13 @@ struct seqplan_isp_ctx {
   int gather_set = 0;
   bool push_primed = false;  // SKIP_COMM: buffers filled by one real step, then reused
   bool defer_bwd_set = false;  // fwd_issue_gathers leaves the backward set to the caller (stacks)
+  // gather tail: forward-set tensors (and the backward set) issued behind the Q|K|V all-to-all
+  // (SEQPLAN_ISP_DEFER_GATHER=1; measured neutral at 7B-32K p = 2/4: the A2A shortens, the rank skew stays)
+  bool defer_gathers = false;
+  // stored-dS attention backward workspace cap, GiB (SEQPLAN_ISP_DS_WS_GB; 0 = two-role kernel)
+  int64_t ds_ws_gb = 16;
+  int tail[SEQPLAN_W_COUNT] = {}, tail_n = 0;
+  cudaEvent_t ev_tail = nullptr;
   bool owns_comm = true;       // false: the comm stream belongs to layer 0 of a stack
   int ag_ctas = 96, ag_kind = kPushBulk;  // all-gathers: bulk-copy push, one chunk stored to every rank
   // reduce-scatter staging: each chunk goes to one destination, so the bulk kernel (one load in
@@ -721,7 +728,18 @@ bool qkv_sliced(const Ctx* c) {
 // forward all-gather of Wqkv is fused into the GEMM (nothing is gathered for it).
 bool qkv_ag_in_gemm(const Ctx* c) { return c->ag_gemm && qkv_sliced(c); }
 
+// Only the tensors the first GEMM needs (norm1, Wqkv) are gathered at step start on the
+// single-block transport paths; the rest of the forward set and the backward set follow the
+// Q|K|V all-to-all (issue_gather_tail), which otherwise shares NVLink with them: 7B-32K p = 4,
+// A2A L0 0.48 ms under the gathers vs 0.22 ms alone (profiles/r2/timeline_7b_s32k_p4.txt). The
+// tail still has the whole attention forward to land before its first consumer (Wo).
+bool defer_gather_tail(const Ctx* c) {
+  return c->defer_gathers && c->world > 1 && !c->group_mode && !c->skip_comm() && !c->fused_a2a && !c->ce_a2a &&
+         !c->defer_bwd_set && !c->recompute;
+}
+
 void fwd_issue_gathers(Ctx* c, cudaStream_t st) {
+  c->tail_n = 0;
   if (c->world == 1) {
     for (int t : {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN})
       gather_weight(c, t, st);
@@ -732,31 +750,52 @@ void fwd_issue_gathers(Ctx* c, cudaStream_t st) {
     ISP_CUDA(cudaEventRecord(c->ev_start, st));
     ISP_CUDA(cudaStreamWaitEvent(cs, c->ev_start, 0));
   }
+  const int fo[] = {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN};
+  const int fo_ag[] = {SEQPLAN_W_NORM1, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN};
+  const bool ag = qkv_ag_in_gemm(c);
+  const int* f = ag ? fo_ag : fo;
+  const int nf = ag ? 5 : 6;
+  const bool defer = defer_gather_tail(c) && !(c->push_mode() && c->push_skip());
+  const int head = defer ? (ag ? 1 : 2) : nf;
+  for (int i = head; i < nf; ++i) c->tail[c->tail_n++] = f[i];
   if (c->push_mode()) {
     // forward set, then the backward re-gather into the second set (its buffers are free since
     // the step-start barrier), so the backward never waits for weights
-    const int fo[] = {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN};
-    const int fo_ag[] = {SEQPLAN_W_NORM1, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN};
     const int bo[] = {SEQPLAN_W_DOWN, SEQPLAN_W_GATE, SEQPLAN_W_NORM2, SEQPLAN_W_O, SEQPLAN_W_QKV, SEQPLAN_W_NORM1};
     c->gather_set = 0;
-    push_gather_set(c, 1, bo, 6, false);
-    if (qkv_ag_in_gemm(c)) push_gather_set(c, 0, fo_ag, 5, !c->push_skip());
-    else push_gather_set(c, 0, fo, 6, !c->push_skip());
-    if (!c->push_skip() && !c->defer_bwd_set) push_gather_set(c, 1, bo, 6, true);
+    push_gather_set(c, 0, f, head, !c->push_skip());
+    if (!c->push_skip() && !c->defer_bwd_set && !defer) push_gather_set(c, 1, bo, 6, true);
     for (int t : fo) c->gathered[t] = c->hp<bf16>(c->off_gath[0][t]);
     return;
   }
   if (!c->group_mode) {
-    const int order[] = {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN};
-    const int order_ag[] = {SEQPLAN_W_NORM1, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN};
     c->evset = 0;
-    if (qkv_ag_in_gemm(c)) gather_pipelined(c, order_ag, 5, cs);
-    else gather_pipelined(c, order, 6, cs);
-    if (!c->defer_bwd_set) prefetch_bwd_set(c);
+    gather_pipelined(c, f, head, cs);
+    if (!c->defer_bwd_set && !defer) prefetch_bwd_set(c);
     return;
   }
   for (int t : {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN})
     gather_weight(c, t, cs);
+}
+
+// The deferred part of fwd_issue_gathers, behind the work already queued on st (the all-to-all).
+void issue_gather_tail(Ctx* c, cudaStream_t st) {
+  if (c->tail_n == 0) return;
+  ISP_CUDA(cudaEventRecord(c->ev_tail, st));
+  ISP_CUDA(cudaStreamWaitEvent(c->comm, c->ev_tail, 0));
+  if (c->push_mode()) {
+    const int bo[] = {SEQPLAN_W_DOWN, SEQPLAN_W_GATE, SEQPLAN_W_NORM2, SEQPLAN_W_O, SEQPLAN_W_QKV, SEQPLAN_W_NORM1};
+    {
+      Span sp(c, c->comm, 1, SEQPLAN_EV_ALL_GATHER, 0);
+      for (int i = 0; i < c->tail_n; ++i) push_gather(c, 0, c->tail[i], c->comm);
+    }
+    Span sp(c, c->comm, 1, SEQPLAN_EV_ALL_GATHER, 1);
+    for (int t : bo) push_gather(c, 1, t, c->comm);
+  } else {
+    gather_pipelined(c, c->tail, c->tail_n, c->comm);
+    prefetch_bwd_set(c);
+  }
+  c->tail_n = 0;
 }
 
 void wait_gathered(Ctx* c, int t, cudaStream_t st) {
@@ -862,6 +901,7 @@ void fwd_phase2(Ctx* c, cudaStream_t st) {
                                  static_cast<int>(c->H), 3, c->qkv_heads, c->cos_t, c->sin_t,
                                  static_cast<int>(c->d), 0, st, kA2ACtas));
   }
+  issue_gather_tail(c, st);
   Span sp(c, st, 0, SEQPLAN_EV_FORWARD, 1);
   KTimer kt(c, st, SEQPLAN_K_ATTN_FWD, 2.0 * double(c->S) * double(c->S) * double(c->Hl), 0);
   AttnTensors at = attn_tensors(c);
@@ -871,6 +911,7 @@ void fwd_phase2(Ctx* c, cudaStream_t st) {
 }
 
 void fwd_phase3(Ctx* c, const bf16* x, bf16* y, cudaStream_t st) {
+  issue_gather_tail(c, st);  // no-op after fwd_phase2
   const int T = static_cast<int>(c->T), H = static_cast<int>(c->H), I = static_cast<int>(c->I);
   if (c->world > 1 && !c->skip_comm() && c->ce_a2a) {
     Span sp(c, st, 0, SEQPLAN_EV_ALL_TO_ALL, 1);
@@ -1156,9 +1197,22 @@ void bwd_phase2(Ctx* c, cudaStream_t st) {
   // back to tokens is then a pure permutation)
   t.rope_cos = c->cos_t;
   t.rope_sin = c->sin_t;
+  // stored-dS backward: the causal dS tiles of up to ds_ws_gb GiB of heads (at least one head's,
+  // up to 32 GiB) per key-tile / dQ launch pair; 0 selects the two-role kernel
+  void* ws = nullptr;
+  if (c->d == 128 && c->ds_ws_gb > 0 && c->S % 128 == 0) {
+    const int64_t per_head = attention_bwd_ds_head_bytes(static_cast<int>(c->S));
+    const int64_t cap = std::max(c->ds_ws_gb << 30, per_head <= (int64_t(32) << 30) ? per_head : int64_t(0));
+    const int64_t g = std::min<int64_t>(c->Dl, cap / per_head);
+    if (g > 0) {
+      t.ds_ws_bytes = g * per_head;
+      ws = t.ds_ws = pool_alloc(c, t.ds_ws_bytes, seqplan::AllocTag::Other, st);
+    }
+  }
   KTimer kt(c, st, SEQPLAN_K_ATTN_BWD, 4.0 * double(c->S) * double(c->S) * double(c->Hl), 0);
   ISP_LAUNCH(3, attention_bwd(t, c->dO_heads, dqkv, dqkv + c->Hl, dqkv + 2 * c->Hl, ld, c->delta, c->dq_acc, st,
                          c->num_sms));
+  if (ws) c->pool->free(ws, st);
 }
 
 void bwd_phase3(Ctx* c, const bf16* x, bf16* dx, cudaStream_t st) {
@@ -1347,6 +1401,8 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   if (const char* e = std::getenv("SEQPLAN_ISP_RS_CE")) c->rs_ce = std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_QKV_SLICE")) c->qkv_slice = std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_AG_GEMM")) c->ag_gemm = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SEQPLAN_ISP_DS_WS_GB")) c->ds_ws_gb = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("SEQPLAN_ISP_DEFER_GATHER")) c->defer_gathers = std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_EARLY_REDUCE")) c->early_reduce = std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_A2A_CE")) c->ce_a2a = c->world > 1 && !c->fused_a2a && std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_RS_CTAS")) c->rs_ctas = std::atoi(e) ? std::atoi(e) : 128;
@@ -1403,6 +1459,7 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   ISP_CUDA(cudaEventCreateWithFlags(&c->ev_red_done, cudaEventDisableTiming));
   for (int t = 0; t < SEQPLAN_W_COUNT; ++t) ISP_CUDA(cudaEventCreateWithFlags(&c->ev_rs_sent[t], cudaEventDisableTiming));
   ISP_CUDA(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
+  ISP_CUDA(cudaEventCreateWithFlags(&c->ev_tail, cudaEventDisableTiming));
 
   // RoPE table, computed like oracle/block_oracle.c:ob_rope_table (double -> fp32)
   {
@@ -1569,6 +1626,7 @@ void seqplan_isp_ctx_destroy(seqplan_isp_ctx* c) {
   for (int t = 0; t < SEQPLAN_W_COUNT; ++t)
     if (c->ev_rs_sent[t]) cudaEventDestroy(c->ev_rs_sent[t]);
   if (c->ev_start) cudaEventDestroy(c->ev_start);
+  if (c->ev_tail) cudaEventDestroy(c->ev_tail);
   delete c;
 }
 
@@ -1771,6 +1829,15 @@ static void fwd_prologue(Ctx* c, cudaStream_t st, bool do_barrier, bool defer_bw
   c->defer_bwd_set = defer_bwd_set;
   fwd_issue_gathers(c, st);
   c->defer_bwd_set = false;
+}
+
+// Backward re-gather of one layer of a stack on its comm stream, ordered after the compute
+// stream's current point (the two-layer window of seqplan_isp_stack_*).
+static void stack_prefetch_bwd(Ctx* c, cudaStream_t st) {
+  if (c->bwd_prefetched) return;
+  ISP_CUDA(cudaEventRecord(c->ev_start, st));
+  ISP_CUDA(cudaStreamWaitEvent(c->comm, c->ev_start, 0));
+  prefetch_bwd_set(c);
 }
 
 static void push_bwd_set(Ctx* c) {
@@ -1985,6 +2052,7 @@ int64_t seqplan_isp_launch_count(const seqplan_isp_ctx* c) { return c ? c->launc
 // ---- multi-layer stacks ------------------------------------------
 struct seqplan_isp_stack {
   std::vector<Ctx*> layers;
+  bool window = true;  // two-layer prefetch window (copy-engine transport); SEQPLAN_ISP_STACK_WINDOW=0: all up front
   // layer boundaries, [T, H] bf16 from the shared pool: act[l] = input of layer l (l >= 1), the
   // checkpoint kept from the forward to layer l's backward (AllocTag::MlpOutput, packed k to a
   // region under consolidate_every_k_mlp, mempool.hpp:345-352); grad[l] = dx of layer l = dy of
@@ -2001,6 +2069,7 @@ int seqplan_isp_stack_create(int layers, int world, int rank, int device, const 
   if (!out || layers < 1) return SEQPLAN_ISP_ERR_INVALID;
   *out = nullptr;
   auto* s = new seqplan_isp_stack();
+  if (const char* e = std::getenv("SEQPLAN_ISP_STACK_WINDOW")) s->window = std::atoi(e) != 0;
   for (int l = 0; l < layers; ++l) {
     Ctx* c = nullptr;
     // one device pool for the stack (layer 0's): checkpoints, a = 1 workspaces and the gradient
@@ -2061,15 +2130,22 @@ int seqplan_isp_stack_fwd(seqplan_isp_stack* s, const void* x, void* y, void* st
   try {
     ISP_CUDA(cudaSetDevice(cur->device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    for (int l = 0; l < L; ++l) {
-      cur = s->layers[size_t(l)];
-      if (cur->group_mode) throw IspError(SEQPLAN_ISP_ERR_INVALID, "stacks run one process per GPU");
-      fwd_prologue(cur, st, l == 0, true);  // one write-after-read barrier covers every layer
-    }
-    for (int l = L; l-- > 0;) push_bwd_set(s->layers[size_t(l)]);
+    for (int l = 0; l < L; ++l)
+      if (s->layers[size_t(l)]->group_mode) throw IspError(SEQPLAN_ISP_ERR_INVALID, "stacks run one process per GPU");
+    // Copy-engine transport (gathers into pool buffers): a two-layer window — layer l+1's gathers
+    // are issued as layer l starts (the comm stream follows the compute stream to that point, so
+    // layer l-1's buffers are back in the pool) and the backward re-gathers one layer ahead —
+    // the reference's double buffer (cost.hpp:147 other_buffers = 2 e Psi / tp). Push transport:
+    // every layer's pinned sets are its own, so all sets are pushed up front.
+    const bool window = !cur->push_mode() && cur->world > 1 && s->window;
+    const int first = window ? 1 : L;
+    for (int l = 0; l < first; ++l) fwd_prologue(s->layers[size_t(l)], st, l == 0, true);
+    if (!window)
+      for (int l = L; l-- > 0;) push_bwd_set(s->layers[size_t(l)]);
     const int64_t bytes = s->layers[0]->T * s->layers[0]->H * 2;
     for (int l = 0; l < L; ++l) {
       cur = s->layers[size_t(l)];
+      if (window && l + 1 < L) fwd_prologue(s->layers[size_t(l + 1)], st, false, true);
       const bf16* in = l == 0 ? static_cast<const bf16*>(x) : s->act[size_t(l)];
       if (l < L - 1 && !s->act[size_t(l + 1)])
         s->act[size_t(l + 1)] = static_cast<bf16*>(pool_alloc(cur, bytes, seqplan::AllocTag::MlpOutput, st));
@@ -2077,6 +2153,7 @@ int seqplan_isp_stack_fwd(seqplan_isp_stack* s, const void* x, void* y, void* st
       fwd_body(cur, in, outp, st);
       cur->last_x = in;
     }
+    if (window) stack_prefetch_bwd(s->layers[size_t(L - 1)], st);
     s->x0 = x;
     s->fwd_done = true;
   } catch (const IspError& e) {
@@ -2095,8 +2172,10 @@ int seqplan_isp_stack_bwd(seqplan_isp_stack* s, const void* dy, void* dx, void* 
     ISP_CUDA(cudaSetDevice(cur->device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t bytes = s->layers[0]->T * s->layers[0]->H * 2;
+    const bool window = !cur->push_mode() && cur->world > 1 && s->window;
     for (int l = L; l-- > 0;) {
       cur = s->layers[size_t(l)];
+      if (window && l > 0) stack_prefetch_bwd(s->layers[size_t(l - 1)], st);  // one layer ahead
       const bf16* g_in = l == L - 1 ? static_cast<const bf16*>(dy) : s->grad[size_t(l + 1)];
       if (l > 0) s->grad[size_t(l)] = static_cast<bf16*>(pool_alloc(cur, bytes, seqplan::AllocTag::Other, st));
       bf16* g_out = l == 0 ? static_cast<bf16*>(dx) : s->grad[size_t(l)];

@@ -64,6 +64,8 @@ def main():
             dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         out[f"L{nl}_ms_per_step"] = ms.item()
         out[f"L{nl}_tokens_per_s_per_layer"] = S * nl / (ms.item() / 1e3)
+        ps = st.layer(0).pool_stats()  # the stack's one device pool (layer 0's)
+        out[f"L{nl}_pool_peak_reserved_gib"] = ps["peak_reserved"] / 2**30
         st.close()
         if world > 1:
             dist.barrier()
