@@ -235,8 +235,9 @@ def parse():
 
 KERNEL_NAMES = {
     "gemm": "tcgen05 GEMM (all linear-layer GEMMs of the step)",
-    "attn_bwd": "tcgen05 causal attention backward (attn_bwd_split_kernel: key-tile dK/dV CTAs + query-tile dQ "
-                "CTAs, no atomics; algorithmic FLOPs 4*S^2*Hl, the recomputed S/dP products not counted)",
+    "attn_bwd": "tcgen05 causal attention backward (stored-dS pair: attn_bwd_split_kernel<0,0,1> key-tile CTAs "
+                "write dK/dV and bulk-store every causal dS tile, attn_bwd_dq_kernel forms dQ = dS K from them; no "
+                "atomics; algorithmic FLOPs 4*S^2*Hl, the recomputed S/dP products not counted)",
     "attn_fwd": "tcgen05 causal attention forward (attn_fwd_fa4_kernel; FLOPs 2*S^2*Hl)",
 }
 

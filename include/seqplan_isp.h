@@ -255,6 +255,14 @@ int seqplan_isp_debug_attention(const void* q, const void* k, const void* v, int
                                 int64_t ld_o, float* lse, int S, int heads, int d, const void* dout,
                                 void* dq, void* dk, void* dv, int64_t ld_d, float* delta, float* dq_acc,
                                 void* stream);
+/* The same with the stored-dS backward's workspace (ws_bytes >= seqplan_isp_debug_attention_ds_bytes(S)
+ * selects it for d = 128: key-tile launch storing the causal dS tiles, then the dQ launch). */
+int seqplan_isp_debug_attention_ws(const void* q, const void* k, const void* v, int64_t ld_qkv, void* o,
+                                   int64_t ld_o, float* lse, int S, int heads, int d, const void* dout,
+                                   void* dq, void* dk, void* dv, int64_t ld_d, float* delta, float* dq_acc,
+                                   void* ws, int64_t ws_bytes, void* stream);
+/* Bytes of one head's causal dS tiles at sequence length S (the stored-dS backward). */
+int64_t seqplan_isp_debug_attention_ds_bytes(int S);
 /* RMSNorm forward (dn == NULL) or backward: dx = dres + d(norm), dg += sum dn*xhat. */
 int seqplan_isp_debug_rmsnorm(const void* x, const void* g, void* y, float* rstd, const void* dn,
                               const void* dres, void* dx, float* dg, int T, int H, float eps, void* stream);

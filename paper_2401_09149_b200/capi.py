@@ -126,6 +126,9 @@ _EXTRA_SIGS = [
     ("seqplan_isp_debug_gather_bench", c_int, [c_vp, c_int, c_int, P(ctypes.c_float)]),
     ("seqplan_isp_debug_attention", c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_int, c_int, c_int,
                                             c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    ("seqplan_isp_debug_attention_ws", c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_int, c_int, c_int,
+                                               c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp]),
+    ("seqplan_isp_debug_attention_ds_bytes", c_i64, [c_int]),
     ("seqplan_isp_debug_rmsnorm", c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_f,
                                           c_vp]),
     ("seqplan_isp_link_local_peers", c_int, [P(c_vp), c_int]),

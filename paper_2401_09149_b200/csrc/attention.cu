@@ -487,6 +487,8 @@ cudaError_t bwd_impl(const AttnTensors& t, const __nv_bfloat16* dout, __nv_bfloa
     // production: atomic-free tcgen05 backward (attention_tc.cu attn_bwd_split_kernel)
     // dq_acc (unused by this path) holds -lse*log2e [heads, S]
     attn_delta_kernel<D><<<num_sms * 8, 256, 0, st>>>(t.o, t.ld_o, dout, delta, t.S, t.heads, t.lse, dq_acc);
+    if (t.ds_ws && t.ds_ws_bytes >= attention_bwd_ds_head_bytes(t.S) && !std::getenv("SEQPLAN_ISP_ATTN_SPLIT_BWD"))
+      return attention_bwd_ds_tc(t, dout, t.ld_o, dq, dk, dv, ld_d, delta, dq_acc, t.ds_ws, t.ds_ws_bytes, st);
     return attention_bwd_nored_tc(t, dout, t.ld_o, dq, dk, dv, ld_d, delta, dq_acc, st);
   }
   cudaError_t e = cudaMemsetAsync(dq_acc, 0, sizeof(float) * static_cast<size_t>(t.heads) * t.S * D, st);

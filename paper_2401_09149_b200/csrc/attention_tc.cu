@@ -15,6 +15,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -871,6 +872,26 @@ __device__ __forceinline__ void bulk_reduce_add_f32(float* gdst, const void* sme
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// Streamed once: L2 evict-first, so the stream does not push the reused operands out of L2.
+__device__ __forceinline__ void bulk_store_stream(void* gdst, const void* smem_src, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+               "r"(smem_u32(smem_src)), "r"(bytes), "l"(pol)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load_stream(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -1242,6 +1263,12 @@ struct BwdSCfg {
   static constexpr int kOffBar = 7 * kTile;
   static constexpr int kBytes = kOffBar + 256 + 1024;
   static_assert(kBytes <= 232448, "exceeds the 227 KB per-CTA shared memory");
+  // key-tile variant staging dS for bulk stores (kDS = 1): a 32 KB staging tile after Q / dO, then
+  // lse | delta, barriers; the alignment slack shrinks to 768 B (the dynamic window starts 1024-aligned)
+  static constexpr int kOffStgD = 6 * kTile, kOffLDD = 7 * kTile, kOffBarD = 7 * kTile + 2048;
+  static constexpr int kSlackD = 768;
+  static constexpr int kBytesD = kOffBarD + 256 + kSlackD;
+  static_assert(kBytesD <= 232448, "exceeds the 227 KB per-CTA shared memory");
 };
 constexpr int kBwdSThreads = 320;
 
@@ -1280,7 +1307,18 @@ __device__ __forceinline__ int split_entry(int e, int T) {
   return -(W / 3 - 1) - 1;
 }
 
-template <int kPolyKV, int kPolyQ>
+// Causal dS tile store (kDS): tile (key tile k, query tile q >= k) of head h of a head group
+// at slot k T - k (k - 1) / 2 + (q - k); each 32 KB tile is the shared-memory image of dS
+// [128 queries x 128 keys] as a no-swizzle MN-major operand: byte (key / 32) * 8192 + (q / 8) * 512
+// + (key % 32) * 16 + (q % 8) * 2 — core matrices of 8 keys x 8 queries (128 B), key groups 128 B
+// apart inside a 32-key block, query groups 512 B apart — so the dQ kernel loads it with one bulk
+// copy and each producing warp's 32 keys x 64 queries are 4 KB contiguous.
+__host__ __device__ __forceinline__ int64_t ds_slot(int k, int q, int T) {
+  return int64_t(k) * T - int64_t(k) * (k - 1) / 2 + (q - k);
+}
+__host__ __device__ __forceinline__ int64_t ds_tiles_per_head(int T) { return int64_t(T) * (T + 1) / 2; }
+
+template <int kPolyKV, int kPolyQ, int kDS = 0>
 __global__ void __launch_bounds__(kBwdSThreads, 1)
     attn_bwd_split_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                           const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mDO,
@@ -1288,12 +1326,17 @@ __global__ void __launch_bounds__(kBwdSThreads, 1)
                           const float* __restrict__ delta, __nv_bfloat16* __restrict__ dq_out,
                           __nv_bfloat16* __restrict__ dk_out, __nv_bfloat16* __restrict__ dv_out, int64_t ld_d, int S,
                           float scale, const __grid_constant__ AttnPush push, const float* __restrict__ rope_cos,
-                          const float* __restrict__ rope_sin, int dbg, long long* trace) {
+                          const float* __restrict__ rope_sin, int dbg, long long* trace,
+                          uint8_t* __restrict__ ds_out, int h0) {
   using L = BwdSCfg;
   constexpr int D = 128;
+  constexpr int kOffLD = kDS == 1 ? L::kOffLDD : L::kOffLD;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
+  if constexpr (kDS == 1) {
+    if (smem - smem_raw > L::kSlackD) __trap();  // the layout assumes a (nearly) 1024-aligned window
+  }
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (kDS == 1 ? L::kOffBarD : L::kOffBar));
   uint64_t* fixed_full = bar + 0;  // KV: K, V   Q: Q, dO
   uint64_t* a_full = bar + 1;      // [3] KV: Q stages   Q: K stages
   uint64_t* a_empty = bar + 4;     // [3]
@@ -1309,8 +1352,9 @@ __global__ void __launch_bounds__(kBwdSThreads, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int lin = static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x);
-  const int entry = split_entry(lin / static_cast<int>(gridDim.y), S / 128);
-  const int h = static_cast<int>(blockIdx.z * gridDim.y) + lin % static_cast<int>(gridDim.y);
+  // kDS: key tiles only (k ascending = work descending), heads h0.. of the group
+  const int entry = kDS ? lin / static_cast<int>(gridDim.y) : split_entry(lin / static_cast<int>(gridDim.y), S / 128);
+  const int h = h0 + static_cast<int>(blockIdx.z * gridDim.y) + lin % static_cast<int>(gridDim.y);
   const bool role_q = entry < 0;
   const int tile = role_q ? -entry - 1 : entry;  // KV: key tile kt; Q: query tile qt
   const int T = S / 128;
@@ -1358,7 +1402,7 @@ __global__ void __launch_bounds__(kBwdSThreads, 1)
         const int sa = i % NA, sb = i & 1;
         if (i >= NA) mbar_wait(&a_empty[sa], ((i / NA) - 1) & 1);
         mbar_arrive_expect_tx(&a_full[sa], L::kTile + (role_q ? 0 : 512));
-        if (!role_q) bulk_load(smem + L::kOffLD + sa * 1024, nlse2 + static_cast<int64_t>(h) * S + row, 512, &a_full[sa]);
+        if (!role_q) bulk_load(smem + kOffLD + sa * 1024, nlse2 + static_cast<int64_t>(h) * S + row, 512, &a_full[sa]);
         for (int c = 0; c < 2; ++c) {
           if (role_q)
             tma_load_2d(smem + L::kOffKq + sa * L::kTile + c * (L::kTile / 2), &mK, &a_full[sa], h * D + c * 64, row);
@@ -1368,7 +1412,7 @@ __global__ void __launch_bounds__(kBwdSThreads, 1)
         if (i >= 2) mbar_wait(&b_empty[sb], ((i >> 1) - 1) & 1);
         mbar_arrive_expect_tx(&b_full[sb], L::kTile + (role_q ? 0 : 512));
         if (!role_q)
-          bulk_load(smem + L::kOffLD + sb * 1024 + 512, delta + static_cast<int64_t>(h) * S + row, 512, &b_full[sb]);
+          bulk_load(smem + kOffLD + sb * 1024 + 512, delta + static_cast<int64_t>(h) * S + row, 512, &b_full[sb]);
         for (int c = 0; c < 2; ++c) {
           if (role_q)
             tma_load_2d(smem + L::kOffVq + sb * L::kTile + c * (L::kTile / 2), &mV, &b_full[sb], h * D + c * 64, row);
@@ -1504,7 +1548,7 @@ __global__ void __launch_bounds__(kBwdSThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(s_free);  // S^T(i+1) may overwrite the S^T columns
         mbar_wait(&a_full[i & 1], (i >> 1) & 1);  // this tile's -lse*log2e (with Q(i)) is in shared memory
-        const uint32_t l4 = smem_u32(smem + L::kOffLD + (i & 1) * 1024 + half * 256);
+        const uint32_t l4 = smem_u32(smem + kOffLD + (i & 1) * 1024 + half * 256);
 #pragma unroll
         for (int j4 = 0; j4 < 16; ++j4) {
           const float4 l = lds_f4(l4 + j4 * 16);  // warp-uniform: shared-memory broadcast
@@ -1529,8 +1573,13 @@ __global__ void __launch_bounds__(kBwdSThreads, 1)
         for (int c = 0; c < 4; ++c) tmem_ld_x16(tP + lo + half * 64 + c * 16, *reinterpret_cast<uint32_t(*)[16]>(&sv[c * 16]));
         tmem_ld_wait();
         mbar_wait(&b_full[i & 1], (i >> 1) & 1);  // this tile's delta (with dO(i)) is in shared memory
-        const uint32_t d4 = smem_u32(smem + L::kOffLD + (i & 1) * 1024 + 512 + half * 256);
+        const uint32_t d4 = smem_u32(smem + kOffLD + (i & 1) * 1024 + 512 + half * 256);
         uint32_t pk[32], dk[32];
+        // kDS: the tile image is the no-swizzle MN-major operand layout (8 keys x 8 queries core
+        // matrices of 128 B, key groups 128 B apart, query groups 2 KB apart), so chunk c of the 32
+        // key rows of this warp is 512 contiguous bytes: one fully coalesced store per chunk (a
+        // swizzled row-per-thread image touches 32 lines per instruction and saturates the LSU;
+        // staging it through shared memory competes with the SS MMAs for the shared-memory port)
 #pragma unroll
         for (int j4 = 0; j4 < 16; ++j4) {
           const float4 dl = lds_f4(d4 + j4 * 16);
@@ -1548,11 +1597,37 @@ __global__ void __launch_bounds__(kBwdSThreads, 1)
         // P^T | dS^T over this warp's own 64 dP^T columns (all read above): A operands of dV / dK
         tmem_st_32x32b_x32(tP + lo + half * 64, pk);
         tmem_st_32x32b_x32(tP + lo + half * 64 + 32, dk);
+
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(ds_full);
         if (tr) trace[i * 8 + 7] = clock64();
+        // kDS: dS leaves after the MMA warp has it (off the tile's critical path). This warp's 32 keys
+        // x 64 queries are 4 KB contiguous in the tile image (ds_slot): chunk c (queries 8c..8c+7)
+        // of its keys is 512 contiguous bytes, one coalesced 16-B store per thread
+        if (kDS != 0 && !(dbg & 512)) {  // dbg 512 / 256: development, no dS store / no bulk store
+          const int64_t toff = ((int64_t(h - h0) * ds_tiles_per_head(T) + ds_slot(tile, tile + i, T)) << 15) +
+                               quad * 8192 + half * 4096;
+          if constexpr (kDS == 1) {  // staged in shared memory, one 4 KB bulk store per warp
+            uint8_t* stg = smem + L::kOffStgD + quad * 8192 + half * 4096;
+            if (lane == 0) bulk_wait_read();  // the previous tile's store has read these rows
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(stg + c * 512 + lane * 16)),
+                           "r"(dk[c * 4]), "r"(dk[c * 4 + 1]), "r"(dk[c * 4 + 2]), "r"(dk[c * 4 + 3])
+                           : "memory");
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0 && !(dbg & 256)) bulk_store_stream(ds_out + toff, stg, 4096, l2_evict_first_policy());
+          } else {
+            uint8_t* dst = ds_out + toff + lane * 16;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              *reinterpret_cast<uint4*>(dst + c * 512) = make_uint4(dk[c * 4], dk[c * 4 + 1], dk[c * 4 + 2], dk[c * 4 + 3]);
+          }
+        }
       };
       for (int i = 0; i < n; ++i) {
         if (dbg & 8) {  // development: MMA pipeline bound (no P / dS math)
@@ -1628,6 +1703,9 @@ __global__ void __launch_bounds__(kBwdSThreads, 1)
         if (j == n - 1) q_tile(j, std::true_type{});
         else q_tile(j, std::false_type{});
       }
+    }
+    if constexpr (kDS == 1) {
+      if (lane == 0) bulk_wait_all();  // the last dS stores are complete
     }
     // epilogue: KV role dK (scaled) | dV; Q role dQ (scaled) -> bf16 rows (or pushed to the owner rank).
     // With rope_cos, dK / dQ leave through the inverse rotary embedding (d/dx of RoPE(x) is R^T)
@@ -1710,6 +1788,153 @@ __global__ void __launch_bounds__(kBwdSThreads, 1)
   }
 }
 
+// dQ from the stored dS tiles (the kDS key-tile kernel): dQ(q) = scale * sum_{k <= q} dS(q, k) K(k),
+// both operands MN-major from shared memory (dS tile: one 32 KB bulk copy; K: TMA), fp32 in TMEM,
+// then the query-tile epilogue (inverse RoPE from fp32; bf16 rows or pushed to the owner rank).
+// One MMA per tile pair; bound by the HBM stream of dS.
+struct BwdDqCfg {
+  static constexpr int kTile = 128 * 128 * 2;
+  static constexpr int kStages = 3;
+  static constexpr int kOffDS = 0, kOffK = kStages * kTile;
+  static constexpr int kOffBar = 2 * kStages * kTile;
+  static constexpr int kBytes = kOffBar + 128 + 1024;
+  static_assert(kBytes <= 232448, "exceeds the 227 KB per-CTA shared memory");
+};
+constexpr int kBwdDqThreads = 192;  // warps 0..3 epilogue (one TMEM lane quadrant each), 4 TMA, 5 MMA
+
+__global__ void __launch_bounds__(kBwdDqThreads, 1)
+    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap mK, const uint8_t* __restrict__ ds,
+                       __nv_bfloat16* __restrict__ dq_out, int64_t ld_d, int S, float scale,
+                       const __grid_constant__ AttnPush push, const float* __restrict__ rope_cos,
+                       const float* __restrict__ rope_sin, int h0) {
+  using L = BwdDqCfg;
+  constexpr int D = 128;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
+  uint64_t* full = bar;        // [3]
+  uint64_t* empty = bar + 3;   // [3]
+  uint64_t* acc_full = bar + 6;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 7);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int lin = static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x);
+  const int T = S / 128;
+  const int qt = T - 1 - lin / static_cast<int>(gridDim.y);  // heaviest (latest) query tiles first
+  const int hg = static_cast<int>(blockIdx.z * gridDim.y) + lin % static_cast<int>(gridDim.y);
+  const int h = h0 + hg;
+  const int n = qt + 1;
+
+  if (warp == 4 && lane == 0) {
+    tma_prefetch(&mK);
+    for (int s = 0; s < L::kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc<128>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      const uint8_t* dsh = ds + (int64_t(hg) * ds_tiles_per_head(T) << 15);
+      const uint64_t pol = l2_evict_first_policy();
+      for (int k = 0; k < n; ++k) {
+        const int s = k % L::kStages;
+        if (k >= L::kStages) mbar_wait(&empty[s], ((k / L::kStages) - 1) & 1);
+        mbar_arrive_expect_tx(&full[s], 2 * L::kTile);
+        bulk_load_stream(smem + L::kOffDS + s * L::kTile, dsh + (ds_slot(k, qt, T) << 15), L::kTile, &full[s], pol);
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d(smem + L::kOffK + s * L::kTile + c * (L::kTile / 2), &mK, &full[s], h * D + c * 64, k * 128);
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      constexpr uint32_t id = make_idesc_bf16(128, 128, true, true);  // A = dS, B = K: both MN-major
+      // A: no-swizzle MN-major (ds_slot layout): for MN-major operands the leading byte offset is the
+      // K-direction core-matrix stride (key groups, 128 B) and the stride byte offset the MN-direction
+      // one (query groups, 512 B); the 16 keys of MMA kk start at (kk / 2) * 8192 + (kk % 2) * 256
+      for (int k = 0; k < n; ++k) {
+        const int s = k % L::kStages;
+        mbar_wait(&full[s], (k / L::kStages) & 1);
+        tc_fence_after();
+        const uint32_t a = smem_u32(smem + L::kOffDS + s * L::kTile), b = smem_u32(smem + L::kOffK + s * L::kTile);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)  // 16 keys per MMA
+          tc_mma_bf16(tmem, make_nosw_desc(a + (kk >> 1) * 8192 + (kk & 1) * 256, 128, 512),
+                      make_sw128_desc(b + kk * 2048, L::kTile / 2, 1024), id, (k > 0 || kk > 0) ? 1u : 0u);
+        tc_commit(&empty[s]);
+      }
+      tc_commit(acc_full);
+    }
+  } else {
+    const int r = warp * 32 + lane;
+    const uint32_t lo = static_cast<uint32_t>(warp * 32) << 16;
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const int tok = qt * 128 + r;
+    int64_t off = static_cast<int64_t>(tok) * ld_d + h * D;
+    __nv_bfloat16* base = dq_out;
+    if (push.p[0]) {  // fused all-to-all: the row goes to the owner rank of the token
+      const int owner = tok / push.T;
+      off = static_cast<int64_t>(tok - owner * push.T) * push.ld + h * D;
+      base = static_cast<__nv_bfloat16*>(push.p[owner]) + push.col_q;
+    }
+    auto store32 = [&](__nv_bfloat16* dst, const float (&v)[32]) {
+      uint4* o4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+      for (int v4 = 0; v4 < 4; ++v4)
+        o4[v4] = make_uint4(pack_bf16(v[v4 * 8], v[v4 * 8 + 1]), pack_bf16(v[v4 * 8 + 2], v[v4 * 8 + 3]),
+                            pack_bf16(v[v4 * 8 + 4], v[v4 * 8 + 5]), pack_bf16(v[v4 * 8 + 6], v[v4 * 8 + 7]));
+    };
+#pragma unroll 1
+    for (int half = 0; half < 2; ++half) {
+      if (rope_cos) {  // rotation pairs (i, i + 64), i in [32 half, 32 half + 32)
+        uint32_t a[32], b[32];
+        tmem_ld_32x32b_x32(tmem + lo + half * 32, a);
+        tmem_ld_32x32b_x32(tmem + lo + 64 + half * 32, b);
+        tmem_ld_wait();
+        const float* cs = rope_cos + static_cast<int64_t>(tok) * (D / 2) + half * 32;
+        const float* sn = rope_sin + static_cast<int64_t>(tok) * (D / 2) + half * 32;
+        float fl[32], fh[32];
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 c4 = *reinterpret_cast<const float4*>(cs + i), s4 = *reinterpret_cast<const float4*>(sn + i);
+          const float cv[4] = {c4.x, c4.y, c4.z, c4.w}, sv4[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float x = __uint_as_float(a[i + e]) * scale, y = __uint_as_float(b[i + e]) * scale;
+            fl[i + e] = x * cv[e] + y * sv4[e];
+            fh[i + e] = y * cv[e] - x * sv4[e];
+          }
+        }
+        store32(base + off + half * 32, fl);
+        store32(base + off + 64 + half * 32, fh);
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          const int col = half * 64 + c * 32;
+          uint32_t a[32];
+          tmem_ld_32x32b_x32(tmem + lo + col, a);
+          tmem_ld_wait();
+          float f[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) f[e] = __uint_as_float(a[e]) * scale;
+          store32(base + off + col, f);
+        }
+      }
+    }
+    if (push.p[0]) __threadfence_system();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc<128>(tmem);
+  }
+}
+
 }  // namespace
 
 long long* g_attn_trace = nullptr;  // development: clock64 trace of CTA (0,0)
@@ -1747,7 +1972,73 @@ cudaError_t attention_bwd_nored_tc(const AttnTensors& t, const __nv_bfloat16* do
   const int dbg = std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0;
   kern<<<lpt_grid(2 * T, t.heads, t.S, 128), kBwdSThreads, L::kBytes, st>>>(
       mq, mk, mv, mdo, nlse2, delta, dq, dk, dv, ld_d, t.S, scale, t.push, t.rope_cos, t.rope_sin, dbg,
-      g_attn_trace);
+      g_attn_trace, nullptr, 0);
+  return cudaGetLastError();
+}
+
+int64_t attention_bwd_ds_head_bytes(int S) { return ds_tiles_per_head(S / 128) << 15; }
+
+// Key-tile kernel storing dS (kDS) + the dQ kernel, per group of heads whose dS tiles fit ws.
+cudaError_t attention_bwd_ds_tc(const AttnTensors& t, const __nv_bfloat16* dout, int64_t ld_dout, __nv_bfloat16* dq,
+                                __nv_bfloat16* dk, __nv_bfloat16* dv, int64_t ld_d, const float* delta,
+                                const float* nlse2, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  if (t.d != 128 || t.S % 128) return cudaErrorInvalidValue;
+  const int64_t per_head = attention_bwd_ds_head_bytes(t.S);
+  const int G = static_cast<int>(std::min<int64_t>(t.heads, ws_bytes / per_head));
+  if (G < 1 || !ws) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(attn_bwd_split_kernel<0, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             BwdSCfg::kBytesD) != cudaSuccess ||
+        cudaFuncSetAttribute(attn_bwd_split_kernel<0, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             BwdSCfg::kBytes) != cudaSuccess ||
+        cudaFuncSetAttribute(attn_bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdDqCfg::kBytes) !=
+            cudaSuccess)
+      return cudaErrorInvalidValue;
+    attr = true;
+  }
+  const int T = t.S / 128;
+  CUtensorMap mq, mk, mv, mdo;
+  const int64_t cols = static_cast<int64_t>(t.heads) * 128;
+  if (!map2d(&mq, t.q, t.S, cols, t.ld_qkv, 128) || !map2d(&mk, t.k, t.S, cols, t.ld_qkv, 128) ||
+      !map2d(&mv, t.v, t.S, cols, t.ld_qkv, 128) || !map2d(&mdo, dout, t.S, cols, ld_dout, 128))
+    return cudaErrorInvalidValue;
+  const float scale = 1.0f / sqrtf(128.0f);
+  const int dbg = std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  const bool direct = std::getenv("SEQPLAN_ISP_DS_DIRECT") != nullptr;  // development: st.global instead of bulk
+  cudaEvent_t tev[3] = {};
+  const bool timed = (dbg & 1024) != 0;  // development: per-kernel event times of the first group
+  if (timed)
+    for (auto& e : tev) cudaEventCreate(&e);
+  for (int h0 = 0; h0 < t.heads; h0 += G) {
+    const int g = std::min(G, t.heads - h0);
+    const dim3 grid = lpt_grid(T, g, t.S, 128);
+    if (timed && h0 == 0) cudaEventRecord(tev[0], st);
+    if (!(dbg & 64)) {
+      if (direct)
+        attn_bwd_split_kernel<0, 0, 2><<<grid, kBwdSThreads, BwdSCfg::kBytes, st>>>(
+            mq, mk, mv, mdo, nlse2, delta, dq, dk, dv, ld_d, t.S, scale, t.push, t.rope_cos, t.rope_sin, dbg,
+            g_attn_trace, w, h0);
+      else
+        attn_bwd_split_kernel<0, 0, 1><<<grid, kBwdSThreads, BwdSCfg::kBytesD, st>>>(
+            mq, mk, mv, mdo, nlse2, delta, dq, dk, dv, ld_d, t.S, scale, t.push, t.rope_cos, t.rope_sin, dbg,
+            g_attn_trace, w, h0);
+    }
+    if (timed && h0 == 0) cudaEventRecord(tev[1], st);
+    if (!(dbg & 128))
+      attn_bwd_dq_kernel<<<grid, kBwdDqThreads, BwdDqCfg::kBytes, st>>>(mk, w, dq, ld_d, t.S, scale, t.push,
+                                                                         t.rope_cos, t.rope_sin, h0);
+    if (timed && h0 == 0) cudaEventRecord(tev[2], st);
+  }
+  if (timed) {
+    float a = 0, b = 0;
+    cudaEventSynchronize(tev[2]);
+    cudaEventElapsedTime(&a, tev[0], tev[1]);
+    cudaEventElapsedTime(&b, tev[1], tev[2]);
+    fprintf(stderr, "attn_bwd_ds: key-tile %.3f ms, dq %.3f ms (group of %d heads)\n", a, b, std::min(G, t.heads));
+    for (auto& e : tev) cudaEventDestroy(e);
+  }
   return cudaGetLastError();
 }
 

@@ -36,11 +36,14 @@ extern "C" int seqplan_isp_debug_gemm(const void* a, int64_t lda, int a_mn, cons
 
 #include "kernels.h"
 
-extern "C" int seqplan_isp_debug_attention(const void* q, const void* k, const void* v, int64_t ld_qkv,
-                                           void* o, int64_t ld_o, float* lse, int S, int heads, int d,
-                                           const void* dout, void* dq, void* dk, void* dv, int64_t ld_d,
-                                           float* delta, float* dq_acc, void* stream) {
+extern "C" int seqplan_isp_debug_attention_ws(const void* q, const void* k, const void* v, int64_t ld_qkv,
+                                              void* o, int64_t ld_o, float* lse, int S, int heads, int d,
+                                              const void* dout, void* dq, void* dk, void* dv, int64_t ld_d,
+                                              float* delta, float* dq_acc, void* ws, int64_t ws_bytes,
+                                              void* stream) {
   isp::AttnTensors t{};
+  t.ds_ws = ws;
+  t.ds_ws_bytes = ws_bytes;
   t.q = static_cast<const __nv_bfloat16*>(q);
   t.k = static_cast<const __nv_bfloat16*>(k);
   t.v = static_cast<const __nv_bfloat16*>(v);
@@ -66,6 +69,16 @@ extern "C" int seqplan_isp_debug_attention(const void* q, const void* k, const v
   if (e != cudaSuccess) fprintf(stderr, "seqplan_isp_debug_attention: %s\n", cudaGetErrorString(e));
   return e == cudaSuccess ? SEQPLAN_ISP_OK : SEQPLAN_ISP_ERR_RUNTIME;
 }
+
+extern "C" int seqplan_isp_debug_attention(const void* q, const void* k, const void* v, int64_t ld_qkv,
+                                           void* o, int64_t ld_o, float* lse, int S, int heads, int d,
+                                           const void* dout, void* dq, void* dk, void* dv, int64_t ld_d,
+                                           float* delta, float* dq_acc, void* stream) {
+  return seqplan_isp_debug_attention_ws(q, k, v, ld_qkv, o, ld_o, lse, S, heads, d, dout, dq, dk, dv, ld_d, delta,
+                                        dq_acc, nullptr, 0, stream);
+}
+
+extern "C" int64_t seqplan_isp_debug_attention_ds_bytes(int S) { return isp::attention_bwd_ds_head_bytes(S); }
 
 extern "C" int seqplan_isp_debug_rmsnorm(const void* x, const void* g, void* y, float* rstd, const void* dn,
                                          const void* dres, void* dx, float* dg, int T, int H, float eps,

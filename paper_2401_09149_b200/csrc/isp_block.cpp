@@ -147,8 +147,9 @@ struct seqplan_isp_ctx {
   // gather tail: forward-set tensors (and the backward set) issued behind the Q|K|V all-to-all
   // (SEQPLAN_ISP_DEFER_GATHER=1; measured neutral at 7B-32K p = 2/4: the A2A shortens, the rank skew stays)
   bool defer_gathers = false;
-  // stored-dS attention backward workspace cap, GiB (SEQPLAN_ISP_DS_WS_GB; 0 = two-role kernel)
-  int64_t ds_ws_gb = 16;
+  // stored-dS attention backward workspace cap, GiB (SEQPLAN_ISP_DS_WS_GB; 0 = two-role kernel);
+  // default: a quarter of the device memory, at most 48 GiB (7B-32K p = 1: all 32 heads' dS, 34.6 GB)
+  int64_t ds_ws_gb = -1;
   int tail[SEQPLAN_W_COUNT] = {}, tail_n = 0;
   cudaEvent_t ev_tail = nullptr;
   bool owns_comm = true;       // false: the comm stream belongs to layer 0 of a stack
@@ -1198,11 +1199,11 @@ void bwd_phase2(Ctx* c, cudaStream_t st) {
   t.rope_cos = c->cos_t;
   t.rope_sin = c->sin_t;
   // stored-dS backward: the causal dS tiles of up to ds_ws_gb GiB of heads (at least one head's,
-  // up to 32 GiB) per key-tile / dQ launch pair; 0 selects the two-role kernel
+  // up to twice the cap) per key-tile / dQ launch pair; 0 selects the two-role kernel
   void* ws = nullptr;
   if (c->d == 128 && c->ds_ws_gb > 0 && c->S % 128 == 0) {
     const int64_t per_head = attention_bwd_ds_head_bytes(static_cast<int>(c->S));
-    const int64_t cap = std::max(c->ds_ws_gb << 30, per_head <= (int64_t(32) << 30) ? per_head : int64_t(0));
+    const int64_t cap = std::max(c->ds_ws_gb << 30, per_head <= (c->ds_ws_gb << 30) * 2 ? per_head : int64_t(0));
     const int64_t g = std::min<int64_t>(c->Dl, cap / per_head);
     if (g > 0) {
       t.ds_ws_bytes = g * per_head;
@@ -1402,6 +1403,11 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   if (const char* e = std::getenv("SEQPLAN_ISP_QKV_SLICE")) c->qkv_slice = std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_AG_GEMM")) c->ag_gemm = std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_DS_WS_GB")) c->ds_ws_gb = std::max(0, std::atoi(e));
+  if (c->ds_ws_gb < 0) {
+    size_t free_b = 0, total_b = 0;
+    ISP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    c->ds_ws_gb = std::min<int64_t>(48, int64_t(total_b >> 30) / 4);
+  }
   if (const char* e = std::getenv("SEQPLAN_ISP_DEFER_GATHER")) c->defer_gathers = std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_EARLY_REDUCE")) c->early_reduce = std::atoi(e) != 0;
   if (const char* e = std::getenv("SEQPLAN_ISP_A2A_CE")) c->ce_a2a = c->world > 1 && !c->fused_a2a && std::atoi(e) != 0;

@@ -64,6 +64,10 @@ struct AttnTensors {
   // before they are rounded to bf16; [S, d/2] fp32 tables, nullptr = none
   const float* rope_cos = nullptr;
   const float* rope_sin = nullptr;
+  // backward only: workspace of the stored-dS backward (attention_bwd_ds_tc); too small for one
+  // head's dS tiles (attention_bwd_ds_head_bytes) selects the two-role kernel
+  void* ds_ws = nullptr;
+  int64_t ds_ws_bytes = 0;
 };
 cudaError_t attention_fwd(const AttnTensors& t, cudaStream_t st, int num_sms);
 // tcgen05/TMEM/TMA forward (attention_tc.cu); attention_fwd dispatches here.
@@ -77,6 +81,13 @@ cudaError_t attention_bwd_tc(const AttnTensors& t, const __nv_bfloat16* dout, in
 cudaError_t attention_bwd_nored_tc(const AttnTensors& t, const __nv_bfloat16* dout, int64_t ld_dout, __nv_bfloat16* dq,
                                    __nv_bfloat16* dk, __nv_bfloat16* dv, int64_t ld_d, const float* delta,
                                    const float* nlse2, cudaStream_t st);
+// Stored-dS backward (d = 128, S % 128 == 0): a key-tile launch (dK, dV, and every causal dS tile
+// stored in bf16 to ws) and a dQ launch (dQ = dS K from the stored tiles) per group of heads whose
+// dS fits ws (attention_bwd_ds_head_bytes(S) per head); otherwise as attention_bwd_nored_tc.
+int64_t attention_bwd_ds_head_bytes(int S);
+cudaError_t attention_bwd_ds_tc(const AttnTensors& t, const __nv_bfloat16* dout, int64_t ld_dout, __nv_bfloat16* dq,
+                                __nv_bfloat16* dk, __nv_bfloat16* dv, int64_t ld_d, const float* delta,
+                                const float* nlse2, void* ws, int64_t ws_bytes, cudaStream_t st);
 // dq/dk/dv written (bf16) with row stride ld_dqkv; scratch: fp32 [heads*S] (delta) and
 // fp32 [heads*S*d] (dq accumulator).
 cudaError_t attention_bwd(const AttnTensors& t, const __nv_bfloat16* dout, __nv_bfloat16* dq,

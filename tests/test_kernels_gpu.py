@@ -24,15 +24,23 @@ def torch_attention(q, k, v):  # [S, h, d] fp32, causal
     return torch.einsum("hqk,khd->qhd", p, v), lse
 
 
-@pytest.mark.parametrize("fused", [False, True])
+def ds_workspace(S, heads, device):
+    """Workspace for every head's causal dS tiles (the stored-dS backward)."""
+    n = capi.lib().seqplan_isp_debug_attention_ds_bytes(S) * heads
+    return torch.empty(n, dtype=torch.uint8, device=device)
+
+
+@pytest.mark.parametrize("mode", ["split", "ds", "fused"])
 @pytest.mark.parametrize("S,heads,d", [(256, 2, 64), (512, 3, 128), (1024, 1, 128), (384, 2, 64)])
-def test_attention_fwd_bwd(cuda, S, heads, d, fused, monkeypatch):
-    # fused: the opt-in fused backward (dQ reduced with fp32 L2 atomics), d = 128 only; default is
-    # the atomic-free two-role backward
-    if fused and d != 128:
-        pytest.skip("the fused tcgen05 backward is d = 128")
-    if fused:
+def test_attention_fwd_bwd(cuda, S, heads, d, mode, monkeypatch):
+    # split: the atomic-free two-role backward (no workspace); ds: the stored-dS backward (key-tile
+    # kernel storing the causal dS tiles + the dQ kernel; what the block runs); fused: the opt-in
+    # fused backward (dQ reduced with fp32 L2 atomics). ds / fused are d = 128 only.
+    if mode != "split" and d != 128:
+        pytest.skip("the stored-dS and fused tcgen05 backwards are d = 128")
+    if mode == "fused":
         monkeypatch.setenv("SEQPLAN_ISP_ATTN_FUSED_BWD", "1")
+    ws = ds_workspace(S, heads, cuda) if mode == "ds" else None
     torch.manual_seed(S + d)
     Hl = heads * d
     qkv = torch.randn(S, 3 * Hl, device=cuda).bfloat16()
@@ -54,10 +62,12 @@ def test_attention_fwd_bwd(cuda, S, heads, d, fused, monkeypatch):
     dqkv = torch.empty(S, 3 * Hl, device=cuda, dtype=torch.bfloat16)
     delta = torch.empty(heads, S, device=cuda)
     dq_acc = torch.empty(heads * S * d, device=cuda)
-    capi.check(l.seqplan_isp_debug_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), 3 * Hl, o.data_ptr(), Hl,
-                                             lse.data_ptr(), S, heads, d, do.data_ptr(), dqkv.data_ptr(),
-                                             dqkv[:, Hl:].data_ptr(), dqkv[:, 2 * Hl:].data_ptr(), 3 * Hl,
-                                             delta.data_ptr(), dq_acc.data_ptr(), st))
+    capi.check(l.seqplan_isp_debug_attention_ws(q.data_ptr(), k.data_ptr(), v.data_ptr(), 3 * Hl, o.data_ptr(), Hl,
+                                                lse.data_ptr(), S, heads, d, do.data_ptr(), dqkv.data_ptr(),
+                                                dqkv[:, Hl:].data_ptr(), dqkv[:, 2 * Hl:].data_ptr(), 3 * Hl,
+                                                delta.data_ptr(), dq_acc.data_ptr(),
+                                                ws.data_ptr() if ws is not None else None,
+                                                ws.numel() if ws is not None else 0, st))
     torch.cuda.synchronize()
     for i, g in enumerate((qf.grad, kf.grad, vf.grad)):
         got = dqkv[:, i * Hl:(i + 1) * Hl].float().view(S, heads, d)
@@ -122,10 +132,12 @@ def chunked_reference(q, k, v, do, chunk=2048):
     (32768, 2, (0, 1)),    # the 7B-32K sequence length
     (131072, 1, (0,)),     # the 20B-128K sequence length: S/128 = 1024 tiles per head
 ])
-def test_attention_long_sequence(cuda, S, heads, check_heads):
+@pytest.mark.parametrize("bwd", ["split", "ds"])
+def test_attention_long_sequence(cuda, S, heads, check_heads, bwd):
     """The production tcgen05 attention (d = 128) at the BASELINE sequence lengths against a chunked
     fp32 reference: rel-L2 <= 1e-2 on o, dq, dk, dv for the checked heads, |lse| abs error small.
-    At S = 128K the backward accumulates dK/dV over 1024 query tiles (SURVEY hard part vi)."""
+    At S = 128K the backward accumulates dK/dV over 1024 query tiles (SURVEY hard part vi).
+    bwd: the two-role kernel, or the stored-dS pair (at 128K one head's dS tiles are 17 GB)."""
     torch.manual_seed(S + heads)
     d = 128
     Hl = heads * d
@@ -141,11 +153,15 @@ def test_attention_long_sequence(cuda, S, heads, check_heads):
     st = torch.cuda.current_stream().cuda_stream
     capi.check(l.seqplan_isp_debug_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), 3 * Hl, o.data_ptr(), Hl,
                                              lse.data_ptr(), S, heads, d, None, None, None, None, 0, None, None, st))
-    capi.check(l.seqplan_isp_debug_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), 3 * Hl, o.data_ptr(), Hl,
-                                             lse.data_ptr(), S, heads, d, do.data_ptr(), dqkv.data_ptr(),
-                                             dqkv[:, Hl:].data_ptr(), dqkv[:, 2 * Hl:].data_ptr(), 3 * Hl,
-                                             delta.data_ptr(), dq_acc.data_ptr(), st))
+    ws = ds_workspace(S, heads, cuda) if bwd == "ds" else None
+    capi.check(l.seqplan_isp_debug_attention_ws(q.data_ptr(), k.data_ptr(), v.data_ptr(), 3 * Hl, o.data_ptr(), Hl,
+                                                lse.data_ptr(), S, heads, d, do.data_ptr(), dqkv.data_ptr(),
+                                                dqkv[:, Hl:].data_ptr(), dqkv[:, 2 * Hl:].data_ptr(), 3 * Hl,
+                                                delta.data_ptr(), dq_acc.data_ptr(),
+                                                ws.data_ptr() if ws is not None else None,
+                                                ws.numel() if ws is not None else 0, st))
     torch.cuda.synchronize()
+    del ws
     for h in check_heads:
         cs = slice(h * d, (h + 1) * d)
         qf, kf, vf, dof = (t[:, cs].float() for t in (q, k, v, do))
@@ -157,3 +173,44 @@ def test_attention_long_sequence(cuda, S, heads, check_heads):
             e = rel(got, ref)
             assert e < 1e-2, (h, "dq dk dv"[i * 3:i * 3 + 2], e)
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("S,heads,group", [(2048, 5, 2), (1024, 4, 3), (4096, 3, 1)])
+def test_attention_bwd_ds_head_groups(cuda, S, heads, group):
+    """The stored-dS backward with a workspace for `group` heads runs ceil(heads/group) launch pairs
+    (head offsets h0); its dq/dk/dv equal the two-role kernel's bit for bit (same fp32 products and
+    summation order) and match the fp32 reference."""
+    torch.manual_seed(S + heads)
+    d = 128
+    Hl = heads * d
+    qkv = torch.randn(S, 3 * Hl, device=cuda).bfloat16()
+    o = torch.empty(S, Hl, device=cuda, dtype=torch.bfloat16)
+    lse = torch.empty(heads, S, device=cuda)
+    do = torch.randn(S, Hl, device=cuda).bfloat16()
+    delta = torch.empty(heads, S, device=cuda)
+    dq_acc = torch.empty(heads * S * d, device=cuda)
+    q, k, v = qkv[:, :Hl], qkv[:, Hl:2 * Hl], qkv[:, 2 * Hl:]
+    l = capi.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    capi.check(l.seqplan_isp_debug_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), 3 * Hl, o.data_ptr(), Hl,
+                                             lse.data_ptr(), S, heads, d, None, None, None, None, 0, None, None, st))
+    ws = torch.full((l.seqplan_isp_debug_attention_ds_bytes(S) * group + 4096,), 0x7f, dtype=torch.uint8,
+                    device=cuda)
+    outs = []
+    for w in (None, ws):
+        dqkv = torch.full((S, 3 * Hl), float("nan"), device=cuda, dtype=torch.bfloat16)
+        capi.check(l.seqplan_isp_debug_attention_ws(q.data_ptr(), k.data_ptr(), v.data_ptr(), 3 * Hl, o.data_ptr(),
+                                                    Hl, lse.data_ptr(), S, heads, d, do.data_ptr(), dqkv.data_ptr(),
+                                                    dqkv[:, Hl:].data_ptr(), dqkv[:, 2 * Hl:].data_ptr(), 3 * Hl,
+                                                    delta.data_ptr(), dq_acc.data_ptr(),
+                                                    w.data_ptr() if w is not None else None,
+                                                    w.numel() if w is not None else 0, st))
+        outs.append(dqkv)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    qf, kf, vf = (t.float().view(S, heads, d).requires_grad_(True) for t in (q, k, v))
+    ref, _ = torch_attention(qf, kf, vf)
+    ref.backward(do.float().view(S, heads, d))
+    for i, g in enumerate((qf.grad, kf.grad, vf.grad)):
+        got = outs[1][:, i * Hl:(i + 1) * Hl].float().view(S, heads, d)
+        assert rel(got, g) < 1e-2, (i, rel(got, g))
