@@ -18,6 +18,10 @@ def run(S, heads, d, bwd=True, iters=5):
     delta = torch.empty(heads, S, device=dev)
     dq_acc = torch.empty(heads * S * d, device=dev)
     l = capi.lib()
+    # the block's default backward: the stored-dS pair with every head's dS tiles in one workspace
+    # (ATTN_BENCH_SPLIT=1: the two-role kernel)
+    nws = 0 if os.environ.get("ATTN_BENCH_SPLIT") or d != 128 else l.seqplan_isp_debug_attention_ds_bytes(S) * heads
+    ws = torch.empty(max(nws, 1), dtype=torch.uint8, device=dev)
     st = torch.cuda.current_stream().cuda_stream
     q, k, v = qkv.data_ptr(), qkv[:, Hl:].data_ptr(), qkv[:, 2 * Hl:].data_ptr()
 
@@ -26,10 +30,10 @@ def run(S, heads, d, bwd=True, iters=5):
                                                  None, None, None, None, 0, None, None, st))
 
     def bw():
-        capi.check(l.seqplan_isp_debug_attention(q, k, v, 3 * Hl, o.data_ptr(), Hl, lse.data_ptr(), S, heads, d,
-                                                 do.data_ptr(), dqkv.data_ptr(), dqkv[:, Hl:].data_ptr(),
-                                                 dqkv[:, 2 * Hl:].data_ptr(), 3 * Hl, delta.data_ptr(),
-                                                 dq_acc.data_ptr(), st))
+        capi.check(l.seqplan_isp_debug_attention_ws(q, k, v, 3 * Hl, o.data_ptr(), Hl, lse.data_ptr(), S, heads, d,
+                                                    do.data_ptr(), dqkv.data_ptr(), dqkv[:, Hl:].data_ptr(),
+                                                    dqkv[:, 2 * Hl:].data_ptr(), 3 * Hl, delta.data_ptr(),
+                                                    dq_acc.data_ptr(), ws.data_ptr() if nws else None, nws, st))
     out = []
     for name, fn, mult in (("fwd", fwd, 2.0), ("bwd", bw, 4.0)):
         if name == "bwd" and not bwd:
