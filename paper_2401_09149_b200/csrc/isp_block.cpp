@@ -1285,13 +1285,17 @@ void layout_heap(Ctx* c) {
     c->off_part[SEQPLAN_W_GATE] = take(size_t(2 * c->I * c->H) * 2);
     c->off_part[SEQPLAN_W_NORM1] = take(size_t(c->H) * 4);
     c->off_part[SEQPLAN_W_NORM2] = take(size_t(c->H) * 4);
-    for (int set = 0; set < 2; ++set)
-      for (int t : {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN})
-        c->off_gath[set][t] = take(size_t(t == SEQPLAN_W_GATE ? 2 * c->I * c->H : c->numel(t)) * 2);
-    for (int t : {SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_DOWN}) c->off_stage[t] = take(size_t(c->numel(t)) * 2);
-    c->off_stage[SEQPLAN_W_GATE] = take(size_t(2 * c->I * c->H) * 2);
-    c->off_stage[SEQPLAN_W_NORM1] = take(size_t(c->H) * 4);
-    c->off_stage[SEQPLAN_W_NORM2] = take(size_t(c->H) * 4);
+    // push transport only: the pinned gather double buffer and the RS staging slots the peers
+    // write into (the copy-engine transport takes both from the device pool, per pass)
+    if (c->push_mode()) {
+      for (int set = 0; set < 2; ++set)
+        for (int t : {SEQPLAN_W_NORM1, SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_NORM2, SEQPLAN_W_GATE, SEQPLAN_W_DOWN})
+          c->off_gath[set][t] = take(size_t(t == SEQPLAN_W_GATE ? 2 * c->I * c->H : c->numel(t)) * 2);
+      for (int t : {SEQPLAN_W_QKV, SEQPLAN_W_O, SEQPLAN_W_DOWN}) c->off_stage[t] = take(size_t(c->numel(t)) * 2);
+      c->off_stage[SEQPLAN_W_GATE] = take(size_t(2 * c->I * c->H) * 2);
+      c->off_stage[SEQPLAN_W_NORM1] = take(size_t(c->H) * 4);
+      c->off_stage[SEQPLAN_W_NORM2] = take(size_t(c->H) * 4);
+    }
   }
   c->heap_bytes = off;
 }
@@ -1549,7 +1553,7 @@ extern "C" {
 
 static int create_ctx(int world, int rank, int device, const seqplan_isp_shape* shape,
                       const seqplan_strategy* strategy, const seqplan_mempool_policy* policy, uint32_t flags,
-                      DevicePool* shared_pool, int premap_layers, seqplan_isp_ctx** out);
+                      DevicePool* shared_pool, int premap_layers, seqplan_isp_ctx** out, int push_override = -1);
 
 int seqplan_isp_ctx_create(int world, int rank, int device, const seqplan_isp_shape* shape,
                            const seqplan_strategy* strategy, const seqplan_mempool_policy* policy,
@@ -1559,7 +1563,7 @@ int seqplan_isp_ctx_create(int world, int rank, int device, const seqplan_isp_sh
 
 static int create_ctx(int world, int rank, int device, const seqplan_isp_shape* shape,
                       const seqplan_strategy* strategy, const seqplan_mempool_policy* policy, uint32_t flags,
-                      DevicePool* shared_pool, int premap_layers, seqplan_isp_ctx** out) {
+                      DevicePool* shared_pool, int premap_layers, seqplan_isp_ctx** out, int push_override) {
   if (!out || !shape) return SEQPLAN_ISP_ERR_INVALID;
   *out = nullptr;
   if (rank < 0 || rank >= world) return SEQPLAN_ISP_ERR_INVALID;
@@ -1588,6 +1592,7 @@ static int create_ctx(int world, int rank, int device, const seqplan_isp_shape* 
   c->flags = flags;
   c->recompute = (strategy && strategy->recompute == 1) || (flags & SEQPLAN_ISP_FLAG_RECOMPUTE);
   c->micro_batches = strategy ? static_cast<int>(strategy->micro_batch_num) : 1;
+  c->push_pref = push_override;  // -1: by world size; SEQPLAN_ISP_PUSH overrides either (setup)
   if (shared_pool) {
     c->pool = shared_pool;
     c->owns_pool = false;
@@ -2076,12 +2081,26 @@ int seqplan_isp_stack_create(int layers, int world, int rank, int device, const 
   *out = nullptr;
   auto* s = new seqplan_isp_stack();
   if (const char* e = std::getenv("SEQPLAN_ISP_STACK_WINDOW")) s->window = std::atoi(e) != 0;
+  // Transport: the push transport's pinned buffers (two gather sets + the RS staging, 3·e·Ψ_blk)
+  // live in every layer's heap for the whole run; when the stack's share would exceed a quarter of
+  // the device, the copy-engine transport with the two-layer gather window (pool buffers, at most
+  // two layers' sets live; cost.hpp:147) is used instead (SEQPLAN_ISP_PUSH still forces either)
+  int push_override = -1;
+  if (shape && world >= 4) {
+    const int64_t H = shape->hidden_dim, I = shape->ffn_dim > 0 ? shape->ffn_dim : seqplan::mlp_intermediate_dim(H);
+    const int64_t psi = 4 * H * H + 3 * I * H + 2 * H;
+    size_t free_b = 0, total_b = 0;
+    if (cudaSetDevice(device) == cudaSuccess && cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
+        int64_t(layers) * 3 * psi * 2 > int64_t(total_b / 4))
+      push_override = 0;
+  }
   for (int l = 0; l < layers; ++l) {
     Ctx* c = nullptr;
     // one device pool for the stack (layer 0's): checkpoints, a = 1 workspaces and the gradient
     // arena of every layer (pre-mapped by the owner) share it, as in the reference's trace
     DevicePool* shared = l == 0 ? nullptr : s->layers[0]->pool;
-    const int st = create_ctx(world, rank, device, shape, strategy, policy, flags, shared, l == 0 ? layers : 1, &c);
+    const int st =
+        create_ctx(world, rank, device, shape, strategy, policy, flags, shared, l == 0 ? layers : 1, &c, push_override);
     if (st != SEQPLAN_ISP_OK) {
       seqplan_isp_stack_destroy(s);
       return st;
