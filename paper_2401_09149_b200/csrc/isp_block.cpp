@@ -158,6 +158,7 @@ struct seqplan_isp_ctx {
   // flight per CTA) is load-latency bound there; 16-B vector stores from 256-thread CTAs
   // (128 B in flight per thread, no shared memory: they co-reside with every compute kernel)
   int rs_ctas = 128;
+  int red_ctas = 0;  // CTAs of the staged-slot reductions (SEQPLAN_ISP_RED_CTAS; default 4 per SM)
   int gemm_sm_budget = 0;  // > 0 when the all-gather holds SMs of its own (kPushBulkWide)
   uint32_t* error_flag = nullptr;  // device, in the heap flags page
 
@@ -692,14 +693,14 @@ void reduce_pushed(Ctx* c, int t, cudaStream_t st) {
     const int64_t half = (c->I / c->world) * c->H, slot = 2 * half;
     bf16* stg = c->hp<bf16>(c->off_stage[t]);
     for (int q = 0; q < c->world; ++q) src.p[q] = stg + q * slot;
-    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, half, false, 1.0f, c->accum ? 1 : 0, c->grad[SEQPLAN_W_GATE], st, c->num_sms * 4));
+    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, half, false, 1.0f, c->accum ? 1 : 0, c->grad[SEQPLAN_W_GATE], st, c->red_ctas));
     for (int q = 0; q < c->world; ++q) src.p[q] = stg + q * slot + half;
-    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, half, false, 1.0f, c->accum ? 1 : 0, c->grad[SEQPLAN_W_UP], st, c->num_sms * 4));
+    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, half, false, 1.0f, c->accum ? 1 : 0, c->grad[SEQPLAN_W_UP], st, c->red_ctas));
   } else {
     const int64_t sh = c->shard(t), esz = norm ? 4 : 2;
     char* stg = c->hp<char>(c->off_stage[t]);
     for (int q = 0; q < c->world; ++q) src.p[q] = stg + q * sh * esz;
-    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, sh, norm, 1.0f, c->accum ? 1 : 0, c->grad[t], st, c->num_sms * 4));
+    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, sh, norm, 1.0f, c->accum ? 1 : 0, c->grad[t], st, c->red_ctas));
   }
 }
 
@@ -1063,14 +1064,14 @@ void reduce_staged(Ctx* c, int t, cudaStream_t st) {
     const int64_t slot = 2 * (c->I / c->world) * c->H, half = slot / 2;
     bf16* stg = static_cast<bf16*>(c->stage[t]);
     for (int q = 0; q < c->world; ++q) src.p[q] = stg + q * slot;
-    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, half, false, 1.0f, c->accum ? 1 : 0, c->grad[SEQPLAN_W_GATE], st, c->num_sms * 4));
+    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, half, false, 1.0f, c->accum ? 1 : 0, c->grad[SEQPLAN_W_GATE], st, c->red_ctas));
     for (int q = 0; q < c->world; ++q) src.p[q] = stg + q * slot + half;
-    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, half, false, 1.0f, c->accum ? 1 : 0, c->grad[SEQPLAN_W_UP], st, c->num_sms * 4));
+    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, half, false, 1.0f, c->accum ? 1 : 0, c->grad[SEQPLAN_W_UP], st, c->red_ctas));
   } else {
     const int64_t sh = c->shard(t), esz = norm ? 4 : 2;
     char* stg = static_cast<char*>(c->stage[t]);
     for (int q = 0; q < c->world; ++q) src.p[q] = stg + q * sh * esz;
-    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, sh, norm, 1.0f, c->accum ? 1 : 0, c->grad[t], st, c->num_sms * 4));
+    ISP_LAUNCH(1, reduce_scatter_pull(src, c->world, 0, sh, norm, 1.0f, c->accum ? 1 : 0, c->grad[t], st, c->red_ctas));
   }
   c->pool->free(c->stage[t], st);
   c->stage[t] = nullptr;
@@ -1418,6 +1419,8 @@ void setup(Ctx* c, const seqplan_isp_shape* shape, const seqplan_mempool_policy*
   if (const char* e = std::getenv("SEQPLAN_ISP_RS_CTAS")) c->rs_ctas = std::atoi(e) ? std::atoi(e) : 128;
   if (const char* e = std::getenv("SEQPLAN_ISP_AG_CTAS")) c->ag_ctas = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("SEQPLAN_ISP_AG_KIND")) c->ag_kind = std::atoi(e);
+  c->red_ctas = c->num_sms * 4;
+  if (const char* e = std::getenv("SEQPLAN_ISP_RED_CTAS")) c->red_ctas = std::max(1, std::atoi(e));
   if (c->ag_kind == kPushBulkWide) c->gemm_sm_budget = c->num_sms - c->ag_ctas;
   layout_heap(c);
   ISP_CUDA(cudaMalloc(&c->heap, c->heap_bytes));
