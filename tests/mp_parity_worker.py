@@ -14,6 +14,23 @@ from paper_2401_09149_b200 import capi  # noqa: E402
 from paper_2401_09149_b200.dist import bootstrap_peers  # noqa: E402
 
 
+def _device(rank):
+    """This rank's GPU and the bootstrap group. MP_RANKS_PER_GPU > 1 oversubscribes the box (e.g.
+    8 ranks on 4 GPUs): rank r uses GPU r % count, and the bootstrap runs over gloo (NCCL refuses
+    two ranks on one device); the block's own transport is CUDA IPC either way."""
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    over = int(os.environ.get("MP_RANKS_PER_GPU", "1")) > 1
+    if over:
+        local %= torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if over:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
+    return local, dev
+
+
 def rel(a, b):
     a = np.asarray(a, np.float64); b = np.asarray(b, np.float64)
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
@@ -26,10 +43,7 @@ def steps_mode(H, D, S, adamw):
     barriers alone. Step 3's y / dx / gradient shards and the final weight shards vs the oracle
     running the same sequence."""
     world, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    local, dev = _device(rank)
     sh = ob.Shape(H=H, D=D, S=S)
     w = ob.make_weights(sh)
     x = torch.from_numpy(ob.make_activation(sh, ob.TID_X)).bfloat16()
@@ -90,10 +104,7 @@ def main():
         return
     fused = len(sys.argv) > 4 and sys.argv[4] == "fused"
     world, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    local, dev = _device(rank)
     sh = ob.Shape(H=H, D=D, S=S)
     w = ob.make_weights(sh)
     x = torch.from_numpy(ob.make_activation(sh, ob.TID_X)).bfloat16()

@@ -175,3 +175,23 @@ def test_multiprocess_parity_ag_into_gemm(n):
         for k, v in row.items():
             if k != "rank":
                 assert v <= 1e-2, (row["rank"], k, v)
+
+
+def test_multiprocess_parity_8_ranks_on_4_gpus():
+    """World size 8 through the multi-process production path (push transport, memop barriers,
+    pull all-to-all, 8 peers) with two ranks per GPU — the p = 8 code path on a 4-GPU box. The
+    ranks of one GPU time-slice, so this is a correctness check only."""
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
+           "--master-addr=127.0.0.1", "--master-port=29588",
+           os.path.join(ROOT, "tests", "mp_parity_worker.py"), "1024", "8", "1024", "selective"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT,
+                       env={**os.environ, "MP_RANKS_PER_GPU": "2"})
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    rows = _json_rows(r.stdout)
+    assert len(rows) == 8
+    for row in rows:
+        for k, v in row.items():
+            if k not in ("rank", "timeline_events"):
+                assert v <= 1e-2, (row["rank"], k, v)
