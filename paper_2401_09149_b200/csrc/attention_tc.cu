@@ -467,6 +467,7 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
+template <int kPolyPairs = 2>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_fa4_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                         const __grid_constant__ CUtensorMap mV, __nv_bfloat16* __restrict__ out, int64_t ld_o,
@@ -659,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float2 sv = make_float2(__uint_as_float(sr[c * 16 + i]), __uint_as_float(sr[c * 16 + i + 1]));
             const float2 xv = __ffma2_rn(sv, sc, nm);
             float2 pv;
-            if (i >= 10) {  // 3 of 8 pairs on the FMA pipe
+            if (i >= 16 - 2 * kPolyPairs) {  // kPolyPairs of 8 pairs on the FMA pipe
               pv = exp2_poly2(xv);
             } else {
               pv.x = fast_exp2(xv.x);
@@ -781,11 +782,24 @@ cudaError_t launch_fwd(const AttnTensors& t, cudaStream_t st) {
 
 cudaError_t launch_fwd_pair(const AttnTensors& t, cudaStream_t st) {
   using L = Fa4Cfg;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_fa4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
+  // exponential pairs of 8 on the FMA-pipe polynomial (development: SEQPLAN_ISP_FWD_POLY)
+  const char* pe = std::getenv("SEQPLAN_ISP_FWD_POLY");
+  // (32K x 32 heads, isolated: 0 -> 7.16 ms, 2 -> 6.98, 3 -> 7.17, 4 -> 7.36; in the power-capped
+  // 7B-32K step all within noise, profiles/r2/attn_fwd_poly_sweep.txt)
+  const int poly = pe ? std::atoi(pe) : 2;
+  auto kern = attn_fwd_fa4_kernel<2>;
+  switch (poly) {
+    case 0: kern = attn_fwd_fa4_kernel<0>; break;
+    case 1: kern = attn_fwd_fa4_kernel<1>; break;
+    case 3: kern = attn_fwd_fa4_kernel<3>; break;
+    case 4: kern = attn_fwd_fa4_kernel<4>; break;
+    default: break;
+  }
+  static bool attr[8] = {};
+  if (!attr[poly & 7]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr[poly & 7] = true;
   }
   CUtensorMap mq, mk, mv;
   const int64_t cols = static_cast<int64_t>(t.heads) * 128;
@@ -806,7 +820,7 @@ cudaError_t launch_fwd_pair(const AttnTensors& t, cudaStream_t st) {
   cfg.attrs = attr_;
   cfg.numAttrs = 1;
   const int dbg = std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0;
-  return cudaLaunchKernelEx(&cfg, attn_fwd_fa4_kernel, mq, mk, mv, t.o, t.ld_o, t.lse, t.S, scale_log2, t.push,
+  return cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, t.o, t.ld_o, t.lse, t.S, scale_log2, t.push,
                             g_attn_trace_fwd, dbg);
 }
 
