@@ -332,6 +332,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2401_09149_b200 import capi
+    from paper_2401_09149_b200.dist import bootstrap_peers
 
     world, rank, local = dist_env()
     if world != args.gpus:
@@ -353,10 +354,7 @@ def main():
         blk = capi.IspBlock(H, D, S, world=world, rank=rank, device=local, flags=flags | extra_flags,
                             recompute=args.recompute)
         if world > 1:
-            handles = [None] * world
-            dist.all_gather_object(handles, blk.ipc_handle())
-            blk.open_peers(handles)
-            dist.barrier()
+            bootstrap_peers(blk, world)
         blk.init_weights(SEED)
         return blk
 

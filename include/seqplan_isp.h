@@ -160,6 +160,20 @@ size_t seqplan_isp_ipc_handle_size(void);
 int seqplan_isp_link_local_peers(seqplan_isp_ctx** ctxs, int world);
 int seqplan_isp_ipc_handle(seqplan_isp_ctx* ctx, void* out);
 int seqplan_isp_open_peers(seqplan_isp_ctx* ctx, const void* handles);
+/* NVLink SHARP reduce-scatter (multi-process push transport, p >= 4; default on where the
+ * GPUs support multicast, SEQPLAN_ISP_NVLS=0 turns it off;
+ * replaces the push-RS staging of the four weight matrices, the reference's RS(e*Psi) priced at
+ * cost.hpp:184-188): after open_peers, rank 0 calls nvls_export (creates the multicast object,
+ * returns its pid and an exported POSIX fd; SEQPLAN_ISP_ERR_UNSUPPORTED when not applicable: then
+ * no rank calls the rest), every rank calls nvls_attach with rank 0's pid / fd (rank 0: 0, -1;
+ * the others duplicate the fd out of rank 0's process with pidfd_getfd), then — after all ranks
+ * attached — nvls_bind. nvls_release abandons it on this rank (the push RS is used again); a
+ * failure on any rank must be followed by nvls_release on all. */
+int seqplan_isp_nvls_export(seqplan_isp_ctx* ctx, int* pid, int* fd);
+int seqplan_isp_nvls_attach(seqplan_isp_ctx* ctx, int pid, int fd);
+int seqplan_isp_nvls_bind(seqplan_isp_ctx* ctx);
+int seqplan_isp_nvls_release(seqplan_isp_ctx* ctx);
+int seqplan_isp_nvls_active(const seqplan_isp_ctx* ctx);
 
 /* Single-process multi-rank mode: p contexts on one device whose "peers" are
  * each other's heaps; collectives run as lock-step phases over all ranks. */

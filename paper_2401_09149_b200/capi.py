@@ -61,6 +61,7 @@ W_NORM1, W_QKV, W_O, W_NORM2, W_GATE, W_UP, W_DOWN = range(7)
 W_NAMES = ["norm1", "qkv", "o", "norm2", "gate", "up", "down"]
 FLAG_NO_OVERLAP, FLAG_FUSED_BWD, FLAG_TIMELINE, FLAG_SKIP_COMM, FLAG_PROFILE = 1, 2, 4, 8, 16
 FLAG_RECOMPUTE = 32  # a = 1 where no Strategy is passed (group mode)
+ERR_UNSUPPORTED = 4
 EV_NAMES = ["forward", "grad_input", "grad_weight", "all_gather", "reduce_scatter", "all_to_all"]
 
 
@@ -98,6 +99,11 @@ _EXTRA_SIGS = [
     ("seqplan_isp_ipc_handle_size", ctypes.c_size_t, []),
     ("seqplan_isp_ipc_handle", c_int, [c_vp, c_vp]),
     ("seqplan_isp_open_peers", c_int, [c_vp, c_vp]),
+    ("seqplan_isp_nvls_export", c_int, [c_vp, P(c_int), P(c_int)]),
+    ("seqplan_isp_nvls_attach", c_int, [c_vp, c_int, c_int]),
+    ("seqplan_isp_nvls_bind", c_int, [c_vp]),
+    ("seqplan_isp_nvls_release", c_int, [c_vp]),
+    ("seqplan_isp_nvls_active", c_int, [c_vp]),
     ("seqplan_isp_group_create", c_int, [c_int, c_int, P(ShapeC), P(PolicyC), c_u32, P(c_vp)]),
     ("seqplan_isp_group_fwd", c_int, [P(c_vp), c_int, P(c_vp), P(c_vp), c_vp]),
     ("seqplan_isp_group_bwd", c_int, [P(c_vp), c_int, P(c_vp), P(c_vp), c_vp]),
@@ -196,7 +202,7 @@ class IspBlock:
     def __init__(self, H, D, S, world=1, rank=0, device=0, policy=None, flags=0, I=0, recompute=False,
                  micro_batches=1):
         l = lib()
-        self.world, self.rank = world, rank
+        self.world, self.rank, self.device = world, rank, device
         self.shape = make_shape(H, D, S, I)
         # micro_batches = n (Strategy::micro_batch_num): n fwd/bwd calls per step, gradients accumulate
         strat = StrategyC(1, int(micro_batches), int(recompute), 1, 1, 1, world, world, 1, 1)
@@ -218,6 +224,28 @@ class IspBlock:
         blob = b"".join(handles)
         buf = ctypes.create_string_buffer(blob, len(blob))
         check(lib().seqplan_isp_open_peers(self.h, buf), self.h, "open_peers")
+
+    # NVLink SHARP reduce-scatter setup (seqplan_isp_nvls_*; dist.bootstrap_nvls drives it)
+    def nvls_export(self):
+        """Rank 0: (pid, fd) of the exported multicast handle, or None when not applicable."""
+        pid, fd = c_int(), c_int()
+        r = lib().seqplan_isp_nvls_export(self.h, ctypes.byref(pid), ctypes.byref(fd))
+        if r == ERR_UNSUPPORTED:
+            return None
+        check(r, self.h, "nvls_export")
+        return pid.value, fd.value
+
+    def nvls_attach(self, pid, fd) -> bool:
+        return lib().seqplan_isp_nvls_attach(self.h, pid, fd) == 0
+
+    def nvls_bind(self) -> bool:
+        return lib().seqplan_isp_nvls_bind(self.h) == 0
+
+    def nvls_release(self):
+        lib().seqplan_isp_nvls_release(self.h)
+
+    def nvls_active(self) -> bool:
+        return bool(lib().seqplan_isp_nvls_active(self.h))
 
     def init_weights(self, seed):
         check(lib().seqplan_isp_init_weights(self.h, seed), self.h, "init_weights")

@@ -145,6 +145,56 @@ __global__ void reduce_scatter_interleave_kernel(PeerPtrs part, int world, int r
   }
 }
 
+// NVLink SHARP reduce-scatter of a bf16 weight-gradient partial: `mc` is the partial at its
+// multicast address (every rank's copy bound at the same offset), so one 16-B multimem.ld_reduce
+// returns the sum over all ranks of 8 elements, accumulated in fp32 inside the NVSwitch (and
+// rounded to bf16); this rank reads only its own shard. rows > 0: the gate|up 64-row interleave
+// (as reduce_scatter_interleave_kernel); the fp32 shard gets scale * sum (or += with accumulate).
+__global__ void nvls_reduce_kernel(const __nv_bfloat16* __restrict__ mc, int world, int rank, int64_t shard8,
+                                   int64_t rows, int64_t cols, float scale, int accumulate,
+                                   float* __restrict__ og, float* __restrict__ ou) {
+  const int64_t rpr = rows / world, c8 = cols / 8;
+  const int64_t total = rows > 0 ? 2 * rpr * c8 : shard8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const __nv_bfloat16* src;
+    float* dst;
+    if (rows > 0) {
+      const bool up = i >= rpr * c8;
+      const int64_t li = up ? i - rpr * c8 : i;
+      const int64_t lrow = li / c8, c = li % c8;
+      const int64_t srow = rank * rpr + lrow;
+      const int64_t irow = (srow / kGuBlock) * 2 * kGuBlock + (up ? kGuBlock : 0) + srow % kGuBlock;
+      src = mc + irow * cols + c * 8;
+      dst = (up ? ou : og) + lrow * cols + c * 8;
+    } else {
+      src = mc + (rank * shard8 + i) * 8;
+      dst = og + i * 8;
+    }
+    uint32_t w[4];
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                 : "l"(src)
+                 : "memory");
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+      acc[2 * e] = f.x * scale;
+      acc[2 * e + 1] = f.y * scale;
+    }
+    float4* o = reinterpret_cast<float4*>(dst);
+    float4 r0 = make_float4(acc[0], acc[1], acc[2], acc[3]), r1 = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    if (accumulate) {
+      const float4 p0 = o[0], p1 = o[1];
+      r0.x += p0.x; r0.y += p0.y; r0.z += p0.z; r0.w += p0.w;
+      r1.x += p1.x; r1.y += p1.y; r1.z += p1.z; r1.w += p1.w;
+    }
+    o[0] = r0;
+    o[1] = r1;
+  }
+}
+
 __device__ __forceinline__ void rotate8(uint4& lo, uint4& hi, const float* c, const float* s,
                                         float sign) {
   uint32_t* a = reinterpret_cast<uint32_t*>(&lo);
@@ -319,6 +369,32 @@ __global__ void __launch_bounds__(256) push_copy_kernel(PushJobs jobs, PeerPtrs 
   __threadfence_system();  // remote stores performed before the stream's flag write
 }
 
+// NVLink SHARP all-gather: this rank's shard blocks (jobs with src_q == 0) stored once, 16 B per
+// thread, to the multicast address `mc` + dst_off — the switch writes every rank's copy, this
+// rank's included — then a system-scope fence so the stores are performed before the stream's flag.
+__global__ void __launch_bounds__(256) nvls_push_kernel(PushJobs jobs, char* mc) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int jb = 0; jb < jobs.n; ++jb) {
+    const PushJob& J = jobs.j[jb];
+    const uint32_t bv = static_cast<uint32_t>(J.blk / 16);  // 16-B units per block (< 2^32)
+    const int64_t total = int64_t(bv) * J.nblk;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total; i += stride) {
+      int64_t b = 0, e = i;
+      if (J.nblk > 1) {  // one job stays below 2^32 units: 32-bit division
+        const uint32_t i32 = static_cast<uint32_t>(i);
+        b = i32 / bv;
+        e = i32 - static_cast<uint32_t>(b) * bv;
+      }
+      const uint4 v = ld_v4(J.src + b * J.src_stride + e * 16);
+      char* d = mc + J.dst_off + b * J.dst_stride + e * 16;
+      asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d), "r"(v.x), "r"(v.y),
+                   "r"(v.z), "r"(v.w)
+                   : "memory");
+    }
+  }
+  asm volatile("fence.sc.sys;" ::: "memory");
+}
+
 // Bulk-copy push (the production weight all-gather / reduce-scatter staging in multi-process
 // mode): one thread per CTA drives the TMA unit — cp.async.bulk global -> shared (mbarrier
 // completion), then cp.async.bulk shared -> peer global for every destination. Tens of such
@@ -466,6 +542,17 @@ cudaError_t reduce_scatter_pull_interleave(const PeerPtrs& part, int world, int 
   return cudaGetLastError();
 }
 
+cudaError_t nvls_reduce_scatter(const __nv_bfloat16* mc_part, int world, int rank, int64_t shard_elems,
+                                int64_t interleave_rows, int64_t cols, float scale, int accumulate, float* out,
+                                float* out_up, cudaStream_t st, int num_ctas) {
+  if (shard_elems % 8 || cols % 8) return cudaErrorInvalidValue;
+  const int64_t units = interleave_rows > 0 ? 2 * interleave_rows / world * cols / 8 : shard_elems / 8;
+  nvls_reduce_kernel<<<ctas(units, 256, num_ctas), 256, 0, st>>>(mc_part, world, rank, shard_elems / 8,
+                                                                 interleave_rows, cols, scale, accumulate, out,
+                                                                 out_up);
+  return cudaGetLastError();
+}
+
 // Units per thread per round of the all-to-all kernels (SEQPLAN_ISP_A2A_UNROLL=1 for A/B).
 int a2a_unroll() {
   static const int u = [] {
@@ -494,6 +581,18 @@ cudaError_t a2a_heads_to_tokens(const PeerPtrs& src, int world, int rank, int T,
   auto kern = a2a_unroll() == 1 ? a2a_to_tokens_kernel<1> : a2a_to_tokens_kernel<4>;
   kern<<<ctas(work, 256, num_ctas), 256, 0, st>>>(src, world, rank, T, H, parts, d,
                                                                    dst, cos_t, sin_t, rope_parts);
+  return cudaGetLastError();
+}
+
+cudaError_t nvls_push(const PushJobs& jobs, char* mc, cudaStream_t st, int num_ctas) {
+  for (int j = 0; j < jobs.n; ++j) {
+    const PushJob& J = jobs.j[j];
+    if (J.blk / 16 * J.nblk >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
+    if (J.blk % 16 || J.src_stride % 16 || J.dst_stride % 16 || J.dst_off % 16 || J.src_q != 0 ||
+        reinterpret_cast<uintptr_t>(J.src) % 16)
+      return cudaErrorInvalidValue;
+  }
+  nvls_push_kernel<<<num_ctas, 256, 0, st>>>(jobs, mc);
   return cudaGetLastError();
 }
 

@@ -109,6 +109,13 @@ cudaError_t allgather_pull_interleave(const PeerPtrs& src_gate, const PeerPtrs& 
                                       cudaStream_t st, int num_ctas);
 // Gradient reduce-scatter fused with the cast/scale: out[i] (+)= scale * sum_q part_q[off + i]
 // (bf16 or fp32 partials, fp32 accumulate, fixed rank order).
+// NVLink SHARP reduce-scatter: this rank's shard of a bf16 partial whose every rank's copy is
+// bound to one multicast object (mc_part = its multicast address), reduced in the switch
+// (multimem.ld_reduce, fp32 accumulation); interleave_rows > 0: the gate|up layout of
+// reduce_scatter_pull_interleave (out = gate, out_up = up shard).
+cudaError_t nvls_reduce_scatter(const __nv_bfloat16* mc_part, int world, int rank, int64_t shard_elems,
+                                int64_t interleave_rows, int64_t cols, float scale, int accumulate, float* out,
+                                float* out_up, cudaStream_t st, int num_ctas);
 cudaError_t reduce_scatter_pull(const PeerPtrs& part, int world, int rank, int64_t shard_elems,
                                 bool part_is_f32, float scale, int accumulate, float* out,
                                 cudaStream_t st, int num_ctas);
@@ -146,6 +153,9 @@ struct PushJobs {
 enum PushKind : int { kPushLsu = 0, kPushBulk = 1, kPushBulkWide = 2 };
 cudaError_t push_copy(const PushJobs& jobs, const PeerPtrs& dst, int world, int rank, cudaStream_t st, int num_ctas,
                       int kind);
+// NVLink SHARP all-gather push: every job's blocks stored once to the multicast address mc +
+// dst_off (multimem.st; the switch writes all ranks' copies); jobs must have src_q == 0.
+cudaError_t nvls_push(const PushJobs& jobs, char* mc, cudaStream_t st, int num_ctas);
 // Cross-GPU barrier over system-scope flags in every rank's heap. epoch increases by one per
 // call; a rank spins (bounded, ~20 s) until all peers have published `epoch`.
 cudaError_t peer_barrier(const PeerPtrs& flags, int world, int rank, uint32_t epoch,

@@ -141,6 +141,8 @@ def main():
         per = flat.size // world
         res[capi.W_NAMES[t]] = rel(blk.grad_shard(t), flat[rank * per:(rank + 1) * per])
     res["timeline_events"] = len(blk.timeline())
+    if os.environ.get("MP_REPORT_NVLS"):
+        res["nvls_active"] = blk.nvls_active()
     print(json.dumps(res), flush=True)
     blk.close()
     dist.barrier()

@@ -195,3 +195,17 @@ def test_multiprocess_parity_8_ranks_on_4_gpus():
         for k, v in row.items():
             if k not in ("rank", "timeline_events"):
                 assert v <= 1e-2, (row["rank"], k, v)
+
+
+def test_multiprocess_nvls_reduce_scatter():
+    """The NVLink SHARP reduce-scatter at p = 4 (the default there where the GPUs support
+    multicast): every rank reports it active, and the block matches the oracle."""
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    rows = _run(4, 1024, 8, 1024, "selective", env={"SEQPLAN_ISP_PUSH": "1", "SEQPLAN_ISP_NVLS": "1",
+                                                     "MP_REPORT_NVLS": "1"})
+    for row in rows:
+        assert row.pop("nvls_active") == 1, row
+        for k, v in row.items():
+            if k not in ("rank", "timeline_events"):
+                assert v <= 1e-2, (row["rank"], k, v)
