@@ -34,8 +34,15 @@ def run_worker(*args, env=None):
     # (compute, comm, reduction, one per peer) get their own hardware queue, so a stream blocked
     # in cuStreamWaitValue32 cannot hold back another rank's stream behind it in a shared queue.
     e = {**os.environ, "CUDA_MODULE_LOADING": "EAGER", "CUDA_DEVICE_MAX_CONNECTIONS": "32", **(env or {})}
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "coresident_worker.py"), *map(str, args)],
-                       capture_output=True, text=True, timeout=180, cwd=ROOT, env=e)
+    cmd = [sys.executable, os.path.join(ROOT, "tests", "coresident_worker.py"), *map(str, args)]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=120, cwd=ROOT, env=e)
+    except subprocess.TimeoutExpired:
+        # Ranks sharing one GPU wait for each other through stream memory operations; when the
+        # box's other CUDA contexts (this pytest process) compete for hardware queues this has
+        # been seen to stall once in ~5 full-suite runs (never in the one-process-per-GPU tests).
+        # One retry; a second stall fails the test.
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=120, cwd=ROOT, env=e)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     line = [l for l in r.stdout.splitlines() if l.startswith("RESULT ")][-1]
     return json.loads(line[len("RESULT "):])
