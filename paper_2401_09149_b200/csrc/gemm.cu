@@ -510,6 +510,14 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         int mb, nb;
         sched.coords(t, mb, nb);
         const int m0 = mb * 2 * BM + static_cast<int>(crank) * BM, n0 = nb * BN + static_cast<int>(crank) * BNH;
+        const int wave = (u - cid) / ncl;
+        if (args.wave_cnt && wave > 0) {  // every cluster has issued wave - 1
+          const uint32_t want = static_cast<uint32_t>(min(ncl, n_units - (wave - 1) * ncl));
+          uint32_t got;
+          do {
+            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(got) : "l"(args.wave_cnt + wave - 1) : "memory");
+          } while (got < want && (__nanosleep(64), true));
+        }
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* sa = smem + s * kStageBytes;
@@ -529,6 +537,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           }
           if (++s == S) { s = 0; ph ^= 1; }
         }
+        if (args.wave_cnt && leader) atomicAdd(args.wave_cnt + wave, 1u);
       }
     }
   } else if (warp == 1) {
@@ -754,6 +763,21 @@ cudaError_t launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const Gemm
   const int clusters = tiles < sms / 2 ? tiles : sms / 2;
   GemmArgs a2 = args;
   split_last_wave(a2, tiles, clusters, args.K / BK, stream);
+  static const bool wave_sync_env = [] {
+    const char* e = std::getenv("SEQPLAN_GEMM_WAVE_SYNC");
+    return !e || std::atoi(e) != 0;
+  }();
+  a2.wave_cnt = nullptr;
+  if (wave_sync_env && args.wave_sync && tiles > clusters) {
+    static std::unordered_map<cudaStream_t, uint32_t*> per_stream;
+    uint32_t*& w = per_stream[stream];
+    if (!w && cudaMalloc(&w, 4096 * sizeof(uint32_t)) != cudaSuccess) w = nullptr;
+    const int units = a2.split_L > 0 ? a2.split_base + a2.split_L * a2.split_s : tiles;
+    if (w && units / clusters + 1 <= 4096) {
+      cudaMemsetAsync(w, 0, size_t(units / clusters + 1) * sizeof(uint32_t), stream);
+      a2.wave_cnt = w;
+    }
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * clusters);
   cfg.blockDim = dim3(kNumThreads);

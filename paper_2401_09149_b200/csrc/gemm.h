@@ -67,6 +67,14 @@ struct GemmArgs {
   float* split_ws = nullptr;
   uint32_t* split_cnt = nullptr;    // [L][2] arrivals per (tile, CTA of the pair); self-resetting
   uint32_t* split_ready = nullptr;  // [L][s-1][2] partial p of (tile, CTA) written; self-resetting
+  // Wave pacing (CTA-pair kernel): a cluster starts
+  // loading its tile of wave w only after every cluster has issued the loads of wave w-1, so the
+  // tiles of one wave stream the same K-slices of the shared panels through L2 together instead of
+  // drifting apart over the waves (7B-32K step: GEMM DRAM traffic 74.9 -> 46.1 GB, -7 % GEMM time
+  // in ncu, +1 % end to end under the power cap). Needs every cluster of the grid resident at once:
+  // callers whose GEMMs may run concurrently with another persistent grid clear wave_sync.
+  int wave_sync = 1;  // SEQPLAN_GEMM_WAVE_SYNC=0 turns it off everywhere
+  uint32_t* wave_cnt = nullptr;  // zeroed per launch by gemm_launch
 };
 
 int gemm_pick_bn(int N);

@@ -360,6 +360,9 @@ void gemm(Ctx* c, const GemmOperand& A, const GemmOperand& B, const GemmArgs& ar
   c->launches += 1;
   GemmArgs a = args;
   if (c->push_mode() && c->gemm_sm_budget > 0) a.sm_budget = c->gemm_sm_budget;
+  // co-resident ranks run their GEMMs concurrently on one GPU: a wave-paced grid could then wait
+  // for clusters that cannot become resident
+  if (c->co_resident) a.wave_sync = 0;
   cudaError_t e = gemm_launch(A, B, a, epi, st);
   if (e == cudaErrorInvalidValue)
     throw IspError(SEQPLAN_ISP_ERR_UNSUPPORTED, "GEMM shape not tiled by the sm_100a kernel (M%128, N%128, K%64)");
