@@ -360,9 +360,11 @@ void gemm(Ctx* c, const GemmOperand& A, const GemmOperand& B, const GemmArgs& ar
   c->launches += 1;
   GemmArgs a = args;
   if (c->push_mode() && c->gemm_sm_budget > 0) a.sm_budget = c->gemm_sm_budget;
-  // co-resident ranks run their GEMMs concurrently on one GPU: a wave-paced grid could then wait
-  // for clusters that cannot become resident
-  if (c->co_resident) a.wave_sync = 0;
+  // Wave pacing: off for co-resident ranks (their GEMMs run concurrently on one GPU: a paced grid
+  // could wait for clusters that cannot become resident) and under the push transport, whose SM
+  // copy / reduction kernels slow some clusters and then hold every cluster at the wave boundary
+  // (7B-32K p = 4: 1.906 M tokens/s without, 1.867 M with; 7B-4K 1.60 vs 1.53 M)
+  if (c->co_resident || c->push_mode()) a.wave_sync = 0;
   cudaError_t e = gemm_launch(A, B, a, epi, st);
   if (e == cudaErrorInvalidValue)
     throw IspError(SEQPLAN_ISP_ERR_UNSUPPORTED, "GEMM shape not tiled by the sm_100a kernel (M%128, N%128, K%64)");
