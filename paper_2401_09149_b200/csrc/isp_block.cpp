@@ -153,6 +153,7 @@ struct seqplan_isp_ctx {
   // stored-dS attention backward workspace cap, GiB (SEQPLAN_ISP_DS_WS_GB; 0 = two-role kernel);
   // default: a quarter of the device memory, at most 48 GiB (7B-32K p = 1: all 32 heads' dS, 34.6 GB)
   int64_t ds_ws_gb = -1;
+  int64_t ds_ws_cached = 0;  // largest workspace the pool has served (its segment stays cached)
   int tail[SEQPLAN_W_COUNT] = {}, tail_n = 0;
   cudaEvent_t ev_tail = nullptr;
   bool owns_comm = true;       // false: the comm stream belongs to layer 0 of a stack
@@ -1269,10 +1270,17 @@ void bwd_phase2(Ctx* c, cudaStream_t st) {
   if (c->d == 128 && c->ds_ws_gb > 0 && c->S % 128 == 0) {
     const int64_t per_head = attention_bwd_ds_head_bytes(static_cast<int>(c->S));
     const int64_t cap = std::max(c->ds_ws_gb << 30, per_head <= (c->ds_ws_gb << 30) * 2 ? per_head : int64_t(0));
-    const int64_t g = std::min<int64_t>(c->Dl, cap / per_head);
+    int64_t g = std::min<int64_t>(c->Dl, cap / per_head);
+    if (g * per_head > c->ds_ws_cached) {  // a new segment: only what the device has free (1 GiB kept)
+      size_t free_b = 0, total_b = 0;
+      ISP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      const int64_t room = std::max<int64_t>(int64_t(free_b) - (int64_t(1) << 30), 0);
+      g = std::min<int64_t>(g, std::max(room, c->ds_ws_cached) / per_head);
+    }
     if (g > 0) {
       t.ds_ws_bytes = g * per_head;
       ws = t.ds_ws = pool_alloc(c, t.ds_ws_bytes, seqplan::AllocTag::Other, st);
+      c->ds_ws_cached = std::max(c->ds_ws_cached, t.ds_ws_bytes);  // the pool keeps the segment
     }
   }
   KTimer kt(c, st, SEQPLAN_K_ATTN_BWD, 4.0 * double(c->S) * double(c->S) * double(c->Hl), 0);
