@@ -55,6 +55,62 @@ def test_peer_bootstrap_gloo_world2():
     assert res == [(0, [0, 1], [64, 64]), (1, [0, 1], [64, 64])]
 
 
+class _FakeNvlsBlock(_FakeBlock):
+    """Records the NVLS bootstrap calls; `fail_attach` ranks report an attach failure."""
+    def __init__(self, rank, supported=True, fail_attach=()):
+        super().__init__(rank)
+        self.device = rank
+        self.supported, self.fail_attach = supported, fail_attach
+        self.calls = []
+
+    def nvls_export(self):
+        self.calls.append("export")
+        return (4242, 7) if self.supported else None
+
+    def nvls_attach(self, pid, fd):
+        self.calls.append(("attach", pid, fd))
+        return self.rank not in self.fail_attach
+
+    def nvls_bind(self):
+        self.calls.append("bind")
+        return True
+
+    def nvls_release(self):
+        self.calls.append("release")
+
+
+def _nvls_worker(rank, world, port, q, supported, fail_attach):
+    import torch.distributed as dist
+    from paper_2401_09149_b200.dist import bootstrap_peers
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    blk = _FakeNvlsBlock(rank, supported, fail_attach)
+    bootstrap_peers(blk, world)
+    q.put((rank, blk.calls))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("supported,fail_attach,port", [(True, (), 29612), (False, (), 29613), (True, (1,), 29614)])
+def test_nvls_bootstrap_agreement_gloo_world2(supported, fail_attach, port):
+    """dist.bootstrap_nvls: rank 0 exports and publishes (pid, fd); the others attach with it (rank
+    0 with (0, -1)); binding happens only when every rank attached, and a failure anywhere
+    releases NVLS on every rank; an unsupported export stops everyone before attaching."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_nvls_worker, args=(r, 2, port, q, supported, fail_attach)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    if not supported:
+        assert res == {0: ["export"], 1: []}
+    elif not fail_attach:
+        assert res == {0: ["export", ("attach", 0, -1), "bind"], 1: [("attach", 4242, 7), "bind"]}
+    else:
+        assert res == {0: ["export", ("attach", 0, -1), "release"], 1: [("attach", 4242, 7), "release"]}
+
+
 def test_bench_dominant_kernel_and_timeline_exposure():
     """bench.py's roofline line reports the tensor-core kernel with the largest share of the step,
     and the timeline cross-check counts comm (or all-to-all) time not covered by compute."""
