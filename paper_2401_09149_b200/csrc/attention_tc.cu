@@ -1806,30 +1806,35 @@ __global__ void __launch_bounds__(kBwdSThreads, 1)
 // both operands MN-major from shared memory (dS tile: one 32 KB bulk copy; K: TMA), fp32 in TMEM,
 // then the query-tile epilogue (inverse RoPE from fp32; bf16 rows or pushed to the owner rank).
 // One MMA per tile pair; bound by the HBM stream of dS.
+// ND dS stages and NK K stages: the dS stream comes from HBM, the K tiles mostly from L2, so the
+// dS ring runs ND - NK tiles ahead of the K ring (more HBM bytes in flight per SM).
+template <int ND, int NK>
 struct BwdDqCfg {
   static constexpr int kTile = 128 * 128 * 2;
-  static constexpr int kStages = 3;
-  static constexpr int kOffDS = 0, kOffK = kStages * kTile;
-  static constexpr int kOffBar = 2 * kStages * kTile;
-  static constexpr int kBytes = kOffBar + 128 + 1024;
+  static constexpr int kOffDS = 0, kOffK = ND * kTile;
+  static constexpr int kOffBar = (ND + NK) * kTile;
+  static constexpr int kBytes = kOffBar + 256 + 1024;
   static_assert(kBytes <= 232448, "exceeds the 227 KB per-CTA shared memory");
 };
 constexpr int kBwdDqThreads = 192;  // warps 0..3 epilogue (one TMEM lane quadrant each), 4 TMA, 5 MMA
 
+template <int ND, int NK>
 __global__ void __launch_bounds__(kBwdDqThreads, 1)
     attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap mK, const uint8_t* __restrict__ ds,
                        __nv_bfloat16* __restrict__ dq_out, int64_t ld_d, int S, float scale,
                        const __grid_constant__ AttnPush push, const float* __restrict__ rope_cos,
                        const float* __restrict__ rope_sin, int h0) {
-  using L = BwdDqCfg;
+  using L = BwdDqCfg<ND, NK>;
   constexpr int D = 128;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
-  uint64_t* full = bar;        // [3]
-  uint64_t* empty = bar + 3;   // [3]
-  uint64_t* acc_full = bar + 6;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 7);
+  uint64_t* full_d = bar;              // [ND]
+  uint64_t* empty_d = bar + ND;        // [ND]
+  uint64_t* full_k = bar + 2 * ND;     // [NK]
+  uint64_t* empty_k = full_k + NK;     // [NK]
+  uint64_t* acc_full = empty_k + NK;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int lin = static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x);
   const int T = S / 128;
@@ -1840,7 +1845,8 @@ __global__ void __launch_bounds__(kBwdDqThreads, 1)
 
   if (warp == 4 && lane == 0) {
     tma_prefetch(&mK);
-    for (int s = 0; s < L::kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < ND; ++s) { mbar_init(&full_d[s], 1); mbar_init(&empty_d[s], 1); }
+    for (int s = 0; s < NK; ++s) { mbar_init(&full_k[s], 1); mbar_init(&empty_k[s], 1); }
     mbar_init(acc_full, 1);
     fence_barrier_init();
   }
@@ -1854,13 +1860,23 @@ __global__ void __launch_bounds__(kBwdDqThreads, 1)
     if (lane == 0) {
       const uint8_t* dsh = ds + (int64_t(hg) * ds_tiles_per_head(T) << 15);
       const uint64_t pol = l2_evict_first_policy();
-      for (int k = 0; k < n; ++k) {
-        const int s = k % L::kStages;
-        if (k >= L::kStages) mbar_wait(&empty[s], ((k / L::kStages) - 1) & 1);
-        mbar_arrive_expect_tx(&full[s], 2 * L::kTile);
-        bulk_load_stream(smem + L::kOffDS + s * L::kTile, dsh + (ds_slot(k, qt, T) << 15), L::kTile, &full[s], pol);
-        for (int c = 0; c < 2; ++c)
-          tma_load_2d(smem + L::kOffK + s * L::kTile + c * (L::kTile / 2), &mK, &full[s], h * D + c * 64, k * 128);
+      constexpr int kLead = ND - NK;  // dS tiles issued ahead of the K tiles
+      for (int i = 0; i < n + kLead; ++i) {
+        if (i < n) {
+          const int s = i % ND;
+          if (i >= ND) mbar_wait(&empty_d[s], ((i / ND) - 1) & 1);
+          mbar_arrive_expect_tx(&full_d[s], L::kTile);
+          bulk_load_stream(smem + L::kOffDS + s * L::kTile, dsh + (ds_slot(i, qt, T) << 15), L::kTile, &full_d[s],
+                           pol);
+        }
+        const int k = i - kLead;
+        if (k >= 0 && k < n) {
+          const int s = k % NK;
+          if (k >= NK) mbar_wait(&empty_k[s], ((k / NK) - 1) & 1);
+          mbar_arrive_expect_tx(&full_k[s], L::kTile);
+          for (int c = 0; c < 2; ++c)
+            tma_load_2d(smem + L::kOffK + s * L::kTile + c * (L::kTile / 2), &mK, &full_k[s], h * D + c * 64, k * 128);
+        }
       }
     }
   } else if (warp == 5) {
@@ -1870,15 +1886,17 @@ __global__ void __launch_bounds__(kBwdDqThreads, 1)
       // K-direction core-matrix stride (key groups, 128 B) and the stride byte offset the MN-direction
       // one (query groups, 512 B); the 16 keys of MMA kk start at (kk / 2) * 8192 + (kk % 2) * 256
       for (int k = 0; k < n; ++k) {
-        const int s = k % L::kStages;
-        mbar_wait(&full[s], (k / L::kStages) & 1);
+        const int sd = k % ND, sk = k % NK;
+        mbar_wait(&full_d[sd], (k / ND) & 1);
+        mbar_wait(&full_k[sk], (k / NK) & 1);
         tc_fence_after();
-        const uint32_t a = smem_u32(smem + L::kOffDS + s * L::kTile), b = smem_u32(smem + L::kOffK + s * L::kTile);
+        const uint32_t a = smem_u32(smem + L::kOffDS + sd * L::kTile), b = smem_u32(smem + L::kOffK + sk * L::kTile);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)  // 16 keys per MMA
           tc_mma_bf16(tmem, make_nosw_desc(a + (kk >> 1) * 8192 + (kk & 1) * 256, 128, 512),
                       make_sw128_desc(b + kk * 2048, L::kTile / 2, 1024), id, (k > 0 || kk > 0) ? 1u : 0u);
-        tc_commit(&empty[s]);
+        tc_commit(&empty_d[sd]);
+        tc_commit(&empty_k[sk]);
       }
       tc_commit(acc_full);
     }
@@ -2006,8 +2024,10 @@ cudaError_t attention_bwd_ds_tc(const AttnTensors& t, const __nv_bfloat16* dout,
                              BwdSCfg::kBytesD) != cudaSuccess ||
         cudaFuncSetAttribute(attn_bwd_split_kernel<0, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              BwdSCfg::kBytes) != cudaSuccess ||
-        cudaFuncSetAttribute(attn_bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdDqCfg::kBytes) !=
-            cudaSuccess)
+        cudaFuncSetAttribute(attn_bwd_dq_kernel<3, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             BwdDqCfg<3, 3>::kBytes) != cudaSuccess ||
+        cudaFuncSetAttribute(attn_bwd_dq_kernel<5, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             BwdDqCfg<5, 2>::kBytes) != cudaSuccess)
       return cudaErrorInvalidValue;
     attr = true;
   }
@@ -2021,6 +2041,12 @@ cudaError_t attention_bwd_ds_tc(const AttnTensors& t, const __nv_bfloat16* dout,
   const int dbg = std::getenv("SEQPLAN_ISP_DBG") ? std::atoi(std::getenv("SEQPLAN_ISP_DBG")) : 0;
   uint8_t* w = static_cast<uint8_t*>(ws);
   const bool direct = std::getenv("SEQPLAN_ISP_DS_DIRECT") != nullptr;  // development: st.global instead of bulk
+  // dQ kernel rings: 3 dS + 3 K stages; SEQPLAN_ISP_DQ_STAGES=52 (5 dS ahead of 2 K) measured slower
+  // (32K x 32 heads: dQ 6.0 vs 5.23 ms)
+  static const bool deep = [] {
+    const char* e = std::getenv("SEQPLAN_ISP_DQ_STAGES");
+    return e && std::atoi(e) == 52;
+  }();
   cudaEvent_t tev[3] = {};
   const bool timed = (dbg & 1024) != 0;  // development: per-kernel event times of the first group
   if (timed)
@@ -2040,9 +2066,14 @@ cudaError_t attention_bwd_ds_tc(const AttnTensors& t, const __nv_bfloat16* dout,
             g_attn_trace, w, h0);
     }
     if (timed && h0 == 0) cudaEventRecord(tev[1], st);
-    if (!(dbg & 128))
-      attn_bwd_dq_kernel<<<grid, kBwdDqThreads, BwdDqCfg::kBytes, st>>>(mk, w, dq, ld_d, t.S, scale, t.push,
-                                                                         t.rope_cos, t.rope_sin, h0);
+    if (!(dbg & 128)) {
+      if (deep)
+        attn_bwd_dq_kernel<5, 2><<<grid, kBwdDqThreads, BwdDqCfg<5, 2>::kBytes, st>>>(
+            mk, w, dq, ld_d, t.S, scale, t.push, t.rope_cos, t.rope_sin, h0);
+      else
+        attn_bwd_dq_kernel<3, 3><<<grid, kBwdDqThreads, BwdDqCfg<3, 3>::kBytes, st>>>(
+            mk, w, dq, ld_d, t.S, scale, t.push, t.rope_cos, t.rope_sin, h0);
+    }
     if (timed && h0 == 0) cudaEventRecord(tev[2], st);
   }
   if (timed) {
